@@ -1,0 +1,346 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each test names the oracle function and what pins it: a
+golden hand-derived example (tests/golden/, cited), a closed form, an
+invariant, a library routine (numpy sort/argmin) on brute force, or the
+paper's own algorithm transcribed independently (tests/seil_paper_sim.py).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.seil_paper_sim import seil_insert, seil_search
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def ordered_d64(a, b):
+    """fp64 ordered sum of squared differences (np.cumsum is sequential)."""
+    df = a.astype(np.float64) - b.astype(np.float64)
+    return np.cumsum(df * df, axis=-1)[..., -1]
+
+
+def rand_problem(seed=0, n=600, d=8, nlist=12, nq=15, scale=1.0):
+    rng = np.random.default_rng(seed)
+    X = (rng.standard_normal((n, d)) * scale).astype(np.float32)
+    Q = (rng.standard_normal((nq, d)) * scale).astype(np.float32)
+    C = (rng.standard_normal((nlist, d)) * scale).astype(np.float32)
+    return X, Q, C
+
+
+# ------------------------------------------------------------------ O1
+def test_probe_equals_full_sort(oracle_mod):
+    X, Q, C = rand_problem(1)
+    P = oracle_mod.probe(Q, C, 7)
+    D = ordered_d64(Q[:, None, :], C[None, :, :])
+    for i in range(Q.shape[0]):
+        order = np.lexsort((np.arange(C.shape[0]), D[i]))
+        assert list(P[i]) == list(order[:7])
+
+
+def test_probe_prefix_and_self(oracle_mod):
+    X, Q, C = rand_problem(2)
+    P3 = oracle_mod.probe(Q, C, 3)
+    P9 = oracle_mod.probe(Q, C, 9)
+    assert np.array_equal(P3, P9[:, :3])                   # S:119 prefix property
+    Pc = oracle_mod.probe(C, C, 1)                          # q = centroid -> itself
+    assert list(Pc[:, 0]) == list(range(C.shape[0]))
+
+
+def test_probe_ties_by_list_id(oracle_mod):
+    C = np.array([[1, 0], [0, 1], [-1, 0], [0, -1]], np.float32)
+    P = oracle_mod.probe(np.zeros((1, 2), np.float32), C, 4)
+    assert list(P[0]) == [0, 1, 2, 3]                       # all equal -> by id
+
+
+# ------------------------------------------------------------------ O2
+def _toy_codebook(t):
+    if "codebook" in t:
+        return np.array(t["codebook"], np.float32)
+    cb = np.zeros((t["M"], 16, t["dsub"]), np.float32)
+    for m, v in enumerate(t["codebook_const"]):
+        cb[m, :, :] = np.array(v, np.float32)
+    return cb
+
+
+@pytest.mark.parametrize("toy", json.load(open(os.path.join(GOLD, "lut_toys.json")))["toys"],
+                         ids=lambda t: t["name"])
+def test_lut_golden(oracle_mod, toy):
+    cb = _toy_codebook(toy)
+    q = np.array([toy["query"]], np.float32)
+    Qv, a, b = oracle_mod.lut(q, cb)
+    assert a[0] == np.float32(toy["a"])
+    assert b[0] == np.float32(toy["b"])
+    if "Qv" in toy:
+        assert Qv[0].tolist() == toy["Qv"]
+        for sc in toy["scores"]:
+            s = sum(int(Qv[0, m, c]) for m, c in enumerate(sc["code"]))
+            assert s == sc["s"]
+    else:
+        assert int(Qv.max()) == toy["Qv_all"] == int(Qv.min())
+
+
+def test_lut_invariants_and_error_bound(oracle_mod):
+    rng = np.random.default_rng(3)
+    d, M = 32, 8
+    cb = rng.standard_normal((M, 16, d // M)).astype(np.float32)
+    Q = rng.standard_normal((50, d)).astype(np.float32)
+    Qv, a, b = oracle_mod.lut(Q, cb)
+    assert (Qv.min(axis=2) == 0).all()                      # min_j Qv[m][j] = 0
+    assert (Qv.max(axis=(1, 2)) == 255).all()               # the widest row spans 255
+    # |b + s/a - ADC| <= M/(2a) (+ fp32 rounding slack) for random codes
+    codes = rng.integers(0, 16, size=(200, M))
+    dsub = d // M
+    for i in range(Q.shape[0]):
+        T = ((Q[i].reshape(M, 1, dsub).astype(np.float64) - cb.astype(np.float64)) ** 2).sum(-1)
+        adc = T[np.arange(M)[None, :], codes].sum(1)
+        s = Qv[i][np.arange(M)[None, :], codes].astype(np.int64).sum(1)
+        est = b[i] + s / a[i]
+        bound = M / (2.0 * a[i]) + 1e-4 * (1 + np.abs(adc))
+        assert (np.abs(est - adc) <= bound).all()
+
+
+# ------------------------------------------------------------------ O4
+def test_assign_lambda0_strict_is_naivera(oracle_mod):
+    X, Q, C = rand_problem(4, n=400)
+    l1, l2 = oracle_mod.assign(X, C, "air", lam=0.0, n_cands=10, strict=True)
+    D = ordered_d64(X[:, None, :], C[None, :, :])
+    for i in range(X.shape[0]):
+        order = np.lexsort((np.arange(C.shape[0]), D[i]))
+        pair = sorted(order[:2].tolist())                   # NaiveRA
+        assert [l1[i], l2[i]] == pair
+
+
+def test_assign_lambda0_nonstrict_is_single(oracle_mod):
+    X, Q, C = rand_problem(5, n=300)
+    l1, l2 = oracle_mod.assign(X, C, "air", lam=0.0, n_cands=10, strict=False)
+    P = oracle_mod.probe(X, C, 1)[:, 0]
+    assert np.array_equal(l1, P) and np.array_equal(l2, P)
+
+
+def test_assign_inverse_residual_closed_form(oracle_mod):
+    # x = 0, c0 = (1,0,...), c1 = (-1.01,0,...) : r' ~ -r.
+    # loss0 = (1+0.5)*1 = 1.5 ; loss1 = 1.0201 + 0.5*(1*-1.01) = 0.5151 -> (0,1)
+    C = np.zeros((4, 4), np.float32)
+    C[0, 0], C[1, 0], C[2, 1], C[3, 1] = 1.0, -1.01, 3.0, -3.0
+    l1, l2 = oracle_mod.assign(np.zeros((1, 4), np.float32), C, "air", 0.5, 10)
+    assert (l1[0], l2[0]) == (0, 1)
+    # x exactly at a centroid (r = 0) -> single
+    l1, l2 = oracle_mod.assign(C[2:3], C, "air", 0.5, 10)
+    assert (l1[0], l2[0]) == (2, 2)
+
+
+def test_assign_exhaustive_argmin_and_rair_condition(oracle_mod):
+    X, Q, C = rand_problem(6, n=500, nlist=9)
+    lam = 0.5
+    l1, l2 = oracle_mod.assign(X, C, "air", lam, n_cands=9)    # N_C = nlist
+    D = ordered_d64(X[:, None, :], C[None, :, :])
+    for i in range(X.shape[0]):
+        order = np.lexsort((np.arange(C.shape[0]), D[i]))
+        c0 = order[0]
+        r0 = C[c0].astype(np.float64) - X[i].astype(np.float64)
+        R = C[order].astype(np.float64) - X[i].astype(np.float64)
+        loss = np.cumsum(R * R, 1)[:, -1] + lam * np.cumsum(r0[None] * R, 1)[:, -1]
+        best = order[int(np.argmin(loss))]                   # exhaustive argmin, first index
+        assert [l1[i], l2[i]] == sorted([int(c0), int(best)])
+        assert l1[i] <= l2[i]                                 # sorted pair
+        # RAIR single-assignment condition
+        rr = float(np.dot(r0, r0))
+        cond = all(float(np.dot(R[j], R[j]) + lam * np.dot(r0, R[j])) >= (1 + lam) * rr - 1e-9 * rr
+                   for j in range(1, C.shape[0]))
+        single = l1[i] == l2[i]
+        if single:
+            assert cond
+
+
+def test_assign_single_mode(oracle_mod):
+    X, Q, C = rand_problem(7, n=200)
+    l1, l2 = oracle_mod.assign(X, C, "single")
+    P = oracle_mod.probe(X, C, 1)[:, 0]
+    assert np.array_equal(l1, P) and np.array_equal(l2, P)
+
+
+# ------------------------------------------------------------------ O5
+def test_encode_concatenation_and_brute_force(oracle_mod):
+    rng = np.random.default_rng(8)
+    M, dsub = 6, 3
+    cb = rng.standard_normal((M, 16, dsub)).astype(np.float32)
+    codes = rng.integers(0, 16, size=(50, M))
+    Xc = np.stack([np.concatenate([cb[m, codes[i, m]] for m in range(M)]) for i in range(50)])
+    assert np.array_equal(oracle_mod.encode(Xc, cb), codes.astype(np.uint8))
+    X = rng.standard_normal((300, M * dsub)).astype(np.float32)
+    got = oracle_mod.encode(X, cb)
+    for m in range(M):
+        sub = X[:, m * dsub:(m + 1) * dsub]
+        D = ordered_d64(sub[:, None, :], cb[m][None, :, :])
+        assert np.array_equal(got[:, m], np.argmin(D, axis=1))                    # first argmin
+
+
+# ------------------------------------------------------------- O7-O10
+def _small_index(oracle_mod, seed=9, n=800, d=8, nlist=10, M=4, mode="air"):
+    X, Q, _ = rand_problem(seed, n=n, d=d, nlist=nlist, nq=12, scale=1.0)
+    C = oracle_mod.kmeans(X, nlist, iters=5, seed=seed)
+    cb = oracle_mod.pq_train(X, M, iters=5, seed=seed)
+    l1, l2 = oracle_mod.assign(X, C, mode)
+    codes = oracle_mod.encode(X, cb)
+    return X, Q, C, cb, l1, l2, codes
+
+
+def test_seil_toy_universe(oracle_mod):
+    toy = json.load(open(os.path.join(GOLD, "seil_toy.json")))
+    C = np.array(toy["centroids"], np.float32)
+    X = np.zeros((5, 2), np.float32)
+    cb = np.zeros((2, 16, 1), np.float32)
+    codes = np.zeros((5, 2), np.uint8)
+    for case in toy["cases"]:
+        q = np.array([case["query"]], np.float32)
+        r = oracle_mod.search(X, toy["l1"], toy["l2"], codes, C, cb, q, k=1,
+                              nprobe=case["nprobe"], refine_factor=5)
+        assert r["probes"][0].tolist() == case["P"]
+        assert int(r["dco"][0, 0]) == len(case["U"])
+        got = sorted(int(v) for v in r["cand_ids"][0, 0] if v != 0xFFFFFFFF)
+        assert got == case["U"]
+
+
+def test_search_exhaustive_reduction(oracle_mod):
+    # nprobe = nlist and bigK >= n -> exactly the exact k-NN (BJ)
+    for mode in ("air", "single"):
+        X, Q, C, cb, l1, l2, codes = _small_index(oracle_mod, mode=mode)
+        k = 10
+        r = oracle_mod.search(X, l1, l2, codes, C, cb, Q, k=k, nprobe=C.shape[0],
+                              refine_factor=X.shape[0] // k + 1)
+        D = ordered_d64(Q[:, None, :], X[None, :, :]).astype(np.float32)
+        for i in range(Q.shape[0]):
+            order = np.lexsort((np.arange(X.shape[0]), D[i]))[:k]
+            assert r["ids"][i].tolist() == order.tolist()
+            assert np.array_equal(r["dists"][i], D[i][order])
+        gt, _ = oracle_mod.exact_knn(X, Q, k)
+        ok = np.mean([len(set(gt[i]) & set(r["ids"][i])) / k for i in range(Q.shape[0])])
+        assert ok == 1.0
+
+
+def test_search_candidates_brute_force(oracle_mod):
+    X, Q, C, cb, l1, l2, codes = _small_index(oracle_mod, seed=10)
+    k, nprobe, rf = 5, 3, 4
+    r = oracle_mod.search(X, l1, l2, codes, C, cb, Q, k=k, nprobe=nprobe, refine_factor=rf)
+    Qv, a, b = oracle_mod.lut(Q, cb)
+    assert np.array_equal(Qv, r["Qv"]) and np.array_equal(a, r["a"])
+    M = cb.shape[0]
+    for i in range(Q.shape[0]):
+        P = r["probes"][i]
+        U = np.nonzero(np.isin(l1, P) | np.isin(l2, P))[0]                  # O7 by numpy
+        s = Qv[i][np.arange(M)[None, :], codes[U]].astype(np.int64).sum(1)  # O8 scalar ADC
+        order = np.lexsort((U, s))[:k * rf]                                   # O9 full sort
+        assert int(r["dco"][i, 0]) == U.size
+        assert r["cand_ids"][i, 0, :order.size].tolist() == U[order].tolist()
+        assert r["cand_scores"][i, 0, :order.size].tolist() == s[order].tolist()
+        cand = U[order]
+        dd = ordered_d64(Q[i][None, :], X[cand]).astype(np.float32)         # O10
+        ro = np.lexsort((cand, dd))[:k]
+        assert r["ids"][i].tolist() == cand[ro].tolist()
+
+
+def test_search_pads_when_universe_small(oracle_mod):
+    toy = json.load(open(os.path.join(GOLD, "seil_toy.json")))
+    C = np.array(toy["centroids"], np.float32)
+    X = np.arange(10, dtype=np.float32).reshape(5, 2)
+    cb = np.zeros((2, 16, 1), np.float32)
+    codes = np.zeros((5, 2), np.uint8)
+    r = oracle_mod.search(X, toy["l1"], toy["l2"], codes, C, cb,
+                          np.array([[-1.0, -1.0]], np.float32), k=5, nprobe=1, refine_factor=2)
+    assert r["ids"][0].tolist()[3:] == [-1, -1]                              # |U| = 3 < k (R13)
+    assert np.isinf(r["dists"][0, 3:]).all()
+
+
+def test_shards_partition(oracle_mod):
+    X, Q, C, cb, l1, l2, codes = _small_index(oracle_mod, seed=11)
+    r1 = oracle_mod.search(X, l1, l2, codes, C, cb, Q, 5, 3, 4, nshards=1)
+    for G in (2, 3, 4):
+        rg = oracle_mod.search(X, l1, l2, codes, C, cb, Q, 5, 3, 4, nshards=G)
+        assert np.array_equal(rg["dco"].sum(1), r1["dco"][:, 0])             # U_s partition U
+        for i in range(Q.shape[0]):
+            for s in range(G):
+                ids = [int(v) for v in rg["cand_ids"][i, s] if v != 0xFFFFFFFF]
+                assert all(v % G == s for v in ids)
+            # final result = first k of the union of per-shard results
+            pool = [(float(rg["shard_dists"][i, s, j]), int(rg["shard_ids"][i, s, j]))
+                    for s in range(G) for j in range(5) if rg["shard_ids"][i, s, j] >= 0]
+            assert [v for _, v in sorted(pool)[:5]] == rg["ids"][i].tolist()
+        # exhaustive case is shard-invariant
+        ex1 = oracle_mod.search(X, l1, l2, codes, C, cb, Q, 5, C.shape[0], X.shape[0], nshards=1)
+        exg = oracle_mod.search(X, l1, l2, codes, C, cb, Q, 5, C.shape[0], X.shape[0], nshards=G)
+        assert np.array_equal(ex1["ids"], exg["ids"])
+
+
+# ------------------------------------------------ R9 / O12 against Alg. 4-5
+def _toy_assignment(seed, n=6000, nlist=6):
+    rng = np.random.default_rng(seed)
+    l1 = rng.integers(0, nlist, n)
+    other = rng.integers(0, nlist, n)
+    single = rng.random(n) < 0.5
+    a = np.where(single, l1, np.minimum(l1, other))
+    b = np.where(single, l1, np.maximum(l1, other))
+    return a.astype(np.int32), b.astype(np.int32)
+
+
+def test_alg5_ascending_reaches_universe_and_dco_identities(oracle_mod):
+    import itertools
+    nlist = 6
+    l1, l2 = _toy_assignment(12, nlist=nlist)
+    lists = seil_insert(l1, l2)
+    subsets = [list(s) for r in range(1, nlist + 1) for s in itertools.combinations(range(nlist), r)]
+    P = np.full((len(subsets), nlist), -1, np.int32)
+    for i, s in enumerate(subsets):
+        P[i, :len(s)] = s
+    for i, s in enumerate(subsets):
+        U = set(np.nonzero(np.isin(l1, s) | np.isin(l2, s))[0].tolist())
+        kept, dco_scan = seil_search(lists, sorted(s))
+        assert len(kept) == len(set(kept)) and set(kept) == U                  # R9 ascending
+        noseil, paper = oracle_mod.dco_variants(l1, l2, nlist, np.array([s], np.int32))
+        assert paper[0] == dco_scan                                              # O12 formula
+        both = sum(int(np.sum((l1 == a) & (l2 == b))) for a in s for b in s if a < b)
+        full = sum(32 * (int(np.sum((l1 == a) & (l2 == b))) // 32) for a in s for b in s if a < b)
+        assert noseil[0] - len(U) == both
+        assert noseil[0] - paper[0] == full
+        if len(s) > 1:
+            kept_desc, _ = seil_search(lists, sorted(s, reverse=True))
+            assert len(kept_desc) > len(set(kept_desc))                         # erratum R9
+
+
+def test_dco_single_assignment_all_equal(oracle_mod):
+    rng = np.random.default_rng(13)
+    l = rng.integers(0, 8, 3000).astype(np.int32)
+    P = np.array([[0, 3, 5], [1, 2, 7]], np.int32)
+    noseil, paper = oracle_mod.dco_variants(l, l, 8, P)
+    for i in range(2):
+        U = int(np.isin(l, P[i]).sum())
+        assert noseil[i] == paper[i] == U
+
+
+# ------------------------------------------------------------------ O13
+def test_exact_knn_brute_force(oracle_mod):
+    X, Q, C = rand_problem(14, n=700)
+    ids, dd = oracle_mod.exact_knn(X, Q, 9)
+    D = ordered_d64(Q[:, None, :], X[None, :, :])
+    for i in range(Q.shape[0]):
+        order = np.lexsort((np.arange(X.shape[0]), D[i]))[:9]
+        assert ids[i].tolist() == order.tolist()
+        assert np.array_equal(dd[i], D[i][order])
+    # 1-D hand check: base {0,3,10}, q=2, K=2 -> (3) then (0)
+    ids, _ = oracle_mod.exact_knn(np.array([[0.], [3.], [10.]], np.float32),
+                                  np.array([[2.]], np.float32), 2)
+    assert ids[0].tolist() == [1, 0]
+
+
+# ------------------------------------------------- O3 (training invariants)
+def test_kmeans_invariants(oracle_mod):
+    X, Q, C = rand_problem(15, n=500)
+    c1 = oracle_mod.kmeans(X, 1, iters=3)
+    assert np.allclose(c1[0], X.astype(np.float64).mean(0), rtol=1e-6, atol=1e-6)
+    _, trace = oracle_mod.kmeans(X, 8, iters=10, return_trace=True)
+    assert np.all(np.diff(trace) <= 1e-9 * trace[0])
+    Xd = X[:20]
+    _, tr = oracle_mod.kmeans(Xd, 20, iters=2, return_trace=True)
+    assert tr[-1] == 0.0                                                           # nlist = n
