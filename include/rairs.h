@@ -1,0 +1,189 @@
+/*
+ * rairs.h -- C ABI of the B200 (sm_100a) RAIRS search library (librairs.so).
+ *
+ * RAIRS = RAIR redundant assignment + SEIL shared-cell lists over an IVF-PQ
+ * 4-bit fast-scan index with exact refine (arXiv 2601.07183).  This library
+ * implements the query-time hot path (Alg. 2 RairsSearch, P:938-947,
+ * with Alg. 5 SeilSearch P:1613-1645) and the index build that feeds it
+ * (Alg. 1 AddVectors P:914-924, Alg. 3 RairAssign P:1194-1206, Alg. 4
+ * SeilInsert P:1517-1555 in its cell-major form, DESIGN.md "Readings" R10).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns rairs_status; on failure rairs_last_error() returns a
+ *    thread-local message valid until the next call on that thread.  Arguments
+ *    are validated before any device work; a failed call leaves the index
+ *    unchanged.  No C++ exception crosses this boundary.
+ *  - "dev" pointers must be CUDA device (or managed) memory on the current
+ *    device; a host pointer there is RAIRS_E_INVALID.  "host" pointers are
+ *    ordinary (pageable or pinned) host memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  All device work is enqueued on it; device outputs are valid
+ *    after the stream is synchronised.  Calls taking host outputs synchronise
+ *    the stream before returning.
+ *  - Ownership: the caller owns every buffer it passes; the library owns the
+ *    index (device memory) and frees it in rairs_index_free().
+ *  - Vector ids: the build takes the rows of ONE shard.  With shard_id = s and
+ *    nshards = G (vector partition id mod G), local row
+ *    r is global id r*G + s.  Results report global ids (int64), ordered by
+ *    (squared L2 distance, id) ascending; missing results are (-1, +inf).
+ *  - Concurrency: search/export calls are read-only on the index and may run
+ *    concurrently on different streams; build/free are exclusive.
+ */
+#ifndef RAIRS_H_
+#define RAIRS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rairs_index_s* rairs_index_t;
+
+typedef enum {
+  RAIRS_OK = 0,
+  RAIRS_E_INVALID = -1,     /* bad argument (checked before any device work) */
+  RAIRS_E_OOM = -2,         /* device allocation failed */
+  RAIRS_E_CUDA = -3,        /* CUDA runtime / launch error */
+  RAIRS_E_UNSUPPORTED = -4, /* valid but not implemented (e.g. nbits != 4) */
+  RAIRS_E_INTERNAL = -5
+} rairs_status;
+
+typedef enum {
+  RAIRS_ASSIGN_SINGLE = 0, /* each vector in its nearest list only (IVFPQfs) */
+  RAIRS_ASSIGN_AIR = 1     /* RAIR second list by the AIR metric (Alg. 3) */
+} rairs_assign;
+
+typedef struct {
+  int32_t nlist;        /* number of IVF lists, 1 <= nlist <= 65536, nlist <= n */
+  int32_t M;            /* PQ subquantizers; d % M == 0; d/M <= 8 */
+  int32_t nbits;        /* must be 4 (16 sub-centroids) */
+  int32_t assignment;   /* rairs_assign */
+  float lambda;         /* AIR lambda (0.5) */
+  int32_t n_cands;      /* N_CANDS (10); clamped to nlist */
+  int32_t strict;       /* 0 = RAIR (non-strict), 1 = SRAIR */
+  int32_t kmeans_iters; /* Lloyd iterations for training (default 25) */
+  int64_t train_sample; /* max training rows; 0 = min(n, 256*nlist) */
+  uint64_t seed;        /* training seed */
+  int32_t shard_id;     /* this index's shard s (0 <= s < nshards) */
+  int32_t nshards;      /* G >= 1 */
+} rairs_build_params;
+
+/* Fill `p` with the paper's defaults for the given shape. */
+void rairs_default_params(rairs_build_params* p, int32_t nlist, int32_t M);
+
+typedef struct {
+  int64_t n;            /* local rows in this shard */
+  int32_t d, nlist, M, M_pad;
+  int64_t n_slots;      /* code slots incl. padding (multiple of 32 per list) */
+  int64_t n_cells;      /* distinct (l1,l2) cells */
+  int64_t n_refs;       /* SEIL references (cells with l1 < l2) */
+  int64_t n_double;     /* vectors assigned to two lists */
+  int32_t max_refs_per_list;
+  int32_t shard_id, nshards;
+  int64_t device_bytes; /* index memory on the device */
+} rairs_index_info;
+
+/* ---- training (B1/B3; not part of the bit-exact contract) ----------------
+ * Coarse k-means (nlist centroids) + PQ codebook (M x 16 x d/M) trained on
+ * the GPU from `base` (dev, [n x d] fp32 row-major).  Outputs are dev
+ * buffers [nlist*d] and [M*16*(d/M)] fp32.  Deterministic for fixed seed. */
+rairs_status rairs_train(const float* base, int64_t n, int32_t d,
+                         const rairs_build_params* p, void* stream,
+                         float* centroids_out, float* codebook_out);
+
+/* ---- build (Alg. 1 AddVectors with Alg. 3 + Alg. 4) ---------------------
+ * base: dev [n x d] fp32, the rows of shard p->shard_id.  centroids: dev
+ * [nlist x d]; codebook: dev [M x 16 x d/M].  Assignment (fp64, O4) and PQ
+ * encoding (fp64, O5) are bit-exact functions of (base, centroids, codebook).
+ * The raw rows are copied into the index (refine store).
+ * Errors: n < 1, d < 1, nlist > n or > 65536, d % M, nbits != 4, n > 2^30. */
+rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
+                                      const float* centroids, const float* codebook,
+                                      const rairs_build_params* p, void* stream,
+                                      rairs_index_t* out);
+
+/* rairs_train + rairs_build_from_trained. */
+rairs_status rairs_build_index(const float* base, int64_t n, int32_t d,
+                               const rairs_build_params* p, void* stream,
+                               rairs_index_t* out);
+
+rairs_status rairs_index_free(rairs_index_t idx);
+rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out);
+
+/* ---- search (Alg. 2 RairsSearch, batched) --------------------------------
+ * queries: dev [nq x d] fp32.  bigK = k*refine_factor.
+ * out_ids: dev [nq x k] int64 global ids; out_dists: dev [nq x k] fp32
+ * squared L2 (reading R14).  dco: dev [nq] int64 or NULL -- number of items
+ * scored per query on this shard (= |U_s(q)|, O12).
+ * Errors: nq < 0, k < 1, nprobe < 1 or > nlist, refine_factor < 1,
+ * k*refine_factor > 4096, nprobe > 1024. */
+rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, int32_t k,
+                          int32_t nprobe, int32_t refine_factor, int64_t* out_ids,
+                          float* out_dists, int64_t* dco, void* stream);
+
+/* Same as rairs_search with HOST buffers: copies queries host->device, runs
+ * the search, copies results device->host and synchronises `stream`. */
+rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int64_t nq,
+                               int32_t k, int32_t nprobe, int32_t refine_factor,
+                               int64_t* out_ids_host, float* out_dists_host, void* stream);
+
+/* Per-stage outputs for parity tests (dev pointers, any may be NULL):
+ * probes [nq x nprobe] i32 (O1); lut_q [nq x M x 16] u8, lut_a/lut_b [nq] f32
+ * (O2); cand_ids/cand_scores [nq x bigK] u32 (O9, global ids, padded with
+ * 0xFFFFFFFF); dco [nq] i64; out_ids/out_dists as rairs_search. */
+rairs_status rairs_search_debug(rairs_index_t idx, const float* queries, int64_t nq,
+                                int32_t k, int32_t nprobe, int32_t refine_factor,
+                                int32_t* probes, uint8_t* lut_q, float* lut_a, float* lut_b,
+                                uint32_t* cand_ids, uint32_t* cand_scores, int64_t* dco,
+                                int64_t* out_ids, float* out_dists, void* stream);
+
+/* ---- shard merge (K7) -----------------------------------------------------
+ * ids/dists: dev [G x nq x k] (per-shard results, e.g. after an NCCL
+ * all_gather).  Output: dev [nq x k], the first k of the union by (dist, id),
+ * padded with (-1, +inf).  O11. */
+rairs_status rairs_merge_topk(const int64_t* ids, const float* dists, int32_t G, int64_t nq,
+                              int32_t k, int64_t* out_ids, float* out_dists, void* stream);
+
+/* ---- exact k-NN ground truth (B7) ------------------------------------------
+ * First K rows of base by (D64(q,x), id) (O13) -- fp64 ordered distances.
+ * base: dev [n x d], queries: dev [nq x d]; out: dev [nq x K] int64 ids and
+ * fp64 distances (either may be NULL).  K <= 256. */
+rairs_status rairs_exact_knn(const float* base, int64_t n, int32_t d, const float* queries,
+                             int64_t nq, int32_t K, int64_t* out_ids, double* out_d64,
+                             void* stream);
+
+/* ---- exports for parity tests ---------------------------------------------
+ * rairs_export_trained: dev [nlist x d] centroids, dev [M x 16 x d/M] codebook.
+ * rairs_export_assignment: dev [n] l1, l2 (sorted pair) and dev [n x M]
+ *   unpacked codes per local row (any may be NULL).
+ * rairs_export_layout: cell-major SEIL (dev, any may be NULL):
+ *   own_off/own_cnt [nlist] i64 (slot offset, item count of list l's owned
+ *   region = its cells (l, j>=l)); ref_ptr [nlist+1] i64 CSR over lists;
+ *   ref_owner [n_refs] i32, ref_start [n_refs] i64 (slot), ref_cnt [n_refs] i64;
+ *   slot_rows [n_slots] u32 (local row, 0xFFFFFFFF = padding). */
+rairs_status rairs_export_trained(rairs_index_t idx, float* centroids, float* codebook,
+                                  void* stream);
+rairs_status rairs_export_assignment(rairs_index_t idx, int32_t* l1, int32_t* l2,
+                                     uint8_t* codes, void* stream);
+rairs_status rairs_export_layout(rairs_index_t idx, int64_t* own_off, int64_t* own_cnt,
+                                 int64_t* ref_ptr, int32_t* ref_owner, int64_t* ref_start,
+                                 int64_t* ref_cnt, uint32_t* slot_rows, void* stream);
+
+/* ---- stage timing (CUDA events on the search stream) ----------------------
+ * When enabled, every search records events around its stages on its stream;
+ * rairs_profile_read synchronises and returns the accumulated milliseconds
+ * and launch counts since the last reset:
+ *   ms[0] coarse (probe selection), ms[1] scan (LUT + SEIL work list +
+ *   fast-scan + top-bigK), ms[2] refine; launches[i] likewise. */
+rairs_status rairs_profile_enable(rairs_index_t idx, int32_t on);
+rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launches3,
+                                int32_t reset);
+
+const char* rairs_last_error(void);
+const char* rairs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAIRS_H_ */

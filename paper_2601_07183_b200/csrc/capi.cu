@@ -1,0 +1,524 @@
+// capi.cu -- extern "C" entry points of librairs.so (see include/rairs.h).
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "index.cuh"
+
+namespace rairs {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static rairs_status invalid(const std::string& msg) {
+  set_error(msg);
+  return RAIRS_E_INVALID;
+}
+
+static bool is_dev_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+#define REQUIRE_DEV(ptr, name)                                                   \
+  do {                                                                           \
+    if (!is_dev_ptr(ptr)) return invalid(std::string(name) + " must be a device pointer"); \
+  } while (0)
+#define OPTIONAL_DEV(ptr, name)                                                  \
+  do {                                                                           \
+    if ((ptr) != nullptr && !is_dev_ptr(ptr))                                    \
+      return invalid(std::string(name) + " must be a device pointer or NULL");   \
+  } while (0)
+
+static rairs_status validate_params(const rairs_build_params* p, int64_t n, int32_t d) {
+  if (!p) return invalid("params is NULL");
+  if (n < 1) return invalid("n must be >= 1");
+  if (d < 1) return invalid("d must be >= 1");
+  if (p->nbits != 4) {
+    set_error("only nbits = 4 is supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if (p->nlist < 1 || p->nlist > 65536) return invalid("nlist must be in [1, 65536]");
+  if (p->M < 1 || d % p->M != 0) return invalid("M must divide d");
+  if (d / p->M > 8) {
+    set_error("d/M > 8 is not supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if (p->assignment != RAIRS_ASSIGN_SINGLE && p->assignment != RAIRS_ASSIGN_AIR)
+    return invalid("assignment must be RAIRS_ASSIGN_SINGLE or RAIRS_ASSIGN_AIR");
+  if (p->nshards < 1 || p->shard_id < 0 || p->shard_id >= p->nshards)
+    return invalid("need 0 <= shard_id < nshards");
+  if (n >= (1ll << 30)) {
+    set_error("more than 2^30 rows per shard is not supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if ((int64_t)n * p->nshards >= 0xFFFFFFFFll) {
+    set_error("global ids must fit in 32 bits");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if (p->assignment == RAIRS_ASSIGN_AIR) {
+    int nc = std::min(p->n_cands, p->nlist);
+    if (nc < 1) return invalid("n_cands must be >= 1");
+    if (nc > 32) {
+      set_error("n_cands > 32 is not supported");
+      return RAIRS_E_UNSUPPORTED;
+    }
+    if (p->strict && nc < 2) return invalid("strict assignment needs n_cands >= 2 and nlist >= 2");
+  }
+  return RAIRS_OK;
+}
+
+static void free_index(rairs_index_s* x) {
+  if (!x) return;
+  cudaFree(x->centroids); cudaFree(x->codebook); cudaFree(x->X); cudaFree(x->l1); cudaFree(x->l2);
+  cudaFree(x->codes); cudaFree(x->slot_rows); cudaFree(x->own_off); cudaFree(x->own_cnt);
+  cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
+  for (auto& es : x->pending)
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
+  for (auto e : x->pool) cudaEventDestroy(e);
+  delete x;
+}
+
+// stage events (only when profiling is on)
+struct StageEvents {
+  rairs_index_s* idx;
+  cudaStream_t s;
+  rairs_index_s::EvSet ev{};
+  bool on;
+  StageEvents(rairs_index_s* i, cudaStream_t st) : idx(i), s(st), on(i->prof) {
+    if (!on) return;
+    for (int k = 0; k < 4; ++k) {
+      if (!idx->pool.empty()) {
+        ev.e[k] = idx->pool.back();
+        idx->pool.pop_back();
+      } else {
+        cudaEventCreate(&ev.e[k]);
+      }
+    }
+  }
+  void mark(int k) {
+    if (on) cudaEventRecord(ev.e[k], s);
+  }
+  void commit() {
+    if (on) idx->pending.push_back(ev);
+  }
+};
+
+static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_t nq, int k,
+                                int nprobe, int rf, int32_t* probes_out, uint8_t* lut_q,
+                                float* lut_a, float* lut_b, uint32_t* cand_ids,
+                                uint32_t* cand_scores, int64_t* dco, int64_t* out_ids,
+                                float* out_dists, cudaStream_t s) {
+  if (nq == 0) return RAIRS_OK;
+  const int bigK = k * rf;
+  int32_t* probes = probes_out;
+  uint64_t* keys = nullptr;
+  if (!probes) RAIRS_CUDA_TRY(cudaMallocAsync(&probes, (size_t)nq * nprobe * 4, s));
+  cudaError_t e = cudaMallocAsync(&keys, (size_t)nq * bigK * 8, s);
+  if (e != cudaSuccess) {
+    if (!probes_out) cudaFreeAsync(probes, s);
+    set_error(std::string("workspace: ") + cudaGetErrorString(e));
+    return RAIRS_E_OOM;
+  }
+  SearchArgs a{};
+  a.queries = queries;
+  a.nq = nq;
+  a.k = k;
+  a.nprobe = nprobe;
+  a.refine_factor = rf;
+  a.probes = probes;
+  a.cand_keys = keys;
+  a.dco = dco;
+  a.lut_q = lut_q;
+  a.lut_a = lut_a;
+  a.lut_b = lut_b;
+  a.out_ids = out_ids;
+  a.out_dists = out_dists;
+
+  StageEvents ev(idx, s);
+  rairs_status st = RAIRS_OK;
+  ev.mark(0);
+  // coarse: P(q) = first nprobe lists by (D64, l)  (O1, exact fp64)
+  ProbeArgs pa{};
+  pa.X = queries;
+  pa.rows = nq;
+  pa.d = idx->d;
+  pa.C = idx->centroids;
+  pa.nl = idx->nlist;
+  pa.L = nprobe;
+  pa.mode = 0;
+  pa.out_idx = probes;
+  st = launch_probe_exact(pa, s);
+  ev.mark(1);
+  if (st == RAIRS_OK) st = launch_scan(idx, a, s);
+  ev.mark(2);
+  if (st == RAIRS_OK && (cand_ids || cand_scores))
+    st = launch_split_keys(keys, nq * bigK, cand_ids, cand_scores, s);
+  if (st == RAIRS_OK) st = launch_refine(idx, a, s);
+  ev.mark(3);
+  ev.commit();
+  if (!probes_out) cudaFreeAsync(probes, s);
+  cudaFreeAsync(keys, s);
+  if (st == RAIRS_OK) {
+    idx->launches[0] += 1;
+    idx->launches[1] += 1;
+    idx->launches[2] += 1;
+  }
+  return st;
+}
+
+static rairs_status validate_search(rairs_index_t idx, int64_t nq, int32_t k, int32_t nprobe,
+                                    int32_t rf) {
+  if (!idx) return invalid("index is NULL");
+  if (nq < 0) return invalid("nq must be >= 0");
+  if (k < 1) return invalid("k must be >= 1");
+  if (nprobe < 1 || nprobe > idx->nlist) return invalid("nprobe must be in [1, nlist]");
+  if (nprobe > 1024) {
+    set_error("nprobe > 1024 is not supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if (rf < 1) return invalid("refine_factor must be >= 1");
+  if ((int64_t)k * rf > 4096) {
+    set_error("k * refine_factor > 4096 is not supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  return RAIRS_OK;
+}
+
+}  // namespace rairs
+
+using namespace rairs;
+
+extern "C" {
+
+const char* rairs_last_error(void) { return g_err.c_str(); }
+const char* rairs_version(void) { return "rairs-b200 0.1 (sm_100a)"; }
+
+void rairs_default_params(rairs_build_params* p, int32_t nlist, int32_t M) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->nlist = nlist;
+  p->M = M;
+  p->nbits = 4;
+  p->assignment = RAIRS_ASSIGN_AIR;
+  p->lambda = 0.5f;
+  p->n_cands = 10;
+  p->strict = 0;
+  p->kmeans_iters = 25;
+  p->train_sample = 0;
+  p->seed = 1234;
+  p->shard_id = 0;
+  p->nshards = 1;
+}
+
+rairs_status rairs_train(const float* base, int64_t n, int32_t d, const rairs_build_params* p,
+                         void* stream, float* centroids_out, float* codebook_out) {
+  RAIRS_TRY(validate_params(p, n, d));
+  if (p->nlist > n) return invalid("nlist must be <= n");
+  REQUIRE_DEV(base, "base");
+  REQUIRE_DEV(centroids_out, "centroids_out");
+  REQUIRE_DEV(codebook_out, "codebook_out");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int iters = p->kmeans_iters > 0 ? p->kmeans_iters : 25;
+  RAIRS_TRY(train_kmeans(base, n, d, p->nlist, iters, p->seed, p->train_sample, centroids_out, s));
+  RAIRS_TRY(train_pq(base, n, d, p->M, iters, p->seed, 65536, codebook_out, s));
+  return RAIRS_OK;
+}
+
+rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
+                                      const float* centroids, const float* codebook,
+                                      const rairs_build_params* p, void* stream,
+                                      rairs_index_t* out) {
+  RAIRS_TRY(validate_params(p, n, d));
+  if (!out) return invalid("out is NULL");
+  REQUIRE_DEV(base, "base");
+  REQUIRE_DEV(centroids, "centroids");
+  REQUIRE_DEV(codebook, "codebook");
+  cudaStream_t s = (cudaStream_t)stream;
+  rairs_index_s* idx = new (std::nothrow) rairs_index_s();
+  if (!idx) return RAIRS_E_OOM;
+  cudaGetDevice(&idx->device);
+  idx->n = n;
+  idx->d = d;
+  idx->nlist = p->nlist;
+  idx->M = p->M;
+  idx->M_pad = (int)round_up(p->M, 16);
+  idx->dsub = d / p->M;
+  idx->shard_id = p->shard_id;
+  idx->nshards = p->nshards;
+  idx->params = *p;
+  rairs_status st = RAIRS_OK;
+  auto fail = [&](rairs_status code) {
+    free_index(idx);
+    return code;
+  };
+#define B_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); return fail(_e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA); } } while (0)
+  const size_t cb_bytes = (size_t)p->M * 16 * idx->dsub * 4;
+  B_TRY(cudaMalloc(&idx->centroids, (size_t)p->nlist * d * 4));
+  B_TRY(cudaMalloc(&idx->codebook, cb_bytes));
+  B_TRY(cudaMalloc(&idx->X, (size_t)n * d * 4));
+  B_TRY(cudaMalloc(&idx->l1, n * 4));
+  B_TRY(cudaMalloc(&idx->l2, n * 4));
+  idx->device_bytes = (size_t)p->nlist * d * 4 + cb_bytes + (size_t)n * d * 4 + n * 8;
+  B_TRY(cudaMemcpyAsync(idx->centroids, centroids, (size_t)p->nlist * d * 4, cudaMemcpyDeviceToDevice, s));
+  B_TRY(cudaMemcpyAsync(idx->codebook, codebook, cb_bytes, cudaMemcpyDeviceToDevice, s));
+  B_TRY(cudaMemcpyAsync(idx->X, base, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, s));
+  // Alg. 3 RairAssign (AIR) or single assignment, exact fp64 (O4)
+  ProbeArgs pa{};
+  pa.X = idx->X;
+  pa.rows = n;
+  pa.d = d;
+  pa.C = idx->centroids;
+  pa.nl = p->nlist;
+  if (p->assignment == RAIRS_ASSIGN_AIR) {
+    pa.mode = 1;
+    pa.L = std::min(p->n_cands, p->nlist);
+    pa.lambda = (double)p->lambda;
+    pa.strict = p->strict;
+  } else {
+    pa.mode = 2;
+    pa.L = 1;
+  }
+  pa.l1 = idx->l1;
+  pa.l2 = idx->l2;
+  st = launch_probe_exact(pa, s);
+  if (st != RAIRS_OK) return fail(st);
+  // Alg. 4 SeilInsert (cell-major) + PQ encoding (O5) into the packed layout
+  st = build_layout(idx, s);
+  if (st != RAIRS_OK) return fail(st);
+  B_TRY(cudaStreamSynchronize(s));
+#undef B_TRY
+  *out = idx;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_build_index(const float* base, int64_t n, int32_t d,
+                               const rairs_build_params* p, void* stream, rairs_index_t* out) {
+  RAIRS_TRY(validate_params(p, n, d));
+  if (p->nlist > n) return invalid("nlist must be <= n");
+  REQUIRE_DEV(base, "base");
+  cudaStream_t s = (cudaStream_t)stream;
+  float *c = nullptr, *cb = nullptr;
+  RAIRS_CUDA_TRY(cudaMalloc(&c, (size_t)p->nlist * d * 4));
+  cudaError_t e = cudaMalloc(&cb, (size_t)p->M * 16 * (d / p->M) * 4);
+  if (e != cudaSuccess) {
+    cudaFree(c);
+    set_error("codebook alloc failed");
+    return RAIRS_E_OOM;
+  }
+  rairs_status st = rairs_train(base, n, d, p, stream, c, cb);
+  if (st == RAIRS_OK) st = rairs_build_from_trained(base, n, d, c, cb, p, stream, out);
+  cudaStreamSynchronize(s);
+  cudaFree(c);
+  cudaFree(cb);
+  return st;
+}
+
+rairs_status rairs_index_free(rairs_index_t idx) {
+  if (!idx) return invalid("index is NULL");
+  cudaDeviceSynchronize();
+  free_index(idx);
+  return RAIRS_OK;
+}
+
+rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out) {
+  if (!idx || !out) return invalid("NULL argument");
+  out->n = idx->n;
+  out->d = idx->d;
+  out->nlist = idx->nlist;
+  out->M = idx->M;
+  out->M_pad = idx->M_pad;
+  out->n_slots = idx->n_slots;
+  out->n_cells = idx->n_cells;
+  out->n_refs = idx->n_refs;
+  out->n_double = idx->n_double;
+  out->max_refs_per_list = idx->max_refs;
+  out->shard_id = idx->shard_id;
+  out->nshards = idx->nshards;
+  out->device_bytes = idx->device_bytes;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, int32_t k,
+                          int32_t nprobe, int32_t refine_factor, int64_t* out_ids,
+                          float* out_dists, int64_t* dco, void* stream) {
+  RAIRS_TRY(validate_search(idx, nq, k, nprobe, refine_factor));
+  if (nq == 0) return RAIRS_OK;
+  REQUIRE_DEV(queries, "queries");
+  REQUIRE_DEV(out_ids, "out_ids");
+  REQUIRE_DEV(out_dists, "out_dists");
+  OPTIONAL_DEV(dco, "dco");
+  return search_impl(idx, queries, nq, k, nprobe, refine_factor, nullptr, nullptr, nullptr,
+                     nullptr, nullptr, nullptr, dco, out_ids, out_dists, (cudaStream_t)stream);
+}
+
+rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int64_t nq,
+                               int32_t k, int32_t nprobe, int32_t refine_factor,
+                               int64_t* out_ids_host, float* out_dists_host, void* stream) {
+  RAIRS_TRY(validate_search(idx, nq, k, nprobe, refine_factor));
+  if (nq == 0) return RAIRS_OK;
+  if (!queries_host || !out_ids_host || !out_dists_host) return invalid("NULL host buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  float* dq = nullptr;
+  int64_t* di = nullptr;
+  float* dd = nullptr;
+  const size_t qb = (size_t)nq * idx->d * 4, ib = (size_t)nq * k * 8, db = (size_t)nq * k * 4;
+  RAIRS_CUDA_TRY(cudaMallocAsync(&dq, qb, s));
+  RAIRS_CUDA_TRY(cudaMallocAsync(&di, ib, s));
+  RAIRS_CUDA_TRY(cudaMallocAsync(&dd, db, s));
+  RAIRS_CUDA_TRY(cudaMemcpyAsync(dq, queries_host, qb, cudaMemcpyHostToDevice, s));
+  rairs_status st = search_impl(idx, dq, nq, k, nprobe, refine_factor, nullptr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, nullptr, di, dd, s);
+  if (st == RAIRS_OK) {
+    cudaMemcpyAsync(out_ids_host, di, ib, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(out_dists_host, dd, db, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(dq, s);
+  cudaFreeAsync(di, s);
+  cudaFreeAsync(dd, s);
+  RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  return st;
+}
+
+rairs_status rairs_search_debug(rairs_index_t idx, const float* queries, int64_t nq, int32_t k,
+                                int32_t nprobe, int32_t refine_factor, int32_t* probes,
+                                uint8_t* lut_q, float* lut_a, float* lut_b, uint32_t* cand_ids,
+                                uint32_t* cand_scores, int64_t* dco, int64_t* out_ids,
+                                float* out_dists, void* stream) {
+  RAIRS_TRY(validate_search(idx, nq, k, nprobe, refine_factor));
+  if (nq == 0) return RAIRS_OK;
+  REQUIRE_DEV(queries, "queries");
+  OPTIONAL_DEV(probes, "probes");
+  OPTIONAL_DEV(lut_q, "lut_q");
+  OPTIONAL_DEV(lut_a, "lut_a");
+  OPTIONAL_DEV(lut_b, "lut_b");
+  OPTIONAL_DEV(cand_ids, "cand_ids");
+  OPTIONAL_DEV(cand_scores, "cand_scores");
+  OPTIONAL_DEV(dco, "dco");
+  REQUIRE_DEV(out_ids, "out_ids");
+  REQUIRE_DEV(out_dists, "out_dists");
+  return search_impl(idx, queries, nq, k, nprobe, refine_factor, probes, lut_q, lut_a, lut_b,
+                     cand_ids, cand_scores, dco, out_ids, out_dists, (cudaStream_t)stream);
+}
+
+rairs_status rairs_merge_topk(const int64_t* ids, const float* dists, int32_t G, int64_t nq,
+                              int32_t k, int64_t* out_ids, float* out_dists, void* stream) {
+  if (G < 1 || k < 1 || nq < 0) return invalid("need G >= 1, k >= 1, nq >= 0");
+  if (nq == 0) return RAIRS_OK;
+  REQUIRE_DEV(ids, "ids");
+  REQUIRE_DEV(dists, "dists");
+  REQUIRE_DEV(out_ids, "out_ids");
+  REQUIRE_DEV(out_dists, "out_dists");
+  return launch_merge(ids, dists, G, nq, k, out_ids, out_dists, (cudaStream_t)stream);
+}
+
+rairs_status rairs_exact_knn(const float* base, int64_t n, int32_t d, const float* queries,
+                             int64_t nq, int32_t K, int64_t* out_ids, double* out_d64,
+                             void* stream) {
+  if (n < 1 || d < 1 || nq < 0) return invalid("need n >= 1, d >= 1, nq >= 0");
+  if (K < 1 || K > n) return invalid("need 1 <= K <= n");
+  if (K > 256) {
+    set_error("K > 256 is not supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if (nq == 0) return RAIRS_OK;
+  REQUIRE_DEV(base, "base");
+  REQUIRE_DEV(queries, "queries");
+  OPTIONAL_DEV(out_ids, "out_ids");
+  OPTIONAL_DEV(out_d64, "out_d64");
+  ProbeArgs pa{};
+  pa.X = queries;
+  pa.rows = nq;
+  pa.d = d;
+  pa.C = base;
+  pa.nl = n;
+  pa.L = K;
+  pa.mode = 0;
+  pa.out_idx64 = out_ids;
+  pa.out_d64 = out_d64;
+  return launch_probe_exact(pa, (cudaStream_t)stream);
+}
+
+rairs_status rairs_export_trained(rairs_index_t idx, float* centroids, float* codebook,
+                                  void* stream) {
+  if (!idx) return invalid("index is NULL");
+  OPTIONAL_DEV(centroids, "centroids");
+  OPTIONAL_DEV(codebook, "codebook");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (centroids)
+    RAIRS_CUDA_TRY(cudaMemcpyAsync(centroids, idx->centroids, (size_t)idx->nlist * idx->d * 4,
+                                   cudaMemcpyDeviceToDevice, s));
+  if (codebook)
+    RAIRS_CUDA_TRY(cudaMemcpyAsync(codebook, idx->codebook, (size_t)idx->M * 16 * idx->dsub * 4,
+                                   cudaMemcpyDeviceToDevice, s));
+  return RAIRS_OK;
+}
+
+rairs_status rairs_export_assignment(rairs_index_t idx, int32_t* l1, int32_t* l2, uint8_t* codes,
+                                     void* stream) {
+  if (!idx) return invalid("index is NULL");
+  OPTIONAL_DEV(l1, "l1");
+  OPTIONAL_DEV(l2, "l2");
+  OPTIONAL_DEV(codes, "codes");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (l1) RAIRS_CUDA_TRY(cudaMemcpyAsync(l1, idx->l1, idx->n * 4, cudaMemcpyDeviceToDevice, s));
+  if (l2) RAIRS_CUDA_TRY(cudaMemcpyAsync(l2, idx->l2, idx->n * 4, cudaMemcpyDeviceToDevice, s));
+  if (codes) RAIRS_TRY(export_codes(idx, codes, s));
+  return RAIRS_OK;
+}
+
+rairs_status rairs_export_layout(rairs_index_t idx, int64_t* own_off, int64_t* own_cnt,
+                                 int64_t* ref_ptr, int32_t* ref_owner, int64_t* ref_start,
+                                 int64_t* ref_cnt, uint32_t* slot_rows, void* stream) {
+  if (!idx) return invalid("index is NULL");
+  OPTIONAL_DEV(own_off, "own_off");
+  OPTIONAL_DEV(own_cnt, "own_cnt");
+  OPTIONAL_DEV(ref_ptr, "ref_ptr");
+  OPTIONAL_DEV(ref_owner, "ref_owner");
+  OPTIONAL_DEV(ref_start, "ref_start");
+  OPTIONAL_DEV(ref_cnt, "ref_cnt");
+  OPTIONAL_DEV(slot_rows, "slot_rows");
+  return export_layout64(idx, own_off, own_cnt, ref_ptr, ref_owner, ref_start, ref_cnt, slot_rows,
+                         (cudaStream_t)stream);
+}
+
+rairs_status rairs_profile_enable(rairs_index_t idx, int32_t on) {
+  if (!idx) return invalid("index is NULL");
+  idx->prof = on != 0;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launches3,
+                                int32_t reset) {
+  if (!idx) return invalid("index is NULL");
+  for (auto& es : idx->pending) {
+    RAIRS_CUDA_TRY(cudaEventSynchronize(es.e[3]));
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.0f;
+      RAIRS_CUDA_TRY(cudaEventElapsedTime(&ms, es.e[k], es.e[k + 1]));
+      idx->ms[k] += ms;
+    }
+    for (int k = 0; k < 4; ++k) idx->pool.push_back(es.e[k]);
+  }
+  idx->pending.clear();
+  for (int k = 0; k < 3; ++k) {
+    if (ms3) ms3[k] = idx->ms[k];
+    if (launches3) launches3[k] = idx->launches[k];
+  }
+  if (reset) {
+    for (int k = 0; k < 3; ++k) {
+      idx->ms[k] = 0;
+      idx->launches[k] = 0;
+    }
+  }
+  return RAIRS_OK;
+}
+
+}  // extern "C"

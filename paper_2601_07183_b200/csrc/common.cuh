@@ -1,0 +1,111 @@
+// common.cuh -- shared device/host helpers for librairs (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/rairs.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "librairs is built for sm_100a (B200) only"
+#endif
+
+namespace rairs {
+
+constexpr uint32_t kSlotPad = 0xFFFFFFFFu;   // padding slot marker in slot_rows
+constexpr int kBlk = 32;                     // items per code block (one warp)
+constexpr uint64_t kKeyInf = ~0ull;
+
+// thread-local error message for rairs_last_error()
+void set_error(const std::string& msg);
+
+struct Status {
+  rairs_status code;
+};
+
+#define RAIRS_CUDA_TRY(expr)                                                    \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::rairs::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+      return (_e == cudaErrorMemoryAllocation) ? RAIRS_E_OOM : RAIRS_E_CUDA;    \
+    }                                                                           \
+  } while (0)
+
+#define RAIRS_CHECK_LAUNCH()                                                    \
+  do {                                                                          \
+    cudaError_t _e = cudaGetLastError();                                        \
+    if (_e != cudaSuccess) {                                                    \
+      ::rairs::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return RAIRS_E_CUDA;                                                      \
+    }                                                                           \
+  } while (0)
+
+#define RAIRS_TRY(expr)                                                         \
+  do {                                                                          \
+    rairs_status _s = (expr);                                                   \
+    if (_s != RAIRS_OK) return _s;                                              \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// ---------------------------------------------------------------------------
+// Exactly-rounded arithmetic (no FMA contraction): the parity contract needs
+// the same fp64 ordered sums / fp32 LUT values as the CPU oracle (R2).
+__device__ __forceinline__ double dsq_diff(float a, float b) {
+  double df = __dsub_rn((double)a, (double)b);
+  return __dmul_rn(df, df);
+}
+
+// u64 bits of a non-negative double: integer order == numeric order.
+__device__ __forceinline__ uint64_t dbits(double v) {
+  return (uint64_t)__double_as_longlong(v);
+}
+
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// (bits, id) lexicographic argmin across a warp; returns the winning pair in
+// every lane.
+__device__ __forceinline__ void warp_min_pair(uint64_t& k, uint32_t& id) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t k2 = __shfl_xor_sync(0xffffffffu, k, o);
+    uint32_t i2 = __shfl_xor_sync(0xffffffffu, id, o);
+    if (k2 < k || (k2 == k && i2 < id)) {
+      k = k2;
+      id = i2;
+    }
+  }
+}
+
+// In-place ascending bitonic sort of n = power-of-two u64 keys in shared
+// memory by all threads of the CTA (caller syncs before; ends with a sync).
+__device__ __forceinline__ void cta_bitonic_sort_u64(uint64_t* a, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool asc = ((lo & size) == 0);
+        uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == asc) {
+          a[lo] = y;
+          a[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+inline int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace rairs

@@ -1,0 +1,104 @@
+// index.cuh -- device-resident RAIRS index (one shard) and kernel launchers.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct rairs_index_s {
+  int device = 0;
+  int64_t n = 0;            // local rows
+  int d = 0, nlist = 0, M = 0, M_pad = 0, dsub = 0;
+  int shard_id = 0, nshards = 1;
+  rairs_build_params params{};
+
+  // trained state (fp32)
+  float* centroids = nullptr;   // [nlist x d]
+  float* codebook = nullptr;    // [M x 16 x dsub]
+  // refine store: raw rows in insertion order
+  float* X = nullptr;           // [n x d]
+  // assignment (sorted pair per local row)
+  int32_t* l1 = nullptr;
+  int32_t* l2 = nullptr;
+
+  // cell-major SEIL layout
+  int64_t n_slots = 0;          // multiple of 32 per list
+  uint8_t* codes = nullptr;     // [n_slots/32][M_pad/16][32 lanes][8 B]
+  uint32_t* slot_rows = nullptr;  // [n_slots] local row or kSlotPad
+  uint32_t* own_off = nullptr;  // [nlist] slot offset of list l's owned region
+  uint32_t* own_cnt = nullptr;  // [nlist] items in it
+  uint32_t* ref_ptr = nullptr;  // [nlist+1] CSR of references per list
+  int32_t* ref_owner = nullptr; // [n_refs]
+  uint32_t* ref_start = nullptr;  // [n_refs] slot
+  uint32_t* ref_cnt = nullptr;  // [n_refs]
+  int64_t n_refs = 0, n_cells = 0, n_double = 0;
+  int max_refs = 0;
+  int64_t device_bytes = 0;
+
+  // stage profiling (CUDA events on the search stream)
+  bool prof = false;
+  struct EvSet { cudaEvent_t e[4]; };
+  std::vector<EvSet> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[3] = {0, 0, 0};
+  int64_t launches[3] = {0, 0, 0};
+};
+
+namespace rairs {
+
+// ---- build-side launchers (build_kernels.cu) -------------------------------
+// Exact fp64 nearest-"lists" selection: for each of `rows` rows of X (row
+// major [rows x d]) the first L of `nl` rows of C by (D64, index).
+//   mode 0: write out_idx [rows x L] (i32) and optionally out_d64 [rows x L].
+//   mode 1: AIR assignment (Alg. 3): L = n_cands; writes l1/l2 sorted pair.
+//   mode 2: single assignment: l1 = l2 = nearest.
+struct ProbeArgs {
+  const float* X;
+  int64_t rows;
+  int d;
+  const float* C;
+  int64_t nl;
+  int L;
+  int mode;
+  double lambda;
+  int strict;
+  int32_t* out_idx;    // mode 0 (i32) or NULL
+  int64_t* out_idx64;  // mode 0 (i64) or NULL
+  double* out_d64;     // mode 0, optional
+  int32_t* l1;         // modes 1/2
+  int32_t* l2;
+};
+rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s);
+
+rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, uint64_t seed,
+                          int64_t max_train, float* centroids_out, cudaStream_t s);
+rairs_status train_pq(const float* X, int64_t n, int d, int M, int iters, uint64_t seed,
+                      int64_t max_train, float* codebook_out, cudaStream_t s);
+rairs_status build_layout(rairs_index_s* idx, cudaStream_t s);
+rairs_status export_codes(const rairs_index_s* idx, uint8_t* codes, cudaStream_t s);
+rairs_status export_layout64(const rairs_index_s* idx, int64_t* own_off, int64_t* own_cnt,
+                             int64_t* ref_ptr, int32_t* ref_owner, int64_t* ref_start,
+                             int64_t* ref_cnt, uint32_t* slot_rows, cudaStream_t s);
+
+// ---- search-side launchers (search_kernels.cu) -----------------------------
+struct SearchArgs {
+  const float* queries;
+  int64_t nq;
+  int k, nprobe, refine_factor;
+  int32_t* probes;       // [nq x nprobe] (workspace or debug output)
+  uint64_t* cand_keys;   // [nq x bigK]   (workspace)
+  int64_t* dco;          // [nq] or NULL
+  uint8_t* lut_q;        // debug [nq x M x 16] or NULL
+  float* lut_a;
+  float* lut_b;
+  int64_t* out_ids;
+  float* out_dists;
+};
+rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
+rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
+rairs_status launch_merge(const int64_t* ids, const float* dists, int G, int64_t nq, int k,
+                          int64_t* out_ids, float* out_dists, cudaStream_t s);
+rairs_status launch_split_keys(const uint64_t* keys, int64_t count, uint32_t* ids,
+                               uint32_t* scores, cudaStream_t s);
+
+}  // namespace rairs

@@ -1,0 +1,88 @@
+"""Index sharding over GPUs: one process per GPU, torch.distributed plumbing.
+
+Partition: vector id x lives on shard
+x mod G. Each rank builds its shard from the SAME trained centroids/codebook
+(rank 0 trains, ``broadcast_trained`` ships them), searches its shard with
+the CUDA kernels, and the per-shard top-k lists are exchanged with ONE
+all_gather (NCCL over NVLink on B200; gloo in the CPU tests) and merged by
+the K7 kernel (rairs_merge_topk): the first k by (distance, id) -- O11.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(n: int, shard_id: int, nshards: int) -> torch.Tensor:
+    """Global ids of shard `shard_id`: {x : x mod G == shard_id}, ascending.
+    Local row r <-> global id r*G + shard_id."""
+    return torch.arange(shard_id, n, nshards, dtype=torch.int64)
+
+
+def broadcast_trained(centroids: torch.Tensor, codebook: torch.Tensor, src: int = 0,
+                      group=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    dist.broadcast(centroids, src=src, group=group)
+    dist.broadcast(codebook, src=src, group=group)
+    return centroids, codebook
+
+
+def gather_shard_results(ids: torch.Tensor, dists: torch.Tensor,
+                         group=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """[nq, k] per rank -> [G, nq, k] on every rank (one all_gather each)."""
+    G = dist.get_world_size(group)
+    nq, k = ids.shape
+    all_ids = torch.empty((G, nq, k), dtype=ids.dtype, device=ids.device)
+    all_d = torch.empty((G, nq, k), dtype=dists.dtype, device=dists.device)
+    dist.all_gather_into_tensor(all_ids, ids.contiguous(), group=group)
+    dist.all_gather_into_tensor(all_d, dists.contiguous(), group=group)
+    return all_ids, all_d
+
+
+class ShardedIndex:
+    """A RAIRS index sharded over the ranks of a process group."""
+
+    def __init__(self, local_index, group=None,
+                 merge: Optional[Callable] = None):
+        self.local = local_index
+        self.group = group
+        if merge is None:
+            from .index import merge_topk
+            merge = merge_topk
+        self.merge = merge
+
+    @staticmethod
+    def build(base_local: torch.Tensor, n_total: int, nlist: int, M: int,
+              train_base: Optional[torch.Tensor] = None, group=None, **kw) -> "ShardedIndex":
+        """base_local: this rank's rows (shard_rows order) on its GPU.
+        train_base: rows used for training on rank 0 (defaults to base_local)."""
+        from .index import Index, train
+        rank, G = dist.get_rank(group), dist.get_world_size(group)
+        d = base_local.shape[1]
+        dev = base_local.device
+        cent = torch.empty((nlist, d), dtype=torch.float32, device=dev)
+        cb = torch.empty((M, 16, d // M), dtype=torch.float32, device=dev)
+        train_kw = {key: kw[key] for key in ("kmeans_iters", "train_sample", "seed") if key in kw}
+        if rank == 0:
+            c0, b0 = train(train_base if train_base is not None else base_local, nlist, M, **train_kw)
+            cent.copy_(c0)
+            cb.copy_(b0)
+        broadcast_trained(cent, cb, src=0, group=group)
+        idx = Index.build(base_local, nlist, M, centroids=cent, codebook=cb,
+                          shard_id=rank, nshards=G, **kw)
+        return ShardedIndex(idx, group=group)
+
+    def search(self, queries: torch.Tensor, k: int, nprobe: int, refine_factor: int = 10):
+        ids, dists = self.local.search(queries, k, nprobe, refine_factor)
+        return sharded_merge(ids, dists, group=self.group, merge=self.merge)
+
+
+def sharded_merge(ids: torch.Tensor, dists: torch.Tensor, group=None,
+                  merge: Optional[Callable] = None):
+    """all_gather per-shard top-k, then merge to the global top-k (O11)."""
+    if merge is None:
+        from .index import merge_topk
+        merge = merge_topk
+    all_ids, all_d = gather_shard_results(ids, dists, group=group)
+    return merge(all_ids, all_d)

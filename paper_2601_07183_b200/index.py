@@ -1,0 +1,239 @@
+"""Python face of the C ABI: build_index / Index.search (BASELINE north_star).
+
+Argument marshalling only -- every step of the search path runs in the CUDA
+kernels of librairs.so. PyTorch provides device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BuildParams, IndexInfo, check, lib
+
+
+def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    return t.detach().to(torch.float32).contiguous()
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream: Optional[torch.cuda.Stream] = None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_params(nlist: int, M: int, nbits: int = 4, assignment: str = "AIR",
+                lambda_: float = 0.5, n_cands: int = 10, strict: bool = False,
+                kmeans_iters: int = 25, train_sample: int = 0, seed: int = 1234,
+                shard_id: int = 0, nshards: int = 1) -> BuildParams:
+    p = BuildParams()
+    lib().rairs_default_params(ctypes.byref(p), int(nlist), int(M))
+    p.nbits = int(nbits)
+    a = assignment.upper()
+    if a not in ("AIR", "SINGLE"):
+        raise ValueError("assignment must be 'AIR' or 'single'")
+    p.assignment = 1 if a == "AIR" else 0
+    p.lambda_ = float(lambda_)
+    p.n_cands = int(n_cands)
+    p.strict = int(bool(strict))
+    p.kmeans_iters = int(kmeans_iters)
+    p.train_sample = int(train_sample)
+    p.seed = int(seed) & (2**64 - 1)
+    p.shard_id = int(shard_id)
+    p.nshards = int(nshards)
+    return p
+
+
+def train(base: torch.Tensor, nlist: int, M: int, **kw) -> Tuple[torch.Tensor, torch.Tensor]:
+    """GPU k-means + PQ codebook training (rairs_train)."""
+    base = _dev_f32(base, "base")
+    n, d = base.shape
+    p = make_params(nlist, M, **kw)
+    cent = torch.empty((nlist, d), dtype=torch.float32, device=base.device)
+    cb = torch.empty((M, 16, d // M), dtype=torch.float32, device=base.device)
+    check(lib().rairs_train(_ptr(base), n, d, ctypes.byref(p), _stream(), _ptr(cent), _ptr(cb)),
+          "rairs_train")
+    return cent, cb
+
+
+class Index:
+    """One shard of a RAIRS index on one GPU (rairs_index_t)."""
+
+    def __init__(self, handle: ctypes.c_void_p, device: torch.device):
+        self._h = handle
+        self.device = device
+        info = self.info()
+        self.n, self.d, self.nlist, self.M = info["n"], info["d"], info["nlist"], info["M"]
+        self.shard_id, self.nshards = info["shard_id"], info["nshards"]
+
+    # ------------------------------------------------------------ build
+    @staticmethod
+    def build(base: torch.Tensor, nlist: int, M: int, nbits: int = 4, assignment: str = "AIR",
+              centroids: Optional[torch.Tensor] = None, codebook: Optional[torch.Tensor] = None,
+              **kw) -> "Index":
+        base = _dev_f32(base, "base")
+        n, d = base.shape
+        p = make_params(nlist, M, nbits=nbits, assignment=assignment, **kw)
+        h = ctypes.c_void_p()
+        if centroids is None and codebook is None:
+            check(lib().rairs_build_index(_ptr(base), n, d, ctypes.byref(p), _stream(),
+                                          ctypes.byref(h)), "rairs_build_index")
+        else:
+            cent = _dev_f32(centroids, "centroids")
+            cb = _dev_f32(codebook, "codebook")
+            check(lib().rairs_build_from_trained(_ptr(base), n, d, _ptr(cent), _ptr(cb),
+                                                 ctypes.byref(p), _stream(), ctypes.byref(h)),
+                  "rairs_build_from_trained")
+        return Index(h, base.device)
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            check(lib().rairs_index_free(self._h), "rairs_index_free")
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def info(self) -> Dict[str, int]:
+        inf = IndexInfo()
+        check(lib().rairs_index_get_info(self._h, ctypes.byref(inf)), "rairs_index_get_info")
+        return {f: getattr(inf, f) for f, _ in IndexInfo._fields_}
+
+    # ----------------------------------------------------------- search
+    def search(self, queries: torch.Tensor, k: int, nprobe: int, refine_factor: int = 10,
+               return_dco: bool = False, stream: Optional[torch.cuda.Stream] = None):
+        """Batched Alg. 2 search on this shard. Returns (ids i64, dists f32) [nq x k]."""
+        q = _dev_f32(queries, "queries")
+        nq = q.shape[0]
+        ids = torch.empty((nq, k), dtype=torch.int64, device=q.device)
+        dists = torch.empty((nq, k), dtype=torch.float32, device=q.device)
+        dco = torch.empty((nq,), dtype=torch.int64, device=q.device) if return_dco else None
+        check(lib().rairs_search(self._h, _ptr(q), nq, int(k), int(nprobe), int(refine_factor),
+                                 _ptr(ids), _ptr(dists), _ptr(dco), _stream(stream)),
+              "rairs_search")
+        return (ids, dists, dco) if return_dco else (ids, dists)
+
+    def search_host(self, queries: np.ndarray, k: int, nprobe: int, refine_factor: int = 10,
+                    out_ids: Optional[np.ndarray] = None, out_dists: Optional[np.ndarray] = None):
+        """Host buffers in/out (rairs_search_host: H2D + search + D2H + sync)."""
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        nq = q.shape[0]
+        ids = out_ids if out_ids is not None else np.empty((nq, k), np.int64)
+        dists = out_dists if out_dists is not None else np.empty((nq, k), np.float32)
+        check(lib().rairs_search_host(self._h, q.ctypes.data_as(ctypes.c_void_p), nq, int(k),
+                                      int(nprobe), int(refine_factor),
+                                      ids.ctypes.data_as(ctypes.c_void_p),
+                                      dists.ctypes.data_as(ctypes.c_void_p), _stream()),
+              "rairs_search_host")
+        return ids, dists
+
+    def search_debug(self, queries: torch.Tensor, k: int, nprobe: int,
+                     refine_factor: int = 10) -> Dict[str, torch.Tensor]:
+        q = _dev_f32(queries, "queries")
+        nq, dev = q.shape[0], q.device
+        bigK = k * refine_factor
+        r = {
+            "probes": torch.empty((nq, nprobe), dtype=torch.int32, device=dev),
+            "Qv": torch.empty((nq, self.M, 16), dtype=torch.uint8, device=dev),
+            "a": torch.empty((nq,), dtype=torch.float32, device=dev),
+            "b": torch.empty((nq,), dtype=torch.float32, device=dev),
+            "cand_ids": torch.empty((nq, bigK), dtype=torch.int32, device=dev),
+            "cand_scores": torch.empty((nq, bigK), dtype=torch.int32, device=dev),
+            "dco": torch.empty((nq,), dtype=torch.int64, device=dev),
+            "ids": torch.empty((nq, k), dtype=torch.int64, device=dev),
+            "dists": torch.empty((nq, k), dtype=torch.float32, device=dev),
+        }
+        check(lib().rairs_search_debug(
+            self._h, _ptr(q), nq, int(k), int(nprobe), int(refine_factor), _ptr(r["probes"]),
+            _ptr(r["Qv"]), _ptr(r["a"]), _ptr(r["b"]), _ptr(r["cand_ids"]), _ptr(r["cand_scores"]),
+            _ptr(r["dco"]), _ptr(r["ids"]), _ptr(r["dists"]), _stream()), "rairs_search_debug")
+        return r
+
+    # ---------------------------------------------------------- exports
+    def export_trained(self) -> Tuple[torch.Tensor, torch.Tensor]:
+        cent = torch.empty((self.nlist, self.d), dtype=torch.float32, device=self.device)
+        cb = torch.empty((self.M, 16, self.d // self.M), dtype=torch.float32, device=self.device)
+        check(lib().rairs_export_trained(self._h, _ptr(cent), _ptr(cb), _stream()),
+              "rairs_export_trained")
+        return cent, cb
+
+    def export_assignment(self) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+        l1 = torch.empty((self.n,), dtype=torch.int32, device=self.device)
+        l2 = torch.empty((self.n,), dtype=torch.int32, device=self.device)
+        codes = torch.empty((self.n, self.M), dtype=torch.uint8, device=self.device)
+        check(lib().rairs_export_assignment(self._h, _ptr(l1), _ptr(l2), _ptr(codes), _stream()),
+              "rairs_export_assignment")
+        return l1, l2, codes
+
+    def export_layout(self) -> Dict[str, torch.Tensor]:
+        info = self.info()
+        nl, nr, ns = info["nlist"], info["n_refs"], info["n_slots"]
+        dev = self.device
+        r = {
+            "own_off": torch.empty((nl,), dtype=torch.int64, device=dev),
+            "own_cnt": torch.empty((nl,), dtype=torch.int64, device=dev),
+            "ref_ptr": torch.empty((nl + 1,), dtype=torch.int64, device=dev),
+            "ref_owner": torch.empty((max(nr, 1),), dtype=torch.int32, device=dev),
+            "ref_start": torch.empty((max(nr, 1),), dtype=torch.int64, device=dev),
+            "ref_cnt": torch.empty((max(nr, 1),), dtype=torch.int64, device=dev),
+            "slot_rows": torch.empty((max(ns, 1),), dtype=torch.int32, device=dev),
+        }
+        check(lib().rairs_export_layout(self._h, *[_ptr(r[k]) for k in
+                                                   ("own_off", "own_cnt", "ref_ptr", "ref_owner",
+                                                    "ref_start", "ref_cnt", "slot_rows")],
+                                        _stream()), "rairs_export_layout")
+        for key in ("ref_owner", "ref_start", "ref_cnt"):
+            r[key] = r[key][:nr]
+        r["slot_rows"] = r["slot_rows"][:ns]
+        return r
+
+    # ------------------------------------------------------- profiling
+    def profile_enable(self, on: bool = True):
+        check(lib().rairs_profile_enable(self._h, int(bool(on))), "rairs_profile_enable")
+
+    def profile_read(self, reset: bool = True) -> Dict[str, object]:
+        ms = (ctypes.c_double * 3)()
+        nl = (ctypes.c_int64 * 3)()
+        check(lib().rairs_profile_read(self._h, ms, nl, int(bool(reset))), "rairs_profile_read")
+        return {"ms": {"coarse": ms[0], "scan": ms[1], "refine": ms[2]},
+                "launches": {"coarse": nl[0], "scan": nl[1], "refine": nl[2]}}
+
+
+def build_index(base: torch.Tensor, nlist: int, M: int, nbits: int = 4,
+                assignment: str = "AIR", **kw) -> Index:
+    """BASELINE north_star API: build_index(base, nlist, M, nbits=4, assignment)."""
+    return Index.build(base, nlist, M, nbits=nbits, assignment=assignment, **kw)
+
+
+def merge_topk(ids: torch.Tensor, dists: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
+    """[G, nq, k] per-shard results -> [nq, k] global top-k by (dist, id) (K7)."""
+    ids = ids.contiguous()
+    dists = dists.to(torch.float32).contiguous()
+    G, nq, k = ids.shape
+    oi = torch.empty((nq, k), dtype=torch.int64, device=ids.device)
+    od = torch.empty((nq, k), dtype=torch.float32, device=ids.device)
+    check(lib().rairs_merge_topk(_ptr(ids), _ptr(dists), G, nq, k, _ptr(oi), _ptr(od), _stream()),
+          "rairs_merge_topk")
+    return oi, od
+
+
+def exact_knn(base: torch.Tensor, queries: torch.Tensor, K: int) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Ground truth (B7): first K by (fp64 ordered distance, id)."""
+    b = _dev_f32(base, "base")
+    q = _dev_f32(queries, "queries")
+    ids = torch.empty((q.shape[0], K), dtype=torch.int64, device=q.device)
+    dd = torch.empty((q.shape[0], K), dtype=torch.float64, device=q.device)
+    check(lib().rairs_exact_knn(_ptr(b), b.shape[0], b.shape[1], _ptr(q), q.shape[0], int(K),
+                                _ptr(ids), _ptr(dd), _stream()), "rairs_exact_knn")
+    return ids, dd
