@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark: batched RAIRS search (IVFPQ fast-scan + AIR + SEIL + refine) on B200.
+
+Step = one pass of the whole hot path (coarse probe selection,
+LUT + uint8 quantisation, SEIL work list, 4-bit fast scan, top-bigK, exact
+refine; plus the NCCL all_gather + top-k merge when N > 1) over one batch of
+10,000 synthetic queries with the index resident in HBM.
+
+Default workload: BASELINE.json configs[1] shape (1M x 128, nlist 1024, PQ
+M=64 x 4-bit, k=10, refine x10) drawn by the paper-like generator "c2pl"
+(DESIGN.md "Input recipe"), at the smallest swept nprobe whose recall10@10
+>= 0.95 (BJ metric "QPS at recall10@10=0.95").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+N > 1: launched by torch.distributed.run, one rank per GPU; the index is
+sharded by id mod N, every rank searches its shard, results are exchanged by
+one NCCL all_gather and merged (strong scaling: total work fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NPROBE_SWEEP = [1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 24, 32, 48, 64, 96, 128]
+L2_FLUSH_BYTES = 256 << 20   # > 126 MB L2
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def recall_at_k(ids, gt_ids, gt_d64, dists, k):
+    """recall k@k; a returned id counts if it is in GT or its fp32 distance
+    equals fp32(k-th GT distance) (tie acceptance)."""
+    import torch
+    hit = (ids[:, :, None] == gt_ids[:, None, :k]).any(-1)
+    kth = gt_d64[:, k - 1].to(torch.float32)[:, None]
+    tie = (dists == kth) & (ids >= 0)
+    return float((hit | tie).float().sum().item()) / (ids.shape[0] * k)
+
+
+def build_workload(args, rank, world, dev):
+    import torch
+    import paper_2601_07183_b200 as rb
+    from synth import get_config, make_dataset
+    spec = get_config(args.config)
+    t0 = time.time()
+    X, Q = make_dataset(spec)
+    gen_s = time.time() - t0
+    rows = np.arange(rank, X.shape[0], world)
+    Xl = torch.from_numpy(X[rows]).to(dev)
+    Qd = torch.from_numpy(Q).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    if world == 1:
+        idx = rb.build_index(Xl, spec.nlist, spec.M, assignment=args.assignment)
+        torch.cuda.synchronize()
+    else:
+        from paper_2601_07183_b200.distributed import ShardedIndex
+        Xtrain = torch.from_numpy(X).to(dev) if rank == 0 else None
+        sh = ShardedIndex.build(Xl, X.shape[0], spec.nlist, spec.M, train_base=Xtrain,
+                                assignment=args.assignment)
+        idx = sh.local
+        del Xtrain
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    return spec, X, Q, Xl, Qd, idx, gen_s, build_s
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2601_07183_b200 as rb
+    from paper_2601_07183_b200.distributed import sharded_merge
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local_rank)
+    spec, X, Q, Xl, Qd, idx, gen_s, build_s = build_workload(args, rank, world, dev)
+    k, rf = spec.k, spec.refine_factor
+
+    def step(nprobe, with_dco=False):
+        if with_dco:
+            ids, dists, dco = idx.search(Qd, k, nprobe, rf, return_dco=True)
+        else:
+            ids, dists = idx.search(Qd, k, nprobe, rf)
+            dco = None
+        if world > 1:
+            ids, dists = sharded_merge(ids, dists)
+        return ids, dists, dco
+
+    # ground truth on the full base (rank 0 data is identical on all ranks)
+    Xfull = torch.from_numpy(X).to(dev)
+    gt_ids, gt_d64 = rb.exact_knn(Xfull, Qd, k)
+    del Xfull
+    torch.cuda.synchronize()
+
+    # recall sweep -> headline nprobe (smallest with recall >= 0.95)
+    sweep = []
+    chosen = None
+    for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
+        ids, dists, _ = step(npb)
+        r = recall_at_k(ids, gt_ids, gt_d64, dists, k)
+        sweep.append({"nprobe": npb, "recall": round(r, 4)})
+        if args.nprobe is None and r >= 0.95:
+            chosen = npb
+            break
+    if args.nprobe is not None:
+        chosen = args.nprobe
+    if chosen is None:
+        chosen = sweep[-1]["nprobe"]
+    ids, dists, dco = step(chosen, with_dco=True)
+    recall = recall_at_k(ids, gt_ids, gt_d64, dists, k)
+    dco_local = int(dco.sum().item())
+    dco_total = dco_local
+    if world > 1:
+        t = torch.tensor([dco_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        dco_total = int(t.item())
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(chosen)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device events per step, L2 flushed between) ----------
+    idx.profile_enable(True)
+    idx.profile_read(reset=True)
+    clk = ClockSampler(local_rank)
+    clk.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()                      # untimed: outside the step's events
+        ev[i][0].record(stream)
+        step(chosen)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = clk.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    prof = idx.profile_read(reset=True)
+    idx.profile_enable(False)
+    t_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    nq = Q.shape[0]
+    qps = nq * args.steps / (t_ms / 1e3)
+
+    # ---------------- e2e: host buffers through the C ABI (H2D + search + D2H) ----------
+    e2e = None
+    if world == 1:
+        import torch as _t
+        qh = _t.from_numpy(Q).pin_memory().numpy()
+        oi = _t.empty((nq, k), dtype=_t.int64).pin_memory().numpy()
+        od = _t.empty((nq, k), dtype=_t.float32).pin_memory().numpy()
+        for _ in range(2):
+            idx.search_host(qh, k, chosen, rf, oi, od)
+        e_times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            idx.search_host(qh, k, chosen, rf, oi, od)   # syncs the stream
+            e_times.append(time.perf_counter() - t0)
+        e2e = {"value": round(nq * args.steps / sum(e_times), 1), "unit": "queries/s",
+               "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 12)}
+
+    # ---------------- roofline of the dominant kernel (the fused scan) ----------------
+    peak, peak_src = load_peaks()
+    scan_ms = prof["ms"]["scan"] / max(1, prof["launches"]["scan"])
+    scan_bytes = dco_local * (spec.M // 2)             # algorithmic code bytes per launch
+    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(idx, X, Q, spec, chosen)
+
+    if rank == 0:
+        info = idx.info()
+        line = {
+            "metric": f"QPS at recall10@10>=0.95 ({spec.name}: {spec.n:,} x {spec.d}, nlist {spec.nlist}, "
+                      f"PQ {spec.M}x4b, AIR+SEIL, refine x{rf})",
+            "value": round(qps, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": spec.name, "n": spec.n, "d": spec.d, "nq_per_batch": nq,
+                       "nlist": spec.nlist, "M": spec.M, "nbits": 4, "k": k, "refine_factor": rf,
+                       "nprobe": chosen, "assignment": args.assignment + "+SEIL(cell-major)",
+                       "parallelism": f"index sharded id mod {world}" if world > 1 else "1 GPU",
+                       "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+            "recall10@10": round(recall, 4), "recall_sweep": sweep,
+            "dco_per_query": round(dco_total / nq, 1),
+            "dco_per_s": round(dco_total * args.steps / (t_ms / 1e3), 1),
+            "stage_ms_per_step": {kk: round(v / args.steps, 4) for kk, v in prof["ms"].items()},
+            "roofline": {"bound": "hbm", "kernel": "scan_kernel (LUT+worklist+fast-scan+top-bigK)",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": scan_bytes,
+                         "avg_launch_ms": round(scan_ms, 4)},
+            "e2e": e2e, "gpu_launches": 3 * args.steps + (args.steps if world > 1 else 0),
+            "clocks": clocks, "wall_s_timed_region": round(wall, 4),
+            "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
+            "index": {k2: info[k2] for k2 in ("n", "n_slots", "n_cells", "n_refs", "n_double",
+                                              "max_refs_per_list", "device_bytes")},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
+    """The CPU oracle (oracle/, plain C + OpenMP, never tuned) on the host cores:
+    oracle assignment + encode of the same base from the same trained state
+    (untimed), then oracle_search timed on a bounded query sample."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    cent, cb = [t.cpu().numpy() for t in idx.export_trained()]
+    l1, l2 = oracle.assign(X, cent, "air")
+    codes = oracle.encode(X, cb)
+    sample = 500
+    t0 = time.perf_counter()
+    oracle.search(X, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
+    dt = time.perf_counter() - t0
+    if dt < 5.0:   # grow the sample toward ~10 s of CPU work, bounded by the batch
+        sample = int(min(Q.shape[0], sample * max(1.0, 10.0 / max(dt, 1e-3))))
+        t0 = time.perf_counter()
+        oracle.search(X, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
+        dt = time.perf_counter() - t0
+    return {"value": round(sample / dt, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {sample} of the {Q.shape[0]} queries, nprobe {nprobe}, "
+                      f"oracle index built from the same trained centroids/codebook (untimed)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from synth import get_config, make_dataset
+    spec = get_config(args.config)
+    X, Q = make_dataset(spec)
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    rows = X[np.random.default_rng(5).permutation(X.shape[0])[:32768]]
+    cent = oracle.kmeans(rows, spec.nlist, iters=4, seed=11)
+    cb = oracle.pq_train(rows, spec.M, iters=4, seed=12)
+    l1, l2 = oracle.assign(X, cent, args.assignment.lower())
+    codes = oracle.encode(X, cb)
+    nprobe = args.nprobe or spec.nprobe
+    sample = 1000
+    for _ in range(args.warmup):
+        oracle.search(X, l1, l2, codes, cent, cb, Q[:64], spec.k, nprobe, spec.refine_factor)
+    times = []
+    for i in range(args.steps):
+        qs = Q[(i * sample) % Q.shape[0]:][:sample]
+        t0 = time.perf_counter()
+        oracle.search(X, l1, l2, codes, cent, cb, qs, spec.k, nprobe, spec.refine_factor)
+        times.append(time.perf_counter() - t0)
+    v = sample * args.steps / sum(times)
+    line = {"impl": "reference",
+            "metric": f"QPS ({spec.name}: {spec.n:,} x {spec.d}, nlist {spec.nlist}, PQ {spec.M}x4b, "
+                      f"AIR+SEIL, refine x{spec.refine_factor})",
+            "value": round(v, 2), "unit": "queries/s", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": spec.name, "n": spec.n, "d": spec.d, "nlist": spec.nlist,
+                       "M": spec.M, "k": spec.k, "refine_factor": spec.refine_factor,
+                       "nprobe": nprobe, "queries_per_step": sample},
+            "cpu_baseline": {"value": round(v, 2), "unit": "queries/s", "cores": cores,
+                             "kind": "oracle",
+                             "sample": f"{sample} queries per step (bounded sample of the 10k batch)"},
+            "e2e": {"value": round(v, 2), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2pl")
+    ap.add_argument("--assignment", default="AIR", choices=["AIR", "single"])
+    ap.add_argument("--nprobe", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

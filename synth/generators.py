@@ -13,8 +13,8 @@ the same shape and value structure. Recipes follow SURVEY.md §8(d):
           x = clip(round(mu_z + 16 g), 0, 255) as float32.
 * ``c2pl`` paper-like variant of c2 that carries the QPS@recall headline:
           rank-16 clusters x = mu_z + B_z g (g ~ N(0, I_16), B_z entries
-          N(0, sigma^2/16)), natural clusters = nlist/16, rounded/clipped to
-          [0, 255] like c2.
+          N(0, sigma^2/16), sigma = 48 calibrated), natural clusters =
+          nlist/16 = 64, rounded/clipped to [0, 255] like c2.
 * ``c3``  BJ configs[2]: 1536-d unit vectors, x = normalize(mu_z + s g),
           mu_c = normalize(N(0, I)), s = 0.6/sqrt(d) (cos(x, mu) ~ 0.85).
 
@@ -61,8 +61,11 @@ CONFIGS = {
                       note="c1 with sigma=3 (SURVEY §8(d) parity stress)"),
     "c2": ConfigSpec("c2", 1_000_000, 128, 10_000, 1024, 64, 10, 16, 10, "bytes",
                      16.0, 2, 1024, note="BJ configs[1]"),
-    "c2pl": ConfigSpec("c2pl", 1_000_000, 128, 10_000, 1024, 64, 10, 16, 10,
-                       "bytes_lowrank", 24.0, 2, 64, rank=16,
+    # sigma / natural clusters frozen from tools/calibrate_pl.py (profiles/calibration_c2pl.jsonl):
+    # AIR double-assigns 45.8 %, single recall10@10 at nprobe 1 = 0.47, AIR reaches 0.95
+    # at nprobe 4 (DCO 5.5k) vs single at nprobe 8 (DCO 8.2k).
+    "c2pl": ConfigSpec("c2pl", 1_000_000, 128, 10_000, 1024, 64, 10, 4, 10,
+                       "bytes_lowrank", 48.0, 2, 64, rank=16,
                        note="paper-like c2 (SURVEY §8(d) '-pl')"),
     "c3": ConfigSpec("c3", 1_000_000, 1536, 10_000, 4096, 384, 10, 32, 10, "sphere",
                      0.6 / np.sqrt(1536.0), 3, 4096, note="BJ configs[2]"),

@@ -1,0 +1,275 @@
+"""GPU (CUDA path, through the C ABI) vs CPU oracle parity. Needs a B200.
+
+The oracle trains the coarse centroids and the PQ codebook (training is outside
+the bit-exact contract, R16); the GPU index is built from that
+trained state (rairs_build_from_trained) and everything downstream must match:
+  * assignment (l1, l2) and PQ codes: bit-exact (O4, O5)
+  * probes, LUT Qv / a / b, candidate (score, id) keys, DCO: bit-exact
+  * refined distances: within 1e-4 relative (they are in fact bit-equal:
+    both sides sum in fp64 in ascending t and round once)
+  * final ids: identical
+Inputs come from synth/ (seeded); no expected value comes from the CUDA path.
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import gpu_available
+
+pytestmark = pytest.mark.gpu
+
+if not gpu_available():  # collected on CPU too; skip at import of fixtures
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch  # noqa: E402
+
+import paper_2601_07183_b200 as rb  # noqa: E402
+from synth import get_config, make_dataset  # noqa: E402
+
+DEV = torch.device("cuda:0")
+U32 = 0xFFFFFFFF
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+class Case:
+    """Oracle-trained index of one config (CPU) + the GPU index built from it."""
+
+    def __init__(self, oracle, name, n=None, nq=None, train_rows=20000, iters=6,
+                 assignment="air", strict=False):
+        spec = get_config(name)
+        self.spec = spec
+        X, Q = make_dataset(spec, n=n, nq=nq)
+        self.X, self.Q = X, Q
+        rows = X[np.random.default_rng(5).permutation(X.shape[0])[:min(train_rows, X.shape[0])]]
+        self.cent = oracle.kmeans(rows, spec.nlist, iters=iters, seed=11)
+        self.cb = oracle.pq_train(rows, spec.M, iters=iters, seed=12)
+        self.l1, self.l2 = oracle.assign(X, self.cent, assignment, strict=strict)
+        self.codes = oracle.encode(X, self.cb)
+        self.assignment, self.strict = assignment, strict
+
+    def gpu_index(self, shard_id=0, nshards=1):
+        rows = np.arange(shard_id, self.X.shape[0], nshards)
+        return rb.Index.build(_t(self.X[rows]), self.spec.nlist, self.spec.M,
+                              assignment=self.assignment.upper(), strict=self.strict,
+                              centroids=_t(self.cent), codebook=_t(self.cb),
+                              shard_id=shard_id, nshards=nshards)
+
+
+_CACHE = {}
+
+
+def case(oracle, name, **kw):
+    key = (name, tuple(sorted(kw.items())))
+    if key not in _CACHE:
+        _CACHE[key] = Case(oracle, name, **kw)
+    return _CACHE[key]
+
+
+def gpu_search(idx, Q, k, nprobe, rf):
+    out = idx.search_debug(_t(Q), k, nprobe, rf)
+    torch.cuda.synchronize()
+    r = {key: v.cpu().numpy() for key, v in out.items()}
+    r["cand_ids"] = r["cand_ids"].view(np.uint32)
+    r["cand_scores"] = r["cand_scores"].view(np.uint32)
+    return r
+
+
+def assert_search_equal(g, o, rows=None, shard=0):
+    sel = slice(None) if rows is None else rows
+    assert np.array_equal(g["probes"], o["probes"][sel]), "probe sets differ (O1)"
+    assert np.array_equal(g["Qv"], o["Qv"][sel]), "quantised LUT differs (O2)"
+    assert np.array_equal(g["a"], o["a"][sel]) and np.array_equal(g["b"], o["b"][sel])
+    assert np.array_equal(g["dco"], o["dco"][sel][:, shard]), "DCO differs (O12)"
+    assert np.array_equal(g["cand_scores"], o["cand_scores"][sel][:, shard]), "scores differ (O8/O9)"
+    assert np.array_equal(g["cand_ids"], o["cand_ids"][sel][:, shard]), "candidate ids differ (O9)"
+    oi = o["shard_ids"][sel][:, shard] if "shard_ids" in o else o["ids"][sel]
+    od = o["shard_dists"][sel][:, shard] if "shard_dists" in o else o["dists"][sel]
+    assert np.array_equal(g["ids"], oi), "final ids differ (O10)"
+    fin = np.isfinite(od)
+    assert np.array_equal(np.isfinite(g["dists"]), fin)
+    assert np.allclose(g["dists"][fin], od[fin], rtol=1e-4, atol=0), "refined distances (1e-4)"
+
+
+# ------------------------------------------------------------------ build
+@pytest.mark.parametrize("name", ["c0", "c0s", "c1", "c1s"])
+def test_build_assignment_codes_layout(oracle_mod, name):
+    c = case(oracle_mod, name)
+    idx = c.gpu_index()
+    l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
+    assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2), "AIR assignment (O4)"
+    assert np.array_equal(codes, c.codes), "PQ codes (O5)"
+    check_layout(idx, c.l1, c.l2)
+    info = idx.info()
+    assert info["n_double"] == int(np.sum(c.l1 != c.l2))
+
+
+def check_layout(idx, l1, l2):
+    """O6 (i)-(iv): stored once; owned region = cells (l, j>=l) in (l2, row)
+    order; references = cells (i<j) with their slot range; padding at ends."""
+    L = {k: v.cpu().numpy() for k, v in idx.export_layout().items()}
+    rows = L["slot_rows"].view(np.uint32)
+    valid = rows != U32
+    n = l1.shape[0]
+    assert valid.sum() == n and np.array_equal(np.sort(rows[valid]), np.arange(n))      # (i)
+    nl = L["own_off"].shape[0]
+    for l in range(nl):
+        off, cnt = int(L["own_off"][l]), int(L["own_cnt"][l])
+        mine = np.nonzero(l1 == l)[0]
+        order = mine[np.lexsort((mine, l2[mine]))]
+        assert np.array_equal(rows[off:off + cnt], order)                             # (ii)
+        end = off + ((cnt + 31) // 32) * 32
+        assert (rows[off + cnt:end] == U32).all()                                      # (iv)
+        refs = []
+        for e in range(int(L["ref_ptr"][l]), int(L["ref_ptr"][l + 1])):
+            refs.append((int(L["ref_owner"][e]), int(L["ref_start"][e]), int(L["ref_cnt"][e])))
+        expect = []
+        for i in range(l):
+            cell = np.nonzero((l1 == i) & (l2 == l))[0]
+            if cell.size:
+                expect.append((i, cell.size))
+        assert [(o, c) for o, _, c in refs] == expect                                  # (iii)
+        for o, s, cn in refs:
+            got = rows[s:s + cn]
+            assert (l1[got] == o).all() and (l2[got] == l).all()
+
+
+# ----------------------------------------------------------------- search
+SEARCH_CASES = [
+    ("c0", 5, 4, 4), ("c0s", 5, 4, 4), ("c0s", 5, 16, 2), ("c0s", 1, 1, 1),
+    ("c1", 10, 8, 4), ("c1", 10, 1, 4), ("c1", 10, 64, 4),
+    ("c1s", 10, 8, 4), ("c1s", 10, 16, 10), ("c1s", 1, 3, 100), ("c1s", 100, 8, 1),
+]
+
+
+@pytest.mark.parametrize("name,k,nprobe,rf", SEARCH_CASES)
+def test_search_parity(oracle_mod, name, k, nprobe, rf):
+    c = case(oracle_mod, name)
+    idx = c.gpu_index()
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, k, nprobe, rf)
+    g = gpu_search(idx, c.Q, k, nprobe, rf)
+    assert_search_equal(g, o)
+
+
+def test_search_modes_single_and_strict(oracle_mod):
+    for kw in ({"assignment": "single"}, {"assignment": "air", "strict": True}):
+        c = case(oracle_mod, "c1s", **kw)
+        idx = c.gpu_index()
+        l1, l2, _ = [t.cpu().numpy() for t in idx.export_assignment()]
+        assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2)
+        o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, 10, 8, 4)
+        assert_search_equal(gpu_search(idx, c.Q, 10, 8, 4), o)
+
+
+def test_exhaustive_reduction_equals_exact_knn(oracle_mod):
+    # nprobe = nlist, bigK >= n  ->  exact k-NN (BJ invariant)
+    c = case(oracle_mod, "c0s")
+    idx = c.gpu_index()
+    k = 5
+    rf = (c.X.shape[0] + k - 1) // k  # bigK >= n
+    g = gpu_search(idx, c.Q, k, c.spec.nlist, rf)
+    gt, _ = oracle_mod.exact_knn(c.X, c.Q, k)
+    assert np.array_equal(g["ids"], gt)
+    assert (g["dco"] == c.X.shape[0]).all()
+
+
+def test_edge_cases(oracle_mod):
+    c = case(oracle_mod, "c1s")
+    idx = c.gpu_index()
+    # queries equal to base rows, a single query, and an empty batch
+    Qs = c.X[[0, 17, 999]]
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, Qs, 3, 2, 7)
+    assert_search_equal(gpu_search(idx, Qs, 3, 2, 7), o)
+    o1 = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q[:1], 10, 8, 4)
+    assert_search_equal(gpu_search(idx, c.Q[:1], 10, 8, 4), o1)
+    ids, dists = idx.search(_t(c.Q[:0]), 10, 8, 4)
+    assert ids.shape == (0, 10)
+    # search == search_host == search_debug results
+    ids, dists = idx.search(_t(c.Q), 10, 8, 4)
+    hi, hd = idx.search_host(c.Q, 10, 8, 4)
+    assert np.array_equal(ids.cpu().numpy(), hi) and np.array_equal(dists.cpu().numpy(), hd)
+
+
+def test_padding_when_universe_smaller_than_k(oracle_mod):
+    c = case(oracle_mod, "c0")
+    idx = c.gpu_index()
+    # k larger than any single list (3000 rows / 16 lists), nprobe=1 -> (-1, inf) tail
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, 1000, 1, 1)
+    g = gpu_search(idx, c.Q, 1000, 1, 1)
+    assert_search_equal(g, o)
+    assert (g["ids"] == -1).any()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_parity(oracle_mod, G):
+    c = case(oracle_mod, "c1s")
+    k, nprobe, rf = 10, 8, 4
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, k, nprobe, rf, nshards=G)
+    per_ids, per_d = [], []
+    for s in range(G):
+        idx = c.gpu_index(shard_id=s, nshards=G)
+        g = gpu_search(idx, c.Q, k, nprobe, rf)
+        assert_search_equal(g, o, shard=s)
+        per_ids.append(g["ids"])
+        per_d.append(g["dists"])
+    mi, md = rb.merge_topk(_t(np.stack(per_ids)), _t(np.stack(per_d)))
+    assert np.array_equal(mi.cpu().numpy(), o["ids"])
+    assert np.allclose(md.cpu().numpy(), o["dists"], rtol=1e-4)
+
+
+def test_exact_knn_kernel(oracle_mod):
+    c = case(oracle_mod, "c1")
+    ids, d64 = rb.exact_knn(_t(c.X), _t(c.Q), 10)
+    gi, gd = oracle_mod.exact_knn(c.X, c.Q, 10)
+    assert np.array_equal(ids.cpu().numpy(), gi)
+    assert np.array_equal(d64.cpu().numpy(), gd)
+
+
+def test_errors_are_reported():
+    X = torch.randn(500, 16, device=DEV)
+    with pytest.raises(rb.RairsError):
+        rb.build_index(X, nlist=8, M=5)                       # M does not divide d
+    with pytest.raises(rb.RairsError):
+        rb.build_index(X, nlist=8, M=8, nbits=8)              # nbits != 4
+    with pytest.raises(rb.RairsError):
+        rb.build_index(X, nlist=1000, M=8)                    # nlist > n
+    idx = rb.build_index(X, nlist=8, M=8, kmeans_iters=3)
+    q = torch.randn(4, 16, device=DEV)
+    for bad in (dict(k=0, nprobe=2), dict(k=3, nprobe=9), dict(k=3, nprobe=0)):
+        with pytest.raises(rb.RairsError):
+            idx.search(q, refine_factor=2, **bad)
+    with pytest.raises(TypeError):
+        idx.search(q.cpu(), 3, 2)                             # host tensor on the device API
+
+
+def test_gpu_training_properties():
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((4000, 16)).astype(np.float32)
+    c1, b1 = rb.train(_t(X), 1, 8, kmeans_iters=3, train_sample=4000)
+    assert np.allclose(c1.cpu().numpy()[0], X.astype(np.float64).mean(0), atol=1e-5)
+    ca, ba = rb.train(_t(X), 32, 8, kmeans_iters=5, seed=3)
+    cb_, bb = rb.train(_t(X), 32, 8, kmeans_iters=5, seed=3)
+    assert torch.equal(ca, cb_) and torch.equal(ba, bb)           # deterministic
+    assert torch.isfinite(ca).all() and torch.isfinite(ba).all()
+
+
+# ------------------------------------------ BJ full sizes, sampled queries
+@pytest.mark.parametrize("name,nprobe", [("c2", 16), ("c2pl", 16), ("c2pl", 64)])
+def test_full_size_sampled(oracle_mod, name, nprobe):
+    """BJ configs[1] at full size (1M x 128, 10k queries) in the bench's launch
+    configuration; the oracle recomputes a sample of 200 queries one by one."""
+    c = case(oracle_mod, name, train_rows=32768, iters=4)
+    spec = c.spec
+    idx = c.gpu_index()
+    rng = np.random.default_rng(7)
+    sample = np.sort(rng.choice(c.Q.shape[0], 200, replace=False))
+    g = gpu_search(idx, c.Q, spec.k, nprobe, spec.refine_factor)   # all 10k queries
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q[sample], spec.k, nprobe,
+                          spec.refine_factor)
+    gs = {key: v[sample] for key, v in g.items()}
+    assert_search_equal(gs, o)
+    # assignment and codes on a sample of rows
+    l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
+    assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2)
+    assert np.array_equal(codes, c.codes)
