@@ -117,7 +117,7 @@ rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out);
  * squared L2 (reading R14).  dco: dev [nq] int64 or NULL -- number of items
  * scored per query on this shard (= |U_s(q)|, O12).
  * Errors: nq < 0, k < 1, nprobe < 1 or > nlist, refine_factor < 1,
- * k*refine_factor > 4096, nprobe > 1024. */
+ * k*refine_factor > 2048 (UNSUPPORTED), nprobe > 1024 (UNSUPPORTED). */
 rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, int32_t k,
                           int32_t nprobe, int32_t refine_factor, int64_t* out_ids,
                           float* out_dists, int64_t* dco, void* stream);
@@ -169,6 +169,15 @@ rairs_status rairs_export_assignment(rairs_index_t idx, int32_t* l1, int32_t* l2
 rairs_status rairs_export_layout(rairs_index_t idx, int64_t* own_off, int64_t* own_cnt,
                                  int64_t* ref_ptr, int32_t* ref_owner, int64_t* ref_start,
                                  int64_t* ref_cnt, uint32_t* slot_rows, void* stream);
+
+/* ---- coarse stage mode ------------------------------------------------------
+ * 0 = auto (tensor-core TF32 filter + fp64 certification when d % 4 == 0 and
+ * nlist >= 64, else exact fp64); 1 = exact fp64 only; 2 = tensor-core path
+ * whenever d % 4 == 0.  Every mode returns exactly the O1 probe set.
+ * rairs_certify_fallbacks: queries whose TF32 filter could not be certified
+ * and were recomputed exactly (host out; synchronises the device). */
+rairs_status rairs_set_coarse_mode(rairs_index_t idx, int32_t mode);
+rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t reset);
 
 /* ---- stage timing (CUDA events on the search stream) ----------------------
  * When enabled, every search records events around its stages on its stream;

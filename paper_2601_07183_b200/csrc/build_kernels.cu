@@ -88,6 +88,10 @@ __global__ void __launch_bounds__(PT) probe_exact_kernel(ProbeArgs a, ProbeSmem 
   for (int64_t g = blockIdx.x; g * R < a.rows; g += gridDim.x) {
     const int64_t r0 = g * R;
     const int nr = (int)((a.rows - r0) < (int64_t)R ? (a.rows - r0) : (int64_t)R);
+    if (a.only_flagged) {
+      const bool mine = (tid < nr) && a.only_flagged[r0 + tid] != 0;
+      if (!__syncthreads_or(mine)) continue;
+    }
     for (int e = tid; e < R * d; e += PT) {
       int r = e / d, t = e - r * d;
       xs[e] = (r < nr) ? (double)a.X[(r0 + r) * d + t] : 0.0;

@@ -80,6 +80,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->centroids); cudaFree(x->codebook); cudaFree(x->X); cudaFree(x->l1); cudaFree(x->l2);
   cudaFree(x->codes); cudaFree(x->slot_rows); cudaFree(x->own_off); cudaFree(x->own_cnt);
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
+  cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
   for (auto& es : x->pending)
     for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
   for (auto e : x->pool) cudaEventDestroy(e);
@@ -145,17 +146,22 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   StageEvents ev(idx, s);
   rairs_status st = RAIRS_OK;
   ev.mark(0);
-  // coarse: P(q) = first nprobe lists by (D64, l)  (O1, exact fp64)
-  ProbeArgs pa{};
-  pa.X = queries;
-  pa.rows = nq;
-  pa.d = idx->d;
-  pa.C = idx->centroids;
-  pa.nl = idx->nlist;
-  pa.L = nprobe;
-  pa.mode = 0;
-  pa.out_idx = probes;
-  st = launch_probe_exact(pa, s);
+  // coarse: P(q) = first nprobe lists by (D64, l)  (O1).  Tensor-core TF32
+  // filter + exact fp64 certify (K1/K2), or the exact fp64 kernel directly.
+  if (coarse_gemm_supported(idx, nprobe)) {
+    st = launch_coarse(idx, queries, nq, nprobe, probes, idx->certify_fallbacks, s);
+  } else {
+    ProbeArgs pa{};
+    pa.X = queries;
+    pa.rows = nq;
+    pa.d = idx->d;
+    pa.C = idx->centroids;
+    pa.nl = idx->nlist;
+    pa.L = nprobe;
+    pa.mode = 0;
+    pa.out_idx = probes;
+    st = launch_probe_exact(pa, s);
+  }
   ev.mark(1);
   if (st == RAIRS_OK) st = launch_scan(idx, a, s);
   ev.mark(2);
@@ -185,8 +191,8 @@ static rairs_status validate_search(rairs_index_t idx, int64_t nq, int32_t k, in
     return RAIRS_E_UNSUPPORTED;
   }
   if (rf < 1) return invalid("refine_factor must be >= 1");
-  if ((int64_t)k * rf > 4096) {
-    set_error("k * refine_factor > 4096 is not supported");
+  if ((int64_t)k * rf > 2048) {
+    set_error("k * refine_factor > 2048 is not supported");
     return RAIRS_E_UNSUPPORTED;
   }
   return RAIRS_OK;
@@ -293,6 +299,10 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   // Alg. 4 SeilInsert (cell-major) + PQ encoding (O5) into the packed layout
   st = build_layout(idx, s);
   if (st != RAIRS_OK) return fail(st);
+  st = coarse_prepare(idx, s);
+  if (st != RAIRS_OK) return fail(st);
+  B_TRY(cudaMalloc(&idx->certify_fallbacks, sizeof(unsigned)));
+  B_TRY(cudaMemsetAsync(idx->certify_fallbacks, 0, sizeof(unsigned), s));
   B_TRY(cudaStreamSynchronize(s));
 #undef B_TRY
   *out = idx;
@@ -487,6 +497,22 @@ rairs_status rairs_export_layout(rairs_index_t idx, int64_t* own_off, int64_t* o
   OPTIONAL_DEV(slot_rows, "slot_rows");
   return export_layout64(idx, own_off, own_cnt, ref_ptr, ref_owner, ref_start, ref_cnt, slot_rows,
                          (cudaStream_t)stream);
+}
+
+rairs_status rairs_set_coarse_mode(rairs_index_t idx, int32_t mode) {
+  if (!idx) return invalid("index is NULL");
+  if (mode < 0 || mode > 2) return invalid("coarse mode must be 0 (auto), 1 (exact), 2 (tensor core)");
+  idx->coarse_mode = mode;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t reset) {
+  if (!idx || !count) return invalid("NULL argument");
+  unsigned v = 0;
+  RAIRS_CUDA_TRY(cudaMemcpy(&v, idx->certify_fallbacks, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  *count = v;
+  if (reset) RAIRS_CUDA_TRY(cudaMemset(idx->certify_fallbacks, 0, sizeof(unsigned)));
+  return RAIRS_OK;
 }
 
 rairs_status rairs_profile_enable(rairs_index_t idx, int32_t on) {

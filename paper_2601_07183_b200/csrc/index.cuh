@@ -32,6 +32,11 @@ struct rairs_index_s {
   uint32_t* ref_start = nullptr;  // [n_refs] slot
   uint32_t* ref_cnt = nullptr;  // [n_refs]
   int64_t n_refs = 0, n_cells = 0, n_double = 0;
+  // coarse stage (K1/K2): fp32 ||c||^2, max ||c||, mode 0 auto / 1 exact / 2 tensor core
+  float* cnorm = nullptr;
+  double cmax = 0.0;
+  int coarse_mode = 0;
+  unsigned* certify_fallbacks = nullptr;  // device counter
   int max_refs = 0;
   int64_t device_bytes = 0;
 
@@ -67,6 +72,7 @@ struct ProbeArgs {
   double* out_d64;     // mode 0, optional
   int32_t* l1;         // modes 1/2
   int32_t* l2;
+  const int32_t* only_flagged;  // mode 0: process only row groups with a flagged row
 };
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s);
 
@@ -79,6 +85,12 @@ rairs_status export_codes(const rairs_index_s* idx, uint8_t* codes, cudaStream_t
 rairs_status export_layout64(const rairs_index_s* idx, int64_t* own_off, int64_t* own_cnt,
                              int64_t* ref_ptr, int32_t* ref_owner, int64_t* ref_start,
                              int64_t* ref_cnt, uint32_t* slot_rows, cudaStream_t s);
+
+// ---- coarse stage (coarse_kernels.cu) ---------------------------------------
+rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s);
+bool coarse_gemm_supported(const rairs_index_s* idx, int nprobe);
+rairs_status launch_coarse(const rairs_index_s* idx, const float* queries, int64_t nq, int nprobe,
+                           int32_t* probes, unsigned* nflag_dev, cudaStream_t s);
 
 // ---- search-side launchers (search_kernels.cu) -----------------------------
 struct SearchArgs {

@@ -22,7 +22,7 @@ namespace rairs {
 
 constexpr int ST = 256;          // scan threads per CTA
 constexpr int SNW = ST / 32;     // warps
-constexpr int BPW = 4;           // blocks per warp per round
+constexpr int BPW = 8;           // blocks per warp per round
 constexpr int ROUND = SNW * BPW * 32;  // max candidates appended per round
 constexpr int RCAP = 512;        // ranges per work-list chunk
 
@@ -42,14 +42,15 @@ struct ScanParams {
   const float* queries;
   int64_t nq;
   const int32_t* probes;
-  int nprobe, bigK, cap;
+  int nprobe, bigK, cap, hshift;
   uint64_t* out_keys;
   int64_t* dco;
   uint8_t* lut_q;
   float* lut_a;
   float* lut_b;
   // shared memory carve-up
-  int off_lut, off_mn, off_span, off_bm, off_P, off_sp, off_rs, off_re, off_bp, off_cand, smem;
+  int off_lut, off_mn, off_span, off_bm, off_P, off_sp, off_rs, off_re, off_bp, off_hist, off_cand,
+      smem;
 };
 
 // ---------------------------------------------------------------------------
@@ -159,20 +160,84 @@ __device__ __forceinline__ uint32_t score_block(const uint64_t* __restrict__ blk
   return acc;
 }
 
-// CTA compaction of the candidate buffer to its bigK smallest keys.
-__device__ void compact_cands(uint64_t* cand, unsigned int* cnt_p, uint64_t* tau_p, int bigK) {
-  const int n = (int)*cnt_p;
-  int np = 2;
-  while (np < n) np <<= 1;
-  for (int i = n + threadIdx.x; i < np; i += blockDim.x) cand[i] = kKeyInf;
+// ---------------------------------------------------------------------------
+// A6 top-bigK selection state (per query, shared memory):
+//  * hist[bin]: number of APPENDED candidates per score bin (bin = s >> hshift).
+//    Every scanned item whose bin <= bthr is appended, and bthr only
+//    decreases, so for bins <= bthr the histogram counts ALL scanned items.
+//  * bthr: smallest bin with cumulative count >= bigK (conservative while
+//    warps race; recomputed lock-free by the warp that crosses a counter).
+//    Items in bins > bthr cannot be among the bigK smallest keys (the bin map
+//    is monotone in s), so they are dropped without touching shared memory.
+//  * tau: exact key threshold, only set by the (rare) sort fallback.
+//  The final result is the exact sort of the survivors: unique keys
+//  (s << 32 | id) make it independent of scheduling (R5).
+constexpr int NBINS = 2048;
+
+__device__ __forceinline__ uint32_t recompute_bthr(const uint32_t* hist, uint32_t upto,
+                                                   uint32_t bigK) {
+  // warp-cooperative: smallest b <= upto with sum_{i<=b} hist[i] >= bigK (else upto)
+  const int lane = lane_id();
+  uint32_t run = 0;
+  for (uint32_t b0 = 0; b0 <= upto; b0 += 32) {
+    const uint32_t b = b0 + lane;
+    uint32_t v = (b <= upto) ? ((volatile const uint32_t*)hist)[b] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, run + v >= bigK && b <= upto);
+    if (hit) return b0 + (uint32_t)(__ffs(hit) - 1);
+    run += __shfl_sync(0xffffffffu, v, 31);
+  }
+  return upto;
+}
+
+// Drop candidates outside (bin <= bthr && key < tau); returns the new count.
+// All threads; starts and ends with a barrier.  cap <= ST * 16.
+__device__ uint32_t filter_cands(uint64_t* cand, uint32_t n, uint32_t bthr, uint64_t tau,
+                                 int hshift, uint32_t* warp_tot) {
+  constexpr int PER = 16;
+  uint64_t v[PER];
+  uint32_t keep = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const uint32_t e = threadIdx.x * PER + i;
+    v[i] = (e < n) ? cand[e] : kKeyInf;
+    const bool k = (e < n) && ((uint32_t)(v[i] >> (32 + hshift)) <= bthr) && (v[i] < tau);
+    if (!k) v[i] = kKeyInf;
+    keep += k ? 1u : 0u;
+  }
+  // exclusive scan of per-thread counts
+  const int lane = lane_id(), warp = warp_id();
+  uint32_t incl = keep;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();  // everyone has read cand[] into registers
+  if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
-  cta_bitonic_sort_u64(cand, np);
-  if (threadIdx.x == 0) {
-    const int keep = min(n, bigK);
-    *cnt_p = (unsigned)keep;
-    if (keep == bigK) *tau_p = cand[bigK - 1];
+  if (warp == 0) {
+    uint32_t w = (lane < SNW) ? warp_tot[lane] : 0u, wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < SNW) warp_tot[lane] = wi - w;
+    if (lane == SNW - 1) warp_tot[SNW] = wi;
   }
   __syncthreads();
+  uint32_t pos = warp_tot[warp] + incl - keep;
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (v[i] != kKeyInf) cand[pos++] = v[i];
+  const uint32_t total = warp_tot[SNW];
+  __syncthreads();
+  return total;
 }
 
 template <int NU>
@@ -190,17 +255,20 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
   uint32_t* rs = reinterpret_cast<uint32_t*>(sm + p.off_rs);
   uint32_t* re = reinterpret_cast<uint32_t*>(sm + p.off_re);
   uint32_t* bp = reinterpret_cast<uint32_t*>(sm + p.off_bp);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sm + p.off_hist);
   uint64_t* cand = reinterpret_cast<uint64_t*>(sm + p.off_cand);
   __shared__ uint32_t warp_tot[SNW + 1];
-  __shared__ unsigned int cand_cnt;
+  __shared__ unsigned int cand_cnt, bthr, since, dco_acc;
   __shared__ uint64_t tau;
   __shared__ float sh_S;
-  __shared__ unsigned long long dco_acc;
 
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int M = p.M, M16 = p.M * 16, MP16 = p.M_pad * 16;
   const int nu_rt = p.M_pad / 16;
   const int bm_words = (p.nlist + 31) >> 5;
+  const int hshift = p.hshift;
+  const uint32_t bigK = (uint32_t)p.bigK;
+  const uint32_t recomp = max(32u, bigK / 2u);
 
   for (int64_t q = blockIdx.x; q < p.nq; q += gridDim.x) {
     const float* qv = p.queries + q * p.d;
@@ -223,7 +291,14 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
       }
     }
     for (int w = tid; w < bm_words; w += ST) bitmap[w] = 0u;
-    if (tid == 0) { cand_cnt = 0; tau = kKeyInf; dco_acc = 0ull; }
+    for (int w = tid; w < NBINS; w += ST) hist[w] = 0u;
+    if (tid == 0) {
+      cand_cnt = 0;
+      bthr = NBINS - 1;
+      since = 0;
+      dco_acc = 0;
+      tau = kKeyInf;
+    }
     __syncthreads();
     if (warp == 0) {
       float s = 0.0f;
@@ -268,7 +343,7 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
     __syncthreads();
     const uint32_t nsrc_total = cta_exclusive_scan(sp, p.nprobe, warp_tot);
 
-    uint64_t my_dco = 0;
+    uint32_t my_dco = 0;
     for (uint32_t cs = 0; cs < nsrc_total; cs += RCAP) {
       const int nsrc = (int)((nsrc_total - cs) < (uint32_t)RCAP ? (nsrc_total - cs) : (uint32_t)RCAP);
       // ---------------- K4: SEIL work list ----------------
@@ -296,7 +371,7 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
         rs[i] = st;
         re[i] = en;
         bp[i] = (en > st) ? (((en - 1) >> 5) - (st >> 5) + 1) : 0u;
-        my_dco += (uint64_t)(en - st);
+        my_dco += en - st;
       }
       __syncthreads();
       const uint32_t nblk = cta_exclusive_scan(bp, nsrc, warp_tot);
@@ -305,7 +380,6 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
       int r = 0;  // per-warp cursor into the range list (monotone in b)
       for (uint32_t base = 0; base < nblk; base += SNW * BPW) {
         const uint64_t tau_r = tau;
-        const uint32_t ts = (uint32_t)(tau_r >> 32);
 #pragma unroll 1
         for (int kk = 0; kk < BPW; ++kk) {
           const uint32_t b = base + kk * SNW + warp;
@@ -316,7 +390,8 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
           const uint32_t slot = gblk * 32u + lane;
           const bool valid = (slot >= st) && (slot < en);
           const uint32_t s = score_block<NU>(p.codes64 + (size_t)gblk * nu_rt * 32, lut, lane, nu_rt);
-          const bool maybe = valid && (s <= ts);
+          const uint32_t bin = s >> hshift;
+          const bool maybe = valid && (bin <= *(volatile uint32_t*)&bthr);
           if (__any_sync(0xffffffffu, maybe)) {
             uint64_t key = kKeyInf;
             if (maybe) {
@@ -327,23 +402,71 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
             const bool pass = maybe && key < tau_r;
             const unsigned bal = __ballot_sync(0xffffffffu, pass);
             if (bal) {
-              unsigned pos = 0;
-              if (lane == 0) pos = atomicAdd(&cand_cnt, (unsigned)__popc(bal));
+              const unsigned c = (unsigned)__popc(bal);
+              unsigned pos = 0, old = 0;
+              if (lane == 0) {
+                pos = atomicAdd(&cand_cnt, c);
+                old = atomicAdd(&since, c);
+              }
               pos = __shfl_sync(0xffffffffu, pos, 0);
-              if (pass) cand[pos + __popc(bal & ((1u << lane) - 1u))] = key;
+              old = __shfl_sync(0xffffffffu, old, 0);
+              if (pass) {
+                cand[pos + __popc(bal & ((1u << lane) - 1u))] = key;
+                atomicAdd(&hist[bin], 1u);
+              }
+              if (old < recomp && old + c >= recomp) {   // this warp refreshes bthr
+                __syncwarp();
+                const uint32_t nb = recompute_bthr(hist, *(volatile uint32_t*)&bthr, bigK);
+                if (lane == 0) {
+                  atomicMin(&bthr, nb);
+                  atomicExch(&since, 0u);
+                }
+              }
             }
           }
         }
         __syncthreads();
-        if ((int)cand_cnt > p.cap - ROUND) compact_cands(cand, &cand_cnt, &tau, p.bigK);
+        if (cand_cnt > (uint32_t)(p.cap - ROUND)) {
+          if (warp == 0) {
+            const uint32_t nb = recompute_bthr(hist, bthr, bigK);
+            if (lane == 0) bthr = nb;
+          }
+          __syncthreads();
+          const uint32_t nk = filter_cands(cand, cand_cnt, bthr, tau, hshift, warp_tot);
+          if (tid == 0) cand_cnt = nk;
+          __syncthreads();
+          if (nk > (uint32_t)(p.cap - ROUND)) {  // pathological ties: exact sort fallback
+            int np = 2;
+            while (np < (int)nk) np <<= 1;
+            for (int i = nk + tid; i < np; i += ST) cand[i] = kKeyInf;
+            __syncthreads();
+            cta_bitonic_sort_u64(cand, np);
+            if (tid == 0) {
+              cand_cnt = bigK;
+              tau = cand[bigK - 1];
+            }
+            __syncthreads();
+          }
+        }
       }
       __syncthreads();
     }
     // DCO = |U_s(q)|: sum of scanned range lengths (valid items only)
-    atomicAdd(&dco_acc, (unsigned long long)my_dco);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
+    if (lane == 0) atomicAdd(&dco_acc, my_dco);
+    if (warp == 0) {
+      const uint32_t nb = recompute_bthr(hist, bthr, bigK);
+      if (lane == 0) bthr = nb;
+    }
     __syncthreads();
-    compact_cands(cand, &cand_cnt, &tau, p.bigK);
-    const int keep = (int)cand_cnt;
+    const uint32_t nk = filter_cands(cand, cand_cnt, bthr, tau, hshift, warp_tot);
+    int np = 2;
+    while (np < (int)nk) np <<= 1;
+    for (int i = nk + tid; i < np; i += ST) cand[i] = kKeyInf;
+    __syncthreads();
+    cta_bitonic_sort_u64(cand, np);
+    const int keep = (int)min(nk, bigK);
     for (int i = tid; i < p.bigK; i += ST)
       p.out_keys[q * p.bigK + i] = (i < keep) ? cand[i] : kKeyInf;
     if (tid == 0 && p.dco) p.dco[q] = (int64_t)dco_acc;
@@ -368,6 +491,7 @@ static int scan_smem_layout(ScanParams& p) {
   p.off_rs = take(RCAP * 4, 16);
   p.off_re = take(RCAP * 4, 16);
   p.off_bp = take((RCAP + 1) * 4, 16);
+  p.off_hist = take(NBINS * 4, 16);
   p.off_cand = take(p.cap * 8, 16);
   p.smem = (int)round_up(o, 16);
   return p.smem;
@@ -408,6 +532,12 @@ rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStre
   p.nprobe = a.nprobe;
   p.bigK = a.k * a.refine_factor;
   p.cap = next_pow2(p.bigK + ROUND);
+  p.hshift = 0;
+  while (((int64_t)p.M * 255) >> p.hshift >= NBINS) ++p.hshift;
+  if (p.cap > ST * 16) {
+    set_error("scan: k * refine_factor too large for the candidate buffer");
+    return RAIRS_E_UNSUPPORTED;
+  }
   p.out_keys = a.cand_keys;
   p.dco = a.dco;
   p.lut_q = a.lut_q;

@@ -198,6 +198,19 @@ class Index:
         r["slot_rows"] = r["slot_rows"][:ns]
         return r
 
+    # ---------------------------------------------------- coarse stage
+    COARSE_MODES = {"auto": 0, "exact": 1, "tensor": 2}
+
+    def set_coarse_mode(self, mode: str = "auto"):
+        """auto | exact (fp64 only) | tensor (TF32 tcgen05 filter + fp64 certify)."""
+        check(lib().rairs_set_coarse_mode(self._h, self.COARSE_MODES[mode]), "rairs_set_coarse_mode")
+
+    def certify_fallbacks(self, reset: bool = True) -> int:
+        v = ctypes.c_int64()
+        check(lib().rairs_certify_fallbacks(self._h, ctypes.byref(v), int(bool(reset))),
+              "rairs_certify_fallbacks")
+        return int(v.value)
+
     # ------------------------------------------------------- profiling
     def profile_enable(self, on: bool = True):
         check(lib().rairs_profile_enable(self._h, int(bool(on))), "rairs_profile_enable")

@@ -273,3 +273,28 @@ def test_full_size_sampled(oracle_mod, name, nprobe):
     l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
     assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2)
     assert np.array_equal(codes, c.codes)
+
+
+# ------------------------------------- coarse stage: tensor-core path == O1
+@pytest.mark.parametrize("name,nprobes", [("c1s", [1, 8, 32]), ("c2pl", [1, 4, 16, 64, 128])])
+def test_coarse_tensor_core_path_equals_exact(oracle_mod, name, nprobes):
+    """K1 (tcgen05 TF32 GEMM) + K2 (fp64 certify) must give exactly O1's probe
+    sets; the certification must succeed for almost every query (otherwise the
+    GEMM is not doing the work and every query falls back to fp64)."""
+    kw = dict(train_rows=32768, iters=4) if name.startswith("c2") else {}
+    c = case(oracle_mod, name, **kw)
+    idx = c.gpu_index()
+    Qd = _t(c.Q)
+    sample = np.arange(0, c.Q.shape[0], max(1, c.Q.shape[0] // 200))
+    for npb in nprobes:
+        idx.set_coarse_mode("exact")
+        pe = idx.search_debug(Qd, c.spec.k, npb, 2)["probes"].cpu().numpy()
+        idx.set_coarse_mode("tensor")
+        idx.certify_fallbacks(reset=True)
+        pt = idx.search_debug(Qd, c.spec.k, npb, 2)["probes"].cpu().numpy()
+        fb = idx.certify_fallbacks(reset=True)
+        assert np.array_equal(pe, pt)
+        assert fb <= max(2, 0.02 * c.Q.shape[0]), f"{fb} uncertified queries at nprobe {npb}"
+        po = oracle_mod.probe(c.Q[sample], c.cent, npb)
+        assert np.array_equal(pt[sample], po)
+    idx.set_coarse_mode("auto")

@@ -42,7 +42,10 @@ def test_library_is_sm100a(rb):
     out = subprocess.check_output(["cuobjdump", "--list-elf", rb.LIB_PATH]).decode()
     assert "sm_100a" in out
     sass = subprocess.check_output(["cuobjdump", "-sass", rb.LIB_PATH]).decode()
-    assert "HMMA" not in sass            # no legacy mma.sync path
+    assert not re.search(r"(?<![A-Z])HMMA", sass)   # no legacy mma.sync path
+    assert "UTCHMMA" in sass                       # tcgen05.mma (coarse TF32 GEMM)
+    assert "UTMALDG" in sass                       # TMA tensor loads
+    assert "LDTM" in sass                          # tcgen05.ld from TMEM
 
 
 def test_version_and_error_channel(rb):
