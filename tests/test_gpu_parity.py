@@ -164,10 +164,10 @@ def test_search_modes_single_and_strict(oracle_mod):
 
 def test_exhaustive_reduction_equals_exact_knn(oracle_mod):
     # nprobe = nlist, bigK >= n  ->  exact k-NN (BJ invariant)
-    c = case(oracle_mod, "c0s")
+    c = case(oracle_mod, "c0s", n=2000)
     idx = c.gpu_index()
     k = 5
-    rf = (c.X.shape[0] + k - 1) // k  # bigK >= n
+    rf = (c.X.shape[0] + k - 1) // k  # bigK >= n (bigK <= 2048 supported)
     g = gpu_search(idx, c.Q, k, c.spec.nlist, rf)
     gt, _ = oracle_mod.exact_knn(c.X, c.Q, k)
     assert np.array_equal(g["ids"], gt)
