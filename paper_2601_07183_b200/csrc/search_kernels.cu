@@ -564,7 +564,13 @@ rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStre
 // ---------------------------------------------------------------------------
 // K6 refine: delta = fp32( sum_t ((double)q_t - (double)x_t)^2 ) in ascending t
 // (O10), candidates ordered by the key (bits(delta) << 32 | id).
+// The bigK candidate rows are gathered coalesced (one warp per row, 128-B
+// segments) into a shared-memory tile of RT rows x RDC dims (odd row stride:
+// conflict-free column reads); each thread then extends its own row's serial
+// fp64 sum over the tile, so the summation order stays ascending in t.
 constexpr int RT = 128;
+constexpr int RDC = 128;           // dims per tile
+constexpr int RSTRIDE = RDC + 1;
 
 __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__ keys,
                                                     int64_t nq, int bigK, int npow, int k,
@@ -575,40 +581,60 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
   extern __shared__ __align__(16) unsigned char sm[];
   uint64_t* rk = reinterpret_cast<uint64_t*>(sm);
   double* qs = reinterpret_cast<double*>(sm + (size_t)npow * 8);
+  float* tile = reinterpret_cast<float*>(sm + (size_t)npow * 8 + (size_t)d * 8);
+  uint32_t* rows = reinterpret_cast<uint32_t*>(tile + RT * RSTRIDE);
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
-    for (int t = threadIdx.x; t < d; t += RT) qs[t] = (double)queries[q * d + t];
-    __syncthreads();
-    for (int c = threadIdx.x; c < npow; c += RT) {
-      uint64_t out = kKeyInf;
+    for (int t = tid; t < d; t += RT) qs[t] = (double)queries[q * d + t];
+    for (int c0 = 0; c0 < npow; c0 += RT) {
+      const int c = c0 + tid;
       const uint64_t key = (c < bigK) ? keys[q * bigK + c] : kKeyInf;
-      if (key != kKeyInf) {
-        const uint32_t gid = (uint32_t)(key & 0xFFFFFFFFu);
-        const float* x = X + (int64_t)(gid / (uint32_t)G) * d;
-        double acc = 0.0;
-        if ((d & 3) == 0) {
-          const float4* x4 = reinterpret_cast<const float4*>(x);
-          for (int t4 = 0; t4 < (d >> 2); ++t4) {
-            const float4 v = __ldg(x4 + t4);
-            double df;
-            df = __dsub_rn(qs[4 * t4 + 0], (double)v.x); acc = __dadd_rn(acc, __dmul_rn(df, df));
-            df = __dsub_rn(qs[4 * t4 + 1], (double)v.y); acc = __dadd_rn(acc, __dmul_rn(df, df));
-            df = __dsub_rn(qs[4 * t4 + 2], (double)v.z); acc = __dadd_rn(acc, __dmul_rn(df, df));
-            df = __dsub_rn(qs[4 * t4 + 3], (double)v.w); acc = __dadd_rn(acc, __dmul_rn(df, df));
+      const uint32_t gid = (uint32_t)(key & 0xFFFFFFFFu);
+      rows[tid] = (key != kKeyInf) ? gid / (uint32_t)G : 0xFFFFFFFFu;
+      __syncthreads();
+      double acc = 0.0;
+      for (int t0 = 0; t0 < d; t0 += RDC) {
+        const int dc = min(RDC, d - t0);
+        // warp w gathers rows [32w, 32w+32): 8 rows x 4 coalesced 128-B loads in
+        // flight per lane before the shared-memory stores
+        for (int rb = 0; rb < 32; rb += 8) {
+          float v[8][RDC / 32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t row = rows[warp * 32 + rb + i];
+            const float* src = X + (size_t)(row == 0xFFFFFFFFu ? 0u : row) * d + t0;
+#pragma unroll
+            for (int j = 0; j < RDC / 32; ++j) {
+              const int t = lane + 32 * j;
+              v[i][j] = (row != 0xFFFFFFFFu && t < dc) ? __ldg(src + t) : 0.0f;
+            }
           }
-        } else {
-          for (int t = 0; t < d; ++t) {
-            double df = __dsub_rn(qs[t], (double)__ldg(x + t));
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < RDC / 32; ++j)
+              tile[(warp * 32 + rb + i) * RSTRIDE + lane + 32 * j] = v[i][j];
+        }
+        __syncthreads();
+        if (key != kKeyInf) {
+          const float* myrow = tile + tid * RSTRIDE;
+          for (int t = 0; t < dc; ++t) {
+            double df = __dsub_rn(qs[t0 + t], (double)myrow[t]);
             acc = __dadd_rn(acc, __dmul_rn(df, df));
           }
         }
+        __syncthreads();
+      }
+      uint64_t out = kKeyInf;
+      if (key != kKeyInf) {
         const float dist = __double2float_rn(acc);
         out = ((uint64_t)__float_as_uint(dist) << 32) | gid;
       }
-      rk[c] = out;
+      if (c < npow) rk[c] = out;
     }
     __syncthreads();
     cta_bitonic_sort_u64(rk, npow);
-    for (int i = threadIdx.x; i < k; i += RT) {
+    for (int i = tid; i < k; i += RT) {
       const uint64_t v = (i < npow) ? rk[i] : kKeyInf;
       if (v != kKeyInf) {
         out_ids[q * k + i] = (int64_t)(uint32_t)(v & 0xFFFFFFFFu);
@@ -626,7 +652,7 @@ rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaSt
   if (a.nq <= 0) return RAIRS_OK;
   const int bigK = a.k * a.refine_factor;
   const int npow = next_pow2(std::max(bigK, 2));
-  const size_t smem = (size_t)npow * 8 + (size_t)idx->d * 8;
+  const size_t smem = (size_t)npow * 8 + (size_t)idx->d * 8 + (size_t)RT * RSTRIDE * 4 + RT * 4;
   if (smem > 220 * 1024) {
     set_error("refine: shared memory budget exceeded");
     return RAIRS_E_UNSUPPORTED;

@@ -33,11 +33,17 @@ def gather_shard_results(ids: torch.Tensor, dists: torch.Tensor,
     """[nq, k] per rank -> [G, nq, k] on every rank (one all_gather each)."""
     G = dist.get_world_size(group)
     nq, k = ids.shape
-    all_ids = torch.empty((G, nq, k), dtype=ids.dtype, device=ids.device)
-    all_d = torch.empty((G, nq, k), dtype=dists.dtype, device=dists.device)
-    dist.all_gather_into_tensor(all_ids, ids.contiguous(), group=group)
-    dist.all_gather_into_tensor(all_d, dists.contiguous(), group=group)
-    return all_ids, all_d
+    if dist.get_backend(group) == "nccl":
+        all_ids = torch.empty((G, nq, k), dtype=ids.dtype, device=ids.device)
+        all_d = torch.empty((G, nq, k), dtype=dists.dtype, device=dists.device)
+        dist.all_gather_into_tensor(all_ids, ids.contiguous(), group=group)
+        dist.all_gather_into_tensor(all_d, dists.contiguous(), group=group)
+        return all_ids, all_d
+    li = [torch.empty_like(ids) for _ in range(G)]
+    ld = [torch.empty_like(dists) for _ in range(G)]
+    dist.all_gather(li, ids.contiguous(), group=group)
+    dist.all_gather(ld, dists.contiguous(), group=group)
+    return torch.stack(li), torch.stack(ld)
 
 
 class ShardedIndex:
