@@ -148,8 +148,9 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   ev.mark(0);
   // coarse: P(q) = first nprobe lists by (D64, l)  (O1).  Tensor-core TF32
   // filter + exact fp64 certify (K1/K2), or the exact fp64 kernel directly.
-  if (coarse_gemm_supported(idx, nprobe)) {
-    st = launch_coarse(idx, queries, nq, nprobe, probes, idx->certify_fallbacks, s);
+  if (coarse_fused_ok(idx, nprobe)) {
+    st = launch_coarse_fused(idx, queries, nq, nprobe, 0, 0.0, 0, probes, nullptr, nullptr,
+                             idx->certify_fallbacks, s);
   } else {
     ProbeArgs pa{};
     pa.X = queries;
@@ -276,6 +277,10 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   B_TRY(cudaMemcpyAsync(idx->centroids, centroids, (size_t)p->nlist * d * 4, cudaMemcpyDeviceToDevice, s));
   B_TRY(cudaMemcpyAsync(idx->codebook, codebook, cb_bytes, cudaMemcpyDeviceToDevice, s));
   B_TRY(cudaMemcpyAsync(idx->X, base, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, s));
+  st = coarse_prepare(idx, s);
+  if (st != RAIRS_OK) return fail(st);
+  B_TRY(cudaMalloc(&idx->certify_fallbacks, sizeof(unsigned)));
+  B_TRY(cudaMemsetAsync(idx->certify_fallbacks, 0, sizeof(unsigned), s));
   // Alg. 3 RairAssign (AIR) or single assignment, exact fp64 (O4)
   ProbeArgs pa{};
   pa.X = idx->X;
@@ -294,15 +299,21 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   }
   pa.l1 = idx->l1;
   pa.l2 = idx->l2;
-  st = launch_probe_exact(pa, s);
+  if (coarse_fused_ok(idx, pa.L) && idx->nlist > 256) {
+    // tensor-core filter + certified fp64 assignment (same result as the exact kernel)
+    unsigned* fb = nullptr;
+    B_TRY(cudaMallocAsync(&fb, sizeof(unsigned), s));
+    B_TRY(cudaMemsetAsync(fb, 0, sizeof(unsigned), s));
+    st = launch_coarse_fused(idx, idx->X, n, pa.L, pa.mode, pa.lambda, pa.strict, nullptr, idx->l1,
+                             idx->l2, fb, s);
+    cudaFreeAsync(fb, s);
+  } else {
+    st = launch_probe_exact(pa, s);
+  }
   if (st != RAIRS_OK) return fail(st);
   // Alg. 4 SeilInsert (cell-major) + PQ encoding (O5) into the packed layout
   st = build_layout(idx, s);
   if (st != RAIRS_OK) return fail(st);
-  st = coarse_prepare(idx, s);
-  if (st != RAIRS_OK) return fail(st);
-  B_TRY(cudaMalloc(&idx->certify_fallbacks, sizeof(unsigned)));
-  B_TRY(cudaMemsetAsync(idx->certify_fallbacks, 0, sizeof(unsigned), s));
   B_TRY(cudaStreamSynchronize(s));
 #undef B_TRY
   *out = idx;

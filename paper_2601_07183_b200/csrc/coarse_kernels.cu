@@ -1,216 +1,298 @@
 // coarse_kernels.cu -- K1/K2: the coarse quantizer on sm_100a tensor cores.
 //
-// K1  G[q][l] = ||c_l||^2 - 2 q.c_l   (FindNearestLists; exhaustive
-//     O(nlist*D) per query P:1216; bulk per batch P:1862-1864), as a
+// K1  g[r][l] = ||c_l||^2 - 2 x_r.c_l  for every row r (a query, or a base
+//     vector at build time) and every list l (FindNearestLists, P:942;
+//     exhaustive O(nlist*D) P:1216; bulk per batch P:1862-1864), as a
 //     hand-written tcgen05.mma kind::tf32 GEMM: operands streamed by TMA
-//     (cp.async.bulk.tensor, 128B swizzle) into a 3-stage shared-memory ring,
-//     one elected thread issues the MMAs, the fp32 accumulator lives in TMEM
-//     (128 lanes x 256 columns) and the epilogue reads it with tcgen05.ld.
-// K2  per query: the first W = nprobe + delta lists by G, their exact fp64
-//     distances D64 (O1), re-rank by (D64, l), and CERTIFY (reading R6): every
-//     list outside the candidate set has G >= G_(W+1), and the TF32 error of G
-//     is bounded by E, so if G_(W+1) - E exceeds the nprobe-th exact distance
-//     (minus ||q||^2) no excluded list can enter the probe set.  Otherwise the
-//     query is flagged and recomputed by the exact fp64 kernel.  The probe set
-//     is therefore always exactly O1's.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
+//     (cp.async.bulk.tensor, 128B swizzle) through a shared-memory ring, one
+//     elected thread issues the MMAs into a double-buffered fp32 accumulator in
+//     TMEM (2 x 128 lanes x 256 columns), and four epilogue warps drain it with
+//     tcgen05.ld while keeping each row's W+1 smallest g in shared memory --
+//     the [rows x nlist] matrix is never written to HBM.
+// K2  per row: merge the split lists, exact fp64 distances D64 (O1) of the W
+//     best, re-rank by (D64, l), and CERTIFY (reading R6): every list outside
+//     the candidate set has g >= g_(W+1) and |g - (D - ||x||^2)| <= E, so if
+//     g_(W+1) - E exceeds the L-th exact distance minus ||x||^2, no excluded
+//     list can enter the first L.  Uncertified rows are recomputed by the exact
+//     fp64 kernel.  Output: probe sets (search), or the RAIR pair (Alg. 3) /
+//     single assignment (build).  Results are always exactly O1 / O4.
 #include <algorithm>
 #include <mutex>
 
 #include "index.cuh"
+#include "tc_helpers.cuh"
 
 namespace rairs {
 
-constexpr int CG_BM = 128, CG_BN = 256, CG_BK = 32, CG_S = 3;
-constexpr uint32_t CG_A_BYTES = CG_BM * CG_BK * 4;   // 16 KB
-constexpr uint32_t CG_B_BYTES = CG_BN * CG_BK * 4;   // 32 KB
-constexpr int CG_THREADS = 128;
-constexpr size_t CG_SMEM = 1024 + CG_S * (CG_A_BYTES + CG_B_BYTES) + 256 + CG_BN * 4;
-
+constexpr int FT_BM = 128, FT_BN = 256, FT_BK = 32;
+constexpr uint32_t FT_A_BYTES = FT_BM * FT_BK * 4;  // 16 KB
+constexpr uint32_t FT_B_BYTES = FT_BN * FT_BK * 4;  // 32 KB
+constexpr int FT_EPI_WARPS = 8;  // warps 0-7 epilogue: lane group w%4, column half w/4
+constexpr int FT_PROD_WARP = FT_EPI_WARPS, FT_MMA_WARP = FT_EPI_WARPS + 1;
+constexpr int FT_THREADS = (FT_EPI_WARPS + 2) * 32;
+constexpr int FT_HALVES = FT_EPI_WARPS / 4;
+constexpr int FT_MAX_WP1 = 112;  // smem: lists + staging + 2-3 operand stages <= 227 KB
 // instruction descriptor: D=F32, A=B=TF32, both K-major, N=256, M=128
-constexpr uint32_t CG_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(CG_BN >> 3) << 17) |
-                              ((uint32_t)(CG_BM >> 4) << 24);
+constexpr uint32_t FT_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(FT_BN >> 3) << 17) |
+                              ((uint32_t)(FT_BM >> 4) << 24);
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  while (!mbar_try_wait(bar, phase)) {
+struct TopWArgs {
+  int64_t rows;
+  int nl, d, Wp1, nsplit, tiles_per_split, ntiles, nstage;
+  const float* cnorm;  // [round_up(nl, 256)], +inf padding
+  // output entries per (row, split): 32 on the register path (sorted), Wp1
+  // on the shared-memory path (unsorted)
+  float* out_v;        // [rows][nsplit][Wout]
+  uint32_t* out_i;
+};
+
+// Per-row candidate list: W+1 slots, UNSORTED, with the running maximum kept in
+// registers.  A value below the maximum replaces it and the maximum is
+// recomputed (the same fixed-length scan in every lane of the warp, so a
+// replacement costs W+1 steps without divergence -- an insertion sort costs up
+// to W+1 divergent shifts per value).  Ties at the boundary may keep either
+// entry: the certificate only needs every excluded list to have g >= g_(W+1).
+__device__ __forceinline__ void topw_rescan(const float* lv, int Wp1, int r, float& mx, int& mp) {
+  mx = -__int_as_float(0x7f800000);
+  mp = 0;
+  for (int i0 = 0; i0 < Wp1; i0 += 8) {  // 8 independent loads in flight
+    float x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (i0 + k < Wp1) ? lv[(i0 + k) * FT_BM + r] : mx;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (x[k] > mx) { mx = x[k]; mp = i0 + k; }
   }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-// K-major operand tile, 128-byte swizzle, 8-row groups 1024 B apart (SBO).
-__device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
-  const uint64_t addr = smem_u32(p);
-  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         (1ull << 46) | (2ull << 61);
-}
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
-__global__ void __launch_bounds__(CG_THREADS, 1)
-    coarse_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
-                            const __grid_constant__ CUtensorMap tmB, const float* __restrict__ cnorm,
-                            int nq, int nlist, int d, float* __restrict__ G, int ldg) {
+template <int KR>
+__global__ void __launch_bounds__(FT_THREADS, 1)
+    coarse_topw_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB, TopWArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
+  const int S = a.nstage, Wp1 = a.Wp1;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + CG_S * CG_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + CG_S * CG_B_BYTES);
-  uint64_t* empty = full + CG_S;
-  uint64_t* done = empty + CG_S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  float* cn = reinterpret_cast<float*>(smem + CG_S * (CG_A_BYTES + CG_B_BYTES) + 256);
+  uint8_t* sB = smem + S * FT_A_BYTES;
+  float* lv = reinterpret_cast<float*>(sB + S * FT_B_BYTES);  // smem path only
+  uint32_t* li = reinterpret_cast<uint32_t*>(lv + (KR > 0 ? 0 : Wp1 * FT_BM));
+  float* gbuf = reinterpret_cast<float*>(li + (KR > 0 ? 0 : Wp1 * FT_BM));  // [32][128] staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(gbuf + 32 * FT_BM);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * CG_BM, n0 = blockIdx.y * CG_BN;
-  const int nk = (d + CG_BK - 1) / CG_BK;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * FT_BM;
+  const int split = blockIdx.y;
+  const int t_begin = split * a.tiles_per_split;
+  const int ntile = min(a.ntiles, t_begin + a.tiles_per_split) - t_begin;
+  const int nk = (a.d + FT_BK - 1) / FT_BK;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < CG_S; ++s) {
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&tfull[k], 1);
+      mbar_init(&tempty[k], FT_EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int j = threadIdx.x; j < CG_BN; j += CG_THREADS)
-    cn[j] = (n0 + j < nlist) ? cnorm[n0 + j] : 0.0f;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(CG_BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  if (KR == 0 && warp < 4) {  // smem path: column half 0 only (see launcher)
+    for (int i = 0; i < Wp1; ++i) {
+      lv[i * FT_BM + tid] = __int_as_float(0x7f800000);
+      li[i * FT_BM + tid] = 0xFFFFFFFFu;
+    }
   }
+  if (warp == FT_MMA_WARP) tmem_alloc(tslot, 512);
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tslot;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      auto issue = [&](int kc) {
-        const int s = kc % CG_S;
-        mbar_expect_tx(&full[s], CG_A_BYTES + CG_B_BYTES);
-        tma_load_2d(sA + s * CG_A_BYTES, &tmA, kc * CG_BK, m0, &full[s]);
-        tma_load_2d(sB + s * CG_B_BYTES, &tmB, kc * CG_BK, n0, &full[s]);
-      };
-      for (int kc = 0; kc < nk && kc < CG_S; ++kc) issue(kc);
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % CG_S;
-        const uint32_t ph = (uint32_t)(kc / CG_S) & 1u;
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        const uint64_t ad = umma_desc_sw128(sA + s * CG_A_BYTES);
-        const uint64_t bd = umma_desc_sw128(sB + s * CG_B_BYTES);
-#pragma unroll
-        for (int k = 0; k < CG_BK / 8; ++k)  // K = 8 tf32 per MMA = 32 B = +2 desc units
-          umma_tf32(tmem, ad + 2 * k, bd + 2 * k, CG_IDESC, (kc | k) != 0 ? 1u : 0u);
-        umma_commit(&empty[s]);
-        if (kc + CG_S < nk) {
-          mbar_wait(&empty[s], ph);
-          issue(kc + CG_S);
+  if (warp == FT_PROD_WARP) {
+    if (lane == 0 && ntile > 0) {  // TMA producer
+      int it = 0;
+      for (int t = 0; t < ntile; ++t) {
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (uint32_t)(it / S) & 1u;
+          if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
+          mbar_expect_tx(&full[s], FT_A_BYTES + FT_B_BYTES);
+          tma_load_2d(sA + s * FT_A_BYTES, &tmA, kc * FT_BK, (int)m0, &full[s]);
+          tma_load_2d(sB + s * FT_B_BYTES, &tmB, kc * FT_BK, (t_begin + t) * FT_BN, &full[s]);
         }
       }
-      umma_commit(done);
     }
     __syncwarp();
-  }
-  mbar_wait(done, 0);
-  tc_fence_after();
-
-  const int row = warp * 32 + lane;
-  const int q = m0 + row;
-  for (int c = 0; c < CG_BN / 32; ++c) {
-    uint32_t v[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32), v);
-    if (q < nq) {
-      float* out = G + (size_t)q * ldg + n0 + c * 32;
-      const int lim = nlist - (n0 + c * 32);
-      if (lim >= 32 && (ldg & 3) == 0) {
+  } else if (warp == FT_MMA_WARP) {
+    if (lane == 0 && ntile > 0) {  // MMA issuer
+      int it = 0;
+      for (int t = 0; t < ntile; ++t) {
+        const int acc = t & 1;
+        const uint32_t aph = (uint32_t)(t >> 1) & 1u;
+        if (t >= 2) mbar_wait(&tempty[acc], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t dt = tmem + (uint32_t)(acc * FT_BN);
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (uint32_t)(it / S) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(sA + s * FT_A_BYTES);
+          const uint64_t bd = umma_desc_sw128(sB + s * FT_B_BYTES);
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 o;
-          o.x = cn[c * 32 + j + 0] - 2.0f * __uint_as_float(v[j + 0]);
-          o.y = cn[c * 32 + j + 1] - 2.0f * __uint_as_float(v[j + 1]);
-          o.z = cn[c * 32 + j + 2] - 2.0f * __uint_as_float(v[j + 2]);
-          o.w = cn[c * 32 + j + 3] - 2.0f * __uint_as_float(v[j + 3]);
-          *reinterpret_cast<float4*>(out + j) = o;
+          for (int k = 0; k < FT_BK / 8; ++k)  // K = 8 tf32 per MMA = 32 B = +2 desc units
+            umma_tf32(dt, ad + 2 * k, bd + 2 * k, FT_IDESC, (kc | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[s]);
         }
-      } else {
+        umma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (KR > 0) {
+    const int lg = warp & 3, half = warp >> 2;   // TMEM lane group, column half
+    const int rrow = lg * 32 + lane;             // row within the tile
+    // epilogue, register path: each row's KR smallest (g, l) kept SORTED in
+    // registers; an insertion computes every slot in parallel from the old
+    // values (new[i] = old[i-1] > g ? old[i-1] : min(old[i], g)), so it has no
+    // dependency chain and no shared-memory round trip.
+    float rv[KR > 0 ? KR : 1];
+    uint32_t ri[KR > 0 ? KR : 1];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < lim) out[j] = cn[c * 32 + j] - 2.0f * __uint_as_float(v[j]);
+    for (int i = 0; i < KR; ++i) {
+      rv[i] = __int_as_float(0x7f800000);
+      ri[i] = 0xFFFFFFFFu;
+    }
+    for (int t = 0; t < ntile; ++t) {
+      const int acc = t & 1;
+      const uint32_t aph = (uint32_t)(t >> 1) & 1u;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int col0 = (t_begin + t) * FT_BN;
+      for (int c = half * (FT_BN / 32 / FT_HALVES); c < (half + 1) * (FT_BN / 32 / FT_HALVES); ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * FT_BN + c * 32), v);
+        uint32_t pass = 0;
+        const float thr = rv[KR - 1];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float g = __ldg(a.cnorm + col0 + c * 32 + j) - 2.0f * __uint_as_float(v[j]);
+          gbuf[j * (FT_BM * FT_HALVES) + warp * 32 + lane] = g;
+          if (g < thr) pass |= 1u << j;
+        }
+        while (__any_sync(0xffffffffu, pass != 0)) {
+          if (pass != 0) {
+            const int j = __ffs(pass) - 1;
+            pass &= pass - 1;
+            const float g = gbuf[j * (FT_BM * FT_HALVES) + warp * 32 + lane];
+            if (g < rv[KR - 1]) {
+              const uint32_t l = (uint32_t)(col0 + c * 32 + j);
+#pragma unroll
+              for (int i = KR - 1; i > 0; --i) {
+                const bool sh = rv[i - 1] > g;
+                const bool here = !sh && rv[i] > g;
+                ri[i] = sh ? ri[i - 1] : (here ? l : ri[i]);
+                rv[i] = sh ? rv[i - 1] : (here ? g : rv[i]);
+              }
+              if (rv[0] > g) { rv[0] = g; ri[0] = l; }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    const int64_t row = m0 + rrow;
+    if (row < a.rows) {
+      float* ov = a.out_v + ((row * a.nsplit + split) * FT_HALVES + half) * KR;
+      uint32_t* oi = a.out_i + ((row * a.nsplit + split) * FT_HALVES + half) * KR;
+#pragma unroll
+      for (int i = 0; i < KR; ++i) {
+        ov[i] = rv[i];
+        oi[i] = ri[i];
+      }
+    }
+  } else if (warp >= 4) {  // shared-memory path: warps 4-7 only release the accumulators
+    for (int t = 0; t < ntile; ++t) {
+      mbar_wait(&tfull[t & 1], (uint32_t)(t >> 1) & 1u);
+      tc_fence_after();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[t & 1]);
+    }
+  } else {  // epilogue, shared-memory path (large W): unsorted list + running max
+    float thr = __int_as_float(0x7f800000);
+    int thr_pos = 0, filled = 0;
+
+    for (int t = 0; t < ntile; ++t) {
+      const int acc = t & 1;
+      const uint32_t aph = (uint32_t)(t >> 1) & 1u;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int col0 = (t_begin + t) * FT_BN;
+      for (int c = 0; c < FT_BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * FT_BN + c * 32), v);
+        uint32_t pass = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float g = __ldg(a.cnorm + col0 + c * 32 + j) - 2.0f * __uint_as_float(v[j]);
+          gbuf[j * FT_BM + tid] = g;
+          if (g < thr) pass |= 1u << j;
+        }
+        // each lane walks only its own passing values
+        while (__any_sync(0xffffffffu, pass != 0)) {
+          if (pass != 0) {
+            const int j = __ffs(pass) - 1;
+            pass &= pass - 1;
+            const float g = gbuf[j * FT_BM + tid];
+            if (g < thr) {
+              const int pos = (filled < Wp1) ? filled++ : thr_pos;
+              lv[pos * FT_BM + tid] = g;
+              li[pos * FT_BM + tid] = (uint32_t)(col0 + c * 32 + j);
+              if (filled == Wp1) topw_rescan(lv, Wp1, tid, thr, thr_pos);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    const int64_t row = m0 + tid;
+    if (row < a.rows) {
+      float* ov = a.out_v + (row * a.nsplit + split) * Wp1;
+      uint32_t* oi = a.out_i + (row * a.nsplit + split) * Wp1;
+      for (int i = 0; i < Wp1; ++i) {
+        ov[i] = lv[i * FT_BM + tid];
+        oi[i] = li[i * FT_BM + tid];
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CG_BN));
+  if (warp == FT_MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
 }
 
 // ---------------------------------------------------------------------------
-// K2: select W candidates by G, exact fp64 re-rank, certify.
-constexpr int SEL_THREADS = 256;
-constexpr int SEL_WARPS = SEL_THREADS / 32;
+// K2: merge splits, exact fp64 re-rank, certify, emit probes / assignment.
+constexpr int CT_THREADS = 256;
+constexpr int CT_WARPS = CT_THREADS / 32;
 
 __device__ __forceinline__ uint32_t ord_f32(float f) {
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
 __device__ void warp_sort_u64(uint64_t* a, int n) {
@@ -247,102 +329,71 @@ __device__ void warp_sort_pairs2(uint64_t* k, uint32_t* id, int n) {
   }
 }
 
-__device__ __forceinline__ float unord_f32(uint32_t o) {
-  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
-}
+struct CertArgs {
+  const float* vals;
+  const uint32_t* ids;
+  int S, Wp1, Wout;
+  const float* X;
+  int64_t rows;
+  int d;
+  const float* C;
+  int nl, L, mode;  // mode 0 probes, 1 AIR pair, 2 single
+  double lambda;
+  int strict;
+  double cmax;
+  int npow_c, npow_w;
+  int32_t* out_idx;
+  int32_t* l1;
+  int32_t* l2;
+  int32_t* flags;
+  unsigned* nflag;
+};
 
-// One warp per query.  The W+1 smallest G values are isolated with a 256-bin
-// histogram over [min G, max G] (the bin map is monotone in G, so the bins up
-// to the first bin whose cumulative count reaches W+1 hold every one of the
-// W+1 smallest), then only those survivors are sorted by (G, l).
-__global__ void __launch_bounds__(SEL_THREADS)
-    coarse_select_kernel(const float* __restrict__ G, int ldg, const float* __restrict__ Q,
-                         const float* __restrict__ C, int64_t nq, int nlist, int d, int nprobe,
-                         int W, int npow_l, int npow_w, double cmax, int32_t* __restrict__ probes,
-                         int32_t* __restrict__ flags, unsigned* __restrict__ nflag) {
+__global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
-  uint64_t* keys = reinterpret_cast<uint64_t*>(sm) + (size_t)warp * npow_l;
-  uint64_t* ck = reinterpret_cast<uint64_t*>(sm) + (size_t)SEL_WARPS * npow_l + (size_t)warp * npow_w;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm) + (size_t)warp * a.npow_c;
+  uint64_t* ck = reinterpret_cast<uint64_t*>(sm) + (size_t)CT_WARPS * a.npow_c + (size_t)warp * a.npow_w;
   uint32_t* ci = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm) +
-                                             (size_t)SEL_WARPS * (npow_l + npow_w)) +
-                 (size_t)warp * npow_w;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm) +
-                                               (size_t)SEL_WARPS * (npow_l + npow_w)) +
-                   (size_t)SEL_WARPS * npow_w + (size_t)warp * 256;
-  const bool all = W >= nlist;
-  const int need = all ? nlist : W + 1;
-  for (int64_t q = (int64_t)blockIdx.x * SEL_WARPS + warp; q < nq;
-       q += (int64_t)gridDim.x * SEL_WARPS) {
-    const float* g = G + (size_t)q * ldg;
-    float gmin = __int_as_float(0x7f800000), gmax = -gmin;
-    for (int l = lane; l < nlist; l += 32) {
-      const float v = g[l];
-      gmin = fminf(gmin, v);
-      gmax = fmaxf(gmax, v);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-      gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
-    }
-    const float scale = (gmax > gmin) ? 255.99f / (gmax - gmin) : 0.0f;
-    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
-    __syncwarp();
-    for (int l = lane; l < nlist; l += 32)
-      atomicAdd(&hist[min(255, (int)((g[l] - gmin) * scale))], 1u);
-    __syncwarp();
-    // first bin b with cumulative count >= need (8 bins per lane)
-    uint32_t h8[8], loc = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) { h8[i] = hist[lane * 8 + i]; loc += h8[i]; }
-    uint32_t inc = loc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    const unsigned hit = __ballot_sync(0xffffffffu, inc >= (uint32_t)need);
-    const int hl = __ffs(hit) - 1;
-    int b = 255;
-    if (lane == hl) {
-      uint32_t run = inc - loc;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        run += h8[i];
-        if (run >= (uint32_t)need) { b = lane * 8 + i; break; }
+                                             (size_t)CT_WARPS * (a.npow_c + a.npow_w)) +
+                 (size_t)warp * a.npow_w;
+  const int W = a.Wp1 - 1;
+  const bool all = W >= a.nl;
+  const int Wc = all ? a.nl : W;
+  const int tot = a.S * a.Wout;
+  for (int64_t r = (int64_t)blockIdx.x * CT_WARPS + warp; r < a.rows;
+       r += (int64_t)gridDim.x * CT_WARPS) {
+    for (int i = lane; i < a.npow_c; i += 32) {
+      uint64_t k = kKeyInf;
+      if (i < tot) {
+        const uint32_t id = a.ids[r * tot + i];
+        if (id != 0xFFFFFFFFu) k = ((uint64_t)ord_f32(a.vals[r * tot + i]) << 32) | id;
       }
+      keys[i] = k;
     }
-    b = __shfl_sync(0xffffffffu, b, hl);
-    // collect survivors as (ord(G) << 32 | l) keys
-    int cnt = 0;
-    for (int l0 = 0; l0 < nlist; l0 += 32) {
-      const int l = l0 + lane;
-      float v = 0.0f;
-      bool keep = false;
-      if (l < nlist) {
-        v = g[l];
-        keep = min(255, (int)((v - gmin) * scale)) <= b;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) keys[cnt + __popc(bal & ((1u << lane) - 1u))] = ((uint64_t)ord_f32(v) << 32) | (uint32_t)l;
-      cnt += __popc(bal);
-    }
-    int np = 2;
-    while (np < cnt) np <<= 1;
-    for (int i = cnt + lane; i < np; i += 32) keys[i] = kKeyInf;
     __syncwarp();
-    warp_sort_u64(keys, np);
-    const int Wc = all ? nlist : W;
+    warp_sort_u64(keys, a.npow_c);
     const float gnext = all ? 0.0f : unord_f32((uint32_t)(keys[W] >> 32));
-    // exact D64 of the candidates (O1)
-    const float* qv = Q + (size_t)q * d;
-    for (int i = lane; i < npow_w; i += 32) {
+    const float* xr = a.X + (size_t)r * a.d;
+    for (int i = lane; i < a.npow_w; i += 32) {
       if (i < Wc) {
         const uint32_t l = (uint32_t)(keys[i] & 0xFFFFFFFFu);
-        const float* c = C + (size_t)l * d;
+        const float* c = a.C + (size_t)l * a.d;
         double acc = 0.0;
-        for (int t = 0; t < d; ++t) acc = __dadd_rn(acc, dsq_diff(qv[t], c[t]));
+        if ((a.d & 3) == 0) {
+          const float4* c4 = reinterpret_cast<const float4*>(c);
+          const float4* x4 = reinterpret_cast<const float4*>(xr);
+#pragma unroll 4
+          for (int t4 = 0; t4 < (a.d >> 2); ++t4) {
+            const float4 cv = __ldg(c4 + t4), xv = __ldg(x4 + t4);
+            acc = __dadd_rn(acc, dsq_diff(xv.x, cv.x));
+            acc = __dadd_rn(acc, dsq_diff(xv.y, cv.y));
+            acc = __dadd_rn(acc, dsq_diff(xv.z, cv.z));
+            acc = __dadd_rn(acc, dsq_diff(xv.w, cv.w));
+          }
+        } else {
+          for (int t = 0; t < a.d; ++t) acc = __dadd_rn(acc, dsq_diff(xr[t], c[t]));
+        }
         ck[i] = dbits(acc);
         ci[i] = l;
       } else {
@@ -351,35 +402,75 @@ __global__ void __launch_bounds__(SEL_THREADS)
       }
     }
     __syncwarp();
-    warp_sort_pairs2(ck, ci, npow_w);
+    warp_sort_pairs2(ck, ci, a.npow_w);
     bool certified = all;
     if (!all) {
       double qn = 0.0;
-      for (int t = lane; t < d; t += 32) qn += (double)qv[t] * (double)qv[t];
+      for (int t = lane; t < a.d; t += 32) qn += (double)xr[t] * (double)xr[t];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) qn += __shfl_xor_sync(0xffffffffu, qn, o);
       const double qnorm = sqrt(qn);
-      const double E = (ldexp(1.0, -8) + d * ldexp(1.0, -22)) * qnorm * cmax +
-                       ldexp(1.0, -22) * (cmax * cmax + 2.0 * qnorm * cmax);
-      const double dnp = __longlong_as_double((long long)ck[nprobe - 1]);
-      certified = ((double)gnext - E) > (dnp - qn) + 1e-10 * (dnp + qn);
+      const double E = (ldexp(1.0, -8) + a.d * ldexp(1.0, -22)) * qnorm * a.cmax +
+                       ldexp(1.0, -22) * (a.cmax * a.cmax + 2.0 * qnorm * a.cmax);
+      const double dL = __longlong_as_double((long long)ck[a.L - 1]);
+      certified = ((double)gnext - E) > (dL - qn) + 1e-10 * (dL + qn);
     }
-    for (int i = lane; i < nprobe; i += 32) probes[q * nprobe + i] = (int32_t)ci[i];
+    if (a.mode == 0) {
+      for (int i = lane; i < a.L; i += 32) a.out_idx[r * a.L + i] = (int32_t)ci[i];
+    } else if (a.mode == 2) {
+      if (lane == 0) { a.l1[r] = (int32_t)ci[0]; a.l2[r] = (int32_t)ci[0]; }
+    } else {
+      // Alg. 3 lines 3-11 over the first L = N_CANDS exact lists (fp64, O4)
+      const int start = a.strict ? 1 : 0;
+      double loss = 0.0;
+      const bool ok = (lane >= start) && (lane < a.L);
+      if (ok) {
+        const float* c0 = a.C + (size_t)ci[0] * a.d;
+        const float* cj = a.C + (size_t)ci[lane] * a.d;
+        double ss = 0.0, ip = 0.0;
+        for (int t = 0; t < a.d; ++t) {
+          const double x = (double)xr[t];
+          const double r0t = __dsub_rn((double)c0[t], x);
+          const double rjt = __dsub_rn((double)cj[t], x);
+          ss = __dadd_rn(ss, __dmul_rn(rjt, rjt));
+          ip = __dadd_rn(ip, __dmul_rn(r0t, rjt));
+        }
+        loss = __dadd_rn(ss, __dmul_rn(a.lambda, ip));
+      }
+      int best = ok ? lane : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double l2v = __shfl_xor_sync(0xffffffffu, loss, o);
+        const int b2 = __shfl_xor_sync(0xffffffffu, best, o);
+        if (b2 != 0x7fffffff && (best == 0x7fffffff || l2v < loss || (l2v == loss && b2 < best))) {
+          loss = l2v;
+          best = b2;
+        }
+      }
+      if (lane == 0) {
+        const int c0 = (int)ci[0], cb = (int)ci[best];
+        a.l1[r] = min(c0, cb);
+        a.l2[r] = max(c0, cb);
+      }
+    }
     if (lane == 0) {
-      flags[q] = certified ? 0 : 1;
-      if (!certified) atomicAdd(nflag, 1u);
+      a.flags[r] = certified ? 0 : 1;
+      if (!certified) atomicAdd(a.nflag, 1u);
     }
     __syncwarp();
   }
 }
 
-__global__ void cnorm_kernel(const float* __restrict__ C, int nlist, int d, float* __restrict__ cn,
-                             double* __restrict__ cmax_out) {
-  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlist; l += gridDim.x * blockDim.x) {
+__global__ void cnorm_kernel(const float* __restrict__ C, int nlist, int npad, int d,
+                             float* __restrict__ cn, double* __restrict__ cmax_out) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < npad; l += gridDim.x * blockDim.x) {
+    if (l >= nlist) {
+      cn[l] = __int_as_float(0x7f800000);
+      continue;
+    }
     double s = 0.0;
     for (int t = 0; t < d; ++t) s += (double)C[(size_t)l * d + t] * (double)C[(size_t)l * d + t];
     cn[l] = (float)s;
-    // max of sqrt via atomicMax on the bit pattern of a non-negative double
     atomicMax(reinterpret_cast<unsigned long long*>(cmax_out),
               (unsigned long long)__double_as_longlong(sqrt(s)));
   }
@@ -400,12 +491,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static bool make_tmap(CUtensorMap* tm, const float* ptr, int64_t rows, int d, int box_rows) {
+bool tma_available() { return get_encode() != nullptr; }
+
+bool make_tmap_f32(CUtensorMap* tm, const float* ptr, int64_t rows, int d, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-  cuuint32_t box[2] = {(cuuint32_t)CG_BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)FT_BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -414,83 +507,167 @@ static bool make_tmap(CUtensorMap* tm, const float* ptr, int64_t rows, int d, in
 }
 
 rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s) {
-  RAIRS_CUDA_TRY(cudaMalloc(&idx->cnorm, (size_t)idx->nlist * 4));
+  const int npad = (int)round_up(idx->nlist, FT_BN);
+  RAIRS_CUDA_TRY(cudaMalloc(&idx->cnorm, (size_t)npad * 4));
   double* dmax = nullptr;
   RAIRS_CUDA_TRY(cudaMallocAsync(&dmax, 8, s));
   RAIRS_CUDA_TRY(cudaMemsetAsync(dmax, 0, 8, s));
-  cnorm_kernel<<<(idx->nlist + 255) / 256, 256, 0, s>>>(idx->centroids, idx->nlist, idx->d,
-                                                        idx->cnorm, dmax);
+  cnorm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(idx->centroids, idx->nlist, npad, idx->d,
+                                                  idx->cnorm, dmax);
   RAIRS_CHECK_LAUNCH();
   RAIRS_CUDA_TRY(cudaMemcpyAsync(&idx->cmax, dmax, 8, cudaMemcpyDeviceToHost, s));
   RAIRS_CUDA_TRY(cudaFreeAsync(dmax, s));
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
-  idx->device_bytes += (size_t)idx->nlist * 4;
+  idx->device_bytes += (size_t)npad * 4;
   return RAIRS_OK;
 }
 
-bool coarse_gemm_supported(const rairs_index_s* idx, int nprobe) {
-  if (idx->coarse_mode == 1) return false;       // forced exact
-  if ((idx->d & 3) != 0 || !get_encode()) return false;
-  if (idx->coarse_mode == 2) return true;        // forced tensor-core path
-  return idx->nlist >= 64 && nprobe < idx->nlist;
+static int coarse_width(int nl, int L) { return std::min(nl, L + 16 + L / 8); }
+
+bool coarse_fused_ok(const rairs_index_s* idx, int L) {
+  if (idx->coarse_mode == 1) return false;  // forced exact
+  if ((idx->d & 3) != 0 || !tma_available()) return false;
+  if (coarse_width(idx->nlist, L) + 1 > FT_MAX_WP1) return false;
+  if (idx->coarse_mode == 2) return true;   // forced tensor-core path
+  return idx->nlist >= 64 && L < idx->nlist;
 }
 
-rairs_status launch_coarse(const rairs_index_s* idx, const float* queries, int64_t nq, int nprobe,
-                           int32_t* probes, unsigned* nflag_dev, cudaStream_t s) {
-  const int nlist = idx->nlist, d = idx->d;
-  const int ldg = (int)round_up(nlist, 4);
-  const int delta = 16 + nprobe / 8;
-  const int W = std::min(nlist, nprobe + delta);
-  const int npow_l = next_pow2(std::max(nlist, 2));
-  const int npow_w = next_pow2(std::max(W, 2));
-  const size_t sel_smem = (size_t)SEL_WARPS * (npow_l * 8 + npow_w * 12 + 256 * 4);
-  if (sel_smem > 220 * 1024) {
-    set_error("coarse select: nlist too large for the materialised path");
+// Rows X[rows x d] against the index's centroids: the first L lists by
+// (D64, l), exactly, via K1 (tensor core) + K2 (certify) + exact fallback.
+rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64_t rows, int L,
+                                 int mode, double lambda, int strict, int32_t* out_idx,
+                                 int32_t* l1, int32_t* l2, unsigned* nflag, cudaStream_t s) {
+  if (rows <= 0) return RAIRS_OK;
+  const int nl = idx->nlist, d = idx->d;
+  const int W = coarse_width(nl, L);
+  const int Wp1 = W + 1;
+  if (Wp1 > FT_MAX_WP1) {
+    set_error("coarse: nprobe too large for the fused tensor-core path");
     return RAIRS_E_UNSUPPORTED;
   }
-  float* G = nullptr;
-  int32_t* flags = nullptr;
-  RAIRS_CUDA_TRY(cudaMallocAsync(&G, (size_t)nq * ldg * 4, s));
-  RAIRS_CUDA_TRY(cudaMallocAsync(&flags, (size_t)nq * 4, s));
-  CUtensorMap tmA, tmB;
-  if (!make_tmap(&tmA, queries, nq, d, CG_BM) || !make_tmap(&tmB, idx->centroids, nlist, d, CG_BN)) {
-    cudaFreeAsync(G, s);
-    cudaFreeAsync(flags, s);
-    set_error("cuTensorMapEncodeTiled failed");
-    return RAIRS_E_CUDA;
+  const int ntiles = (int)ceil_div(nl, FT_BN);
+  const bool reg = Wp1 <= 32;               // register-resident sorted lists
+  const int KR = Wp1 <= 16 ? 16 : (Wp1 <= 24 ? 24 : 32);
+  const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
+  const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
+  const int nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
+  if (1024 + (size_t)nstage * (FT_A_BYTES + FT_B_BYTES) + lists_bytes + 256 > 227 * 1024) {
+    set_error("coarse: shared memory budget exceeded");
+    return RAIRS_E_UNSUPPORTED;
   }
+  const size_t smem = 1024 + (size_t)nstage * (FT_A_BYTES + FT_B_BYTES) + lists_bytes +
+                      (2 * nstage + 4) * 8 + 16;
   static bool attr_set = false;
   if (!attr_set) {
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_gemm_tf32_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG_SMEM));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<0>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<24>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<32>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  dim3 grid((unsigned)ceil_div(nq, CG_BM), (unsigned)ceil_div(nlist, CG_BN));
-  coarse_gemm_tf32_kernel<<<grid, CG_THREADS, CG_SMEM, s>>>(tmA, tmB, idx->cnorm, (int)nq, nlist, d,
-                                                            G, ldg);
-  RAIRS_CHECK_LAUNCH();
-  RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_select_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
-  const int sgrid = (int)std::min<int64_t>(ceil_div(nq, SEL_WARPS), 148 * 16);
-  coarse_select_kernel<<<sgrid, SEL_THREADS, sel_smem, s>>>(G, ldg, queries, idx->centroids, nq,
-                                                            nlist, d, nprobe, W, npow_l, npow_w,
-                                                            idx->cmax, probes, flags, nflag_dev);
-  RAIRS_CHECK_LAUNCH();
-  // exact fp64 recomputation of the (rare) uncertified queries
-  ProbeArgs pa{};
-  pa.X = queries;
-  pa.rows = nq;
-  pa.d = d;
-  pa.C = idx->centroids;
-  pa.nl = nlist;
-  pa.L = nprobe;
-  pa.mode = 0;
-  pa.out_idx = probes;
-  pa.only_flagged = flags;
-  rairs_status st = launch_probe_exact(pa, s);
-  cudaFreeAsync(G, s);
-  cudaFreeAsync(flags, s);
-  return st;
+  const int64_t CH = 1 << 21;  // rows per chunk (bounds the candidate buffers)
+  const int npow_w = next_pow2(std::max(W, 2));
+  for (int64_t r0 = 0; r0 < rows; r0 += CH) {
+    const int64_t nr = std::min<int64_t>(CH, rows - r0);
+    const int64_t mtiles = ceil_div(nr, FT_BM);
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148, mtiles)));
+    const int tps = (int)ceil_div(ntiles, nsplit);
+    nsplit = (int)ceil_div(ntiles, tps);
+    const int npow_c = next_pow2(std::max(nsplit * Wout, 2));
+    const size_t csmem = (size_t)CT_WARPS * ((size_t)npow_c * 8 + (size_t)npow_w * 12);
+    if (csmem > 220 * 1024) {
+      set_error("coarse certify: shared memory budget exceeded");
+      return RAIRS_E_UNSUPPORTED;
+    }
+    float* vals = nullptr;
+    uint32_t* ids = nullptr;
+    int32_t* flags = nullptr;
+    RAIRS_CUDA_TRY(cudaMallocAsync(&vals, (size_t)nr * nsplit * Wout * 4, s));
+    RAIRS_CUDA_TRY(cudaMallocAsync(&ids, (size_t)nr * nsplit * Wout * 4, s));
+    RAIRS_CUDA_TRY(cudaMallocAsync(&flags, (size_t)nr * 4, s));
+    const float* Xc = X + (size_t)r0 * d;
+    CUtensorMap tmA, tmB;
+    if (!make_tmap_f32(&tmA, Xc, nr, d, FT_BM) || !make_tmap_f32(&tmB, idx->centroids, nl, d, FT_BN)) {
+      cudaFreeAsync(vals, s); cudaFreeAsync(ids, s); cudaFreeAsync(flags, s);
+      set_error("cuTensorMapEncodeTiled failed");
+      return RAIRS_E_CUDA;
+    }
+    TopWArgs ta{};
+    ta.rows = nr;
+    ta.nl = nl;
+    ta.d = d;
+    ta.Wp1 = Wp1;
+    ta.nsplit = nsplit;
+    ta.tiles_per_split = tps;
+    ta.ntiles = ntiles;
+    ta.nstage = nstage;
+    ta.cnorm = idx->cnorm;
+    ta.out_v = vals;
+    ta.out_i = ids;
+    const dim3 tgrid((unsigned)mtiles, (unsigned)nsplit);
+    if (reg && KR == 16)
+      coarse_topw_kernel<16><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    else if (reg && KR == 24)
+      coarse_topw_kernel<24><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    else if (reg)
+      coarse_topw_kernel<32><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    else
+      coarse_topw_kernel<0><<<dim3((unsigned)mtiles, (unsigned)nsplit), FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    RAIRS_CHECK_LAUNCH();
+    CertArgs ca{};
+    ca.vals = vals;
+    ca.ids = ids;
+    ca.S = nsplit;
+    ca.Wp1 = Wp1;
+    ca.Wout = Wout;
+    ca.X = Xc;
+    ca.rows = nr;
+    ca.d = d;
+    ca.C = idx->centroids;
+    ca.nl = nl;
+    ca.L = L;
+    ca.mode = mode;
+    ca.lambda = lambda;
+    ca.strict = strict;
+    ca.cmax = idx->cmax;
+    ca.npow_c = npow_c;
+    ca.npow_w = npow_w;
+    ca.out_idx = out_idx ? out_idx + r0 * L : nullptr;
+    ca.l1 = l1 ? l1 + r0 : nullptr;
+    ca.l2 = l2 ? l2 + r0 : nullptr;
+    ca.flags = flags;
+    ca.nflag = nflag;
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_certify_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+    const int cgrid = (int)std::min<int64_t>(ceil_div(nr, CT_WARPS), 148 * 16);
+    coarse_certify_kernel<<<cgrid, CT_THREADS, csmem, s>>>(ca);
+    RAIRS_CHECK_LAUNCH();
+    // exact fp64 recomputation of the (rare) uncertified rows
+    ProbeArgs pa{};
+    pa.X = Xc;
+    pa.rows = nr;
+    pa.d = d;
+    pa.C = idx->centroids;
+    pa.nl = nl;
+    pa.L = L;
+    pa.mode = mode;
+    pa.lambda = lambda;
+    pa.strict = strict;
+    pa.out_idx = ca.out_idx;
+    pa.l1 = ca.l1;
+    pa.l2 = ca.l2;
+    pa.only_flagged = flags;
+    rairs_status st = launch_probe_exact(pa, s);
+    cudaFreeAsync(vals, s);
+    cudaFreeAsync(ids, s);
+    cudaFreeAsync(flags, s);
+    if (st != RAIRS_OK) return st;
+  }
+  return RAIRS_OK;
 }
 
 }  // namespace rairs

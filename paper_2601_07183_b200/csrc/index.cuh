@@ -88,9 +88,12 @@ rairs_status export_layout64(const rairs_index_s* idx, int64_t* own_off, int64_t
 
 // ---- coarse stage (coarse_kernels.cu) ---------------------------------------
 rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s);
-bool coarse_gemm_supported(const rairs_index_s* idx, int nprobe);
-rairs_status launch_coarse(const rairs_index_s* idx, const float* queries, int64_t nq, int nprobe,
-                           int32_t* probes, unsigned* nflag_dev, cudaStream_t s);
+bool coarse_fused_ok(const rairs_index_s* idx, int L);
+// first L lists of each row of X by (D64, l): mode 0 -> out_idx [rows x L];
+// mode 1 -> RAIR pair (l1, l2); mode 2 -> single (l1 = l2 = nearest).
+rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64_t rows, int L,
+                                 int mode, double lambda, int strict, int32_t* out_idx,
+                                 int32_t* l1, int32_t* l2, unsigned* nflag, cudaStream_t s);
 
 // ---- search-side launchers (search_kernels.cu) -----------------------------
 struct SearchArgs {
