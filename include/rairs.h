@@ -179,6 +179,15 @@ rairs_status rairs_export_layout(rairs_index_t idx, int64_t* own_off, int64_t* o
 rairs_status rairs_set_coarse_mode(rairs_index_t idx, int32_t mode);
 rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t reset);
 
+/* ---- scan mode --------------------------------------------------------------
+ * 0 = auto (list-major tensor-core scan when supported), 1 = query-major SIMT
+ * fast scan (one CTA per query, shared-memory LUT lookups), 2 = list-major:
+ * (query, probe) pairs grouped by list, scores of each list's items for all its
+ * queries as one exact u8 x u8 -> s32 tcgen05 contraction of one-hot codes and
+ * quantised LUTs (the paper's query-batch cache optimisation).
+ * Both modes produce identical candidates. */
+rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode);
+
 /* ---- stage timing (CUDA events on the search stream) ----------------------
  * When enabled, every search records events around its stages on its stream;
  * rairs_profile_read synchronises and returns the accumulated milliseconds

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = [
     "rairs_search_debug", "rairs_merge_topk", "rairs_exact_knn", "rairs_export_trained",
     "rairs_export_assignment", "rairs_export_layout", "rairs_profile_enable",
     "rairs_profile_read", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
-    "rairs_certify_fallbacks",
+    "rairs_certify_fallbacks", "rairs_set_scan_mode",
 ]
 
 
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         "rairs_profile_read": [_P, _P, _P, _I32],
         "rairs_set_coarse_mode": [_P, _I32],
         "rairs_certify_fallbacks": [_P, _P, _I32],
+        "rairs_set_scan_mode": [_P, _I32],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

@@ -81,6 +81,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->codes); cudaFree(x->slot_rows); cudaFree(x->own_off); cudaFree(x->own_cnt);
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
+  cudaFree(x->list_items); cudaFree(x->ref_item_off);
   for (auto& es : x->pending)
     for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
   for (auto e : x->pool) cudaEventDestroy(e);
@@ -164,7 +165,10 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
     st = launch_probe_exact(pa, s);
   }
   ev.mark(1);
-  if (st == RAIRS_OK) st = launch_scan(idx, a, s);
+  if (st == RAIRS_OK) {
+    if (listmajor_ok(idx, nprobe, bigK)) st = launch_listmajor(idx, a, s);
+    else st = launch_scan(idx, a, s);
+  }
   ev.mark(2);
   if (st == RAIRS_OK && (cand_ids || cand_scores))
     st = launch_split_keys(keys, nq * bigK, cand_ids, cand_scores, s);
@@ -251,6 +255,17 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   cudaStream_t s = (cudaStream_t)stream;
   rairs_index_s* idx = new (std::nothrow) rairs_index_s();
   if (!idx) return RAIRS_E_OOM;
+  {
+    // search workspaces come from the stream-ordered pool: keep freed blocks
+    // cached instead of returning them to the driver at every sync
+    int dev = 0;
+    cudaMemPool_t pool;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   cudaGetDevice(&idx->device);
   idx->n = n;
   idx->d = d;
@@ -313,6 +328,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   if (st != RAIRS_OK) return fail(st);
   // Alg. 4 SeilInsert (cell-major) + PQ encoding (O5) into the packed layout
   st = build_layout(idx, s);
+  if (st != RAIRS_OK) return fail(st);
+  st = listmajor_prepare(idx, s);
   if (st != RAIRS_OK) return fail(st);
   B_TRY(cudaStreamSynchronize(s));
 #undef B_TRY
@@ -514,6 +531,13 @@ rairs_status rairs_set_coarse_mode(rairs_index_t idx, int32_t mode) {
   if (!idx) return invalid("index is NULL");
   if (mode < 0 || mode > 2) return invalid("coarse mode must be 0 (auto), 1 (exact), 2 (tensor core)");
   idx->coarse_mode = mode;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode) {
+  if (!idx) return invalid("index is NULL");
+  if (mode < 0 || mode > 2) return invalid("scan mode must be 0 (auto), 1 (SIMT), 2 (list-major)");
+  idx->scan_mode = mode;
   return RAIRS_OK;
 }
 

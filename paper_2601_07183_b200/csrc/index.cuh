@@ -37,6 +37,11 @@ struct rairs_index_s {
   double cmax = 0.0;
   int coarse_mode = 0;
   unsigned* certify_fallbacks = nullptr;  // device counter
+  // list-major scan (NEXT-1): mode 0 auto / 1 SIMT query-major / 2 list-major
+  int scan_mode = 0;
+  uint32_t* list_items = nullptr;    // [nlist] N_l = own_cnt + sum of ref_cnt
+  uint32_t* ref_item_off = nullptr;  // [n_refs] item offset inside the list-task
+  int64_t max_list_items = 0;
   int max_refs = 0;
   int64_t device_bytes = 0;
 
@@ -94,6 +99,12 @@ bool coarse_fused_ok(const rairs_index_s* idx, int L);
 rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64_t rows, int L,
                                  int mode, double lambda, int strict, int32_t* out_idx,
                                  int32_t* l1, int32_t* l2, unsigned* nflag, cudaStream_t s);
+
+// ---- list-major tensor-core scan (listmajor_kernels.cu) ----------------------
+rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s);
+bool listmajor_ok(const rairs_index_s* idx, int nprobe, int bigK);
+struct SearchArgs;
+rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 
 // ---- search-side launchers (search_kernels.cu) -----------------------------
 struct SearchArgs {

@@ -205,7 +205,7 @@ __device__ uint32_t filter_cands(uint64_t* cand, uint32_t n, uint32_t bthr, uint
   for (int i = 0; i < PER; ++i) {
     const uint32_t e = threadIdx.x * PER + i;
     v[i] = (e < n) ? cand[e] : kKeyInf;
-    const bool k = (e < n) && ((uint32_t)(v[i] >> (32 + hshift)) <= bthr) && (v[i] < tau);
+    const bool k = (e < n) && ((uint32_t)(v[i] >> (32 + hshift)) <= bthr) && (v[i] <= tau);
     if (!k) v[i] = kKeyInf;
     keep += k ? 1u : 0u;
   }

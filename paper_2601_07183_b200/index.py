@@ -205,6 +205,12 @@ class Index:
         """auto | exact (fp64 only) | tensor (TF32 tcgen05 filter + fp64 certify)."""
         check(lib().rairs_set_coarse_mode(self._h, self.COARSE_MODES[mode]), "rairs_set_coarse_mode")
 
+    SCAN_MODES = {"auto": 0, "simt": 1, "listmajor": 2}
+
+    def set_scan_mode(self, mode: str = "auto"):
+        """auto | simt (query-major LUT-lookup scan) | listmajor (tcgen05 one-hot x LUT)."""
+        check(lib().rairs_set_scan_mode(self._h, self.SCAN_MODES[mode]), "rairs_set_scan_mode")
+
     def certify_fallbacks(self, reset: bool = True) -> int:
         v = ctypes.c_int64()
         check(lib().rairs_certify_fallbacks(self._h, ctypes.byref(v), int(bool(reset))),

@@ -67,7 +67,8 @@ def case(oracle, name, **kw):
     return _CACHE[key]
 
 
-def gpu_search(idx, Q, k, nprobe, rf):
+def gpu_search(idx, Q, k, nprobe, rf, scan="auto"):
+    idx.set_scan_mode(scan)
     out = idx.search_debug(_t(Q), k, nprobe, rf)
     torch.cuda.synchronize()
     r = {key: v.cpu().numpy() for key, v in out.items()}
@@ -143,12 +144,13 @@ SEARCH_CASES = [
 ]
 
 
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
 @pytest.mark.parametrize("name,k,nprobe,rf", SEARCH_CASES)
-def test_search_parity(oracle_mod, name, k, nprobe, rf):
+def test_search_parity(oracle_mod, name, k, nprobe, rf, scan):
     c = case(oracle_mod, name)
     idx = c.gpu_index()
     o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, k, nprobe, rf)
-    g = gpu_search(idx, c.Q, k, nprobe, rf)
+    g = gpu_search(idx, c.Q, k, nprobe, rf, scan)
     assert_search_equal(g, o)
 
 
@@ -255,8 +257,9 @@ def test_gpu_training_properties():
 
 
 # ------------------------------------------ BJ full sizes, sampled queries
-@pytest.mark.parametrize("name,nprobe", [("c2", 16), ("c2pl", 16), ("c2pl", 64)])
-def test_full_size_sampled(oracle_mod, name, nprobe):
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
+@pytest.mark.parametrize("name,nprobe", [("c2", 16), ("c2pl", 4), ("c2pl", 64)])
+def test_full_size_sampled(oracle_mod, name, nprobe, scan):
     """BJ configs[1] at full size (1M x 128, 10k queries) in the bench's launch
     configuration; the oracle recomputes a sample of 200 queries one by one."""
     c = case(oracle_mod, name, train_rows=32768, iters=4)
@@ -264,7 +267,7 @@ def test_full_size_sampled(oracle_mod, name, nprobe):
     idx = c.gpu_index()
     rng = np.random.default_rng(7)
     sample = np.sort(rng.choice(c.Q.shape[0], 200, replace=False))
-    g = gpu_search(idx, c.Q, spec.k, nprobe, spec.refine_factor)   # all 10k queries
+    g = gpu_search(idx, c.Q, spec.k, nprobe, spec.refine_factor, scan)   # all 10k queries
     o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q[sample], spec.k, nprobe,
                           spec.refine_factor)
     gs = {key: v[sample] for key, v in g.items()}
@@ -298,3 +301,21 @@ def test_coarse_tensor_core_path_equals_exact(oracle_mod, name, nprobes):
         po = oracle_mod.probe(c.Q[sample], c.cent, npb)
         assert np.array_equal(pt[sample], po)
     idx.set_coarse_mode("auto")
+
+
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
+def test_massive_score_ties(oracle_mod, scan):
+    """Many identical vectors -> identical codes and scores: exercises the
+    exact-sort fallback of the top-bigK selection (keys unique by id)."""
+    rng = np.random.default_rng(21)
+    base = rng.standard_normal((12, 16)).astype(np.float32)
+    X = base[rng.integers(0, 12, 6000)] + 0.0
+    Q = base[rng.integers(0, 12, 30)] + rng.standard_normal((30, 16)).astype(np.float32) * 0.01
+    cent = oracle_mod.kmeans(X, 16, iters=3, seed=1)
+    cb = oracle_mod.pq_train(X, 8, iters=3, seed=2)
+    l1, l2 = oracle_mod.assign(X, cent, "air")
+    codes = oracle_mod.encode(X, cb)
+    idx = rb.Index.build(_t(X), 16, 8, centroids=_t(cent), codebook=_t(cb))
+    for k, nprobe, rf in ((10, 4, 10), (5, 16, 20), (50, 8, 8)):
+        o = oracle_mod.search(X, l1, l2, codes, cent, cb, Q, k, nprobe, rf)
+        assert_search_equal(gpu_search(idx, Q, k, nprobe, rf, scan), o)
