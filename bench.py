@@ -201,6 +201,7 @@ def run_ours(args):
     # ---------------- timed region (device events per step, L2 flushed between) ----------
     idx.profile_enable(True)
     idx.profile_read(reset=True)
+    idx.kernels_launched(reset=True)
     clk = ClockSampler(local_rank)
     clk.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -222,6 +223,7 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     prof = idx.profile_read(reset=True)
     idx.profile_enable(False)
+    kernels = idx.kernels_launched(reset=True) + (args.steps if world > 1 else 0)  # + K7 merge
     t_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
@@ -249,16 +251,18 @@ def run_ours(args):
         e2e = {"value": round(nq * args.steps / sum(e_times), 1), "unit": "queries/s",
                "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 12)}
 
-    # ---------------- roofline of the dominant kernel (the fused scan) ----------------
+    # ---------------- roofline of the dominant stage (the fast scan, A3-A6) ----------------
     peak, peak_src = load_peaks()
+    scan_mode = idx.scan_path(k, chosen, rf)
     scan_ms = prof["ms"]["scan"] / max(1, prof["launches"]["scan"])
     scan_bytes = dco_local * (spec.M // 2)             # algorithmic code bytes per launch
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
         except Exception:
             traffic = None
 
@@ -284,13 +288,18 @@ def run_ours(args):
             "dco_per_query": round(dco_total / nq, 1),
             "dco_per_s": round(dco_total * args.steps / (t_ms / 1e3), 1),
             "stage_ms_per_step": {kk: round(v / args.steps, 4) for kk, v in prof["ms"].items()},
-            "roofline": {"bound": "hbm", "kernel": "scan_kernel (LUT+worklist+fast-scan+top-bigK)",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("fast-scan stage A3-A6: lut_tiles_kernel + list grouping + "
+                                    "lm_tensor_kernel (tcgen05 kind::i8 one-hot x LUT) + "
+                                    "lm_select_kernel" if scan_mode == "listmajor"
+                                    else "scan_kernel (LUT + SEIL work list + fast scan + top-bigK)"),
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "peak_source": peak_src,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": scan_bytes,
+                         "algorithmic_bytes_per_unit": f"M/2 = {spec.M // 2} B per DCO",
                          "avg_launch_ms": round(scan_ms, 4)},
-            "e2e": e2e, "gpu_launches": 3 * args.steps + (args.steps if world > 1 else 0),
+            "e2e": e2e, "gpu_launches": kernels,
             "clocks": clocks, "wall_s_timed_region": round(wall, 4),
             "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
             "index": {k2: info[k2] for k2 in ("n", "n_slots", "n_cells", "n_refs", "n_double",

@@ -197,6 +197,17 @@ rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode);
 rairs_status rairs_profile_enable(rairs_index_t idx, int32_t on);
 rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launches3,
                                 int32_t reset);
+/* Number of CUDA kernels the library launched for searches on this index
+ * since the last reset (host-side count, always on): *kernels receives it;
+ * reset != 0 zeroes the counter. RAIRS_E_INVALID on NULL arguments. */
+rairs_status rairs_profile_kernels(rairs_index_t idx, int64_t* kernels, int32_t reset);
+
+/* Which kernels a search with these parameters would use (no device work):
+ * *coarse_path = 1 exact fp64 probe kernel, 2 tensor-core TF32 filter +
+ * certification; *scan_path = 1 SIMT query-major scan, 2 list-major tcgen05
+ * scan. Either pointer may be NULL. Same validation as rairs_search. */
+rairs_status rairs_search_plan(rairs_index_t idx, int32_t k, int32_t nprobe,
+                               int32_t refine_factor, int32_t* coarse_path, int32_t* scan_path);
 
 const char* rairs_last_error(void);
 const char* rairs_version(void);

@@ -31,7 +31,8 @@ EXPORTED_SYMBOLS = [
     "rairs_search_debug", "rairs_merge_topk", "rairs_exact_knn", "rairs_export_trained",
     "rairs_export_assignment", "rairs_export_layout", "rairs_profile_enable",
     "rairs_profile_read", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
-    "rairs_certify_fallbacks", "rairs_set_scan_mode",
+    "rairs_certify_fallbacks", "rairs_set_scan_mode", "rairs_profile_kernels",
+    "rairs_search_plan",
 ]
 
 
@@ -101,6 +102,8 @@ def lib() -> ctypes.CDLL:
         "rairs_set_coarse_mode": [_P, _I32],
         "rairs_certify_fallbacks": [_P, _P, _I32],
         "rairs_set_scan_mode": [_P, _I32],
+        "rairs_profile_kernels": [_P, _P, _I32],
+        "rairs_search_plan": [_P, _I32, _I32, _I32, _P, _P],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "index.cuh"
+#include "tc_helpers.cuh"
 
 namespace rairs {
 
@@ -362,12 +363,14 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
   float* Xt = nullptr;
   int32_t *asg = nullptr, *asg_sorted = nullptr, *iota = nullptr, *idx_sorted = nullptr;
   int32_t *seg_s = nullptr, *seg_e = nullptr;
+  unsigned* nflag = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   rairs_status st = RAIRS_OK;
   auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
     cudaFree(d_rows); cudaFree(Xt); cudaFree(asg); cudaFree(asg_sorted); cudaFree(iota);
-    cudaFree(idx_sorted); cudaFree(seg_s); cudaFree(seg_e); cudaFree(tmp);
+    cudaFree(idx_sorted); cudaFree(seg_s); cudaFree(seg_e); cudaFree(tmp); cudaFree(nflag);
   };
 #define KM_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return _e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA; } } while (0)
   KM_TRY(cudaMalloc(&d_rows, nt * sizeof(int64_t)));
@@ -390,11 +393,27 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
   KM_TRY(cudaMalloc(&tmp, tmp_bytes));
   std::vector<int32_t> hs(k), he(k);
   std::vector<float> hc;
+  // large nlist: assignment on tensor cores (fp64 over k x d per row is too slow)
+  const bool use_tc = k >= 1024 && (d & 3) == 0 && tma_available();
+  if (use_tc) KM_TRY(cudaMalloc(&nflag, sizeof(unsigned)));
   for (int it = 0; it < iters; ++it) {
-    ProbeArgs pa{};
-    pa.X = Xt; pa.rows = nt; pa.d = d; pa.C = cent; pa.nl = k; pa.L = 1; pa.mode = 0;
-    pa.out_idx = asg;
-    st = launch_probe_exact(pa, s);
+    if (use_tc) {
+      // nearest centroid through the tensor-core coarse path (TF32 filter +
+      // fp64 certification + exact fallback: the same argmin as probe_exact)
+      rairs_index_s tmp{};
+      tmp.centroids = cent;
+      tmp.nlist = k;
+      tmp.d = d;
+      st = coarse_prepare(&tmp, s);
+      if (st == RAIRS_OK)
+        st = launch_coarse_fused(&tmp, Xt, nt, 1, 0, 0.0, 0, asg, nullptr, nullptr, nflag, s);
+      cudaFreeAsync(tmp.cnorm, s);
+    } else {
+      ProbeArgs pa{};
+      pa.X = Xt; pa.rows = nt; pa.d = d; pa.C = cent; pa.nl = k; pa.L = 1; pa.mode = 0;
+      pa.out_idx = asg;
+      st = launch_probe_exact(pa, s);
+    }
     if (st != RAIRS_OK) { cleanup(); return st; }
     KM_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, asg, asg_sorted, iota, idx_sorted,
                                            (int)nt, 0, end_bit, s));

@@ -81,7 +81,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->codes); cudaFree(x->slot_rows); cudaFree(x->own_off); cudaFree(x->own_cnt);
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
-  cudaFree(x->list_items); cudaFree(x->ref_item_off);
+  cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
   for (auto& es : x->pending)
     for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
   for (auto e : x->pool) cudaEventDestroy(e);
@@ -165,14 +165,26 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
     st = launch_probe_exact(pa, s);
   }
   ev.mark(1);
+  int64_t nk = coarse_fused_ok(idx, nprobe) ? 3 : 1;  // topw + certify + exact fallback
   if (st == RAIRS_OK) {
-    if (listmajor_ok(idx, nprobe, bigK)) st = launch_listmajor(idx, a, s);
-    else st = launch_scan(idx, a, s);
+    if (listmajor_ok(idx, nprobe, bigK)) {
+      st = launch_listmajor(idx, a, s);
+      nk += 6;  // count, scan, scatter, lut_tiles, tensor, select
+    } else {
+      st = launch_scan(idx, a, s);
+      nk += 1;
+    }
   }
   ev.mark(2);
-  if (st == RAIRS_OK && (cand_ids || cand_scores))
+  if (st == RAIRS_OK && (cand_ids || cand_scores)) {
     st = launch_split_keys(keys, nq * bigK, cand_ids, cand_scores, s);
-  if (st == RAIRS_OK) st = launch_refine(idx, a, s);
+    nk += 1;
+  }
+  if (st == RAIRS_OK) {
+    st = launch_refine(idx, a, s);
+    nk += 1;
+  }
+  if (st == RAIRS_OK) idx->kernels += nk;
   ev.mark(3);
   ev.commit();
   if (!probes_out) cudaFreeAsync(probes, s);
@@ -547,6 +559,21 @@ rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t 
   RAIRS_CUDA_TRY(cudaMemcpy(&v, idx->certify_fallbacks, sizeof(unsigned), cudaMemcpyDeviceToHost));
   *count = v;
   if (reset) RAIRS_CUDA_TRY(cudaMemset(idx->certify_fallbacks, 0, sizeof(unsigned)));
+  return RAIRS_OK;
+}
+
+rairs_status rairs_search_plan(rairs_index_t idx, int32_t k, int32_t nprobe, int32_t refine_factor,
+                               int32_t* coarse_path, int32_t* scan_path) {
+  RAIRS_TRY(validate_search(idx, 1, k, nprobe, refine_factor));
+  if (coarse_path) *coarse_path = coarse_fused_ok(idx, nprobe) ? 2 : 1;
+  if (scan_path) *scan_path = listmajor_ok(idx, nprobe, k * refine_factor) ? 2 : 1;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_profile_kernels(rairs_index_t idx, int64_t* kernels, int32_t reset) {
+  if (!idx || !kernels) return invalid("NULL argument");
+  *kernels = idx->kernels;
+  if (reset) idx->kernels = 0;
   return RAIRS_OK;
 }
 

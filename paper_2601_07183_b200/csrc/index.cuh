@@ -42,6 +42,8 @@ struct rairs_index_s {
   uint32_t* list_items = nullptr;    // [nlist] N_l = own_cnt + sum of ref_cnt
   uint32_t* ref_item_off = nullptr;  // [n_refs] item offset inside the list-task
   int64_t max_list_items = 0;
+  uint64_t* list_base = nullptr;     // [nlist + 1] prefix of N_l (into list_ids)
+  uint32_t* list_ids = nullptr;      // [sum N_l] global id of item i of list-task l
   int max_refs = 0;
   int64_t device_bytes = 0;
 
@@ -52,6 +54,7 @@ struct rairs_index_s {
   std::vector<cudaEvent_t> pool;
   double ms[3] = {0, 0, 0};
   int64_t launches[3] = {0, 0, 0};
+  int64_t kernels = 0;  // kernels launched by searches (rairs_profile_kernels)
 };
 
 namespace rairs {

@@ -1,105 +1,29 @@
-// listmajor_kernels.cu -- NEXT-1: list-major batched fast scan on tensor cores.
+// listmajor_kernels.cu -- list-major batched fast scan on tensor cores (A3-A6).
 //
 // The paper's query-batch cache optimisation ("group the tasks by
 // lists, and process all the queries for the same list back to back") on B200:
 // for a list l probed by the queries Q_l of a batch, the integer scores of all
 // (item, query) pairs are ONE exact u8 x u8 -> s32 contraction
 //     S[x][q] = sum_m Qv_q[m][code_m(x)] = sum_{m,j} onehot(x)[m*16+j] * Qv_q[m][j]
-// (K = 16*M), issued as tcgen05.mma.kind::i8 (M = 128 items, N = |Q_l| padded to
-// 16, K = 32 per instruction) with the accumulator in TMEM.  The one-hot A tile
-// is expanded in shared memory from the 4-bit codes (each code byte read ONCE
-// per list-task instead of once per (list, query)); the B tile is the queries'
-// quantised LUT rows.  Integer sums are exact (<= 16*M*255 < 2^31), so the
-// scores are bit-identical to the SIMT lookup scan (O8).
+// (K = 16*M), issued as tcgen05.mma.kind::i8 (M = 128 items, N = |Q_l| tile
+// padded to 16, K = 32 per instruction) with A (the one-hot rows, expanded from
+// the 4-bit codes in registers and written with tcgen05.st) in TMEM, B (the
+// queries' quantised LUT rows) in shared memory and the accumulator in TMEM.
+// Each code byte is read ONCE per list-task instead of once per (list, query).
+// Integer sums are exact (<= 16*M*255 < 2^31): scores are bit-identical to O8.
 //
 // Pipeline for a batch (all on the search stream, no host sync):
-//   lut_batch_kernel   O2 LUT per query -> global [nq][16*M_pad] u8
-//   lm_count / lm_scan / lm_scatter / lm_bitmap   group (query, probe) by list
-//   lm_tensor_kernel   persistent; task = (list, 128-item tile, 256-query tile)
-//                      -> scores of valid pairs into a per-list score block
-//   lm_select_kernel   per query: SEIL ranges (R9 dedup) over its score rows,
-//                      histogram-threshold top-bigK (same rule as scan_kernel)
+//   lm_count / lm_scan / lm_scatter   group the (query, probe) pairs by list
+//   lut_tiles_kernel   O2 LUT per query, written into its list-tasks' B tiles
+//   lm_tensor_kernel   persistent; task = (list, query tile) -> u16/u32 score
+//                      rows (sentinel for SEIL-skipped references, R9)
+//   lm_select_kernel   per query: DCO, two-pass histogram top-bigK by (s, id)
 #include <algorithm>
 
 #include "index.cuh"
 #include "tc_helpers.cuh"
 
 namespace rairs {
-
-// ---------------------------------------------------------------------------
-// O2 LUT, one WARP per query (same arithmetic as scan_kernel's prologue).
-constexpr int LW = 8;  // warps (queries) per CTA
-
-__device__ __forceinline__ float lm_lut_T(const float* __restrict__ q,
-                                          const float* __restrict__ cb, int m, int j, int dsub) {
-  const float* c = cb + ((int64_t)m * 16 + j) * dsub;
-  const float* qs = q + (int64_t)m * dsub;
-  float acc = 0.0f;
-  for (int t = 0; t < dsub; ++t) {
-    float diff = __fsub_rn(__ldg(qs + t), __ldg(c + t));
-    acc = __fadd_rn(acc, __fmul_rn(diff, diff));
-  }
-  return acc;
-}
-
-__global__ void __launch_bounds__(LW * 32) lut_batch_kernel(const float* __restrict__ queries,
-                                                            int64_t nq, int d,
-                                                            const float* __restrict__ cb, int M,
-                                                            int M_pad, int dsub,
-                                                            uint8_t* __restrict__ lut,
-                                                            float* __restrict__ a_out,
-                                                            float* __restrict__ b_out,
-                                                            uint8_t* __restrict__ lut_dbg) {
-  const int lane = lane_id();
-  const int M16 = M * 16, K = M_pad * 16;
-  for (int64_t q = (int64_t)blockIdx.x * LW + warp_id(); q < nq; q += (int64_t)gridDim.x * LW) {
-    const float* qv = queries + q * d;
-    // pass 1: per-subquantizer min and span (16-lane groups), S = max span
-    float S = 0.0f, bsum = 0.0f;
-    for (int e0 = 0; e0 < M16; e0 += 32) {
-      const int e = e0 + lane;
-      const bool act = e < M16;
-      const float T = act ? lm_lut_T(qv, cb, e >> 4, e & 15, dsub) : 0.0f;
-      float lo = act ? T : __int_as_float(0x7f800000);
-      float hi = act ? T : -__int_as_float(0x7f800000);
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      const float span = __fsub_rn(hi, lo);
-      if (act) S = fmaxf(S, span);
-      // b = sum_m mn_m in ascending m (fp32): lanes 0 and 16 hold m = e0/16, e0/16+1
-      const float lo0 = __shfl_sync(0xffffffffu, lo, 0), lo1 = __shfl_sync(0xffffffffu, lo, 16);
-      if (e0 + 0 < M16) bsum = __fadd_rn(bsum, lo0);
-      if (e0 + 16 < M16) bsum = __fadd_rn(bsum, lo1);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) S = fmaxf(S, __shfl_xor_sync(0xffffffffu, S, o));
-    const float a = (S > 0.0f) ? __fdiv_rn(255.0f, S) : 1.0f;
-    // pass 2: quantise (recomputing T: identical fp32 values)
-    for (int e0 = 0; e0 < K; e0 += 32) {
-      const int e = e0 + lane;
-      const int m = e >> 4;
-      uint32_t v = 0;
-      const bool act = m < M;
-      const float T = act ? lm_lut_T(qv, cb, m, e & 15, dsub) : 0.0f;
-      float lo = act ? T : __int_as_float(0x7f800000);
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      if (act && S > 0.0f) {
-        const float t2 = __fmul_rn(__fsub_rn(T, lo), a);
-        v = (uint32_t)min(255, __float2int_rn(t2));
-      }
-      lut[q * K + e] = (uint8_t)v;
-      if (lut_dbg && act) lut_dbg[q * M16 + e] = (uint8_t)v;
-    }
-    if (lane == 0) {
-      if (a_out) a_out[q] = a;
-      if (b_out) b_out[q] = bsum;
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Grouping of (query, probe) pairs by list.
@@ -147,8 +71,8 @@ __global__ void __launch_bounds__(SCN) lm_scan_kernel(const uint32_t* __restrict
     if (l < nlist) {
       c = cnt[l];
       const uint32_t ni = nitems[l];
-      s = (uint64_t)c * ni;
-      t = (c > 0 && ni > 0) ? (uint32_t)(((c + qtile - 1) / qtile) * ((ni + itile - 1) / itile)) : 0u;
+      s = (uint64_t)c * ((ni + 7u) & ~7u);   // score rows padded to 8 items (16-B aligned)
+      t = (c + 15u) & ~15u;  // LUT-tile rows of list l (query tiles padded to 16)
     }
     uint32_t ic = c, it = t;
     uint64_t is = s;
@@ -200,14 +124,111 @@ __global__ void __launch_bounds__(SCN) lm_scan_kernel(const uint32_t* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// O2 LUT per query, written straight into the pre-tiled, pre-swizzled LUT
+// tiles of every list-task the query belongs to (one row per (query, probe)):
+// tile t of list l holds the rows of queries t*QT.. of Q_l as nchunk K-chunks
+// of [Npad rows x 128 B] in the 128-B-swizzled K-major layout tcgen05 reads,
+// so the tensor kernel fetches a whole B tile with ONE bulk copy.
+// One WARP per query, lane = subquantizer m (m = lane, lane+32, ...): the 16
+// distances T[m][j] are computed in registers (fp32, ascending t, no FMA --
+// R2), the codebook is staged transposed in shared memory ([j][t][m]: lanes
+// read consecutive words).  b = sum_m mn_m is summed by lane 0 in ascending m.
+constexpr int LW = 8;  // warps (queries) per CTA
+constexpr int LUT_MAX_DSUB = 8;
+
+__device__ __forceinline__ float lut_T(const float* qs, const float* smc, int m, int j, int dsub,
+                                       int M) {
+  float acc = 0.0f;
+#pragma unroll
+  for (int t = 0; t < LUT_MAX_DSUB; ++t) {
+    if (t < dsub) {
+      const float diff = __fsub_rn(qs[t], smc[(j * dsub + t) * M + m]);
+      acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+    }
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
+    const float* __restrict__ queries, int64_t nq, int d, const float* __restrict__ cb, int M,
+    int M_pad, int dsub, const int32_t* __restrict__ probes, int nprobe,
+    const uint32_t* __restrict__ qslot, const uint32_t* __restrict__ qcnt,
+    const uint32_t* __restrict__ lrow, int QT, uint8_t* __restrict__ tiles,
+    float* __restrict__ a_out, float* __restrict__ b_out, uint8_t* __restrict__ lut_dbg) {
+  extern __shared__ __align__(16) float smc[];  // [16][dsub][M] codebook, then [LW][M] mn
+  const int lane = lane_id(), warp = warp_id();
+  const int K = M_pad * 16;
+  for (int e = threadIdx.x; e < M * 16 * dsub; e += blockDim.x) {
+    const int m = e / (16 * dsub), j = (e / dsub) % 16, t = e % dsub;
+    smc[(j * dsub + t) * M + m] = cb[e];
+  }
+  __syncthreads();
+  float* mnw = smc + 16 * dsub * M + warp * M;
+  for (int64_t q = (int64_t)blockIdx.x * LW + warp; q < nq; q += (int64_t)gridDim.x * LW) {
+    const float* qv = queries + q * d;
+    float S = 0.0f;
+    for (int m = lane; m < M; m += 32) {  // pass 1: per-subquantizer min and span
+      float qs[LUT_MAX_DSUB];
+#pragma unroll
+      for (int t = 0; t < LUT_MAX_DSUB; ++t) qs[t] = (t < dsub) ? __ldg(qv + m * dsub + t) : 0.0f;
+      float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float T = lut_T(qs, smc, m, j, dsub, M);
+        lo = fminf(lo, T);
+        hi = fmaxf(hi, T);
+      }
+      mnw[m] = lo;
+      S = fmaxf(S, __fsub_rn(hi, lo));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S = fmaxf(S, __shfl_xor_sync(0xffffffffu, S, o));
+    const float a = (S > 0.0f) ? __fdiv_rn(255.0f, S) : 1.0f;
+    __syncwarp();
+    if (lane == 0) {
+      float bsum = 0.0f;
+      for (int m = 0; m < M; ++m) bsum = __fadd_rn(bsum, mnw[m]);  // ascending m (O2 step 5)
+      if (a_out) a_out[q] = a;
+      if (b_out) b_out[q] = bsum;
+    }
+    for (int m = lane; m < M_pad; m += 32) {  // pass 2: quantise, write every tile row
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+      if (m < M) {
+        float qs[LUT_MAX_DSUB];
+#pragma unroll
+        for (int t = 0; t < LUT_MAX_DSUB; ++t) qs[t] = (t < dsub) ? __ldg(qv + m * dsub + t) : 0.0f;
+        const float lo = mnw[m];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float T = lut_T(qs, smc, m, j, dsub, M);
+          uint32_t v = 0;
+          if (S > 0.0f) v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T, lo), a)));
+          w[j >> 2] |= v << (8 * (j & 3));
+        }
+        if (lut_dbg)
+          *reinterpret_cast<uint4*>(lut_dbg + (size_t)q * M * 16 + m * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      const int c = m >> 3, kk = m & 7;
+      for (int p = 0; p < nprobe; ++p) {
+        const int l = probes[q * nprobe + p];
+        const uint32_t j = qslot[q * nprobe + p], Ql = qcnt[l];
+        const uint32_t t = j / (uint32_t)QT, jq = j - t * (uint32_t)QT;
+        const uint32_t Npad = (t < Ql / (uint32_t)QT) ? (uint32_t)QT : ((Ql - t * QT + 15u) & ~15u);
+        uint8_t* base = tiles + ((size_t)lrow[l] + (size_t)t * QT) * K;
+        *reinterpret_cast<uint4*>(base + (size_t)c * Npad * 128 + jq * 128 + ((kk ^ (jq & 7)) << 4)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    __syncwarp();  // mnw reuse
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Tensor-core scoring, one list at a time (CTAs claim lists atomically).
-constexpr int LM_THREADS = 256;   // 2 threads per item row (4 subquantizers of a chunk each)
 constexpr int LM_IT = 128;        // items per tile (MMA M)
-constexpr int LM_QT = 64;         // queries per tile (MMA N <= 64, TMEM columns)
+constexpr int LM_QT = 64;         // max queries per tile (MMA N <= 64)
 constexpr int LM_MAXREF = 128;    // references per list on this path
-constexpr uint32_t LM_A_BYTES = LM_IT * 128;   // one 128-B K-chunk per item row
-constexpr uint32_t LM_BC_BYTES = LM_QT * 128;  // one K-chunk of the LUT tile
-constexpr int LM_BRES_MAX = 64 * 1024;         // LUT tile resident for all K if it fits
+constexpr uint32_t LM_B_MAX = 64 * 1024;  // LUT tile bytes (QT x K)
 
 struct LMArgs {
   const uint64_t* codes64;
@@ -218,9 +239,9 @@ struct LMArgs {
   const uint32_t* ref_start;
   const uint32_t* ref_item_off;  // item offset of each reference inside its list-task
   const uint32_t* list_items;    // N_l = own_cnt + sum of the list's ref_cnt
-  int NU, nchunk;                // code units of 16 subquantizers; K chunks of 8 subq (128 B)
-  const uint8_t* lut;            // [nq][K]
-  int K, b_resident;
+  int K, QT;                     // LUT bytes per query (16 * M_pad); queries per tile
+  const uint8_t* tiles;          // pre-tiled LUT (lut_tiles_kernel)
+  const uint32_t* lrow;          // [nlist] first LUT-tile row of list l
   const int32_t* probes;
   int nprobe;
   const uint32_t* qptr;
@@ -232,12 +253,13 @@ struct LMArgs {
   int nlist;
 };
 
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                        uint32_t idesc, uint32_t accum) {
+// D[tmem] (+)= A[tmem] x B[smem desc]  (A: 128 item rows x 32 K-bytes, 8 columns)
+__device__ __forceinline__ void umma_i8_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
 
@@ -252,81 +274,95 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// (no "memory" clobber: ordinary loads may be hoisted above these stores; the
-// fence.proxy.async / barrier asm that publishes the tile does carry one)
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
-                                             uint32_t w) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z),
-               "r"(w));
+// 32 columns x 32 lanes (this warp's lane quarter) of 32-bit words
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
 }
 
-// 16-byte one-hot of a 4-bit code: byte n = 1.  c = 8*(n&7) < 64; (hi:lo) =
-// 1 << c as two PTX shl (shift counts >= 32 -- including c-32 wrapped for
-// c < 32 -- produce 0); bit 3 of n picks words (0,1) or (2,3).
-__device__ __forceinline__ void onehot16(uint32_t n, uint32_t& w0, uint32_t& w1, uint32_t& w2,
-                                         uint32_t& w3) {
-  const uint32_t c = (n & 7u) << 3;
-  uint32_t lo, hi;
-  asm("shl.b32 %0, 1, %1;" : "=r"(lo) : "r"(c));
-  asm("shl.b32 %0, 1, %1;" : "=r"(hi) : "r"(c - 32u));
-  const bool h = (n & 8u) != 0;
-  w0 = h ? 0u : lo;
-  w1 = h ? 0u : hi;
-  w2 = h ? lo : 0u;
-  w3 = h ? hi : 0u;
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >= 32 -> 0
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+  return r;
 }
 
-// Warp-specialised pipeline (no CTA barrier per chunk):
-//   warps 0-3  generators: warp g expands the one-hot rows of items 32g..32g+31
-//              for each K-chunk into a 4-stage shared-memory ring, then arrives
-//              on full[stage] (4 arrivals);
-//   warp 4     MMA issuer: waits full[stage], issues 4 x tcgen05.mma.kind::i8
-//              into one of 2 TMEM accumulators, commits empty[stage] and, after
-//              the last chunk of a tile, tfull[acc];
-//   warps 5-8  epilogue: wait tfull[acc], tcgen05.ld the scores (lane group
-//              warp%4), store the valid (item, query) scores, arrive tempty[acc].
-// The LUT tile of a 64-query tile is loaded once (all K) at the start of the
-// query tile; a CTA barrier separates query tiles (no MMA in flight then).
-constexpr int LM_GEN_WARPS = 4, LM_MMA_WARP = 4;
-constexpr int LM_WS_THREADS = 9 * 32;
-constexpr int LM_STAGES = 2;  // 2 x 16 KB A ring + 64 KB LUT tile -> 2 CTAs per SM
+// Warp-specialised pipeline (no CTA barrier per tile):
+//   generators  LM_GROUPS groups of four warps (group g takes item tiles
+//               t = g mod LM_GROUPS); warp w owns item rows 32(w%4).. (TMEM lane
+//               quarter w%4).  Per K-chunk (8 subquantizers = 128 one-hot bytes
+//               per row) it expands the 4-bit codes into 32 words in registers
+//               and writes them to one of its group's 4 TMEM A stages with
+//               tcgen05.st, then arrives on full[stage].  Codes of the group's
+//               next tile are loaded while the current one is expanded.
+//   MMA warp    waits full[stage], issues 4 x tcgen05.mma.kind::i8 (A from
+//               TMEM, B = LUT tile in shared memory) into one of 2 TMEM
+//               accumulators, commits empty[stage] and, after a tile, tfull[acc].
+//   epilogue    8 warps, 2 per lane quarter (alternating 16-column blocks):
+//               tcgen05.ld the scores, store the (item, query) scores /
+//               sentinels, arrive tempty[acc].
+// The LUT tile of a query tile arrives by one cp.async.bulk (pre-tiled by
+// lut_tiles_kernel); a CTA barrier separates query tiles.  TMEM: the A ring
+// (32 columns per stage) then two 64-column accumulators.
+constexpr int LM_GROUPS = 1;  // generator groups (1: two CTAs per SM; 2: one CTA per SM)
+constexpr int LM_GEN_WARPS = 4 * LM_GROUPS, LM_MMA_WARP = LM_GEN_WARPS;
+constexpr int LM_EPI0 = LM_GEN_WARPS + 1, LM_EPI_WARPS = 8;
+constexpr int LM_WS_THREADS = (LM_EPI0 + LM_EPI_WARPS) * 32;
+constexpr int LM_GSTAGES = 4, LM_STAGES = LM_GSTAGES * LM_GROUPS;  // A ring: 4 stages per group
+constexpr uint32_t LM_ACC_COL = 32 * LM_STAGES;                      // accumulators after the ring
+constexpr uint32_t LM_TMEM_COLS = LM_GROUPS == 1 ? 256 : 512;
+constexpr int LM_CTAS_PER_SM = 3 - LM_GROUPS;
 
-__global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
+template <int NU>
+__global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kernel(LMArgs a) {
+  constexpr int NCHUNK = 2 * NU;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
-  uint8_t* sA = smem;                                    // LM_STAGES x 16 KB
-  uint8_t* sB = smem + LM_STAGES * LM_A_BYTES;           // nchunk x 8 KB (resident LUT tile)
-  int32_t* owners = reinterpret_cast<int32_t*>(sB + (size_t)a.nchunk * LM_BC_BYTES);  // [LM_MAXREF]
-  uint32_t* refoff = reinterpret_cast<uint32_t*>(owners + LM_MAXREF);                // [LM_MAXREF+1]
-  uint32_t* skipT = refoff + LM_MAXREF + 1;            // [LM_MAXREF][2]: queries skipping ref j
-  uint32_t* qid = skipT + LM_MAXREF * 2;               // [LM_QT]
+  uint8_t* sB = smem;                                                    // <= LM_B_MAX
+  int32_t* owners = reinterpret_cast<int32_t*>(sB + LM_B_MAX);          // [LM_MAXREF]
+  uint32_t* refoff = reinterpret_cast<uint32_t*>(owners + LM_MAXREF);   // [LM_MAXREF+1]
+  uint32_t* skipT = refoff + LM_MAXREF + 1;  // [LM_MAXREF][2]: queries skipping ref j
+  uint32_t* qid = skipT + LM_MAXREF * 2;     // [LM_QT]
   uint64_t* full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(qid + LM_QT) + 7) & ~(uintptr_t)7);  // [LM_STAGES]
   uint64_t* empty = full + LM_STAGES;
-  uint64_t* tfull = empty + LM_STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;          // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + LM_STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint64_t* bfull = tempty + 2;         // LUT tile landed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
   __shared__ uint32_t sh_list;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < LM_STAGES; ++s) {
-      mbar_init(&full[s], LM_GEN_WARPS);
+      mbar_init(&full[s], 4);  // the 4 lane-quarter warps of the tile's generator group
       mbar_init(&empty[s], 1);
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&tfull[k], 1);
-      mbar_init(&tempty[k], 4);
+      mbar_init(&tempty[k], LM_EPI_WARPS);
     }
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == LM_MMA_WARP) tmem_alloc(tslot, 2 * LM_QT);
+  if (warp == LM_MMA_WARP) tmem_alloc(tslot, LM_TMEM_COLS);
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  uint32_t chunk_ctr = 0;  // chunks produced/consumed so far (same sequence in every role)
+  // chunks produced / consumed so far per generator group (same values in every
+  // role).  Each group owns its own 4-stage half of the A ring, so a group is
+  // never more than one phase ahead of the MMA on any of its stages (an
+  // mbarrier parity wait cannot tell phase k from phase k+2).
+  uint32_t gcnt0 = 0, gcnt1 = 0;
   uint32_t tile_ctr = 0;   // item tiles so far
+  uint32_t qt_ctr = 0;     // query tiles so far (bfull phase)
 
   for (;;) {
     if (tid == 0) sh_list = atomicAdd(a.list_counter, 1u);
@@ -336,7 +372,8 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
     if (l >= (uint32_t)a.nlist) break;
     const uint32_t Ql = a.qptr[l + 1] - a.qptr[l];
     const uint32_t Nl = a.list_items[l];
-    if (Ql == 0 || Nl == 0) continue;  // uniform across the CTA
+    const uint32_t Nl8 = (Nl + 7u) & ~7u;  // score row stride
+    if (Ql == 0 || Nl == 0) continue;      // uniform across the CTA
     const uint32_t own = a.own_cnt[l], own0 = a.own_off[l];
     const uint32_t r0 = a.ref_ptr[l], nref = a.ref_ptr[l + 1] - r0;
     for (uint32_t j = tid; j < nref; j += LM_WS_THREADS) {
@@ -345,10 +382,15 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
     }
     if (tid == 0) refoff[nref] = Nl;
     const uint32_t ntiles = (Nl + LM_IT - 1) / LM_IT;
-    for (uint32_t q0 = 0; q0 < Ql; q0 += LM_QT) {
-      const int nq_tile = (int)min(Ql - q0, (uint32_t)LM_QT);
+    for (uint32_t q0 = 0; q0 < Ql; q0 += a.QT) {
+      const int nq_tile = (int)min(Ql - q0, (uint32_t)a.QT);
       const int Npad = ((nq_tile + 15) / 16) * 16;
       __syncthreads();  // previous query tile fully drained (epilogue waited on its MMAs)
+      if (tid == 0) {   // the LUT tile: one bulk copy (already in the UMMA layout)
+        const uint32_t bytes = (uint32_t)Npad * (uint32_t)a.K;
+        mbar_expect_tx(bfull, bytes);
+        bulk_g2s(sB, a.tiles + ((size_t)a.lrow[l] + q0) * a.K, bytes, bfull);
+      }
       for (uint32_t j = tid; j < nref * 2; j += LM_WS_THREADS) skipT[j] = 0u;
       if (tid < LM_QT) qid[tid] = (tid < nq_tile) ? a.list_q[a.qptr[l] + q0 + tid] : 0xFFFFFFFFu;
       __syncthreads();
@@ -365,31 +407,17 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
           if (lo < (int)nref && owners[lo] == pl) atomicOr(&skipT[lo * 2 + (tid >> 5)], 1u << (tid & 31));
         }
       }
-      {  // LUT rows of the tile's queries for every K-chunk (128B-swizzled per chunk)
-        const int pieces = a.nchunk * Npad * 8;
-#pragma unroll 4
-        for (int e = tid; e < pieces; e += LM_WS_THREADS) {
-          const int c = e / (Npad * 8), rem = e - c * Npad * 8, jq = rem >> 3, k = rem & 7;
-          uint4 v = make_uint4(0, 0, 0, 0);
-          const uint32_t q = qid[jq];
-          if (q != 0xFFFFFFFFu)
-            v = __ldg(reinterpret_cast<const uint4*>(a.lut + (size_t)q * a.K + c * 128) + k);
-          st_shared_v4(smem_u32(sB + c * LM_BC_BYTES) + jq * 128 + ((k ^ (jq & 7)) << 4), v.x, v.y,
-                       v.z, v.w);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
 
       if (warp < LM_GEN_WARPS) {
-        // ---------------- generators ----------------
-        const int row = warp * 32 + lane;
-        uint32_t cc = chunk_ctr;
-        for (uint32_t t = 0; t < ntiles; ++t) {
+        // ---------------- generators (2 groups of 4: even / odd item tiles) ----------------
+        const int quarter = warp & 3, grp = warp >> 2;  // grp < LM_GROUPS
+        const int row = quarter * 32 + lane;
+        const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16);
+        auto load_codes = [&](uint32_t t, uint64_t* w) {
           const uint32_t item = t * LM_IT + row;
-          const bool ivalid = item < Nl;
-          uint32_t slot = 0;
-          if (ivalid) {
+          if (t < ntiles && item < Nl) {
+            uint32_t slot;
             if (item < own) {
               slot = own0 + item;
             } else {
@@ -397,47 +425,67 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
               while (refoff[j + 1] <= item) ++j;
               slot = a.ref_start[r0 + j] + (item - refoff[j]);
             }
-          }
-          const uint64_t* cw = a.codes64 + ((size_t)(slot >> 5) * a.NU) * 32 + (slot & 31);
-          uint64_t w64 = ivalid ? __ldg(cw) : 0ull;
-          for (int c = 0; c < a.nchunk; ++c, ++cc) {
-            const int s = cc % LM_STAGES;
-            const uint64_t cur = w64;
-            if ((c & 1) == 1 && ivalid && (c >> 1) + 1 < a.NU) w64 = __ldg(cw + ((c >> 1) + 1) * 32);
-            if (cc >= LM_STAGES) mbar_wait(&empty[s], ((cc / LM_STAGES) - 1) & 1u);
-            const uint32_t w32 = (uint32_t)(cur >> (32 * (c & 1)));
-            const uint32_t arow = smem_u32(sA + s * LM_A_BYTES) + row * 128;
+            const uint64_t* cw = a.codes64 + ((size_t)(slot >> 5) * NU) * 32 + (slot & 31);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              uint32_t x = 0, y = 0, z = 0, w = 0;
-              if (ivalid) onehot16((w32 >> (4 * k)) & 15u, x, y, z, w);
-              st_shared_v4(arow + ((k ^ (row & 7)) << 4), x, y, z, w);
+            for (int u = 0; u < NU; ++u) w[u] = __ldg(cw + u * 32);
+          } else {
+#pragma unroll
+            for (int u = 0; u < NU; ++u) w[u] = 0ull;
+          }
+        };
+        uint64_t cur[NU], nxt[NU];
+        load_codes((uint32_t)grp, cur);
+        for (uint32_t t = (uint32_t)grp; t < ntiles; t += LM_GROUPS) {
+          load_codes(t + LM_GROUPS, nxt);  // this group's next tile
+          uint32_t cc = (grp ? gcnt1 : gcnt0) + (t / LM_GROUPS) * NCHUNK;  // group chunk index
+#pragma unroll
+          for (int c = 0; c < NCHUNK; ++c, ++cc) {
+            const int s = grp * LM_GSTAGES + (int)(cc % LM_GSTAGES);
+            const uint32_t w32 = (uint32_t)(cur[c >> 1] >> (32 * (c & 1)));
+            uint32_t v[32];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // one-hot of nibble n: byte n of 16 = 1
+              const uint32_t sh = ((w32 >> (4 * k)) & 15u) << 3;
+              v[4 * k + 0] = shl_clamp(1u, sh);
+              v[4 * k + 1] = shl_clamp(1u, sh - 32u);
+              v[4 * k + 2] = shl_clamp(1u, sh - 64u);
+              v[4 * k + 3] = shl_clamp(1u, sh - 96u);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (cc >= LM_GSTAGES) mbar_wait(&empty[s], ((cc / LM_GSTAGES) - 1) & 1u);
+            tc_fence_after();
+            tmem_st32(tq + (uint32_t)(s * 32), v);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
           }
+#pragma unroll
+          for (int u = 0; u < NU; ++u) cur[u] = nxt[u];
         }
       } else if (warp == LM_MMA_WARP) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
           const uint32_t idesc =
               (2u << 4) | ((uint32_t)(Npad >> 3) << 17) | ((uint32_t)(LM_IT >> 4) << 24);
-          uint32_t cc = chunk_ctr, tc = tile_ctr;
+          mbar_wait(bfull, qt_ctr & 1u);
+          tc_fence_after();
+          uint32_t tc = tile_ctr;
           for (uint32_t t = 0; t < ntiles; ++t, ++tc) {
+            const int grp = (int)(t % LM_GROUPS);
+            uint32_t cc = (grp ? gcnt1 : gcnt0) + (t / LM_GROUPS) * NCHUNK;
             const int acc = tc & 1;
             if (tc >= 2) mbar_wait(&tempty[acc], ((tc >> 1) - 1) & 1u);
             tc_fence_after();
-            const uint32_t dt = tmem + (uint32_t)(acc * LM_QT);
-            for (int c = 0; c < a.nchunk; ++c, ++cc) {
-              const int s = cc % LM_STAGES;
-              mbar_wait(&full[s], (cc / LM_STAGES) & 1u);
+            const uint32_t dt = tmem + LM_ACC_COL + (uint32_t)(acc * LM_QT);
+            for (int c = 0; c < NCHUNK; ++c, ++cc) {
+              const int s = grp * LM_GSTAGES + (int)(cc % LM_GSTAGES);
+              mbar_wait(&full[s], (cc / LM_GSTAGES) & 1u);
               tc_fence_after();
-              const uint64_t ad = umma_desc_sw128(sA + s * LM_A_BYTES);
-              const uint64_t bd = umma_desc_sw128(sB + c * LM_BC_BYTES);
+              const uint64_t bd = umma_desc_sw128(sB + (size_t)c * Npad * 128);
 #pragma unroll
-              for (int k = 0; k < 4; ++k)  // K = 32 bytes per MMA = +2 desc units
-                umma_i8(dt, ad + 2 * k, bd + 2 * k, idesc, (c | k) != 0 ? 1u : 0u);
+              for (int k = 0; k < 4; ++k)  // K = 32 bytes per MMA: 8 TMEM columns, +2 desc units
+                umma_i8_ta(dt, tmem + (uint32_t)(s * 32 + 8 * k), bd + 2 * k, idesc,
+                           (c | k) != 0 ? 1u : 0u);
               umma_commit(&empty[s]);
             }
             umma_commit(&tfull[acc]);
@@ -445,8 +493,9 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
         }
         __syncwarp();
       } else {
-        // ---------------- epilogue ----------------
-        const int lg = warp & 3;  // TMEM lane group of this warp
+        // ---------------- epilogue (8 warps: 2 per TMEM lane quarter) ----------------
+        const int lg = warp & 3;               // TMEM lane quarter of this warp
+        const int half = (warp - LM_EPI0) >> 2;  // column half: blocks 16*half, +32, ...
         const int row = lg * 32 + lane;
         uint32_t tc = tile_ctr;
         for (uint32_t t = 0; t < ntiles; ++t, ++tc) {
@@ -462,19 +511,39 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
           uint64_t ok = (nq_tile >= 64) ? ~0ull : ((1ull << nq_tile) - 1ull);
           if (myref >= 0) ok &= ~((uint64_t)skipT[myref * 2] | ((uint64_t)skipT[myref * 2 + 1] << 32));
           if (!ivalid) ok = 0;
+          // every (row item < Nl8, tile query) cell is written: the score, or the
+          // sentinel (all ones) for a skipped reference (R9) / row padding, so the
+          // selection can stream whole rows with 16-B loads
+          const bool inrow = item < Nl8;
           mbar_wait(&tfull[acc], (tc >> 1) & 1u);
           tc_fence_after();
-          const uint64_t base = a.sbase[l] + (uint64_t)q0 * Nl + item;
-          for (int cb = 0; cb < Npad; cb += 16) {
+          const uint64_t base = a.sbase[l] + (uint64_t)q0 * Nl8 + item;
+          for (int cb = 16 * half; cb < Npad; cb += 32) {
             uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * LM_QT + cb), v);
-            if ((ok >> cb) & 0xFFFFull) {
+            tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + LM_ACC_COL + (uint32_t)(acc * LM_QT + cb), v);
+            if (inrow) {
+              const int jn = min(16, nq_tile - cb);
+              const uint32_t okb = (uint32_t)(ok >> cb) & 0xFFFFu;
+              if (a.score_u32) {
+                uint32_t* p = reinterpret_cast<uint32_t*>(a.S) + base + (uint64_t)cb * Nl8;
+                if (jn == 16) {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if ((ok >> (cb + j)) & 1ull) {
-                  const uint64_t o = base + (uint64_t)(cb + j) * Nl;
-                  if (a.score_u32) reinterpret_cast<uint32_t*>(a.S)[o] = v[j];
-                  else reinterpret_cast<uint16_t*>(a.S)[o] = (uint16_t)v[j];
+                  for (int j = 0; j < 16; ++j) p[(size_t)j * Nl8] = ((okb >> j) & 1u) ? v[j] : 0xFFFFFFFFu;
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j)
+                    if (j < jn) p[(size_t)j * Nl8] = ((okb >> j) & 1u) ? v[j] : 0xFFFFFFFFu;
+                }
+              } else {
+                uint16_t* p = reinterpret_cast<uint16_t*>(a.S) + base + (uint64_t)cb * Nl8;
+                if (jn == 16) {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j)
+                    p[(size_t)j * Nl8] = ((okb >> j) & 1u) ? (uint16_t)v[j] : (uint16_t)0xFFFFu;
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j)
+                    if (j < jn) p[(size_t)j * Nl8] = ((okb >> j) & 1u) ? (uint16_t)v[j] : (uint16_t)0xFFFFu;
                 }
               }
             }
@@ -484,15 +553,21 @@ __global__ void __launch_bounds__(LM_WS_THREADS, 2) lm_tensor_kernel(LMArgs a) {
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
       }
-      chunk_ctr += ntiles * a.nchunk;
+      if (LM_GROUPS == 2) {
+        gcnt0 += ((ntiles + 1) / 2) * NCHUNK;
+        gcnt1 += (ntiles / 2) * NCHUNK;
+      } else {
+        gcnt0 += ntiles * NCHUNK;
+      }
       tile_ctr += ntiles;
+      ++qt_ctr;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == LM_MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem, 2 * LM_QT);
+    tmem_dealloc(tmem, LM_TMEM_COLS);
   }
 }
 
@@ -518,6 +593,8 @@ struct SelArgs {
   const uint32_t* ref_item_off;
   const uint32_t* list_items;
   const uint32_t* slot_rows;
+  const uint64_t* list_base;
+  const uint32_t* list_ids;
   const uint64_t* sbase;
   const void* S;
   int score_u32;
@@ -588,96 +665,175 @@ __device__ void warp_sort_keys(uint64_t* a, int n) {
   }
 }
 
-__global__ void __launch_bounds__(SW_WARPS * 32) lm_select_kernel(SelArgs a) {
+// One WARP per query: exact top-bigK of the keys (s << 32 | id) over U(q).
+// The query's score rows (one per probed list, padded to 8 items; skipped
+// references and padding hold the all-ones sentinel, R9) are streamed twice
+// with 16-B loads:
+//   pass 1  histogram of s >> hshift over every valid item -> the smallest bin
+//           b* whose cumulative count reaches bigK: every item of the top-bigK
+//           has bin <= b*, and only ~bigK + |bin b*| items do;
+//   pass 2  items with bin <= b* are appended as PRE-keys (s << 32 | p << 22 |
+//           item) -- no id load on the streaming path;
+//   finish  the ids of the (few) candidates are loaded in one batch, the keys
+//           sorted, the first bigK written.
+// If more than `cap` items share bins <= b* (massive score ties) the warp
+// switches to exact mode: candidates are resolved to (s, id) keys, sorted and
+// cut to bigK (tau = the bigK-th key), later items are compared against tau.
+// DCO = owned + non-skipped referenced items (R17).
+__device__ __forceinline__ uint32_t sel_pos(uint32_t p, uint32_t item) {
+  return (p << 22) | item;
+}
+
+template <bool U32>
+__device__ __forceinline__ void sel_resolve(const SelArgs& a, int64_t q, uint64_t* cand,
+                                            uint32_t n) {
+  const int lane = lane_id();
+  for (uint32_t i = lane; i < n; i += 32) {  // independent loads, all in flight
+    const uint64_t v = cand[i];
+    const uint32_t pos = (uint32_t)v, p = pos >> 22, item = pos & ((1u << 22) - 1u);
+    const uint32_t l = (uint32_t)a.probes[q * a.nprobe + p];
+    const uint32_t id = __ldg(a.list_ids + a.list_base[l] + item);
+    cand[i] = (v & 0xFFFFFFFF00000000ull) | id;
+  }
+  __syncwarp();
+}
+
+template <bool U32>
+__global__ void __launch_bounds__(SW_WARPS * 32, 1) lm_select_kernel(SelArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
   uint32_t* hist = reinterpret_cast<uint32_t*>(sm) + warp * SW_NB;
   uint64_t* cand = reinterpret_cast<uint64_t*>(reinterpret_cast<uint32_t*>(sm) + SW_WARPS * SW_NB) +
                    (size_t)warp * a.cap;
   const uint32_t bigK = (uint32_t)a.bigK;
+  constexpr uint32_t SENT = U32 ? 0xFFFFFFFFu : 0xFFFFu;
+  constexpr int PER = U32 ? 4 : 8;  // scores per 16-B vector
   for (int64_t q = (int64_t)blockIdx.x * SW_WARPS + warp; q < a.nq;
        q += (int64_t)gridDim.x * SW_WARPS) {
     for (int i = lane; i < SW_NB; i += 32) hist[i] = 0u;
     __syncwarp();
-    uint32_t cnt = 0, bthr = SW_NB - 1, since = 0, dco = 0;
-    uint64_t tau = kKeyInf;
     const uint32_t* qb = a.qbits + (size_t)q * a.qwords;
+    // ---- pass 1: DCO and the score histogram
+    uint32_t dco = 0;
     for (int p = 0; p < a.nprobe; ++p) {
       const uint32_t l = (uint32_t)a.probes[q * a.nprobe + p];
-      const uint32_t Nl = a.list_items[l];
-      const uint64_t row = a.sbase[l] + (uint64_t)a.qslot[q * a.nprobe + p] * Nl;
+      const uint32_t Nl = a.list_items[l], Nl8 = (Nl + 7u) & ~7u;
       const uint32_t r0 = a.ref_ptr[l], nref = a.ref_ptr[l + 1] - r0;
-      for (int src = -1; src < (int)nref; ++src) {
-        uint32_t n, slot0;
-        uint64_t off;
-        if (src < 0) {
-          n = a.own_cnt[l];
-          slot0 = a.own_off[l];
-          off = row;
-        } else {
-          const int o = a.ref_owner[r0 + src];
-          if ((qb[o >> 5] >> (o & 31)) & 1u) continue;   // owner probed: scanned there (R9)
-          n = a.ref_cnt[r0 + src];
-          slot0 = a.ref_start[r0 + src];
-          off = row + a.ref_item_off[r0 + src];
+      uint32_t c = 0;
+      for (uint32_t j = lane; j < nref; j += 32) {
+        const int o = a.ref_owner[r0 + j];
+        if (!((qb[o >> 5] >> (o & 31)) & 1u)) c += a.ref_cnt[r0 + j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      dco += a.own_cnt[l] + c;
+      const uint64_t row = a.sbase[l] + (uint64_t)a.qslot[q * a.nprobe + p] * Nl8;
+      const uint4* rv = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
+      const uint32_t nv = Nl8 / PER;
+      for (uint32_t v0 = 0; v0 < nv; v0 += 64) {
+        uint4 x[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t vi = v0 + 32 * u + lane;
+          x[u] = (vi < nv) ? __ldg(rv + vi) : make_uint4(~0u, ~0u, ~0u, ~0u);
         }
-        dco += n;
-        for (uint32_t i00 = 0; i00 < n; i00 += 128) {
-          uint32_t sv[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {  // 4 independent loads in flight per lane
-            const uint32_t i = i00 + 32 * u + lane;
-            sv[u] = 0;
-            if (i < n)
-              sv[u] = a.score_u32 ? reinterpret_cast<const uint32_t*>(a.S)[off + i]
-                                  : (uint32_t)reinterpret_cast<const uint16_t*>(a.S)[off + i];
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t w4[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+          for (int e = 0; e < PER; ++e) {
+            const uint32_t sc = U32 ? w4[e] : ((w4[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+            if (sc != SENT) atomicAdd(&hist[sc >> a.hshift], 1u);
           }
+        }
+      }
+    }
+    __syncwarp();
+    const uint32_t bstar = warp_bthr(hist, bigK);
+    uint32_t thr = min(SENT - 1u, (uint32_t)(((uint64_t)(bstar + 1) << a.hshift) - 1u));
+    // ---- pass 2: collect the items with bin <= b*
+    uint32_t cnt = 0;
+    bool exact = false;
+    uint64_t tau = kKeyInf;
+    for (int p = 0; p < a.nprobe; ++p) {
+      const uint32_t l = (uint32_t)a.probes[q * a.nprobe + p];
+      const uint32_t Nl = a.list_items[l], Nl8 = (Nl + 7u) & ~7u;
+      const uint64_t row = a.sbase[l] + (uint64_t)a.qslot[q * a.nprobe + p] * Nl8;
+      const uint32_t* lids = a.list_ids + a.list_base[l];
+      const uint4* rv = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
+      const uint32_t nv = Nl8 / PER;
+      for (uint32_t v0 = 0; v0 < nv; v0 += 64) {
+        uint4 x[2];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t i = i00 + 32 * u + lane;
-            if (i00 + 32 * u >= n) break;   // warp-uniform
-            const bool valid = i < n;
-            const uint32_t s = sv[u];
-            const uint32_t bin = s >> a.hshift;
-            const bool maybe = valid && bin <= bthr;
-            if (!__any_sync(0xffffffffu, maybe)) continue;
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t vi = v0 + 32 * u + lane;
+          x[u] = (vi < nv) ? __ldcs(rv + vi) : make_uint4(~0u, ~0u, ~0u, ~0u);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t w4[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+          uint32_t pm = 0;  // this lane's items with score <= thr (the sentinel never passes)
+          if (U32) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pm |= (w4[e] <= thr ? 1u : 0u) << e;
+          } else {
+            const uint32_t t2 = thr | (thr << 16);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t cm = __vcmpleu2(w4[e], t2);  // 0xFFFF per passing half
+              pm |= ((cm & 1u) | ((cm >> 15) & 2u)) << (2 * e);
+            }
+          }
+          const uint32_t item0 = (v0 + 32 * u + lane) * PER;
+          while (__any_sync(0xffffffffu, pm != 0)) {
+            bool pass = pm != 0;
             uint64_t key = kKeyInf;
-            if (maybe) {
-              const uint32_t r = a.slot_rows[slot0 + i];
-              key = ((uint64_t)s << 32) | (r * (uint32_t)a.nshards + (uint32_t)a.shard_id);
-            }
-            const bool pass = maybe && key < tau;
-            const unsigned bal = __ballot_sync(0xffffffffu, pass);
             if (pass) {
-              cand[cnt + __popc(bal & ((1u << lane) - 1u))] = key;
-              atomicAdd(&hist[bin], 1u);
-            }
-            cnt += __popc(bal);
-            since += __popc(bal);
-            __syncwarp();
-            if (since >= 64) {
-              since = 0;
-              bthr = min(bthr, warp_bthr(hist, bigK));
-            }
-            if (cnt + 32 > (uint32_t)a.cap) {
-              bthr = min(bthr, warp_bthr(hist, bigK));
-              cnt = warp_filter(cand, cnt, bthr, tau, a.hshift);
-              if (cnt + 32 > (uint32_t)a.cap) {   // pathological ties: sort, keep bigK exactly
-                int np = 2;
-                while (np < (int)cnt) np <<= 1;
-                for (int e = cnt + lane; e < np; e += 32) cand[e] = kKeyInf;
-                __syncwarp();
-                warp_sort_keys(cand, np);
-                cnt = bigK;
-                tau = cand[bigK - 1];
+              const int e = __ffs(pm) - 1;
+              pm &= pm - 1u;
+              uint32_t sc;
+              if (U32) {
+                sc = e == 0 ? w4[0] : e == 1 ? w4[1] : e == 2 ? w4[2] : w4[3];
+              } else {
+                const uint32_t ww = (e >> 1) == 0 ? w4[0] : (e >> 1) == 1 ? w4[1]
+                                  : (e >> 1) == 2 ? w4[2] : w4[3];
+                sc = (ww >> (16 * (e & 1))) & 0xFFFFu;
               }
+              if (sc > thr) {
+                pass = false;  // thr tightened (exact mode) since pm was formed
+              } else if (!exact) {
+                key = ((uint64_t)sc << 32) | sel_pos((uint32_t)p, item0 + e);
+              } else {
+                key = ((uint64_t)sc << 32) | __ldg(lids + item0 + e);
+                pass = key < tau;
+              }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, pass);
+            if (pass) cand[cnt + __popc(bal & ((1u << lane) - 1u))] = key;
+            cnt += __popc(bal);
+            __syncwarp();
+            if (cnt + 32 > (uint32_t)a.cap) {  // massive ties: exact (s, id) keys, keep bigK
+              if (!exact) {
+                sel_resolve<U32>(a, q, cand, cnt);
+                exact = true;
+              }
+              int np = 2;
+              while (np < (int)cnt) np <<= 1;
+              for (int f = cnt + lane; f < np; f += 32) cand[f] = kKeyInf;
+              __syncwarp();
+              warp_sort_keys(cand, np);
+              cnt = bigK;
+              tau = cand[bigK - 1];
+              thr = min(thr, (uint32_t)(tau >> 32));
             }
           }
         }
       }
     }
-    bthr = min(bthr, warp_bthr(hist, bigK));
-    cnt = warp_filter(cand, cnt, bthr, tau, a.hshift);
+    if (!exact) sel_resolve<U32>(a, q, cand, cnt);
+    cnt = warp_filter(cand, cnt, bstar, tau, a.hshift);
     int np = 2;
     while (np < (int)cnt) np <<= 1;
     for (int e = cnt + lane; e < np; e += 32) cand[e] = kKeyInf;
@@ -693,13 +849,31 @@ __global__ void __launch_bounds__(SW_WARPS * 32) lm_select_kernel(SelArgs a) {
 // ---------------------------------------------------------------------------
 static int sel_cap(int bigK) { return next_pow2(2 * bigK + 64); }
 
+static int lm_qt(int K) {  // queries per LUT tile: QT x K <= LM_B_MAX, multiple of 16, <= 64
+  int qt = (int)(LM_B_MAX / (uint32_t)K);
+  qt = std::min(qt, LM_QT);
+  return qt - (qt % 16);
+}
+
+static bool lm_nu_ok(int NU) { return NU == 1 || NU == 2 || NU == 3 || NU == 4 || NU == 6 || NU == 8; }
+
 bool listmajor_ok(const rairs_index_s* idx, int nprobe, int bigK) {
   if (idx->scan_mode == 1) return false;            // forced SIMT query-major scan
-  if (!idx->list_items || !idx->ref_item_off) return false;
+  if (!idx->list_items || !idx->ref_item_off || !idx->list_ids) return false;
   if (idx->max_refs > LM_MAXREF) return false;
-  if ((size_t)(idx->M_pad / 8) * LM_BC_BYTES + 4 * LM_A_BYTES > 200 * 1024) return false;
+  if (!lm_nu_ok(idx->M_pad / 16) || lm_qt(idx->M_pad * 16) < 16) return false;
   if ((size_t)SW_WARPS * (SW_NB * 4 + (size_t)sel_cap(bigK) * 8) > 200 * 1024) return false;
+  if (nprobe > 1024 || idx->max_list_items >= (1 << 22)) return false;  // pre-key packing
   return true;
+}
+
+template <int NU>
+static cudaError_t launch_lm_tensor(const LMArgs& la, size_t tsm, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(lm_tensor_kernel<NU>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+  if (e != cudaSuccess) return e;
+  lm_tensor_kernel<NU><<<148 * LM_CTAS_PER_SM, LM_WS_THREADS, tsm, s>>>(la);
+  return cudaGetLastError();
 }
 
 rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s) {
@@ -708,28 +882,31 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   const int nprobe = sa.nprobe, nlist = idx->nlist;
   const int bigK = sa.k * sa.refine_factor;
   const int K = idx->M_pad * 16;
+  const int QT = lm_qt(K);
   const int qwords = (nlist + 31) / 32;
   const int64_t npairs = nq * nprobe;
   const int score_u32 = ((int64_t)idx->M * 255 > 65535) ? 1 : 0;
-  uint8_t* lut = nullptr;
-  uint32_t *cnt = nullptr, *qslot = nullptr, *qptr = nullptr, *tptr = nullptr, *list_q = nullptr,
+  uint8_t* tiles = nullptr;
+  uint32_t *cnt = nullptr, *qslot = nullptr, *qptr = nullptr, *lrow = nullptr, *list_q = nullptr,
            *qbits = nullptr, *totals = nullptr;
   uint64_t* sbase = nullptr;
   void* S = nullptr;
   // bound on the score buffer: every (query, probe) pair times the largest list-task
-  const size_t s_elems = (size_t)npairs * (size_t)std::max<int64_t>(idx->max_list_items, 1);
+  const size_t s_elems = (size_t)npairs * (size_t)round_up(std::max<int64_t>(idx->max_list_items, 1), 8);
   const size_t s_bytes = s_elems * (score_u32 ? 4 : 2);
+  // LUT tiles: every (query, probe) row, plus <= 15 padding rows per list
+  const size_t tile_bytes = ((size_t)npairs + 15 * (size_t)nlist) * K;
   auto cleanup = [&]() {
-    cudaFreeAsync(lut, s); cudaFreeAsync(cnt, s); cudaFreeAsync(qslot, s); cudaFreeAsync(qptr, s);
-    cudaFreeAsync(tptr, s); cudaFreeAsync(list_q, s); cudaFreeAsync(qbits, s);
+    cudaFreeAsync(tiles, s); cudaFreeAsync(cnt, s); cudaFreeAsync(qslot, s); cudaFreeAsync(qptr, s);
+    cudaFreeAsync(lrow, s); cudaFreeAsync(list_q, s); cudaFreeAsync(qbits, s);
     cudaFreeAsync(totals, s); cudaFreeAsync(sbase, s); cudaFreeAsync(S, s);
   };
 #define LM_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return _e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA; } } while (0)
-  LM_TRY(cudaMallocAsync(&lut, (size_t)nq * K, s));
+  LM_TRY(cudaMallocAsync(&tiles, tile_bytes, s));
   LM_TRY(cudaMallocAsync(&cnt, (size_t)(nlist + 1) * 4 + 16, s));
   LM_TRY(cudaMallocAsync(&qslot, (size_t)npairs * 4, s));
   LM_TRY(cudaMallocAsync(&qptr, (size_t)(nlist + 1) * 4, s));
-  LM_TRY(cudaMallocAsync(&tptr, (size_t)(nlist + 1) * 4, s));
+  LM_TRY(cudaMallocAsync(&lrow, (size_t)(nlist + 1) * 4, s));
   LM_TRY(cudaMallocAsync(&list_q, (size_t)npairs * 4, s));
   LM_TRY(cudaMallocAsync(&qbits, (size_t)nq * qwords * 4, s));
   LM_TRY(cudaMallocAsync(&totals, 16, s));
@@ -738,18 +915,23 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(cudaMemsetAsync(cnt, 0, (size_t)(nlist + 1) * 4 + 16, s));
   LM_TRY(cudaMemsetAsync(qbits, 0, (size_t)nq * qwords * 4, s));
   unsigned* list_counter = cnt + nlist + 1;  // zeroed tail of cnt
-  // 1. quantised LUTs (O2), one warp per query
-  lut_batch_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq, LW), 1 << 30), LW * 32, 0, s>>>(
-      sa.queries, nq, idx->d, idx->codebook, idx->M, idx->M_pad, idx->dsub, lut, sa.lut_a, sa.lut_b,
-      sa.lut_q);
-  LM_TRY(cudaGetLastError());
-  // 2. group (query, probe) pairs by list
+  // 1. group (query, probe) pairs by list
   const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npairs, 256), 148 * 8));
   lm_count_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, cnt, qslot);
-  lm_scan_kernel<<<1, SCN, 0, s>>>(cnt, idx->list_items, nlist, qptr, sbase, tptr, totals, LM_QT,
+  lm_scan_kernel<<<1, SCN, 0, s>>>(cnt, idx->list_items, nlist, qptr, sbase, lrow, totals, QT,
                                    LM_IT);
   lm_scatter_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, nprobe, qptr, qslot, list_q, qbits, qwords);
   LM_TRY(cudaGetLastError());
+  // 2. quantised LUTs (O2), one warp per query, written into the list-task tiles
+  {
+    if (idx->dsub > LUT_MAX_DSUB) { cleanup(); set_error("list-major: d/M > 8"); return RAIRS_E_UNSUPPORTED; }
+    const size_t lsm = ((size_t)16 * idx->dsub * idx->M + (size_t)LW * idx->M) * 4;
+    LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    lut_tiles_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq, LW), 1 << 30), LW * 32, lsm, s>>>(
+        sa.queries, nq, idx->d, idx->codebook, idx->M, idx->M_pad, idx->dsub, sa.probes, nprobe,
+        qslot, cnt, lrow, QT, tiles, sa.lut_a, sa.lut_b, sa.lut_q);
+    LM_TRY(cudaGetLastError());
+  }
   // 3. tensor-core scores, one list at a time
   LMArgs la{};
   la.codes64 = reinterpret_cast<const uint64_t*>(idx->codes);
@@ -760,11 +942,10 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.ref_start = idx->ref_start;
   la.ref_item_off = idx->ref_item_off;
   la.list_items = idx->list_items;
-  la.NU = idx->M_pad / 16;
-  la.nchunk = idx->M_pad / 8;
-  la.lut = lut;
   la.K = K;
-  la.b_resident = 1;  // LUT tile (64 queries x K) resident per query tile
+  la.QT = QT;
+  la.tiles = tiles;
+  la.lrow = lrow;
   la.probes = sa.probes;
   la.nprobe = nprobe;
   la.qptr = qptr;
@@ -774,12 +955,17 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.S = S;
   la.score_u32 = score_u32;
   la.nlist = nlist;
-  const size_t tsm = 1024 + LM_STAGES * LM_A_BYTES + (size_t)la.nchunk * LM_BC_BYTES + LM_MAXREF * 8 +
-                     8 + LM_MAXREF * 8 + LM_QT * 4 + (2 * LM_STAGES + 4) * 8 + 64;
-  LM_TRY(cudaFuncSetAttribute(lm_tensor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-  const int per_sm = (tsm <= 110 * 1024) ? 2 : 1;
-  lm_tensor_kernel<<<148 * per_sm, LM_WS_THREADS, tsm, s>>>(la);
-  LM_TRY(cudaGetLastError());
+  const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 +
+                     (2 * LM_STAGES + 5) * 8 + 64;
+  switch (idx->M_pad / 16) {
+    case 1: LM_TRY(launch_lm_tensor<1>(la, tsm, s)); break;
+    case 2: LM_TRY(launch_lm_tensor<2>(la, tsm, s)); break;
+    case 3: LM_TRY(launch_lm_tensor<3>(la, tsm, s)); break;
+    case 4: LM_TRY(launch_lm_tensor<4>(la, tsm, s)); break;
+    case 6: LM_TRY(launch_lm_tensor<6>(la, tsm, s)); break;
+    case 8: LM_TRY(launch_lm_tensor<8>(la, tsm, s)); break;
+    default: cleanup(); set_error("list-major: unsupported M"); return RAIRS_E_INTERNAL;
+  }
   // 4. per-query selection (warp per query)
   SelArgs sl{};
   sl.probes = sa.probes;
@@ -801,6 +987,8 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.ref_item_off = idx->ref_item_off;
   sl.list_items = idx->list_items;
   sl.slot_rows = idx->slot_rows;
+  sl.list_base = idx->list_base;
+  sl.list_ids = idx->list_ids;
   sl.sbase = sbase;
   sl.S = S;
   sl.score_u32 = score_u32;
@@ -809,8 +997,14 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.out_keys = sa.cand_keys;
   sl.dco = sa.dco;
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
-  LM_TRY(cudaFuncSetAttribute(lm_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-  lm_select_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq, SW_WARPS), 1 << 30), SW_WARPS * 32, ssm, s>>>(sl);
+  const unsigned sgrid = (unsigned)std::min<int64_t>(ceil_div(nq, SW_WARPS), 1 << 30);
+  if (score_u32) {
+    LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    lm_select_kernel<true><<<sgrid, SW_WARPS * 32, ssm, s>>>(sl);
+  } else {
+    LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    lm_select_kernel<false><<<sgrid, SW_WARPS * 32, ssm, s>>>(sl);
+  }
   LM_TRY(cudaGetLastError());
   cleanup();
   return RAIRS_OK;
@@ -833,6 +1027,31 @@ __global__ void lm_items_kernel(const uint32_t* __restrict__ own_cnt,
   }
 }
 
+// item -> global id of every list-task (owned region, then references in
+// ascending owner order): the selection's slow path needs one load per item
+__global__ void lm_ids_kernel(const uint32_t* __restrict__ own_off,
+                              const uint32_t* __restrict__ own_cnt,
+                              const uint32_t* __restrict__ ref_ptr,
+                              const uint32_t* __restrict__ ref_start,
+                              const uint32_t* __restrict__ ref_cnt,
+                              const uint32_t* __restrict__ slot_rows,
+                              const uint64_t* __restrict__ list_base, int nlist, int shard_id,
+                              int nshards, uint32_t* __restrict__ list_ids) {
+  for (int l = blockIdx.x; l < nlist; l += gridDim.x) {
+    uint32_t* out = list_ids + list_base[l];
+    const uint32_t own = own_cnt[l], o0 = own_off[l];
+    for (uint32_t i = threadIdx.x; i < own; i += blockDim.x)
+      out[i] = slot_rows[o0 + i] * (uint32_t)nshards + (uint32_t)shard_id;
+    uint32_t off = own;
+    for (uint32_t j = ref_ptr[l]; j < ref_ptr[l + 1]; ++j) {
+      const uint32_t c = ref_cnt[j], s0 = ref_start[j];
+      for (uint32_t i = threadIdx.x; i < c; i += blockDim.x)
+        out[off + i] = slot_rows[s0 + i] * (uint32_t)nshards + (uint32_t)shard_id;
+      off += c;
+    }
+  }
+}
+
 rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
   RAIRS_CUDA_TRY(cudaMalloc(&idx->list_items, (size_t)idx->nlist * 4));
   RAIRS_CUDA_TRY(cudaMalloc(&idx->ref_item_off, (size_t)std::max<int64_t>(idx->n_refs, 1) * 4));
@@ -845,8 +1064,22 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
                                  cudaMemcpyDeviceToHost, s));
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
   idx->max_list_items = 0;
-  for (uint32_t v : h) idx->max_list_items = std::max<int64_t>(idx->max_list_items, v);
-  idx->device_bytes += (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4;
+  std::vector<uint64_t> base(idx->nlist + 1, 0);
+  for (int l = 0; l < idx->nlist; ++l) {
+    idx->max_list_items = std::max<int64_t>(idx->max_list_items, h[l]);
+    base[l + 1] = base[l] + h[l];
+  }
+  RAIRS_CUDA_TRY(cudaMalloc(&idx->list_base, (size_t)(idx->nlist + 1) * 8));
+  RAIRS_CUDA_TRY(cudaMalloc(&idx->list_ids, (size_t)std::max<uint64_t>(base[idx->nlist], 1) * 4));
+  RAIRS_CUDA_TRY(cudaMemcpyAsync(idx->list_base, base.data(), (size_t)(idx->nlist + 1) * 8,
+                                 cudaMemcpyHostToDevice, s));
+  lm_ids_kernel<<<std::min(idx->nlist, 148 * 8), 256, 0, s>>>(
+      idx->own_off, idx->own_cnt, idx->ref_ptr, idx->ref_start, idx->ref_cnt, idx->slot_rows,
+      idx->list_base, idx->nlist, idx->shard_id, idx->nshards, idx->list_ids);
+  RAIRS_CHECK_LAUNCH();
+  RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  idx->device_bytes += (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4 +
+                       (size_t)(idx->nlist + 1) * 8 + (size_t)base[idx->nlist] * 4;
   return RAIRS_OK;
 }
 

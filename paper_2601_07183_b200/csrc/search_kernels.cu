@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "index.cuh"
+#include "tc_helpers.cuh"
 
 namespace rairs {
 
@@ -648,8 +649,135 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
   }
 }
 
+// K6 refine, staged variant (d = 4*D4 <= 128, bigK <= 128): a persistent CTA
+// walks queries.  Warp w gathers the rows w, w+8, ... of a query with one
+// coalesced 16-B-per-lane load per row (all of its rows in flight at once)
+// into registers; the NEXT query's rows are loaded while thread c runs
+// candidate c's serial fp64 sum (ascending t, O10 -- the same order and
+// rounding as refine_kernel) over the current query's padded shared tile.
+// The top-k by the unique key (bits(delta) << 32 | id) is found by rank
+// counting.
+constexpr int RS_THREADS = 256;
+constexpr int RS_ROWS = 128;
+
+template <int D4>
+__global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
+    const uint64_t* __restrict__ keys, int64_t nq, int bigK, int k,
+    const float* __restrict__ queries, const float* __restrict__ X, int G,
+    int64_t* __restrict__ out_ids, float* __restrict__ out_dists) {
+  constexpr int D = 4 * D4, RSF = D + 4;  // tile row stride (floats): conflict-free float4 reads
+  extern __shared__ __align__(16) float tile[];  // [bigK rounded to 8][RSF]
+  __shared__ double qs[D];
+  __shared__ uint64_t rk[RS_ROWS];
+  __shared__ uint32_t gids[RS_ROWS];
+  __shared__ uint32_t nvalid;
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const int myrow = warp + 8 * lane;  // lane j (< 16) fetches the key of row warp + 8j
+  uint32_t gid = 0xFFFFFFFFu;
+  float4 v[16];
+  auto fetch = [&](int64_t q) {
+    gid = 0xFFFFFFFFu;
+    uint32_t rowi = 0;
+    if (lane < 16 && myrow < bigK) {
+      const uint64_t key = __ldg(keys + q * bigK + myrow);
+      if (key != kKeyInf) {
+        gid = (uint32_t)(key & 0xFFFFFFFFu);
+        rowi = gid / (uint32_t)G;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t g = __shfl_sync(0xffffffffu, gid, j);
+      const uint32_t r = __shfl_sync(0xffffffffu, rowi, j);
+      v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g != 0xFFFFFFFFu && lane < D4) v[j] = __ldg(reinterpret_cast<const float4*>(X + (size_t)r * D) + lane);
+    }
+  };
+  int64_t q = blockIdx.x;
+  if (q < nq) fetch(q);
+  for (; q < nq; q += gridDim.x) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (warp + 8 * j < bigK && lane < D4)
+        *reinterpret_cast<float4*>(tile + (warp + 8 * j) * RSF + 4 * lane) = v[j];
+    if (lane < 16 && myrow < bigK) gids[myrow] = gid;
+    if (tid < D) qs[tid] = (double)queries[q * D + tid];
+    if (tid == 0) nvalid = 0;
+    __syncthreads();
+    const int64_t qn = q + gridDim.x;
+    if (qn < nq) fetch(qn);  // next query's rows in flight during this query's compute
+    if (tid < bigK) {
+      const uint32_t g = gids[tid];
+      uint64_t out = kKeyInf;
+      if (g != 0xFFFFFFFFu) {
+        const float4* xr = reinterpret_cast<const float4*>(tile + tid * RSF);
+        double acc = 0.0;
+#pragma unroll 8
+        for (int i = 0; i < D4; ++i) {
+          const float4 xv = xr[i];
+          double df;
+          df = __dsub_rn(qs[4 * i + 0], (double)xv.x); acc = __dadd_rn(acc, __dmul_rn(df, df));
+          df = __dsub_rn(qs[4 * i + 1], (double)xv.y); acc = __dadd_rn(acc, __dmul_rn(df, df));
+          df = __dsub_rn(qs[4 * i + 2], (double)xv.z); acc = __dadd_rn(acc, __dmul_rn(df, df));
+          df = __dsub_rn(qs[4 * i + 3], (double)xv.w); acc = __dadd_rn(acc, __dmul_rn(df, df));
+        }
+        out = ((uint64_t)__float_as_uint(__double2float_rn(acc)) << 32) | g;
+        atomicAdd(&nvalid, 1u);
+      }
+      rk[tid] = out;
+    }
+    __syncthreads();
+    if (tid < bigK) {
+      const uint64_t kc = rk[tid];
+      if (kc != kKeyInf) {
+        int rank = 0;
+#pragma unroll 8
+        for (int j = 0; j < bigK; ++j) rank += (rk[j] < kc) ? 1 : 0;
+        if (rank < k) {
+          out_ids[q * k + rank] = (int64_t)(uint32_t)(kc & 0xFFFFFFFFu);
+          out_dists[q * k + rank] = __uint_as_float((uint32_t)(kc >> 32));
+        }
+      }
+    }
+    for (int i = (int)nvalid + tid; i < k; i += RS_THREADS) {
+      out_ids[q * k + i] = -1;
+      out_dists[q * k + i] = __int_as_float(0x7f800000);
+    }
+    __syncthreads();  // tile / gids / rk / nvalid free for the next query
+  }
+}
+
+template <int D4>
+static rairs_status launch_refine_stage(const rairs_index_s* idx, const SearchArgs& a, int bigK,
+                                        cudaStream_t s) {
+  const size_t smem = (size_t)round_up(bigK, 8) * (4 * D4 + 4) * 4;
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(refine_stage_kernel<D4>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, refine_stage_kernel<D4>,
+                                                               RS_THREADS, smem));
+  const int grid = (int)std::min<int64_t>(a.nq, (int64_t)148 * std::max(occ, 1));
+  refine_stage_kernel<D4><<<grid, RS_THREADS, smem, s>>>(a.cand_keys, a.nq, bigK, a.k, a.queries,
+                                                          idx->X, idx->nshards, a.out_ids,
+                                                          a.out_dists);
+  RAIRS_CHECK_LAUNCH();
+  return RAIRS_OK;
+}
+
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s) {
   if (a.nq <= 0) return RAIRS_OK;
+  {
+    const int bigK = a.k * a.refine_factor;
+    if (bigK <= RS_ROWS) {
+      switch (idx->d) {
+        case 32: return launch_refine_stage<8>(idx, a, bigK, s);
+        case 64: return launch_refine_stage<16>(idx, a, bigK, s);
+        case 96: return launch_refine_stage<24>(idx, a, bigK, s);
+        case 128: return launch_refine_stage<32>(idx, a, bigK, s);
+        default: break;
+      }
+    }
+  }
   const int bigK = a.k * a.refine_factor;
   const int npow = next_pow2(std::max(bigK, 2));
   const size_t smem = (size_t)npow * 8 + (size_t)idx->d * 8 + (size_t)RT * RSTRIDE * 4 + RT * 4;

@@ -228,6 +228,20 @@ class Index:
         return {"ms": {"coarse": ms[0], "scan": ms[1], "refine": ms[2]},
                 "launches": {"coarse": nl[0], "scan": nl[1], "refine": nl[2]}}
 
+    def scan_path(self, k: int, nprobe: int, refine_factor: int) -> str:
+        """'listmajor' or 'simt': the scan kernels a search with these parameters uses."""
+        sp = ctypes.c_int32()
+        check(lib().rairs_search_plan(self._h, k, nprobe, refine_factor, None, ctypes.byref(sp)),
+              "rairs_search_plan")
+        return "listmajor" if sp.value == 2 else "simt"
+
+    def kernels_launched(self, reset: bool = True) -> int:
+        """Kernels the library launched for searches since the last reset."""
+        v = ctypes.c_int64()
+        check(lib().rairs_profile_kernels(self._h, ctypes.byref(v), int(bool(reset))),
+              "rairs_profile_kernels")
+        return int(v.value)
+
 
 def build_index(base: torch.Tensor, nlist: int, M: int, nbits: int = 4,
                 assignment: str = "AIR", **kw) -> Index:

@@ -69,7 +69,14 @@ CONFIGS = {
                        note="paper-like c2 (SURVEY §8(d) '-pl')"),
     "c3": ConfigSpec("c3", 1_000_000, 1536, 10_000, 4096, 384, 10, 32, 10, "sphere",
                      0.6 / np.sqrt(1536.0), 3, 4096, note="BJ configs[2]"),
+    # large configs: drawn on the device by synth.gpu_generators (torch Philox)
+    "c4": ConfigSpec("c4", 10_000_000, 96, 10_000, 16384, 48, 10, 32, 10, "aniso",
+                     1.0, 4, 16384, note="BJ configs[3]"),
+    "c5": ConfigSpec("c5", 100_000_000, 128, 10_000, 65536, 64, 10, 64, 10, "gauss_gpu",
+                     0.25, 5, 65536, note="BJ configs[4] (one 10k batch of the 100k queries)"),
 }
+
+GPU_KINDS = ("aniso", "gauss_gpu")
 
 
 def get_config(name: str, **overrides) -> ConfigSpec:
@@ -153,6 +160,11 @@ def make_dataset(spec: ConfigSpec, n: Optional[int] = None,
         means /= np.linalg.norm(means, axis=1, keepdims=True)
         base = _draw_sphere(rng, spec, means, n)
         qry = _draw_sphere(rng, spec, means, nq)
+    elif spec.kind in GPU_KINDS:
+        import torch
+        from .gpu_generators import make_dataset_torch
+        b, q = make_dataset_torch(spec, torch.device("cpu"), n=n, nq=nq)
+        return b.numpy(), q.numpy()
     else:
         raise ValueError(f"unknown generator kind {spec.kind!r}")
     return np.ascontiguousarray(base), np.ascontiguousarray(qry)

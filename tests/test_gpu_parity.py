@@ -154,6 +154,17 @@ def test_search_parity(oracle_mod, name, k, nprobe, rf, scan):
     assert_search_equal(g, o)
 
 
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
+def test_search_parity_many_queries(oracle_mod, scan):
+    # 2,000 queries x nprobe 16 over 64 lists: ~500 queries per list -> 8 LUT/query
+    # tiles per list-task in the list-major kernel; several queries per CTA in the
+    # pipelined refine kernel
+    c = case(oracle_mod, "c1s", nq=2000)
+    idx = c.gpu_index()
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, 10, 16, 10)
+    assert_search_equal(gpu_search(idx, c.Q, 10, 16, 10, scan), o)
+
+
 def test_search_modes_single_and_strict(oracle_mod):
     for kw in ({"assignment": "single"}, {"assignment": "air", "strict": True}):
         c = case(oracle_mod, "c1s", **kw)

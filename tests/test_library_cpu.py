@@ -44,6 +44,8 @@ def test_library_is_sm100a(rb):
     sass = subprocess.check_output(["cuobjdump", "-sass", rb.LIB_PATH]).decode()
     assert not re.search(r"(?<![A-Z])HMMA", sass)   # no legacy mma.sync path
     assert "UTCHMMA" in sass                       # tcgen05.mma (coarse TF32 GEMM)
+    assert "UTCIMMA" in sass                       # tcgen05.mma kind::i8 (list-major scan)
+    assert "STTM" in sass                          # tcgen05.st (one-hot A operand in TMEM)
     assert "UTMALDG" in sass                       # TMA tensor loads
     assert "LDTM" in sass                          # tcgen05.ld from TMEM
 

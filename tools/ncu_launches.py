@@ -15,7 +15,8 @@ def main():
         if hdr and len(r) == len(hdr):
             data.append(dict(zip(hdr, r)))
     agg = collections.OrderedDict()
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "second": 1e6, "s": 1e6}
     for d in data:
         v = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1.0)
         agg.setdefault(d["Kernel Name"][:70], []).append(v)

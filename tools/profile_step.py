@@ -1,0 +1,28 @@
+"""Build one index and run a few search batches (for ncu launch lists / captures).
+
+  python tools/profile_step.py [config] [nprobe] [scan_mode] [reps]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2601_07183_b200 as rb  # noqa: E402
+from synth import get_config, make_dataset  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2pl"
+spec = get_config(cfg)
+npb = int(sys.argv[2]) if len(sys.argv) > 2 else spec.nprobe
+mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+X, Q = make_dataset(spec)
+dev = torch.device("cuda:0")
+idx = rb.build_index(torch.from_numpy(X).to(dev), spec.nlist, spec.M)
+idx.set_scan_mode(mode)
+Qd = torch.from_numpy(Q).to(dev)
+torch.cuda.synchronize()
+for _ in range(reps):
+    ids, dists = idx.search(Qd, spec.k, npb, spec.refine_factor)
+torch.cuda.synchronize()
+print("profile_step OK", cfg, npb, mode, reps, ids.shape)

@@ -1,0 +1,42 @@
+"""Write profiles/traffic_<config>.json from an `ncu --set full` capture: DRAM
+bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of each kernel
+of the fast-scan stage (A3-A6) and their sum, which bench.py reports as the
+roofline `traffic` of that stage.
+
+  python tools/traffic_from_ncu.py <report.ncu-rep> <config> [out.json]
+"""
+import csv
+import json
+import subprocess
+import sys
+
+STAGE = ("lut_tiles_kernel", "lm_count_kernel", "lm_scan_kernel", "lm_scatter_kernel",
+         "lm_tensor_kernel", "lm_select_kernel", "scan_kernel")
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def main():
+    rep, cfg = sys.argv[1], sys.argv[2]
+    out = sys.argv[3] if len(sys.argv) > 3 else f"profiles/traffic_{cfg}.json"
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+    ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    it, ik = hdr.index("gpu__time_duration.sum"), hdr.index("Kernel Name")
+    per = {}
+    for r in rows[2:]:
+        name = r[ik].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
+        b = (float(r[ir]) * UNIT.get(units[ir], 1) + float(r[iw]) * UNIT.get(units[iw], 1))
+        per.setdefault(name, []).append((b, float(r[it])))
+    kern = {k: {"dram_bytes": sum(x[0] for x in v) / len(v), "duration": sum(x[1] for x in v) / len(v),
+                "duration_unit": units[it], "launches": len(v)} for k, v in per.items()}
+    stage = sum(v["dram_bytes"] for k, v in kern.items() if k in STAGE)
+    json.dump({"config": cfg, "source": rep, "dram_bytes_per_launch": stage,
+               "stage_kernels": [k for k in kern if k in STAGE], "kernels": kern},
+              open(out, "w"), indent=1)
+    print(json.dumps({"dram_bytes_per_launch": stage, "kernels": list(kern)}))
+
+
+if __name__ == "__main__":
+    main()
