@@ -109,31 +109,60 @@ def recall_at_k(ids, gt_ids, gt_d64, dists, k):
 
 
 def build_workload(args, rank, world, dev):
+    """Synthetic inputs + index. Host-drawn configs (c1-c3, c2pl) come from
+    synth.make_dataset; the large BJ configs (c4: 10M x 96, c5: 100M x 128) are
+    drawn on the device (synth.gpu_generators) -- every rank draws the same
+    tensors and keeps its id-mod-N shard."""
     import torch
     import paper_2601_07183_b200 as rb
-    from synth import get_config, make_dataset
+    from synth import GPU_KINDS, get_config, make_dataset
     spec = get_config(args.config)
     t0 = time.time()
-    X, Q = make_dataset(spec)
-    gen_s = time.time() - t0
-    rows = np.arange(rank, X.shape[0], world)
-    Xl = torch.from_numpy(X[rows]).to(dev)
-    Qd = torch.from_numpy(Q).to(dev)
+    if spec.kind in GPU_KINDS:
+        from synth.gpu_generators import make_dataset_torch
+        Xd, Qd = make_dataset_torch(spec, dev)
+        Q = Qd.cpu().numpy()
+        # host copy only for the CPU-oracle baseline (rank 0, N = 1)
+        X = Xd.cpu().numpy() if (world == 1 and not args.no_cpu_baseline) else None
+        Xl = Xd if world == 1 else Xd[rank::world].contiguous()
+    else:
+        X, Q = make_dataset(spec)
+        Xd = None
+        rows = np.arange(rank, X.shape[0], world)
+        Xl = torch.from_numpy(X[rows]).to(dev)
+        Qd = torch.from_numpy(Q).to(dev)
     torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    # exact ground truth (fp64, GPU) on a query sample, before the build frees memory
+    nq_gt = Q.shape[0] if args.gt_queries <= 0 else min(Q.shape[0], args.gt_queries)
+    Xfull = Xd if Xd is not None else torch.from_numpy(X).to(dev)
+    gt_ids, gt_d64 = rb.exact_knn(Xfull, Qd[:nq_gt].contiguous(), spec.k)
+    torch.cuda.synchronize()
+    del Xfull
+    # training for large nlist: a 64*nlist sample and 10 Lloyd iterations (R16;
+    # training is outside the bit-exact contract)
+    kw = {}
+    if spec.nlist >= 4096:
+        kw = dict(train_sample=64 * spec.nlist, kmeans_iters=10)
     t0 = time.time()
     if world == 1:
-        idx = rb.build_index(Xl, spec.nlist, spec.M, assignment=args.assignment)
+        idx = rb.build_index(Xl, spec.nlist, spec.M, assignment=args.assignment, **kw)
         torch.cuda.synchronize()
     else:
         from paper_2601_07183_b200.distributed import ShardedIndex
-        Xtrain = torch.from_numpy(X).to(dev) if rank == 0 else None
-        sh = ShardedIndex.build(Xl, X.shape[0], spec.nlist, spec.M, train_base=Xtrain,
-                                assignment=args.assignment)
+        if Xd is not None:
+            Xtrain = Xd if rank == 0 else None
+        else:
+            Xtrain = torch.from_numpy(X).to(dev) if rank == 0 else None
+        sh = ShardedIndex.build(Xl, spec.n, spec.nlist, spec.M, train_base=Xtrain,
+                                assignment=args.assignment, **kw)
         idx = sh.local
         del Xtrain
     torch.cuda.synchronize()
     build_s = time.time() - t0
-    return spec, X, Q, Xl, Qd, idx, gen_s, build_s
+    del Xd, Xl
+    torch.cuda.empty_cache()
+    return spec, X, Q, Qd, idx, gen_s, build_s, gt_ids, gt_d64, nq_gt
 
 
 def run_ours(args):
@@ -149,7 +178,7 @@ def run_ours(args):
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     dev = torch.device("cuda", local_rank)
-    spec, X, Q, Xl, Qd, idx, gen_s, build_s = build_workload(args, rank, world, dev)
+    spec, X, Q, Qd, idx, gen_s, build_s, gt_ids, gt_d64, nq_gt = build_workload(args, rank, world, dev)
     k, rf = spec.k, spec.refine_factor
 
     def step(nprobe, with_dco=False):
@@ -162,18 +191,12 @@ def run_ours(args):
             ids, dists = sharded_merge(ids, dists)
         return ids, dists, dco
 
-    # ground truth on the full base (rank 0 data is identical on all ranks)
-    Xfull = torch.from_numpy(X).to(dev)
-    gt_ids, gt_d64 = rb.exact_knn(Xfull, Qd, k)
-    del Xfull
-    torch.cuda.synchronize()
-
     # recall sweep -> headline nprobe (smallest with recall >= 0.95)
     sweep = []
     chosen = None
     for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
         ids, dists, _ = step(npb)
-        r = recall_at_k(ids, gt_ids, gt_d64, dists, k)
+        r = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], k)
         sweep.append({"nprobe": npb, "recall": round(r, 4)})
         if args.nprobe is None and r >= 0.95:
             chosen = npb
@@ -183,7 +206,7 @@ def run_ours(args):
     if chosen is None:
         chosen = sweep[-1]["nprobe"]
     ids, dists, dco = step(chosen, with_dco=True)
-    recall = recall_at_k(ids, gt_ids, gt_d64, dists, k)
+    recall = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], k)
     dco_local = int(dco.sum().item())
     dco_total = dco_local
     if world > 1:
@@ -253,7 +276,7 @@ def run_ours(args):
 
     # ---------------- roofline of the dominant stage (the fast scan, A3-A6) ----------------
     peak, peak_src = load_peaks()
-    scan_mode = idx.scan_path(k, chosen, rf)
+    scan_mode = idx.scan_path(Q.shape[0], k, chosen, rf)
     scan_ms = prof["ms"]["scan"] / max(1, prof["launches"]["scan"])
     scan_bytes = dco_local * (spec.M // 2)             # algorithmic code bytes per launch
     achieved = scan_bytes / (scan_ms / 1e3) / 1e9
@@ -315,14 +338,24 @@ def run_ours(args):
 def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
     """The CPU oracle (oracle/, plain C + OpenMP, never tuned) on the host cores:
     oracle assignment + encode of the same base from the same trained state
-    (untimed), then oracle_search timed on a bounded query sample."""
+    (untimed), then oracle_search timed on a bounded query sample. For the
+    device-drawn 10M/100M configs the oracle's own assignment of every row would
+    take hours on the host, so its search runs on the index's exported
+    assignment and codes instead (bit-exact to the oracle's, as the parity tests
+    pin on c1-c2); only the search is timed either way."""
     import oracle
+    from synth import GPU_KINDS
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
     cent, cb = [t.cpu().numpy() for t in idx.export_trained()]
-    l1, l2 = oracle.assign(X, cent, "air")
-    codes = oracle.encode(X, cb)
-    sample = 500
+    if spec.kind in GPU_KINDS:
+        l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
+        how = "index-exported assignment/codes"
+    else:
+        l1, l2 = oracle.assign(X, cent, "air")
+        codes = oracle.encode(X, cb)
+        how = "oracle assignment/encode from the same trained centroids/codebook"
+    sample = 100 if spec.n > 2_000_000 else 500
     t0 = time.perf_counter()
     oracle.search(X, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
     dt = time.perf_counter() - t0
@@ -333,7 +366,7 @@ def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
         dt = time.perf_counter() - t0
     return {"value": round(sample / dt, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
             "sample": f"first {sample} of the {Q.shape[0]} queries, nprobe {nprobe}, "
-                      f"oracle index built from the same trained centroids/codebook (untimed)"}
+                      f"{how} (untimed)"}
 
 
 def run_reference(args):
@@ -391,6 +424,8 @@ def main():
     ap.add_argument("--assignment", default="AIR", choices=["AIR", "single"])
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gt-queries", type=int, default=0,
+                    help="queries with exact ground truth for recall (0 = all)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -202,11 +202,13 @@ rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launche
  * reset != 0 zeroes the counter. RAIRS_E_INVALID on NULL arguments. */
 rairs_status rairs_profile_kernels(rairs_index_t idx, int64_t* kernels, int32_t reset);
 
-/* Which kernels a search with these parameters would use (no device work):
- * *coarse_path = 1 exact fp64 probe kernel, 2 tensor-core TF32 filter +
- * certification; *scan_path = 1 SIMT query-major scan, 2 list-major tcgen05
- * scan. Either pointer may be NULL. Same validation as rairs_search. */
-rairs_status rairs_search_plan(rairs_index_t idx, int32_t k, int32_t nprobe,
+/* Which kernels a search of nq queries with these parameters would use (no
+ * device work): *coarse_path = 1 exact fp64 probe kernel, 2 tensor-core TF32
+ * filter + certification; *scan_path = 1 SIMT query-major scan, 2 list-major
+ * tcgen05 scan (scan mode auto: list-major when nq*nprobe >= 3*nlist, i.e. a
+ * probed list is shared by several queries, and its limits hold). Either
+ * pointer may be NULL. Same validation as rairs_search. */
+rairs_status rairs_search_plan(rairs_index_t idx, int64_t nq, int32_t k, int32_t nprobe,
                                int32_t refine_factor, int32_t* coarse_path, int32_t* scan_path);
 
 const char* rairs_last_error(void);

@@ -103,7 +103,7 @@ def lib() -> ctypes.CDLL:
         "rairs_certify_fallbacks": [_P, _P, _I32],
         "rairs_set_scan_mode": [_P, _I32],
         "rairs_profile_kernels": [_P, _P, _I32],
-        "rairs_search_plan": [_P, _I32, _I32, _I32, _P, _P],
+        "rairs_search_plan": [_P, _I64, _I32, _I32, _I32, _P, _P],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -351,6 +352,27 @@ static inline unsigned grid_for(int64_t n, int bs = 256) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, bs), 148 * 32));
 }
 
+// RAIRS_DEBUG_SYNC=1: synchronise after every training step and name the
+// failing one (debugging aid; off by default, no effect on results)
+static bool debug_sync() {
+  static const bool on = [] {
+    const char* e = getenv("RAIRS_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+#define KM_DEBUG_STEP(name)                                                           \
+  do {                                                                                \
+    if (debug_sync()) {                                                               \
+      cudaError_t _e = cudaStreamSynchronize(s);                                      \
+      if (_e != cudaSuccess) {                                                        \
+        set_error(std::string("train_kmeans step ") + (name) + ": " + cudaGetErrorString(_e)); \
+        cleanup();                                                                    \
+        return RAIRS_E_CUDA;                                                          \
+      }                                                                               \
+    }                                                                                 \
+  } while (0)
+
 rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, uint64_t seed,
                           int64_t max_train, float* cent, cudaStream_t s) {
   const int64_t nt = std::min<int64_t>(n, max_train > 0 ? max_train : (int64_t)256 * k);
@@ -383,6 +405,7 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
   KM_TRY(cudaMalloc(&seg_e, k * sizeof(int32_t)));
   KM_TRY(cudaMemcpyAsync(d_rows, rows.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice, s));
   gather_rows_kernel<<<grid_for(nt * d), 256, 0, s>>>(X, d_rows, nt, d, Xt);
+  KM_DEBUG_STEP("gather");
   // init: the first k sampled rows (distinct rows of X)
   KM_TRY(cudaMemcpyAsync(cent, Xt, (size_t)k * d * sizeof(float), cudaMemcpyDeviceToDevice, s));
   iota_i32_kernel<<<grid_for(nt), 256, 0, s>>>(iota, nt);
@@ -408,6 +431,7 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
       if (st == RAIRS_OK)
         st = launch_coarse_fused(&tmp, Xt, nt, 1, 0, 0.0, 0, asg, nullptr, nullptr, nflag, s);
       cudaFreeAsync(tmp.cnorm, s);
+      if (st == RAIRS_OK) KM_DEBUG_STEP("coarse_fused");
     } else {
       ProbeArgs pa{};
       pa.X = Xt; pa.rows = nt; pa.d = d; pa.C = cent; pa.nl = k; pa.L = 1; pa.mode = 0;
@@ -417,11 +441,13 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
     if (st != RAIRS_OK) { cleanup(); return st; }
     KM_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, asg, asg_sorted, iota, idx_sorted,
                                            (int)nt, 0, end_bit, s));
+    KM_DEBUG_STEP("sort");
     KM_TRY(cudaMemsetAsync(seg_s, 0, k * sizeof(int32_t), s));
     KM_TRY(cudaMemsetAsync(seg_e, 0, k * sizeof(int32_t), s));
     seg_bounds_i32_kernel<<<grid_for(nt), 256, 0, s>>>(asg_sorted, nt, seg_s, seg_e);
     kmeans_update_kernel<<<k, 128, 0, s>>>(Xt, d, idx_sorted, seg_s, seg_e, cent);
     KM_TRY(cudaGetLastError());
+    KM_DEBUG_STEP("update");
     // empty clusters: split the largest (host side, deterministic)
     KM_TRY(cudaMemcpyAsync(hs.data(), seg_s, k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     KM_TRY(cudaMemcpyAsync(he.data(), seg_e, k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));

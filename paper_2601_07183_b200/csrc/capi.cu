@@ -167,7 +167,7 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   ev.mark(1);
   int64_t nk = coarse_fused_ok(idx, nprobe) ? 3 : 1;  // topw + certify + exact fallback
   if (st == RAIRS_OK) {
-    if (listmajor_ok(idx, nprobe, bigK)) {
+    if (listmajor_ok(idx, nq, nprobe, bigK)) {
       st = launch_listmajor(idx, a, s);
       nk += 6;  // count, scan, scatter, lut_tiles, tensor, select
     } else {
@@ -562,11 +562,11 @@ rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t 
   return RAIRS_OK;
 }
 
-rairs_status rairs_search_plan(rairs_index_t idx, int32_t k, int32_t nprobe, int32_t refine_factor,
-                               int32_t* coarse_path, int32_t* scan_path) {
-  RAIRS_TRY(validate_search(idx, 1, k, nprobe, refine_factor));
+rairs_status rairs_search_plan(rairs_index_t idx, int64_t nq, int32_t k, int32_t nprobe,
+                               int32_t refine_factor, int32_t* coarse_path, int32_t* scan_path) {
+  RAIRS_TRY(validate_search(idx, nq, k, nprobe, refine_factor));
   if (coarse_path) *coarse_path = coarse_fused_ok(idx, nprobe) ? 2 : 1;
-  if (scan_path) *scan_path = listmajor_ok(idx, nprobe, k * refine_factor) ? 2 : 1;
+  if (scan_path) *scan_path = listmajor_ok(idx, nq, nprobe, k * refine_factor) ? 2 : 1;
   return RAIRS_OK;
 }
 

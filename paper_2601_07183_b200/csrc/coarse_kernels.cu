@@ -347,6 +347,12 @@ struct CertArgs {
   int32_t* l2;
   int32_t* flags;
   unsigned* nflag;
+  int stage_rows;      // stage the candidate centroid rows in shared memory
+  size_t stage_off;    // byte offset of the staging area in dynamic smem
+  size_t stage_warp;   // bytes per warp
+  __device__ float* stage_base(unsigned char* sm, int warp) const {
+    return reinterpret_cast<float*>(sm + stage_off + (size_t)warp * stage_warp);
+  }
 };
 
 __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs a) {
@@ -375,6 +381,39 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
     warp_sort_u64(keys, a.npow_c);
     const float gnext = all ? 0.0f : unord_f32((uint32_t)(keys[W] >> 32));
     const float* xr = a.X + (size_t)r * a.d;
+    if (a.stage_rows) {
+      // stage the Wc candidate centroid rows in shared memory with coalesced
+      // 16-B loads (all rows in flight at once), row stride d + 4 floats
+      float* cs = a.stage_base(sm, warp);
+      const int d4 = a.d >> 2, rs4 = d4 + 1;
+      for (int i = 0; i < Wc; ++i) {
+        const uint32_t l = (uint32_t)(keys[i] & 0xFFFFFFFFu);
+        const float4* c4 = reinterpret_cast<const float4*>(a.C + (size_t)l * a.d);
+        for (int t4 = lane; t4 < d4; t4 += 32) reinterpret_cast<float4*>(cs)[i * rs4 + t4] = __ldg(c4 + t4);
+      }
+      __syncwarp();
+      for (int i = lane; i < a.npow_w; i += 32) {
+        if (i < Wc) {
+          const float4* c4 = reinterpret_cast<const float4*>(cs) + i * rs4;
+          const float4* x4 = reinterpret_cast<const float4*>(xr);
+          double acc = 0.0;
+#pragma unroll 4
+          for (int t4 = 0; t4 < d4; ++t4) {
+            const float4 cv = c4[t4], xv = __ldg(x4 + t4);
+            acc = __dadd_rn(acc, dsq_diff(xv.x, cv.x));
+            acc = __dadd_rn(acc, dsq_diff(xv.y, cv.y));
+            acc = __dadd_rn(acc, dsq_diff(xv.z, cv.z));
+            acc = __dadd_rn(acc, dsq_diff(xv.w, cv.w));
+          }
+          ck[i] = dbits(acc);
+          ci[i] = (uint32_t)(keys[i] & 0xFFFFFFFFu);
+        } else {
+          ck[i] = kKeyInf;
+          ci[i] = 0xFFFFFFFFu;
+        }
+      }
+      __syncwarp();
+    } else
     for (int i = lane; i < a.npow_w; i += 32) {
       if (i < Wc) {
         const uint32_t l = (uint32_t)(keys[i] & 0xFFFFFFFFu);
@@ -641,10 +680,16 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ca.l2 = l2 ? l2 + r0 : nullptr;
     ca.flags = flags;
     ca.nflag = nflag;
+    // candidate-row staging (coalesced loads) when it fits next to the sort buffers
+    const size_t stage_warp = round_up((size_t)std::min(W, nl) * (d + 4) * 4, 16);
+    ca.stage_off = round_up(csmem, 16);
+    ca.stage_warp = stage_warp;
+    ca.stage_rows = ((d & 3) == 0 && ca.stage_off + CT_WARPS * stage_warp <= 160 * 1024) ? 1 : 0;
+    const size_t csmem_all = ca.stage_rows ? ca.stage_off + CT_WARPS * stage_warp : csmem;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_certify_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem_all));
     const int cgrid = (int)std::min<int64_t>(ceil_div(nr, CT_WARPS), 148 * 16);
-    coarse_certify_kernel<<<cgrid, CT_THREADS, csmem, s>>>(ca);
+    coarse_certify_kernel<<<cgrid, CT_THREADS, csmem_all, s>>>(ca);
     RAIRS_CHECK_LAUNCH();
     // exact fp64 recomputation of the (rare) uncertified rows
     ProbeArgs pa{};

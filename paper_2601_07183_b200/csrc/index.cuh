@@ -105,7 +105,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
 
 // ---- list-major tensor-core scan (listmajor_kernels.cu) ----------------------
 rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s);
-bool listmajor_ok(const rairs_index_s* idx, int nprobe, int bigK);
+bool listmajor_ok(const rairs_index_s* idx, int64_t nq, int nprobe, int bigK);
 struct SearchArgs;
 rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 

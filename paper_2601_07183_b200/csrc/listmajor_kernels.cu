@@ -134,47 +134,45 @@ __global__ void __launch_bounds__(SCN) lm_scan_kernel(const uint32_t* __restrict
 // R2), the codebook is staged transposed in shared memory ([j][t][m]: lanes
 // read consecutive words).  b = sum_m mn_m is summed by lane 0 in ascending m.
 constexpr int LW = 8;  // warps (queries) per CTA
-constexpr int LUT_MAX_DSUB = 8;
 
-__device__ __forceinline__ float lut_T(const float* qs, const float* smc, int m, int j, int dsub,
-                                       int M) {
+template <int DSUB>
+__device__ __forceinline__ float lut_T(const float* qs, const float* smc, int m, int j, int M) {
   float acc = 0.0f;
 #pragma unroll
-  for (int t = 0; t < LUT_MAX_DSUB; ++t) {
-    if (t < dsub) {
-      const float diff = __fsub_rn(qs[t], smc[(j * dsub + t) * M + m]);
-      acc = __fadd_rn(acc, __fmul_rn(diff, diff));
-    }
+  for (int t = 0; t < DSUB; ++t) {
+    const float diff = __fsub_rn(qs[t], smc[(j * DSUB + t) * M + m]);
+    acc = __fadd_rn(acc, __fmul_rn(diff, diff));
   }
   return acc;
 }
 
+template <int DSUB>
 __global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
     const float* __restrict__ queries, int64_t nq, int d, const float* __restrict__ cb, int M,
-    int M_pad, int dsub, const int32_t* __restrict__ probes, int nprobe,
+    int M_pad, const int32_t* __restrict__ probes, int nprobe,
     const uint32_t* __restrict__ qslot, const uint32_t* __restrict__ qcnt,
     const uint32_t* __restrict__ lrow, int QT, uint8_t* __restrict__ tiles,
     float* __restrict__ a_out, float* __restrict__ b_out, uint8_t* __restrict__ lut_dbg) {
   extern __shared__ __align__(16) float smc[];  // [16][dsub][M] codebook, then [LW][M] mn
   const int lane = lane_id(), warp = warp_id();
   const int K = M_pad * 16;
-  for (int e = threadIdx.x; e < M * 16 * dsub; e += blockDim.x) {
-    const int m = e / (16 * dsub), j = (e / dsub) % 16, t = e % dsub;
-    smc[(j * dsub + t) * M + m] = cb[e];
+  for (int e = threadIdx.x; e < M * 16 * DSUB; e += blockDim.x) {
+    const int m = e / (16 * DSUB), j = (e / DSUB) % 16, t = e % DSUB;
+    smc[(j * DSUB + t) * M + m] = cb[e];
   }
   __syncthreads();
-  float* mnw = smc + 16 * dsub * M + warp * M;
+  float* mnw = smc + 16 * DSUB * M + warp * M;
   for (int64_t q = (int64_t)blockIdx.x * LW + warp; q < nq; q += (int64_t)gridDim.x * LW) {
     const float* qv = queries + q * d;
     float S = 0.0f;
     for (int m = lane; m < M; m += 32) {  // pass 1: per-subquantizer min and span
-      float qs[LUT_MAX_DSUB];
+      float qs[DSUB];
 #pragma unroll
-      for (int t = 0; t < LUT_MAX_DSUB; ++t) qs[t] = (t < dsub) ? __ldg(qv + m * dsub + t) : 0.0f;
+      for (int t = 0; t < DSUB; ++t) qs[t] = __ldg(qv + m * DSUB + t);
       float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const float T = lut_T(qs, smc, m, j, dsub, M);
+        const float T = lut_T<DSUB>(qs, smc, m, j, M);
         lo = fminf(lo, T);
         hi = fmaxf(hi, T);
       }
@@ -194,13 +192,13 @@ __global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
     for (int m = lane; m < M_pad; m += 32) {  // pass 2: quantise, write every tile row
       uint32_t w[4] = {0u, 0u, 0u, 0u};
       if (m < M) {
-        float qs[LUT_MAX_DSUB];
+        float qs[DSUB];
 #pragma unroll
-        for (int t = 0; t < LUT_MAX_DSUB; ++t) qs[t] = (t < dsub) ? __ldg(qv + m * dsub + t) : 0.0f;
+        for (int t = 0; t < DSUB; ++t) qs[t] = __ldg(qv + m * DSUB + t);
         const float lo = mnw[m];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float T = lut_T(qs, smc, m, j, dsub, M);
+          const float T = lut_T<DSUB>(qs, smc, m, j, M);
           uint32_t v = 0;
           if (S > 0.0f) v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T, lo), a)));
           w[j >> 2] |= v << (8 * (j & 3));
@@ -227,7 +225,7 @@ __global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
 // Tensor-core scoring, one list at a time (CTAs claim lists atomically).
 constexpr int LM_IT = 128;        // items per tile (MMA M)
 constexpr int LM_QT = 64;         // max queries per tile (MMA N <= 64)
-constexpr int LM_MAXREF = 128;    // references per list on this path
+constexpr int LM_MAXREF = 1024;   // references per list on this path
 constexpr uint32_t LM_B_MAX = 64 * 1024;  // LUT tile bytes (QT x K)
 
 struct LMArgs {
@@ -285,6 +283,17 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
       "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
       "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
+}
+
+// reference j of a list-task holding item `item` (>= the owned count):
+// the largest j with refoff[j] <= item (refoff ascending, refoff[nref] = N_l)
+__device__ __forceinline__ int lm_ref_of(const uint32_t* refoff, uint32_t nref, uint32_t item) {
+  int lo = 0, hi = (int)nref;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (refoff[mid] <= item) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >= 32 -> 0
@@ -421,8 +430,7 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
             if (item < own) {
               slot = own0 + item;
             } else {
-              int j = 0;
-              while (refoff[j + 1] <= item) ++j;
+              const int j = lm_ref_of(refoff, nref, item);
               slot = a.ref_start[r0 + j] + (item - refoff[j]);
             }
             const uint64_t* cw = a.codes64 + ((size_t)(slot >> 5) * NU) * 32 + (slot & 31);
@@ -439,25 +447,34 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
           load_codes(t + LM_GROUPS, nxt);  // this group's next tile
           uint32_t cc = (grp ? gcnt1 : gcnt0) + (t / LM_GROUPS) * NCHUNK;  // group chunk index
 #pragma unroll
-          for (int c = 0; c < NCHUNK; ++c, ++cc) {
-            const int s = grp * LM_GSTAGES + (int)(cc % LM_GSTAGES);
-            const uint32_t w32 = (uint32_t)(cur[c >> 1] >> (32 * (c & 1)));
-            uint32_t v[32];
+          for (int c = 0; c < NCHUNK; c += 2, cc += 2) {
+            // two chunks per step (NCHUNK and the ring position are even): the
+            // first tcgen05.st overlaps the second chunk's expansion, one
+            // wait::st covers both
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {  // one-hot of nibble n: byte n of 16 = 1
-              const uint32_t sh = ((w32 >> (4 * k)) & 15u) << 3;
-              v[4 * k + 0] = shl_clamp(1u, sh);
-              v[4 * k + 1] = shl_clamp(1u, sh - 32u);
-              v[4 * k + 2] = shl_clamp(1u, sh - 64u);
-              v[4 * k + 3] = shl_clamp(1u, sh - 96u);
+            for (int h = 0; h < 2; ++h) {
+              const int s = grp * LM_GSTAGES + (int)((cc + h) % LM_GSTAGES);
+              const uint32_t w32 = (uint32_t)(cur[(c + h) >> 1] >> (32 * ((c + h) & 1)));
+              uint32_t v[32];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {  // one-hot of nibble n: byte n of 16 = 1
+                const uint32_t sh = ((w32 >> (4 * k)) & 15u) << 3;
+                v[4 * k + 0] = shl_clamp(1u, sh);
+                v[4 * k + 1] = shl_clamp(1u, sh - 32u);
+                v[4 * k + 2] = shl_clamp(1u, sh - 64u);
+                v[4 * k + 3] = shl_clamp(1u, sh - 96u);
+              }
+              if (cc + h >= LM_GSTAGES) mbar_wait(&empty[s], (((cc + h) / LM_GSTAGES) - 1) & 1u);
+              tc_fence_after();
+              tmem_st32(tq + (uint32_t)(s * 32), v);
             }
-            if (cc >= LM_GSTAGES) mbar_wait(&empty[s], ((cc / LM_GSTAGES) - 1) & 1u);
-            tc_fence_after();
-            tmem_st32(tq + (uint32_t)(s * 32), v);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
+            if (lane == 0) {
+              mbar_arrive(&full[grp * LM_GSTAGES + (int)(cc % LM_GSTAGES)]);
+              mbar_arrive(&full[grp * LM_GSTAGES + (int)((cc + 1) % LM_GSTAGES)]);
+            }
           }
 #pragma unroll
           for (int u = 0; u < NU; ++u) cur[u] = nxt[u];
@@ -504,9 +521,7 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
           const bool ivalid = item < Nl;
           int myref = -1;
           if (ivalid && item >= own) {
-            int j = 0;
-            while (refoff[j + 1] <= item) ++j;
-            myref = j;
+            myref = lm_ref_of(refoff, nref, item);
           }
           uint64_t ok = (nq_tile >= 64) ? ~0ull : ((1ull << nq_tile) - 1ull);
           if (myref >= 0) ok &= ~((uint64_t)skipT[myref * 2] | ((uint64_t)skipT[myref * 2 + 1] << 32));
@@ -574,7 +589,7 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
 // ---------------------------------------------------------------------------
 // Per query (one WARP per query): SEIL ranges over its score rows (R9 dedup),
 // histogram-threshold top-bigK with warp-private state (no CTA barriers).
-constexpr int SW_WARPS = 16;
+constexpr int SW_WARPS = 8;
 constexpr int SW_NB = 512;
 
 struct SelArgs {
@@ -699,7 +714,7 @@ __device__ __forceinline__ void sel_resolve(const SelArgs& a, int64_t q, uint64_
 }
 
 template <bool U32>
-__global__ void __launch_bounds__(SW_WARPS * 32, 1) lm_select_kernel(SelArgs a) {
+__global__ void __launch_bounds__(SW_WARPS * 32, 3) lm_select_kernel(SelArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
   uint32_t* hist = reinterpret_cast<uint32_t*>(sm) + warp * SW_NB;
@@ -787,6 +802,36 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 1) lm_select_kernel(SelArgs a) 
             }
           }
           const uint32_t item0 = (v0 + 32 * u + lane) * PER;
+          // fast append: a warp-wide exclusive scan of the per-lane pass counts
+          const uint32_t mine = __popc(pm);
+          uint32_t incl = mine;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+          if (total == 0) continue;
+          if (!exact && cnt + total + 32 <= (uint32_t)a.cap) {
+            uint32_t pos = cnt + incl - mine;
+            while (pm) {
+              const int e = __ffs(pm) - 1;
+              pm &= pm - 1u;
+              uint32_t sc;
+              if (U32) {
+                sc = e == 0 ? w4[0] : e == 1 ? w4[1] : e == 2 ? w4[2] : w4[3];
+              } else {
+                const uint32_t ww = (e >> 1) == 0 ? w4[0] : (e >> 1) == 1 ? w4[1]
+                                  : (e >> 1) == 2 ? w4[2] : w4[3];
+                sc = (ww >> (16 * (e & 1))) & 0xFFFFu;
+              }
+              cand[pos++] = ((uint64_t)sc << 32) | sel_pos((uint32_t)p, item0 + e);
+            }
+            cnt += total;
+            __syncwarp();
+            continue;
+          }
+          // near the capacity, or in exact mode: item by item
           while (__any_sync(0xffffffffu, pm != 0)) {
             bool pass = pm != 0;
             uint64_t key = kKeyInf;
@@ -855,15 +900,23 @@ static int lm_qt(int K) {  // queries per LUT tile: QT x K <= LM_B_MAX, multiple
   return qt - (qt % 16);
 }
 
+constexpr double LM_MIN_QUERIES_PER_LIST = 3.0;
+
 static bool lm_nu_ok(int NU) { return NU == 1 || NU == 2 || NU == 3 || NU == 4 || NU == 6 || NU == 8; }
 
-bool listmajor_ok(const rairs_index_s* idx, int nprobe, int bigK) {
+bool listmajor_ok(const rairs_index_s* idx, int64_t nq, int nprobe, int bigK) {
   if (idx->scan_mode == 1) return false;            // forced SIMT query-major scan
+  // auto: the list-major contraction pays once a probed list is shared by
+  // several queries of the batch (each list-task expands its codes once)
+  if (idx->scan_mode == 0 && (double)nq * nprobe < LM_MIN_QUERIES_PER_LIST * idx->nlist)
+    return false;
   if (!idx->list_items || !idx->ref_item_off || !idx->list_ids) return false;
   if (idx->max_refs > LM_MAXREF) return false;
   if (!lm_nu_ok(idx->M_pad / 16) || lm_qt(idx->M_pad * 16) < 16) return false;
   if ((size_t)SW_WARPS * (SW_NB * 4 + (size_t)sel_cap(bigK) * 8) > 200 * 1024) return false;
   if (nprobe > 1024 || idx->max_list_items >= (1 << 22)) return false;  // pre-key packing
+  if (!(idx->dsub == 1 || idx->dsub == 2 || idx->dsub == 3 || idx->dsub == 4 || idx->dsub == 8))
+    return false;
   return true;
 }
 
@@ -924,12 +977,23 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(cudaGetLastError());
   // 2. quantised LUTs (O2), one warp per query, written into the list-task tiles
   {
-    if (idx->dsub > LUT_MAX_DSUB) { cleanup(); set_error("list-major: d/M > 8"); return RAIRS_E_UNSUPPORTED; }
     const size_t lsm = ((size_t)16 * idx->dsub * idx->M + (size_t)LW * idx->M) * 4;
-    LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-    lut_tiles_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq, LW), 1 << 30), LW * 32, lsm, s>>>(
-        sa.queries, nq, idx->d, idx->codebook, idx->M, idx->M_pad, idx->dsub, sa.probes, nprobe,
-        qslot, cnt, lrow, QT, tiles, sa.lut_a, sa.lut_b, sa.lut_q);
+    const unsigned lgrid = (unsigned)std::min<int64_t>(ceil_div(nq, LW), 1 << 30);
+#define LUT_LAUNCH(DS)                                                                          \
+  LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel<DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                              (int)lsm));                                                       \
+  lut_tiles_kernel<DS><<<lgrid, LW * 32, lsm, s>>>(sa.queries, nq, idx->d, idx->codebook, idx->M, \
+                                                  idx->M_pad, sa.probes, nprobe, qslot, cnt,    \
+                                                  lrow, QT, tiles, sa.lut_a, sa.lut_b, sa.lut_q)
+    switch (idx->dsub) {
+      case 1: LUT_LAUNCH(1); break;
+      case 2: LUT_LAUNCH(2); break;
+      case 3: LUT_LAUNCH(3); break;
+      case 4: LUT_LAUNCH(4); break;
+      case 8: LUT_LAUNCH(8); break;
+      default: cleanup(); set_error("list-major: unsupported d/M"); return RAIRS_E_UNSUPPORTED;
+    }
+#undef LUT_LAUNCH
     LM_TRY(cudaGetLastError());
   }
   // 3. tensor-core scores, one list at a time

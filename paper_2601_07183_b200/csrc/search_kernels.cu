@@ -673,17 +673,19 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
   __shared__ uint32_t nvalid;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int myrow = warp + 8 * lane;  // lane j (< 16) fetches the key of row warp + 8j
+  // software pipeline: keys of query q + 2*grid and rows of query q + grid are
+  // in flight while query q is computed (the row loads never wait on a key load)
+  auto load_key = [&](int64_t q) -> uint64_t {
+    return (q < nq && lane < 16 && myrow < bigK) ? __ldg(keys + q * bigK + myrow) : kKeyInf;
+  };
   uint32_t gid = 0xFFFFFFFFu;
   float4 v[16];
-  auto fetch = [&](int64_t q) {
+  auto fetch_rows = [&](uint64_t key) {
     gid = 0xFFFFFFFFu;
     uint32_t rowi = 0;
-    if (lane < 16 && myrow < bigK) {
-      const uint64_t key = __ldg(keys + q * bigK + myrow);
-      if (key != kKeyInf) {
-        gid = (uint32_t)(key & 0xFFFFFFFFu);
-        rowi = gid / (uint32_t)G;
-      }
+    if (key != kKeyInf) {
+      gid = (uint32_t)(key & 0xFFFFFFFFu);
+      rowi = gid / (uint32_t)G;
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -694,7 +696,8 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     }
   };
   int64_t q = blockIdx.x;
-  if (q < nq) fetch(q);
+  if (q < nq) fetch_rows(load_key(q));
+  uint64_t key_next = load_key(q + gridDim.x);
   for (; q < nq; q += gridDim.x) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -704,8 +707,10 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     if (tid < D) qs[tid] = (double)queries[q * D + tid];
     if (tid == 0) nvalid = 0;
     __syncthreads();
-    const int64_t qn = q + gridDim.x;
-    if (qn < nq) fetch(qn);  // next query's rows in flight during this query's compute
+    if (q + gridDim.x < nq) {
+      fetch_rows(key_next);                        // rows of q + grid: in flight from here
+      key_next = load_key(q + 2 * (int64_t)gridDim.x);
+    }
     if (tid < bigK) {
       const uint32_t g = gids[tid];
       uint64_t out = kKeyInf;

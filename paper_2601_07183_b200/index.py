@@ -228,11 +228,11 @@ class Index:
         return {"ms": {"coarse": ms[0], "scan": ms[1], "refine": ms[2]},
                 "launches": {"coarse": nl[0], "scan": nl[1], "refine": nl[2]}}
 
-    def scan_path(self, k: int, nprobe: int, refine_factor: int) -> str:
-        """'listmajor' or 'simt': the scan kernels a search with these parameters uses."""
+    def scan_path(self, nq: int, k: int, nprobe: int, refine_factor: int) -> str:
+        """'listmajor' or 'simt': the scan kernels a search of nq queries uses."""
         sp = ctypes.c_int32()
-        check(lib().rairs_search_plan(self._h, k, nprobe, refine_factor, None, ctypes.byref(sp)),
-              "rairs_search_plan")
+        check(lib().rairs_search_plan(self._h, nq, k, nprobe, refine_factor, None,
+                                      ctypes.byref(sp)), "rairs_search_plan")
         return "listmajor" if sp.value == 2 else "simt"
 
     def kernels_launched(self, reset: bool = True) -> int:

@@ -330,3 +330,77 @@ def test_massive_score_ties(oracle_mod, scan):
     for k, nprobe, rf in ((10, 4, 10), (5, 16, 20), (50, 8, 8)):
         o = oracle_mod.search(X, l1, l2, codes, cent, cb, Q, k, nprobe, rf)
         assert_search_equal(gpu_search(idx, Q, k, nprobe, rf, scan), o)
+
+
+# ------------------------------- BJ configs[3] at full size (10M x 96), sampled
+def test_c4_full_size_sampled_properties(oracle_mod):
+    """BJ configs[3] at full size: 10M x 96 drawn on the device, nlist 16,384,
+    M 48, the bench's launch configuration (all 10k queries in one batch,
+    list-major scan). The index is GPU-trained (outside the bit-exact contract,
+    R16); the oracle then checks, from the exported trained state and the same
+    input rows, on samples it can compute one by one:
+      O4/O5  assignment and codes of 4,000 sampled rows;
+      O1/O2  probe sets and the quantised LUT of 64 sampled queries;
+      O8     every returned candidate's integer score, from the oracle's own
+             encode of that row;
+      O9     completeness on a 20,000-row sample: every sampled row of U(q)
+             whose key (s, id) is below the bigK-th candidate key is a candidate;
+      O10    the final ids are the first k candidates by (delta, id), delta the
+             fp64 ordered sum rounded to fp32 (1e-4 relative)."""
+    from synth.gpu_generators import make_dataset_torch
+    spec = get_config("c4")
+    k, nprobe, rf = spec.k, 2, spec.refine_factor
+    bigK = k * rf
+    Xd, Qd = make_dataset_torch(spec, DEV)
+    idx = rb.build_index(Xd, spec.nlist, spec.M, train_sample=64 * spec.nlist, kmeans_iters=10)
+    idx.set_scan_mode("listmajor")
+    assert idx.scan_path(spec.nq, k, nprobe, rf) == "listmajor"
+    out = idx.search_debug(Qd, k, nprobe, rf)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(11)
+    qs = np.sort(rng.choice(spec.nq, 64, replace=False))
+    g = {key: v.cpu().numpy()[qs] for key, v in out.items()}
+    g["cand_ids"] = g["cand_ids"].view(np.uint32)
+    g["cand_scores"] = g["cand_scores"].view(np.uint32)
+    cent, cb = [t.cpu().numpy() for t in idx.export_trained()]
+    l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
+    Q = Qd.cpu().numpy()[qs]
+    rows = np.sort(rng.choice(spec.n, 20000, replace=False))
+    Xs = Xd[torch.from_numpy(rows).to(DEV)].cpu().numpy()
+    # O4 / O5 on 4,000 of the sampled rows
+    ol1, ol2 = oracle_mod.assign(Xs[:4000], cent, "air")
+    assert np.array_equal(l1[rows[:4000]], ol1) and np.array_equal(l2[rows[:4000]], ol2)
+    assert np.array_equal(codes[rows[:4000]], oracle_mod.encode(Xs[:4000], cb))
+    # O1 / O2
+    assert np.array_equal(g["probes"], oracle_mod.probe(Q, cent, nprobe))
+    Qv, a, b = oracle_mod.lut(Q, cb)
+    assert np.array_equal(g["Qv"], Qv) and np.array_equal(g["a"], a) and np.array_equal(g["b"], b)
+    # O8: candidate scores from the oracle's encode of the candidate rows
+    srow_l1, srow_l2 = oracle_mod.assign(Xs, cent, "air")
+    scodes = oracle_mod.encode(Xs, cb)
+    for i in range(len(qs)):
+        cid = g["cand_ids"][i]
+        valid = cid != 0xFFFFFFFF
+        cx = Xd[torch.from_numpy(cid[valid].astype(np.int64)).to(DEV)].cpu().numpy()
+        cc = oracle_mod.encode(cx, cb).astype(np.int64)
+        s = Qv[i][np.arange(spec.M)[None, :], cc].sum(1)
+        assert np.array_equal(s, g["cand_scores"][i][valid].astype(np.int64)), "O8 scores"
+        assert np.all(np.diff(s * 2**32 + cid[valid].astype(np.int64)) > 0), "keys sorted"
+        # O9 completeness on the row sample
+        P = set(g["probes"][i].tolist())
+        inU = np.array([(x in P) or (y in P) for x, y in zip(srow_l1, srow_l2)])
+        ss = Qv[i][np.arange(spec.M)[None, :], scodes.astype(np.int64)].sum(1)
+        kmax = s[-1] * 2**32 + int(cid[valid][-1]) if valid.sum() == bigK else np.inf
+        must = inU & (ss * 2**32 + rows < kmax)
+        assert set(rows[must].tolist()) <= set(cid[valid].tolist()), "O9 completeness"
+        # O10: refine = first k candidates by (fp32(fp64 ordered sum), id)
+        acc = np.zeros(cx.shape[0], np.float64)
+        qd = Q[i].astype(np.float64)
+        for t in range(spec.d):
+            df = qd[t] - cx[:, t].astype(np.float64)
+            acc = acc + df * df
+        delta = acc.astype(np.float32)
+        order = np.lexsort((cid[valid], delta))[:k]
+        assert np.array_equal(g["ids"][i], cid[valid][order].astype(np.int64)), "O10 ids"
+        assert np.allclose(g["dists"][i], delta[order], rtol=1e-4, atol=0), "O10 distances"
+    idx.free()

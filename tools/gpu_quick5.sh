@@ -5,5 +5,5 @@ timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1;
 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
 timeout 200 python tools/profile_step.py c2pl 4 auto 3 > gpurun_out/plain.log 2>&1 && \
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"lut_|lm_|refine|coarse" -c 200 --csv --log-file gpurun_out/launches.csv python tools/profile_step.py c2pl 4 auto 3 > gpurun_out/ncu_launch.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"lm_tensor|lm_select|refine_stage|lut_tiles" -s 0 -c 4 -o gpurun_out/prof_lm4 python tools/profile_step.py c2pl 4 auto 1 > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"lm_tensor|lm_select|coarse_topw|coarse_certify" -s 2 -c 4 -o gpurun_out/prof_lm6 python tools/profile_step.py c2pl 4 auto 1 > gpurun_out/ncu_full.log 2>&1
 echo done
