@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <queue>
 #include <vector>
 
 #include "index.cuh"
@@ -459,10 +460,15 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
       hc.resize((size_t)k * d);
       KM_TRY(cudaMemcpyAsync(hc.data(), cent, hc.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
       KM_TRY(cudaStreamSynchronize(s));
+      // max-heap on (count, -index): the same choice as a linear scan for the
+      // first largest cluster, in O(log k) per empty cluster
+      std::priority_queue<std::pair<int64_t, int>> heap;
+      for (int j = 0; j < k; ++j) heap.push({cnt[j], -j});
       for (int l = 0; l < k; ++l) {
         if (cnt[l] > 0) continue;
-        int big = 0;
-        for (int j = 1; j < k; ++j) if (cnt[j] > cnt[big]) big = j;
+        while (heap.top().first != cnt[-heap.top().second]) heap.pop();  // stale entries
+        const int big = -heap.top().second;
+        heap.pop();
         for (int t = 0; t < d; ++t) {
           float v = hc[(size_t)big * d + t];
           float eps = (v != 0.0f ? std::fabs(v) : 1.0f) / 1024.0f;
@@ -471,6 +477,8 @@ rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, ui
         }
         cnt[l] = cnt[big] / 2;
         cnt[big] -= cnt[l];
+        heap.push({cnt[big], -big});
+        heap.push({cnt[l], -l});
       }
       KM_TRY(cudaMemcpyAsync(cent, hc.data(), hc.size() * sizeof(float), cudaMemcpyHostToDevice, s));
       KM_TRY(cudaStreamSynchronize(s));

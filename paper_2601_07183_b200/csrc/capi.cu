@@ -7,6 +7,25 @@
 #include "index.cuh"
 
 namespace rairs {
+bool debug_sync_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RAIRS_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+rairs_status debug_sync_point(cudaStream_t s, const char* what) {
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("after ") + what + ": " + cudaGetErrorString(e));
+    return RAIRS_E_CUDA;
+  }
+  return RAIRS_OK;
+}
+}  // namespace rairs
+
+namespace rairs {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
@@ -334,6 +353,7 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
     st = launch_coarse_fused(idx, idx->X, n, pa.L, pa.mode, pa.lambda, pa.strict, nullptr, idx->l1,
                              idx->l2, fb, s);
     cudaFreeAsync(fb, s);
+    if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "build: coarse assignment");
   } else {
     st = launch_probe_exact(pa, s);
   }

@@ -17,6 +17,8 @@
 //     fp64 kernel.  Output: probe sets (search), or the RAIR pair (Alg. 3) /
 //     single assignment (build).  Results are always exactly O1 / O4.
 #include <algorithm>
+#include <climits>
+#include <cstdio>
 #include <mutex>
 
 #include "index.cuh"
@@ -77,8 +79,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   uint8_t* sB = smem + S * FT_A_BYTES;
   float* lv = reinterpret_cast<float*>(sB + S * FT_B_BYTES);  // smem path only
   uint32_t* li = reinterpret_cast<uint32_t*>(lv + (KR > 0 ? 0 : Wp1 * FT_BM));
-  float* gbuf = reinterpret_cast<float*>(li + (KR > 0 ? 0 : Wp1 * FT_BM));  // [32][128] staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(gbuf + 32 * FT_BM);
+  // g staging: [32][128] on the shared-memory path (warps 0-3), [32][256] on the
+  // register path (8 epilogue warps: column j of warp w's rows at j*256 + 32w + lane)
+  float* gbuf = reinterpret_cast<float*>(li + (KR > 0 ? 0 : Wp1 * FT_BM));
+  uint64_t* full = reinterpret_cast<uint64_t*>(gbuf + 32 * FT_BM * (KR > 0 ? FT_HALVES : 1));
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -561,7 +565,7 @@ rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s) {
   return RAIRS_OK;
 }
 
-static int coarse_width(int nl, int L) { return std::min(nl, L + 16 + L / 8); }
+static int coarse_width(int nl, int L) { return std::min(nl, L + 8 + L / 8); }
 
 bool coarse_fused_ok(const rairs_index_s* idx, int L) {
   if (idx->coarse_mode == 1) return false;  // forced exact
@@ -613,9 +617,16 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   for (int64_t r0 = 0; r0 < rows; r0 += CH) {
     const int64_t nr = std::min<int64_t>(CH, rows - r0);
     const int64_t mtiles = ceil_div(nr, FT_BM);
-    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148, mtiles)));
-    const int tps = (int)ceil_div(ntiles, nsplit);
-    nsplit = (int)ceil_div(ntiles, tps);
+    // column splits: minimise (waves of one CTA per SM) x (tiles per CTA), with
+    // the per-row candidate lists of all splits (nsplit * Wout) <= 512 for K2
+    int tps = ntiles, best_cost = INT32_MAX;
+    for (int t = ntiles; t >= 1; --t) {
+      const int ns = (int)ceil_div(ntiles, t);
+      if (ns * Wout > 512 && t != ntiles) break;
+      const int cost = (int)ceil_div(mtiles * ns, 148) * t;
+      if (cost < best_cost) { best_cost = cost; tps = t; }
+    }
+    const int nsplit = (int)ceil_div(ntiles, tps);
     const int npow_c = next_pow2(std::max(nsplit * Wout, 2));
     const size_t csmem = (size_t)CT_WARPS * ((size_t)npow_c * 8 + (size_t)npow_w * 12);
     if (csmem > 220 * 1024) {
@@ -657,6 +668,12 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     else
       coarse_topw_kernel<0><<<dim3((unsigned)mtiles, (unsigned)nsplit), FT_THREADS, smem, s>>>(tmA, tmB, ta);
     RAIRS_CHECK_LAUNCH();
+    if (debug_sync_enabled()) {
+      char what[160];
+      snprintf(what, sizeof(what), "coarse_topw_kernel (rows %lld..%lld of %lld, X=%p, Xc=%p)",
+               (long long)r0, (long long)(r0 + nr), (long long)rows, (const void*)X, (const void*)Xc);
+      RAIRS_TRY(debug_sync_point(s, what));
+    }
     CertArgs ca{};
     ca.vals = vals;
     ca.ids = ids;
@@ -691,6 +708,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     const int cgrid = (int)std::min<int64_t>(ceil_div(nr, CT_WARPS), 148 * 16);
     coarse_certify_kernel<<<cgrid, CT_THREADS, csmem_all, s>>>(ca);
     RAIRS_CHECK_LAUNCH();
+    RAIRS_DEBUG_POINT(s, "coarse_certify_kernel");
     // exact fp64 recomputation of the (rare) uncertified rows
     ProbeArgs pa{};
     pa.X = Xc;
@@ -707,6 +725,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     pa.l2 = ca.l2;
     pa.only_flagged = flags;
     rairs_status st = launch_probe_exact(pa, s);
+    if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "probe_exact fallback");
     cudaFreeAsync(vals, s);
     cudaFreeAsync(ids, s);
     cudaFreeAsync(flags, s);

@@ -50,6 +50,18 @@ struct Status {
   } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// RAIRS_DEBUG_SYNC=1: synchronise after the named launch and report a fault
+// there (debugging aid for large builds; off by default, no effect on results)
+bool debug_sync_enabled();
+rairs_status debug_sync_point(cudaStream_t s, const char* what);
+#define RAIRS_DEBUG_POINT(s, what)                                  \
+  do {                                                              \
+    if (::rairs::debug_sync_enabled()) {                            \
+      rairs_status _ds = ::rairs::debug_sync_point((s), (what));    \
+      if (_ds != RAIRS_OK) return _ds;                              \
+    }                                                               \
+  } while (0)
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // ---------------------------------------------------------------------------

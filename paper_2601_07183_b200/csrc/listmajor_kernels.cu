@@ -19,6 +19,7 @@
 //                      rows (sentinel for SEIL-skipped references, R9)
 //   lm_select_kernel   per query: DCO, two-pass histogram top-bigK by (s, id)
 #include <algorithm>
+#include <cstdlib>
 
 #include "index.cuh"
 #include "tc_helpers.cuh"
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
 // Tensor-core scoring, one list at a time (CTAs claim lists atomically).
 constexpr int LM_IT = 128;        // items per tile (MMA M)
 constexpr int LM_QT = 64;         // max queries per tile (MMA N <= 64)
-constexpr int LM_MAXREF = 1024;   // references per list on this path
+constexpr int LM_MAXREF = 2048;   // references per list on this path
 constexpr uint32_t LM_B_MAX = 64 * 1024;  // LUT tile bytes (QT x K)
 
 struct LMArgs {
@@ -302,6 +303,14 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >=
   return r;
 }
 
+template <int G>
+__device__ __forceinline__ uint32_t gcnt_of(const uint32_t (&gc)[G], int g) {
+  uint32_t v = gc[0];
+#pragma unroll
+  for (int i = 1; i < G; ++i) v = (g == i) ? gc[i] : v;  // no dynamic register indexing
+  return v;
+}
+
 // Warp-specialised pipeline (no CTA barrier per tile):
 //   generators  LM_GROUPS groups of four warps (group g takes item tiles
 //               t = g mod LM_GROUPS); warp w owns item rows 32(w%4).. (TMEM lane
@@ -319,17 +328,26 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >=
 // The LUT tile of a query tile arrives by one cp.async.bulk (pre-tiled by
 // lut_tiles_kernel); a CTA barrier separates query tiles.  TMEM: the A ring
 // (32 columns per stage) then two 64-column accumulators.
-constexpr int LM_GROUPS = 1;  // generator groups (1: two CTAs per SM; 2: one CTA per SM)
-constexpr int LM_GEN_WARPS = 4 * LM_GROUPS, LM_MMA_WARP = LM_GEN_WARPS;
-constexpr int LM_EPI0 = LM_GEN_WARPS + 1, LM_EPI_WARPS = 8;
-constexpr int LM_WS_THREADS = (LM_EPI0 + LM_EPI_WARPS) * 32;
-constexpr int LM_GSTAGES = 4, LM_STAGES = LM_GSTAGES * LM_GROUPS;  // A ring: 4 stages per group
-constexpr uint32_t LM_ACC_COL = 32 * LM_STAGES;                      // accumulators after the ring
-constexpr uint32_t LM_TMEM_COLS = LM_GROUPS == 1 ? 256 : 512;
-constexpr int LM_CTAS_PER_SM = 3 - LM_GROUPS;
+// Pipeline shape: G generator groups of 4 warps, GS TMEM A stages per group.
+template <int G, int GS>
+struct LMShape {
+  static constexpr int GEN_WARPS = 4 * G, MMA_WARP = 4 * G, EPI0 = 4 * G + 1, EPI_WARPS = 8;
+  static constexpr int THREADS = (EPI0 + EPI_WARPS) * 32;
+  static constexpr int STAGES = G * GS;
+  static constexpr uint32_t ACC_COL = 32 * STAGES;  // accumulators after the A ring
+  static constexpr uint32_t COLS_USED = ACC_COL + 2 * 64;
+  static constexpr uint32_t TMEM_COLS = COLS_USED <= 256 ? 256 : 512;
+  static constexpr int CTAS_PER_SM = TMEM_COLS == 256 ? 2 : 1;
+};
 
-template <int NU>
-__global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kernel(LMArgs a) {
+template <int NU, int G, int GS>
+__global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_PER_SM)
+    lm_tensor_kernel(LMArgs a) {
+  using SH = LMShape<G, GS>;
+  constexpr int LM_GROUPS = G, LM_GSTAGES = GS, LM_STAGES = SH::STAGES;
+  constexpr int LM_GEN_WARPS = SH::GEN_WARPS, LM_MMA_WARP = SH::MMA_WARP, LM_EPI0 = SH::EPI0;
+  constexpr int LM_EPI_WARPS = SH::EPI_WARPS, LM_WS_THREADS = SH::THREADS;
+  constexpr uint32_t LM_ACC_COL = SH::ACC_COL, LM_TMEM_COLS = SH::TMEM_COLS;
   constexpr int NCHUNK = 2 * NU;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -369,7 +387,9 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
   // role).  Each group owns its own 4-stage half of the A ring, so a group is
   // never more than one phase ahead of the MMA on any of its stages (an
   // mbarrier parity wait cannot tell phase k from phase k+2).
-  uint32_t gcnt0 = 0, gcnt1 = 0;
+  uint32_t gcnt[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) gcnt[g] = 0;
   uint32_t tile_ctr = 0;   // item tiles so far
   uint32_t qt_ctr = 0;     // query tiles so far (bfull phase)
 
@@ -441,11 +461,12 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
             for (int u = 0; u < NU; ++u) w[u] = 0ull;
           }
         };
-        uint64_t cur[NU], nxt[NU];
+        uint64_t cur[NU], nxt[NU], nxt2[NU];  // codes of this group's tiles t, t+G, t+2G
         load_codes((uint32_t)grp, cur);
+        load_codes((uint32_t)grp + LM_GROUPS, nxt);
         for (uint32_t t = (uint32_t)grp; t < ntiles; t += LM_GROUPS) {
-          load_codes(t + LM_GROUPS, nxt);  // this group's next tile
-          uint32_t cc = (grp ? gcnt1 : gcnt0) + (t / LM_GROUPS) * NCHUNK;  // group chunk index
+          load_codes(t + 2 * LM_GROUPS, nxt2);  // two of this group's tiles ahead
+          uint32_t cc = gcnt_of(gcnt, grp) + (t / LM_GROUPS) * NCHUNK;  // group chunk index
 #pragma unroll
           for (int c = 0; c < NCHUNK; c += 2, cc += 2) {
             // two chunks per step (NCHUNK and the ring position are even): the
@@ -477,7 +498,10 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
             }
           }
 #pragma unroll
-          for (int u = 0; u < NU; ++u) cur[u] = nxt[u];
+          for (int u = 0; u < NU; ++u) {
+            cur[u] = nxt[u];
+            nxt[u] = nxt2[u];
+          }
         }
       } else if (warp == LM_MMA_WARP) {
         // ---------------- MMA issuer ----------------
@@ -489,7 +513,7 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
           uint32_t tc = tile_ctr;
           for (uint32_t t = 0; t < ntiles; ++t, ++tc) {
             const int grp = (int)(t % LM_GROUPS);
-            uint32_t cc = (grp ? gcnt1 : gcnt0) + (t / LM_GROUPS) * NCHUNK;
+            uint32_t cc = gcnt_of(gcnt, grp) + (t / LM_GROUPS) * NCHUNK;
             const int acc = tc & 1;
             if (tc >= 2) mbar_wait(&tempty[acc], ((tc >> 1) - 1) & 1u);
             tc_fence_after();
@@ -568,12 +592,9 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
       }
-      if (LM_GROUPS == 2) {
-        gcnt0 += ((ntiles + 1) / 2) * NCHUNK;
-        gcnt1 += (ntiles / 2) * NCHUNK;
-      } else {
-        gcnt0 += ntiles * NCHUNK;
-      }
+#pragma unroll
+      for (int g = 0; g < G; ++g)  // tiles t = g mod G of this query tile
+        gcnt[g] += ((ntiles + (uint32_t)(G - 1 - g)) / (uint32_t)G) * NCHUNK;
       tile_ctr += ntiles;
       ++qt_ctr;
     }
@@ -590,7 +611,7 @@ __global__ void __launch_bounds__(LM_WS_THREADS, LM_CTAS_PER_SM) lm_tensor_kerne
 // Per query (one WARP per query): SEIL ranges over its score rows (R9 dedup),
 // histogram-threshold top-bigK with warp-private state (no CTA barriers).
 constexpr int SW_WARPS = 8;
-constexpr int SW_NB = 512;
+constexpr int SW_NB = 1024;
 
 struct SelArgs {
   const int32_t* probes;
@@ -920,13 +941,30 @@ bool listmajor_ok(const rairs_index_s* idx, int64_t nq, int nprobe, int bigK) {
   return true;
 }
 
-template <int NU>
+template <int NU, int G, int GS>
 static cudaError_t launch_lm_tensor(const LMArgs& la, size_t tsm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(lm_tensor_kernel<NU>,
+  using SH = LMShape<G, GS>;
+  cudaError_t e = cudaFuncSetAttribute(lm_tensor_kernel<NU, G, GS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
   if (e != cudaSuccess) return e;
-  lm_tensor_kernel<NU><<<148 * LM_CTAS_PER_SM, LM_WS_THREADS, tsm, s>>>(la);
+  lm_tensor_kernel<NU, G, GS><<<148 * SH::CTAS_PER_SM, SH::THREADS, tsm, s>>>(la);
   return cudaGetLastError();
+}
+
+// pipeline shape (generator groups x stages per group); RAIRS_LM_SHAPE=0..3
+// selects one for experiments, the default is shape 0
+template <int NU>
+static cudaError_t launch_lm_tensor_shape(const LMArgs& la, size_t tsm, cudaStream_t s) {
+  static const int shape = [] {
+    const char* e = getenv("RAIRS_LM_SHAPE");
+    return e ? atoi(e) : 0;
+  }();
+  switch (shape) {
+    case 1: return launch_lm_tensor<NU, 2, 4>(la, tsm, s);   // 1 CTA/SM, 8 generator warps
+    case 2: return launch_lm_tensor<NU, 4, 2>(la, tsm, s);   // 1 CTA/SM, 16 generator warps
+    case 3: return launch_lm_tensor<NU, 2, 2>(la, tsm, s);   // 2 CTAs/SM, 8 generator warps
+    default: return launch_lm_tensor<NU, 1, 4>(la, tsm, s);  // 2 CTAs/SM, 4 generator warps
+  }
 }
 
 rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s) {
@@ -1019,15 +1057,14 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.S = S;
   la.score_u32 = score_u32;
   la.nlist = nlist;
-  const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 +
-                     (2 * LM_STAGES + 5) * 8 + 64;
+  const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 + (2 * 8 + 5) * 8 + 64;
   switch (idx->M_pad / 16) {
-    case 1: LM_TRY(launch_lm_tensor<1>(la, tsm, s)); break;
-    case 2: LM_TRY(launch_lm_tensor<2>(la, tsm, s)); break;
-    case 3: LM_TRY(launch_lm_tensor<3>(la, tsm, s)); break;
-    case 4: LM_TRY(launch_lm_tensor<4>(la, tsm, s)); break;
-    case 6: LM_TRY(launch_lm_tensor<6>(la, tsm, s)); break;
-    case 8: LM_TRY(launch_lm_tensor<8>(la, tsm, s)); break;
+    case 1: LM_TRY(launch_lm_tensor_shape<1>(la, tsm, s)); break;
+    case 2: LM_TRY(launch_lm_tensor_shape<2>(la, tsm, s)); break;
+    case 3: LM_TRY(launch_lm_tensor_shape<3>(la, tsm, s)); break;
+    case 4: LM_TRY(launch_lm_tensor_shape<4>(la, tsm, s)); break;
+    case 6: LM_TRY(launch_lm_tensor_shape<6>(la, tsm, s)); break;
+    case 8: LM_TRY(launch_lm_tensor_shape<8>(la, tsm, s)); break;
     default: cleanup(); set_error("list-major: unsupported M"); return RAIRS_E_INTERNAL;
   }
   // 4. per-query selection (warp per query)
