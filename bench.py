@@ -225,6 +225,7 @@ def run_ours(args):
     idx.profile_enable(True)
     idx.profile_read(reset=True)
     idx.kernels_launched(reset=True)
+    idx.certify_fallbacks(reset=True)
     clk = ClockSampler(local_rank)
     clk.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -247,6 +248,7 @@ def run_ours(args):
     prof = idx.profile_read(reset=True)
     idx.profile_enable(False)
     kernels = idx.kernels_launched(reset=True) + (args.steps if world > 1 else 0)  # + K7 merge
+    fallbacks = idx.certify_fallbacks(reset=True)
     t_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
@@ -323,6 +325,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_unit": f"M/2 = {spec.M // 2} B per DCO",
                          "avg_launch_ms": round(scan_ms, 4)},
             "e2e": e2e, "gpu_launches": kernels,
+            "coarse_uncertified_per_step": round(fallbacks / args.steps, 1),
             "clocks": clocks, "wall_s_timed_region": round(wall, 4),
             "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
             "index": {k2: info[k2] for k2 in ("n", "n_slots", "n_cells", "n_refs", "n_double",

@@ -617,16 +617,11 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   for (int64_t r0 = 0; r0 < rows; r0 += CH) {
     const int64_t nr = std::min<int64_t>(CH, rows - r0);
     const int64_t mtiles = ceil_div(nr, FT_BM);
-    // column splits: minimise (waves of one CTA per SM) x (tiles per CTA), with
-    // the per-row candidate lists of all splits (nsplit * Wout) <= 512 for K2
-    int tps = ntiles, best_cost = INT32_MAX;
-    for (int t = ntiles; t >= 1; --t) {
-      const int ns = (int)ceil_div(ntiles, t);
-      if (ns * Wout > 512 && t != ntiles) break;
-      const int cost = (int)ceil_div(mtiles * ns, 148) * t;
-      if (cost < best_cost) { best_cost = cost; tps = t; }
-    }
-    const int nsplit = (int)ceil_div(ntiles, tps);
+    // column splits: enough CTAs to cover the SMs once (more splits only add
+    // per-CTA fixed cost and K2 merge work -- measured on c2pl)
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148, mtiles)));
+    const int tps = (int)ceil_div(ntiles, nsplit);
+    nsplit = (int)ceil_div(ntiles, tps);
     const int npow_c = next_pow2(std::max(nsplit * Wout, 2));
     const size_t csmem = (size_t)CT_WARPS * ((size_t)npow_c * 8 + (size_t)npow_w * 12);
     if (csmem > 220 * 1024) {

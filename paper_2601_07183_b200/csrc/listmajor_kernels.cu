@@ -19,6 +19,7 @@
 //                      rows (sentinel for SEIL-skipped references, R9)
 //   lm_select_kernel   per query: DCO, two-pass histogram top-bigK by (s, id)
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "index.cuh"
@@ -250,6 +251,8 @@ struct LMArgs {
   void* S;
   int score_u32;
   int nlist;
+  int diag;  // timing diagnostics only (RAIRS_LM_DIAG): 1 no stores, 2 no expansion, 4 no MMA,
+            // 8 no tcgen05.st, 16 no tcgen05.ld
 };
 
 // D[tmem] (+)= A[tmem] x B[smem desc]  (A: 128 item rows x 32 K-bytes, 8 columns)
@@ -259,6 +262,25 @@ __device__ __forceinline__ void umma_i8_ta(uint32_t tmem_d, uint32_t tmem_a, uin
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+// warp-wide variants: every lane executes them with the same (warp-uniform)
+// operands, one elected lane issues -- the operands stay in uniform registers
+// (no per-instruction lane waterfall around a lone-lane issue)
+__device__ __forceinline__ void umma_i8_ta_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
       : "memory");
 }
 
@@ -303,6 +325,18 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >=
   return r;
 }
 
+// diag & 64: accumulate the cycles a role spends in a wait (printed by CTA 0)
+__device__ __forceinline__ void lm_wait(uint64_t* bar, uint32_t phase, bool prof,
+                                        unsigned long long& acc) {
+  if (!prof) {
+    mbar_wait(bar, phase);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, phase);
+  acc += (unsigned long long)(clock64() - t0);
+}
+
 template <int G>
 __device__ __forceinline__ uint32_t gcnt_of(const uint32_t (&gc)[G], int g) {
   uint32_t v = gc[0];
@@ -344,7 +378,9 @@ template <int NU, int G, int GS>
 __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_PER_SM)
     lm_tensor_kernel(LMArgs a) {
   using SH = LMShape<G, GS>;
-  constexpr int LM_GROUPS = G, LM_GSTAGES = GS, LM_STAGES = SH::STAGES;
+  constexpr int LM_GROUPS = G, LM_STAGES = SH::STAGES;
+  constexpr int LM_GPAIRS = GS / 2;  // pair-stages (two chunks each) per group
+  static_assert(GS % 2 == 0, "stages come in pairs");
   constexpr int LM_GEN_WARPS = SH::GEN_WARPS, LM_MMA_WARP = SH::MMA_WARP, LM_EPI0 = SH::EPI0;
   constexpr int LM_EPI_WARPS = SH::EPI_WARPS, LM_WS_THREADS = SH::THREADS;
   constexpr uint32_t LM_ACC_COL = SH::ACC_COL, LM_TMEM_COLS = SH::TMEM_COLS;
@@ -368,7 +404,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < LM_STAGES; ++s) {
+    for (int s = 0; s < LM_GROUPS * LM_GPAIRS; ++s) {
       mbar_init(&full[s], 4);  // the 4 lane-quarter warps of the tile's generator group
       mbar_init(&empty[s], 1);
     }
@@ -383,6 +419,9 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  const bool prof = (a.diag & 64) != 0 && blockIdx.x == 0;
+  unsigned long long t_wait = 0, t_wait2 = 0, t_setup = 0, n_tiles_done = 0;
+  const long long t_kernel0 = clock64();
   // chunks produced / consumed so far per generator group (same values in every
   // role).  Each group owns its own 4-stage half of the A ring, so a group is
   // never more than one phase ahead of the MMA on any of its stages (an
@@ -394,6 +433,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   uint32_t qt_ctr = 0;     // query tiles so far (bfull phase)
 
   for (;;) {
+    const long long t_s0 = clock64();
     if (tid == 0) sh_list = atomicAdd(a.list_counter, 1u);
     __syncthreads();
     const uint32_t l = sh_list;
@@ -438,6 +478,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
       }
       __syncthreads();
 
+      if (prof && lane == 0) t_setup += (unsigned long long)(clock64() - t_s0);
       if (warp < LM_GEN_WARPS) {
         // ---------------- generators (2 groups of 4: even / odd item tiles) ----------------
         const int quarter = warp & 3, grp = warp >> 2;  // grp < LM_GROUPS
@@ -469,33 +510,31 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           uint32_t cc = gcnt_of(gcnt, grp) + (t / LM_GROUPS) * NCHUNK;  // group chunk index
 #pragma unroll
           for (int c = 0; c < NCHUNK; c += 2, cc += 2) {
-            // two chunks per step (NCHUNK and the ring position are even): the
+            // one pair-stage (two K-chunks, 64 TMEM columns) per hand-off: the
             // first tcgen05.st overlaps the second chunk's expansion, one
-            // wait::st covers both
+            // wait::st / arrive / MMA commit per pair
+            const uint32_t pc = cc >> 1;                       // group pair index
+            const int ps = grp * LM_GPAIRS + (int)(pc % LM_GPAIRS);
+            if (pc >= (uint32_t)LM_GPAIRS) lm_wait(&empty[ps], ((pc / LM_GPAIRS) - 1) & 1u, prof, t_wait);
+            tc_fence_after();
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int s = grp * LM_GSTAGES + (int)((cc + h) % LM_GSTAGES);
               const uint32_t w32 = (uint32_t)(cur[(c + h) >> 1] >> (32 * ((c + h) & 1)));
               uint32_t v[32];
 #pragma unroll
               for (int k = 0; k < 8; ++k) {  // one-hot of nibble n: byte n of 16 = 1
-                const uint32_t sh = ((w32 >> (4 * k)) & 15u) << 3;
+                const uint32_t sh = (a.diag & 2) ? 0u : ((w32 >> (4 * k)) & 15u) << 3;
                 v[4 * k + 0] = shl_clamp(1u, sh);
                 v[4 * k + 1] = shl_clamp(1u, sh - 32u);
                 v[4 * k + 2] = shl_clamp(1u, sh - 64u);
                 v[4 * k + 3] = shl_clamp(1u, sh - 96u);
               }
-              if (cc + h >= LM_GSTAGES) mbar_wait(&empty[s], (((cc + h) / LM_GSTAGES) - 1) & 1u);
-              tc_fence_after();
-              tmem_st32(tq + (uint32_t)(s * 32), v);
+              if (!(a.diag & 8)) tmem_st32(tq + (uint32_t)((2 * ps + h) * 32), v);
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (!(a.diag & 8)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-              mbar_arrive(&full[grp * LM_GSTAGES + (int)(cc % LM_GSTAGES)]);
-              mbar_arrive(&full[grp * LM_GSTAGES + (int)((cc + 1) % LM_GSTAGES)]);
-            }
+            if (lane == 0) mbar_arrive(&full[ps]);
           }
 #pragma unroll
           for (int u = 0; u < NU; ++u) {
@@ -504,32 +543,38 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           }
         }
       } else if (warp == LM_MMA_WARP) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+        {
           const uint32_t idesc =
               (2u << 4) | ((uint32_t)(Npad >> 3) << 17) | ((uint32_t)(LM_IT >> 4) << 24);
-          mbar_wait(bfull, qt_ctr & 1u);
+          lm_wait(bfull, qt_ctr & 1u, prof, t_wait2);
           tc_fence_after();
           uint32_t tc = tile_ctr;
           for (uint32_t t = 0; t < ntiles; ++t, ++tc) {
             const int grp = (int)(t % LM_GROUPS);
             uint32_t cc = gcnt_of(gcnt, grp) + (t / LM_GROUPS) * NCHUNK;
             const int acc = tc & 1;
-            if (tc >= 2) mbar_wait(&tempty[acc], ((tc >> 1) - 1) & 1u);
+            if (tc >= 2) lm_wait(&tempty[acc], ((tc >> 1) - 1) & 1u, prof, t_wait2);
             tc_fence_after();
             const uint32_t dt = tmem + LM_ACC_COL + (uint32_t)(acc * LM_QT);
-            for (int c = 0; c < NCHUNK; ++c, ++cc) {
-              const int s = grp * LM_GSTAGES + (int)(cc % LM_GSTAGES);
-              mbar_wait(&full[s], (cc / LM_GSTAGES) & 1u);
+            for (int c = 0; c < NCHUNK; c += 2, cc += 2) {
+              const uint32_t pc = cc >> 1;
+              const int ps = grp * LM_GPAIRS + (int)(pc % LM_GPAIRS);
+              lm_wait(&full[ps], (pc / LM_GPAIRS) & 1u, prof, t_wait);
               tc_fence_after();
-              const uint64_t bd = umma_desc_sw128(sB + (size_t)c * Npad * 128);
+              if (!(a.diag & 4)) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)  // K = 32 bytes per MMA: 8 TMEM columns, +2 desc units
-                umma_i8_ta(dt, tmem + (uint32_t)(s * 32 + 8 * k), bd + 2 * k, idesc,
-                           (c | k) != 0 ? 1u : 0u);
-              umma_commit(&empty[s]);
+                for (int h = 0; h < 2; ++h) {
+                  const uint64_t bd = umma_desc_sw128(sB + (size_t)(c + h) * Npad * 128);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)  // K = 32 bytes per MMA: 8 TMEM columns, +2 desc units
+                    umma_i8_ta_warp(dt, tmem + (uint32_t)((2 * ps + h) * 32 + 8 * k), bd + 2 * k,
+                                    idesc, ((c + h) | k) != 0 ? 1u : 0u);
+                }
+              }
+              umma_commit_warp(&empty[ps]);
             }
-            umma_commit(&tfull[acc]);
+            umma_commit_warp(&tfull[acc]);
           }
         }
         __syncwarp();
@@ -554,13 +599,18 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           // sentinel (all ones) for a skipped reference (R9) / row padding, so the
           // selection can stream whole rows with 16-B loads
           const bool inrow = item < Nl8;
-          mbar_wait(&tfull[acc], (tc >> 1) & 1u);
+          lm_wait(&tfull[acc], (tc >> 1) & 1u, prof, t_wait);
           tc_fence_after();
           const uint64_t base = a.sbase[l] + (uint64_t)q0 * Nl8 + item;
           for (int cb = 16 * half; cb < Npad; cb += 32) {
             uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + LM_ACC_COL + (uint32_t)(acc * LM_QT + cb), v);
-            if (inrow) {
+            if (!(a.diag & 16)) {
+              tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + LM_ACC_COL + (uint32_t)(acc * LM_QT + cb), v);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0u;
+            }
+            if (inrow && !(a.diag & 1)) {
               const int jn = min(16, nq_tile - cb);
               const uint32_t okb = (uint32_t)(ok >> cb) & 0xFFFFu;
               if (a.score_u32) {
@@ -592,6 +642,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
       }
+      if (prof) n_tiles_done += ntiles;
 #pragma unroll
       for (int g = 0; g < G; ++g)  // tiles t = g mod G of this query tile
         gcnt[g] += ((ntiles + (uint32_t)(G - 1 - g)) / (uint32_t)G) * NCHUNK;
@@ -601,6 +652,11 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   }
   tc_fence_before();
   __syncthreads();
+  if (prof && lane == 0) {
+    const char* role = warp < LM_GEN_WARPS ? "gen" : (warp == LM_MMA_WARP ? "mma" : "epi");
+    printf("LMPROF cta0 warp %2d %s total %lld setup %llu wait %llu wait2 %llu tiles %llu\n", warp,
+           role, (long long)(clock64() - t_kernel0), t_setup, t_wait, t_wait2, n_tiles_done);
+  }
   if (warp == LM_MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem, LM_TMEM_COLS);
@@ -1057,6 +1113,13 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.S = S;
   la.score_u32 = score_u32;
   la.nlist = nlist;
+  {
+    static const int diag = [] {
+      const char* e = getenv("RAIRS_LM_DIAG");
+      return e ? atoi(e) : 0;
+    }();
+    la.diag = diag;
+  }
   const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 + (2 * 8 + 5) * 8 + 64;
   switch (idx->M_pad / 16) {
     case 1: LM_TRY(launch_lm_tensor_shape<1>(la, tsm, s)); break;
