@@ -276,6 +276,26 @@ def run_ours(args):
         e2e = {"value": round(nq * args.steps / sum(e_times), 1), "unit": "queries/s",
                "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 12)}
 
+    # ---------------- one query at a time (paper's latency workload) ------------
+    lat = None
+    if world == 1 and args.latency_queries > 0:
+        nl = min(args.latency_queries, Q.shape[0])
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        for i in range(5):
+            idx.search(Qd[i:i + 1], k, chosen, rf)
+        ts = []
+        for i in range(nl):
+            ev0.record(stream)
+            idx.search(Qd[i:i + 1], k, chosen, rf)
+            ev1.record(stream)
+            ev1.synchronize()
+            ts.append(ev0.elapsed_time(ev1))
+        ts = np.array(ts)
+        lat = {"queries": nl, "nprobe": chosen, "p50_ms": round(float(np.percentile(ts, 50)), 4),
+               "p99_ms": round(float(np.percentile(ts, 99)), 4),
+               "scan_path": idx.scan_path(1, k, chosen, rf)}
+
     # ---------------- roofline of the dominant stage (the fast scan, A3-A6) ----------------
     peak, peak_src = load_peaks()
     scan_mode = idx.scan_path(Q.shape[0], k, chosen, rf)
@@ -326,6 +346,7 @@ def run_ours(args):
                          "avg_launch_ms": round(scan_ms, 4)},
             "e2e": e2e, "gpu_launches": kernels,
             "coarse_uncertified_per_step": round(fallbacks / args.steps, 1),
+            "latency_1q": lat,
             "clocks": clocks, "wall_s_timed_region": round(wall, 4),
             "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
             "index": {k2: info[k2] for k2 in ("n", "n_slots", "n_cells", "n_refs", "n_double",
@@ -427,6 +448,8 @@ def main():
     ap.add_argument("--assignment", default="AIR", choices=["AIR", "single"])
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency-queries", type=int, default=200,
+                    help="single-query searches timed for p50/p99 latency (0 = skip)")
     ap.add_argument("--gt-queries", type=int, default=0,
                     help="queries with exact ground truth for recall (0 = all)")
     args = ap.parse_args()

@@ -240,6 +240,187 @@ static rairs_status launch_probe_R(const ProbeArgs& a, cudaStream_t s) {
   return RAIRS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Exact fallback for a FEW flagged rows over MANY lists (large nlist): each
+// flagged row is split over PX_S centroid ranges handled by different CTAs
+// (exact fp64 ordered D64 per (row, list), O1; per-range first L by (D64, l)),
+// then one CTA per row merges the PX_S partial lists and writes the same
+// outputs as probe_exact_kernel (probes / RAIR pair / single).  Rows beyond
+// PX_CAP keep their flag for the tiled exact kernel.
+constexpr int PX_S = 64;
+constexpr int PX_CAP = 2048;
+constexpr int PX_T = 256;
+
+__global__ void flag_compact_kernel(const int32_t* __restrict__ flags, int64_t rows,
+                                    uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (flags[r]) {
+      const uint32_t i = atomicAdd(count, 1u);
+      if (i < (uint32_t)PX_CAP) list[i] = (uint32_t)r;
+    }
+  }
+}
+
+__device__ void cta_sort_pairs(uint64_t* k, uint32_t* id, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool asc = ((lo & size) == 0);
+        const uint64_t ka = k[lo], kb = k[hi];
+        const uint32_t ia = id[lo], ib = id[hi];
+        const bool gt = (ka > kb) || (ka == kb && ia > ib);
+        if (gt == asc) { k[lo] = kb; k[hi] = ka; id[lo] = ib; id[hi] = ia; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PX_T) probe_split_kernel(ProbeArgs a,
+                                                           const uint32_t* __restrict__ list,
+                                                           const uint32_t* __restrict__ count,
+                                                           int per, int npow,
+                                                           uint64_t* __restrict__ tk,
+                                                           uint32_t* __restrict__ ti) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm);
+  uint32_t* ids = reinterpret_cast<uint32_t*>(keys + npow);
+  double* xs = reinterpret_cast<double*>(ids + npow + (npow & 1));
+  const int64_t n = min(*count, (uint32_t)PX_CAP);
+  for (int64_t w = blockIdx.x; w < n * PX_S; w += gridDim.x) {
+    const int64_t i = w / PX_S;
+    const int sp = (int)(w - i * PX_S);
+    const int64_t r = list[i];
+    for (int t = threadIdx.x; t < a.d; t += PX_T) xs[t] = (double)a.X[r * a.d + t];
+    __syncthreads();
+    const int64_t l0 = (int64_t)sp * per;
+    for (int e = threadIdx.x; e < npow; e += PX_T) {
+      const int64_t l = l0 + e;
+      uint64_t key = kKeyInf;
+      if (e < per && l < a.nl) {
+        const float* c = a.C + l * a.d;
+        double acc = 0.0;
+        for (int t = 0; t < a.d; ++t) {  // ascending t, fp64 ordered (O1)
+          const double df = __dsub_rn(xs[t], (double)__ldg(c + t));
+          acc = __dadd_rn(acc, __dmul_rn(df, df));
+        }
+        key = dbits(acc);
+      }
+      keys[e] = key;
+      ids[e] = (uint32_t)l;
+    }
+    __syncthreads();
+    cta_sort_pairs(keys, ids, npow);
+    for (int j = threadIdx.x; j < a.L; j += PX_T) {
+      tk[(i * PX_S + sp) * a.L + j] = j < npow ? keys[j] : kKeyInf;
+      ti[(i * PX_S + sp) * a.L + j] = j < npow ? ids[j] : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(PX_T) probe_merge_kernel(ProbeArgs a,
+                                                           const uint32_t* __restrict__ list,
+                                                           const uint32_t* __restrict__ count,
+                                                           int npow, const uint64_t* __restrict__ tk,
+                                                           const uint32_t* __restrict__ ti,
+                                                           int32_t* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm);
+  uint32_t* ids = reinterpret_cast<uint32_t*>(keys + npow);
+  const int64_t n = min(*count, (uint32_t)PX_CAP);
+  const int L = a.L, lane = lane_id(), warp = warp_id();
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t row = list[i];
+    for (int e = threadIdx.x; e < npow; e += PX_T) {
+      const bool v = e < PX_S * L;
+      keys[e] = v ? tk[i * PX_S * L + e] : kKeyInf;
+      ids[e] = v ? ti[i * PX_S * L + e] : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    cta_sort_pairs(keys, ids, npow);
+    if (a.mode == 0) {
+      for (int j = threadIdx.x; j < L; j += PX_T) {
+        if (a.out_idx) a.out_idx[row * L + j] = (int32_t)ids[j];
+        if (a.out_idx64) a.out_idx64[row * L + j] = (int64_t)ids[j];
+        if (a.out_d64) a.out_d64[row * L + j] = __longlong_as_double((long long)keys[j]);
+      }
+    } else if (a.mode == 2) {
+      if (threadIdx.x == 0) { a.l1[row] = (int32_t)ids[0]; a.l2[row] = (int32_t)ids[0]; }
+    } else if (warp == 0) {
+      // Alg. 3 lines 3-11 over the first L = N_CANDS exact lists (fp64, O4)
+      const int start = a.strict ? 1 : 0;
+      double loss = 0.0;
+      const bool ok = (lane >= start) && (lane < L);
+      if (ok) {
+        const float* c0 = a.C + (int64_t)ids[0] * a.d;
+        const float* cj = a.C + (int64_t)ids[lane] * a.d;
+        const float* xr = a.X + row * a.d;
+        double ss = 0.0, ip = 0.0;
+        for (int t = 0; t < a.d; ++t) {
+          const double x = (double)xr[t];
+          const double r0t = __dsub_rn((double)c0[t], x);
+          const double rjt = __dsub_rn((double)cj[t], x);
+          ss = __dadd_rn(ss, __dmul_rn(rjt, rjt));
+          ip = __dadd_rn(ip, __dmul_rn(r0t, rjt));
+        }
+        loss = __dadd_rn(ss, __dmul_rn(a.lambda, ip));
+      }
+      int best = ok ? lane : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double l2v = __shfl_xor_sync(0xffffffffu, loss, o);
+        const int b2 = __shfl_xor_sync(0xffffffffu, best, o);
+        if (b2 != 0x7fffffff && (best == 0x7fffffff || l2v < loss || (l2v == loss && b2 < best))) {
+          loss = l2v;
+          best = b2;
+        }
+      }
+      if (lane == 0) {
+        const int c0 = (int)ids[0], cb = (int)ids[best];
+        a.l1[row] = min(c0, cb);
+        a.l2[row] = max(c0, cb);
+      }
+    }
+    if (threadIdx.x == 0 && flags) flags[row] = 0;  // done: the tiled kernel skips it
+    __syncthreads();
+  }
+}
+
+// Split-path exact fallback for flagged rows (large nlist); leaves flags set
+// only for rows it did not handle.  Returns RAIRS_OK without work when the
+// shape does not qualify.
+rairs_status launch_probe_split(const ProbeArgs& a, int32_t* flags, cudaStream_t s) {
+  if (a.rows <= 0 || !a.only_flagged || a.nl < 8192) return RAIRS_OK;
+  const int per = (int)ceil_div(a.nl, PX_S);
+  const int npow_s = next_pow2(std::max(per, a.L));
+  const int npow_m = next_pow2(PX_S * a.L);
+  const size_t sm_s = (size_t)npow_s * 12 + 8 + (size_t)a.d * 8;
+  const size_t sm_m = (size_t)npow_m * 12 + 8;
+  if (sm_s > 200 * 1024 || sm_m > 200 * 1024) return RAIRS_OK;
+  uint32_t *list = nullptr, *count = nullptr, *ti = nullptr;
+  uint64_t* tk = nullptr;
+  auto cleanup = [&]() { cudaFreeAsync(list, s); cudaFreeAsync(count, s); cudaFreeAsync(tk, s); cudaFreeAsync(ti, s); };
+#define PX_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return RAIRS_E_CUDA; } } while (0)
+  PX_TRY(cudaMallocAsync(&list, PX_CAP * 4, s));
+  PX_TRY(cudaMallocAsync(&count, 4, s));
+  PX_TRY(cudaMallocAsync(&tk, (size_t)PX_CAP * PX_S * a.L * 8, s));
+  PX_TRY(cudaMallocAsync(&ti, (size_t)PX_CAP * PX_S * a.L * 4, s));
+  PX_TRY(cudaMemsetAsync(count, 0, 4, s));
+  flag_compact_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.rows, 256), 148 * 32)), 256, 0, s>>>(
+      a.only_flagged, a.rows, list, count);
+  PX_TRY(cudaFuncSetAttribute(probe_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+  probe_split_kernel<<<148 * 4, PX_T, sm_s, s>>>(a, list, count, per, npow_s, tk, ti);
+  PX_TRY(cudaFuncSetAttribute(probe_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
+  probe_merge_kernel<<<148 * 2, PX_T, sm_m, s>>>(a, list, count, npow_m, tk, ti, flags);
+  PX_TRY(cudaGetLastError());
+  cleanup();
+  return RAIRS_OK;
+#undef PX_TRY
+}
+
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s) {
   if (a.rows <= 0) return RAIRS_OK;
   if (a.L < 1 || a.L > 1024 || a.L > a.nl) {

@@ -620,6 +620,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     // column splits: enough CTAs to cover the SMs once (more splits only add
     // per-CTA fixed cost and K2 merge work -- measured on c2pl)
     int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148, mtiles)));
+    nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys
     const int tps = (int)ceil_div(ntiles, nsplit);
     nsplit = (int)ceil_div(ntiles, tps);
     const int npow_c = next_pow2(std::max(nsplit * Wout, 2));
@@ -719,7 +720,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     pa.l1 = ca.l1;
     pa.l2 = ca.l2;
     pa.only_flagged = flags;
-    rairs_status st = launch_probe_exact(pa, s);
+    rairs_status st = launch_probe_split(pa, flags, s);  // large nlist: split rows over CTAs
+    if (st == RAIRS_OK) st = launch_probe_exact(pa, s);   // remaining flagged rows
     if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "probe_exact fallback");
     cudaFreeAsync(vals, s);
     cudaFreeAsync(ids, s);

@@ -83,6 +83,8 @@ struct ProbeArgs {
   const int32_t* only_flagged;  // mode 0: process only row groups with a flagged row
 };
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s);
+// few flagged rows x many lists: split exact fallback (clears the flags it handles)
+rairs_status launch_probe_split(const ProbeArgs& a, int32_t* flags, cudaStream_t s);
 
 rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, uint64_t seed,
                           int64_t max_train, float* centroids_out, cudaStream_t s);

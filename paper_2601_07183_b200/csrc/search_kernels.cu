@@ -698,18 +698,20 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
   int64_t q = blockIdx.x;
   if (q < nq) fetch_rows(load_key(q));
   uint64_t key_next = load_key(q + gridDim.x);
+  float qv = (q < nq && tid < D) ? __ldg(queries + q * D + tid) : 0.0f;  // query, one ahead
   for (; q < nq; q += gridDim.x) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       if (warp + 8 * j < bigK && lane < D4)
         *reinterpret_cast<float4*>(tile + (warp + 8 * j) * RSF + 4 * lane) = v[j];
     if (lane < 16 && myrow < bigK) gids[myrow] = gid;
-    if (tid < D) qs[tid] = (double)queries[q * D + tid];
+    if (tid < D) qs[tid] = (double)qv;
     if (tid == 0) nvalid = 0;
     __syncthreads();
     if (q + gridDim.x < nq) {
       fetch_rows(key_next);                        // rows of q + grid: in flight from here
       key_next = load_key(q + 2 * (int64_t)gridDim.x);
+      if (tid < D) qv = __ldg(queries + (q + gridDim.x) * D + tid);
     }
     if (tid < bigK) {
       const uint32_t g = gids[tid];

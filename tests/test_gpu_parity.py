@@ -404,3 +404,31 @@ def test_c4_full_size_sampled_properties(oracle_mod):
         assert np.array_equal(g["ids"][i], cid[valid][order].astype(np.int64)), "O10 ids"
         assert np.allclose(g["dists"][i], delta[order], rtol=1e-4, atol=0), "O10 distances"
     idx.free()
+
+
+def test_exact_fallback_split_path_large_nlist(oracle_mod):
+    """8,192 centroids packed in a tiny ball far from the origin: the TF32
+    filter can never certify (its error bound dwarfs the distance gaps), so
+    every query and every base row goes through the exact fallback -- the
+    split path (first 2,048 flagged rows per chunk) and the tiled kernel (the
+    rest). Probes and the RAIR assignment must equal O1 / O4 exactly."""
+    rng = np.random.default_rng(3)
+    center = rng.standard_normal(32).astype(np.float32)
+    center *= np.float32(100.0 / np.linalg.norm(center))
+    cent = (center + np.float32(1e-3) * rng.standard_normal((8192, 32))).astype(np.float32)
+    X = (center + np.float32(2e-3) * rng.standard_normal((6000, 32))).astype(np.float32)
+    Q = (center + np.float32(2e-3) * rng.standard_normal((300, 32))).astype(np.float32)
+    cb = oracle_mod.pq_train(X, 8, iters=2, seed=1)
+    idx = rb.Index.build(_t(X), 8192, 8, centroids=_t(cent), codebook=_t(cb))
+    l1, l2, _ = [t.cpu().numpy() for t in idx.export_assignment()]
+    ol1, ol2 = oracle_mod.assign(X, cent, "air")
+    assert np.array_equal(l1, ol1) and np.array_equal(l2, ol2)
+    Qd = _t(Q)
+    idx.set_coarse_mode("tensor")
+    for npb in (1, 10, 64):
+        idx.certify_fallbacks(reset=True)
+        pt = idx.search_debug(Qd, 10, npb, 2)["probes"].cpu().numpy()
+        fb = idx.certify_fallbacks(reset=True)
+        assert fb == Q.shape[0], f"expected every query uncertified, got {fb}"
+        assert np.array_equal(pt, oracle_mod.probe(Q, cent, npb))
+    idx.free()
