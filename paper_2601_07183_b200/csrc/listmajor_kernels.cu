@@ -761,10 +761,9 @@ __device__ void warp_sort_keys(uint64_t* a, int n) {
 // The query's score rows (one per probed list, padded to 8 items; skipped
 // references and padding hold the all-ones sentinel, R9) are streamed twice
 // with 16-B loads:
-//   pass 1  histogram of s >> hshift over the items of the nearest probed
-//           list(s) (>= 2 bigK items) -> the smallest bin b* whose cumulative
-//           count reaches bigK: the bigK-th score of any subset of U(q) bounds
-//           that of U(q), so every item of the top-bigK has bin <= b*;
+//   pass 1  histogram of s >> hshift over every valid item -> the smallest bin
+//           b* whose cumulative count reaches bigK: every item of the top-bigK
+//           has bin <= b*, and only ~bigK + |bin b*| items do;
 //   pass 2  items with bin <= b* are appended as PRE-keys (s << 32 | p << 22 |
 //           item) -- no id load on the streaming path;
 //   finish  the ids of the (few) candidates are loaded in one batch, the keys
@@ -806,10 +805,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 3) lm_select_kernel(SelArgs a) 
     for (int i = lane; i < SW_NB; i += 32) hist[i] = 0u;
     __syncwarp();
     const uint32_t* qb = a.qbits + (size_t)q * a.qwords;
-    // ---- pass 1: DCO, and the score histogram of the nearest probed lists
-    // only (until >= 2 bigK items): any subset of U(q) gives a valid cut, and
-    // the top-bigK come mostly from the nearest lists, so the cut stays tight
-    uint32_t dco = 0, hist_items = 0;
+    // ---- pass 1: DCO and the score histogram
+    uint32_t dco = 0;
     for (int p = 0; p < a.nprobe; ++p) {
       const uint32_t l = (uint32_t)a.probes[q * a.nprobe + p];
       const uint32_t Nl = a.list_items[l], Nl8 = (Nl + 7u) & ~7u;
@@ -822,8 +819,6 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 3) lm_select_kernel(SelArgs a) 
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
       dco += a.own_cnt[l] + c;
-      if (hist_items >= 2 * bigK) continue;
-      hist_items += Nl;
       const uint64_t row = a.sbase[l] + (uint64_t)a.qslot[q * a.nprobe + p] * Nl8;
       const uint4* rv = reinterpret_cast<const uint4*>(
           reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
