@@ -148,7 +148,7 @@ __device__ __forceinline__ float lut_T(const float* qs, const float* smc, int m,
   return acc;
 }
 
-template <int DSUB>
+template <int DSUB, int MPL>
 __global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
     const float* __restrict__ queries, int64_t nq, int d, const float* __restrict__ cb, int M,
     int M_pad, const int32_t* __restrict__ probes, int nprobe,
@@ -164,59 +164,84 @@ __global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
   }
   __syncthreads();
   float* mnw = smc + 16 * DSUB * M + warp * M;
+  // MPL: subquantizers per lane (ceil(M_pad / 32) <= 4 on the list-major path)
   for (int64_t q = (int64_t)blockIdx.x * LW + warp; q < nq; q += (int64_t)gridDim.x * LW) {
     const float* qv = queries + q * d;
+    // the destination of this query's row in each probed list-task's tile:
+    // lane p (< nprobe) resolves probe p once; the row loop reads it by shuffle
+    auto dst_of = [&](int p, uint64_t& base, uint32_t& npad, uint32_t& jqo) {
+      const int l = probes[q * nprobe + p];
+      const uint32_t j = qslot[q * nprobe + p], Ql = qcnt[l];
+      const uint32_t t = j / (uint32_t)QT;
+      jqo = j - t * (uint32_t)QT;
+      npad = (t < Ql / (uint32_t)QT) ? (uint32_t)QT : ((Ql - t * QT + 15u) & ~15u);
+      base = ((uint64_t)lrow[l] + (uint64_t)t * QT) * K;
+    };
+    uint64_t dst_base = 0;
+    uint32_t dst_npad = 0, dst_jq = 0;
+    if (lane < nprobe) dst_of(lane, dst_base, dst_npad, dst_jq);
+    float T[MPL][16];
     float S = 0.0f;
-    for (int m = lane; m < M; m += 32) {  // pass 1: per-subquantizer min and span
-      float qs[DSUB];
 #pragma unroll
-      for (int t = 0; t < DSUB; ++t) qs[t] = __ldg(qv + m * DSUB + t);
-      float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+    for (int u = 0; u < MPL; ++u) {  // pass 1: distances, per-subquantizer min and span
+      const int m = lane + 32 * u;
+      if (m < M) {
+        float qs[DSUB];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float T = lut_T<DSUB>(qs, smc, m, j, M);
-        lo = fminf(lo, T);
-        hi = fmaxf(hi, T);
+        for (int t = 0; t < DSUB; ++t) qs[t] = __ldg(qv + m * DSUB + t);
+        float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          T[u][j] = lut_T<DSUB>(qs, smc, m, j, M);
+          lo = fminf(lo, T[u][j]);
+          hi = fmaxf(hi, T[u][j]);
+        }
+        mnw[m] = lo;
+        S = fmaxf(S, __fsub_rn(hi, lo));
       }
-      mnw[m] = lo;
-      S = fmaxf(S, __fsub_rn(hi, lo));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) S = fmaxf(S, __shfl_xor_sync(0xffffffffu, S, o));
     const float a = (S > 0.0f) ? __fdiv_rn(255.0f, S) : 1.0f;
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && (a_out || b_out)) {  // parity/debug outputs only
       float bsum = 0.0f;
       for (int m = 0; m < M; ++m) bsum = __fadd_rn(bsum, mnw[m]);  // ascending m (O2 step 5)
       if (a_out) a_out[q] = a;
       if (b_out) b_out[q] = bsum;
     }
-    for (int m = lane; m < M_pad; m += 32) {  // pass 2: quantise, write every tile row
+#pragma unroll
+    for (int u = 0; u < MPL; ++u) {  // pass 2: quantise, write every tile row
+      const int m = lane + 32 * u;
+      if (32 * u >= M_pad) break;  // warp-uniform
       uint32_t w[4] = {0u, 0u, 0u, 0u};
       if (m < M) {
-        float qs[DSUB];
-#pragma unroll
-        for (int t = 0; t < DSUB; ++t) qs[t] = __ldg(qv + m * DSUB + t);
         const float lo = mnw[m];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float T = lut_T<DSUB>(qs, smc, m, j, M);
           uint32_t v = 0;
-          if (S > 0.0f) v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T, lo), a)));
+          if (S > 0.0f) v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T[u][j], lo), a)));
           w[j >> 2] |= v << (8 * (j & 3));
         }
         if (lut_dbg)
           *reinterpret_cast<uint4*>(lut_dbg + (size_t)q * M * 16 + m * 16) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      const int c = m >> 3, kk = m & 7;
-      for (int p = 0; p < nprobe; ++p) {
-        const int l = probes[q * nprobe + p];
-        const uint32_t j = qslot[q * nprobe + p], Ql = qcnt[l];
-        const uint32_t t = j / (uint32_t)QT, jq = j - t * (uint32_t)QT;
-        const uint32_t Npad = (t < Ql / (uint32_t)QT) ? (uint32_t)QT : ((Ql - t * QT + 15u) & ~15u);
-        uint8_t* base = tiles + ((size_t)lrow[l] + (size_t)t * QT) * K;
-        *reinterpret_cast<uint4*>(base + (size_t)c * Npad * 128 + jq * 128 + ((kk ^ (jq & 7)) << 4)) =
-            make_uint4(w[0], w[1], w[2], w[3]);
+      {  // all lanes take part in the shuffles; lanes m >= M_pad store nothing
+        const int c = m >> 3, kk = m & 7;
+        for (int p = 0; p < nprobe; ++p) {
+          uint64_t base;
+          uint32_t npad, jq;
+          if (p < 32) {  // warp-uniform
+            base = __shfl_sync(0xffffffffu, dst_base, p);
+            npad = __shfl_sync(0xffffffffu, dst_npad, p);
+            jq = __shfl_sync(0xffffffffu, dst_jq, p);
+          } else {
+            dst_of(p, base, npad, jq);
+          }
+          if (m >= M_pad) continue;
+          *reinterpret_cast<uint4*>(tiles + base + (size_t)c * npad * 128 + jq * 128 +
+                                    ((kk ^ (jq & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
       }
     }
     __syncwarp();  // mnw reuse
@@ -1073,20 +1098,29 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   {
     const size_t lsm = ((size_t)16 * idx->dsub * idx->M + (size_t)LW * idx->M) * 4;
     const unsigned lgrid = (unsigned)std::min<int64_t>(ceil_div(nq, LW), 1 << 30);
-#define LUT_LAUNCH(DS)                                                                          \
-  LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel<DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                              (int)lsm));                                                       \
-  lut_tiles_kernel<DS><<<lgrid, LW * 32, lsm, s>>>(sa.queries, nq, idx->d, idx->codebook, idx->M, \
-                                                  idx->M_pad, sa.probes, nprobe, qslot, cnt,    \
-                                                  lrow, QT, tiles, sa.lut_a, sa.lut_b, sa.lut_q)
+#define LUT_LAUNCH(DS, MP)                                                                   \
+  LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel<DS, MP>,                                      \
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));       \
+  lut_tiles_kernel<DS, MP><<<lgrid, LW * 32, lsm, s>>>(sa.queries, nq, idx->d, idx->codebook, \
+                                                      idx->M, idx->M_pad, sa.probes, nprobe,  \
+                                                      qslot, cnt, lrow, QT, tiles, sa.lut_a,   \
+                                                      sa.lut_b, sa.lut_q)
+#define LUT_LAUNCH_D(DS)                                  \
+  switch ((idx->M_pad + 31) / 32) {                        \
+    case 1: LUT_LAUNCH(DS, 1); break;                      \
+    case 2: LUT_LAUNCH(DS, 2); break;                      \
+    case 3: LUT_LAUNCH(DS, 3); break;                      \
+    default: LUT_LAUNCH(DS, 4); break;                     \
+  }
     switch (idx->dsub) {
-      case 1: LUT_LAUNCH(1); break;
-      case 2: LUT_LAUNCH(2); break;
-      case 3: LUT_LAUNCH(3); break;
-      case 4: LUT_LAUNCH(4); break;
-      case 8: LUT_LAUNCH(8); break;
+      case 1: LUT_LAUNCH_D(1); break;
+      case 2: LUT_LAUNCH_D(2); break;
+      case 3: LUT_LAUNCH_D(3); break;
+      case 4: LUT_LAUNCH_D(4); break;
+      case 8: LUT_LAUNCH_D(8); break;
       default: cleanup(); set_error("list-major: unsupported d/M"); return RAIRS_E_UNSUPPORTED;
     }
+#undef LUT_LAUNCH_D
 #undef LUT_LAUNCH
     LM_TRY(cudaGetLastError());
   }
