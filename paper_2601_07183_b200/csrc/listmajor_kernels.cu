@@ -30,10 +30,15 @@ namespace rairs {
 // ---------------------------------------------------------------------------
 // Grouping of (query, probe) pairs by list.
 __global__ void lm_count_kernel(const int32_t* __restrict__ probes, int64_t total,
-                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ qslot) {
+                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ qslot,
+                                uint32_t* __restrict__ qbits, int64_t nbits_words) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x)
     qslot[e] = atomicAdd(&cnt[probes[e]], 1u);
+  // the per-query probe bitmaps are zeroed here (lm_scatter, launched next, sets them)
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nbits_words;
+       w += (int64_t)gridDim.x * blockDim.x)
+    qbits[w] = 0u;
 }
 
 __global__ void lm_scatter_kernel(const int32_t* __restrict__ probes, int64_t total, int nprobe,
@@ -786,9 +791,11 @@ __device__ void warp_sort_keys(uint64_t* a, int n) {
 // The query's score rows (one per probed list, padded to 8 items; skipped
 // references and padding hold the all-ones sentinel, R9) are streamed twice
 // with 16-B loads:
-//   pass 1  histogram of s >> hshift over every valid item -> the smallest bin
-//           b* whose cumulative count reaches bigK: every item of the top-bigK
-//           has bin <= b*, and only ~bigK + |bin b*| items do;
+//   pass 1  histogram of s >> hshift over the minimum of every 16-B vector
+//           (8 or 4 items) -> the smallest bin b* whose cumulative count
+//           reaches bigK: the bigK-th score of any subset of U(q) bounds that
+//           of U(q), so every item of the top-bigK has bin <= b*; the vector
+//           minima hold almost all top items, so few more than bigK pass;
 //   pass 2  items with bin <= b* are appended as PRE-keys (s << 32 | p << 22 |
 //           item) -- no id load on the streaming path;
 //   finish  the ids of the (few) candidates are loaded in one batch, the keys
@@ -816,7 +823,7 @@ __device__ __forceinline__ void sel_resolve(const SelArgs& a, int64_t q, uint64_
 }
 
 template <bool U32>
-__global__ void __launch_bounds__(SW_WARPS * 32, 3) lm_select_kernel(SelArgs a) {
+__global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
   uint32_t* hist = reinterpret_cast<uint32_t*>(sm) + warp * SW_NB;
@@ -857,12 +864,17 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 3) lm_select_kernel(SelArgs a) 
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const uint32_t w4[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-#pragma unroll
-          for (int e = 0; e < PER; ++e) {
-            const uint32_t sc = U32 ? w4[e] : ((w4[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-            if (sc != SENT) atomicAdd(&hist[sc >> a.hshift], 1u);
+          // histogram of the per-vector minima: a subset of U(q) (so the cut
+          // stays valid) that holds almost every top item -- the bigK best
+          // items rarely share a vector -- at one atomic per 8 (4) items
+          uint32_t mn;
+          if (U32) {
+            mn = min(min(x[u].x, x[u].y), min(x[u].z, x[u].w));
+          } else {
+            const uint32_t m2 = __vminu2(__vminu2(x[u].x, x[u].y), __vminu2(x[u].z, x[u].w));
+            mn = min(m2 & 0xFFFFu, m2 >> 16);
           }
+          if (mn != SENT) atomicAdd(&hist[mn >> a.hshift], 1u);
         }
       }
     }
@@ -1085,11 +1097,10 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(cudaMallocAsync(&sbase, (size_t)(nlist + 1) * 8, s));
   LM_TRY(cudaMallocAsync(&S, std::max<size_t>(s_bytes, 16), s));
   LM_TRY(cudaMemsetAsync(cnt, 0, (size_t)(nlist + 1) * 4 + 16, s));
-  LM_TRY(cudaMemsetAsync(qbits, 0, (size_t)nq * qwords * 4, s));
   unsigned* list_counter = cnt + nlist + 1;  // zeroed tail of cnt
   // 1. group (query, probe) pairs by list
   const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npairs, 256), 148 * 8));
-  lm_count_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, cnt, qslot);
+  lm_count_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, cnt, qslot, qbits, nq * qwords);
   lm_scan_kernel<<<1, SCN, 0, s>>>(cnt, idx->list_items, nlist, qptr, sbase, lrow, totals, QT,
                                    LM_IT);
   lm_scatter_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, nprobe, qptr, qslot, list_q, qbits, qwords);
@@ -1097,7 +1108,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   // 2. quantised LUTs (O2), one warp per query, written into the list-task tiles
   {
     const size_t lsm = ((size_t)16 * idx->dsub * idx->M + (size_t)LW * idx->M) * 4;
-    const unsigned lgrid = (unsigned)std::min<int64_t>(ceil_div(nq, LW), 1 << 30);
+    const unsigned lgrid = (unsigned)std::min<int64_t>(ceil_div(nq, LW), 148 * 3);  // persistent
 #define LUT_LAUNCH(DS, MP)                                                                   \
   LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel<DS, MP>,                                      \
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));       \
@@ -1195,7 +1206,8 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.out_keys = sa.cand_keys;
   sl.dco = sa.dco;
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
-  const unsigned sgrid = (unsigned)std::min<int64_t>(ceil_div(nq, SW_WARPS), 1 << 30);
+  // persistent: 4 CTAs per SM, warps loop over queries (no partial last wave)
+  const unsigned sgrid = (unsigned)std::min<int64_t>(ceil_div(nq, SW_WARPS), 148 * 4);
   if (score_u32) {
     LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
     lm_select_kernel<true><<<sgrid, SW_WARPS * 32, ssm, s>>>(sl);
