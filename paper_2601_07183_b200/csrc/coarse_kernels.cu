@@ -390,10 +390,20 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
       // 16-B loads (all rows in flight at once), row stride d + 4 floats
       float* cs = a.stage_base(sm, warp);
       const int d4 = a.d >> 2, rs4 = d4 + 1;
-      for (int i = 0; i < Wc; ++i) {
-        const uint32_t l = (uint32_t)(keys[i] & 0xFFFFFFFFu);
-        const float4* c4 = reinterpret_cast<const float4*>(a.C + (size_t)l * a.d);
-        for (int t4 = lane; t4 < d4; t4 += 32) reinterpret_cast<float4*>(cs)[i * rs4 + t4] = __ldg(c4 + t4);
+      for (int i0 = 0; i0 < Wc; i0 += 8) {  // 8 rows' loads in flight before the stores
+        for (int t4 = lane; t4 < d4; t4 += 32) {
+          float4 r[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (i0 + u < Wc) {
+              const uint32_t l = (uint32_t)(keys[i0 + u] & 0xFFFFFFFFu);
+              r[u] = __ldg(reinterpret_cast<const float4*>(a.C + (size_t)l * a.d) + t4);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (i0 + u < Wc) reinterpret_cast<float4*>(cs)[(i0 + u) * rs4 + t4] = r[u];
+        }
       }
       __syncwarp();
       for (int i = lane; i < a.npow_w; i += 32) {
