@@ -346,6 +346,7 @@ struct CertArgs {
   int strict;
   double cmax;
   int npow_c, npow_w;
+  int capped_kr;       // > 0: capped register lists of this length (see launcher)
   int32_t* out_idx;
   int32_t* l1;
   int32_t* l2;
@@ -383,7 +384,18 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
     }
     __syncwarp();
     warp_sort_u64(keys, a.npow_c);
-    const float gnext = all ? 0.0f : unord_f32((uint32_t)(keys[W] >> 32));
+    float gnext = all ? 0.0f : unord_f32((uint32_t)(keys[W] >> 32));
+    if (!all && a.capped_kr > 0) {
+      // bound from the capped lists: min over full lists of their largest kept value
+      float gb = __int_as_float(0x7f800000);
+      for (int gi = lane; gi < tot / a.capped_kr; gi += 32) {
+        const uint32_t id = a.ids[r * tot + gi * a.capped_kr + a.capped_kr - 1];
+        if (id != 0xFFFFFFFFu) gb = fminf(gb, a.vals[r * tot + gi * a.capped_kr + a.capped_kr - 1]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gb = fminf(gb, __shfl_xor_sync(0xffffffffu, gb, o));
+      gnext = fminf(gnext, gb);
+    }
     const float* xr = a.X + (size_t)r * a.d;
     if (a.stage_rows) {
       // stage the Wc candidate centroid rows in shared memory with coalesced
@@ -580,7 +592,9 @@ static int coarse_width(int nl, int L) { return std::min(nl, L + 8 + L / 8); }
 bool coarse_fused_ok(const rairs_index_s* idx, int L) {
   if (idx->coarse_mode == 1) return false;  // forced exact
   if ((idx->d & 3) != 0 || !tma_available()) return false;
-  if (coarse_width(idx->nlist, L) + 1 > FT_MAX_WP1) return false;
+  const int wp1 = coarse_width(idx->nlist, L) + 1;
+  const bool capped_ok = ceil_div(idx->nlist, FT_BN) >= 8 && wp1 <= 256;  // capped register lists
+  if (wp1 > FT_MAX_WP1 && !capped_ok) return false;
   if (idx->coarse_mode == 2) return true;   // forced tensor-core path
   return idx->nlist >= 64 && L < idx->nlist;
 }
@@ -594,12 +608,18 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   const int nl = idx->nlist, d = idx->d;
   const int W = coarse_width(nl, L);
   const int Wp1 = W + 1;
-  if (Wp1 > FT_MAX_WP1) {
+  if (Wp1 > FT_MAX_WP1 && !(ceil_div(nl, FT_BN) >= 8 && Wp1 <= 256)) {
     set_error("coarse: nprobe too large for the fused tensor-core path");
     return RAIRS_E_UNSUPPORTED;
   }
   const int ntiles = (int)ceil_div(nl, FT_BN);
-  const bool reg = Wp1 <= 32;               // register-resident sorted lists
+  // register-resident sorted lists; for W + 1 > 32 the lists are CAPPED at 32
+  // per (row, column split, half) and K2 lowers its bound to the smallest
+  // 32nd value of any full list (the excluded columns of a group are no
+  // smaller than the largest value it kept), so the certificate stays valid
+  const int nl_tiles = (int)ceil_div(nl, FT_BN);
+  const bool capped = Wp1 > 32 && nl_tiles >= 8;
+  const bool reg = Wp1 <= 32 || capped;
   const int KR = Wp1 <= 16 ? 16 : (Wp1 <= 24 ? 24 : 32);
   const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
   const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
@@ -630,6 +650,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     // column splits: enough CTAs to cover the SMs once (more splits only add
     // per-CTA fixed cost and K2 merge work -- measured on c2pl)
     int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148, mtiles)));
+    if (capped)  // >= 4 capped lists per needed 32 candidates: a group rarely holds > 32 of them
+      nsplit = std::max<int>(nsplit, (int)std::min<int64_t>(ntiles, ceil_div(4 * ceil_div(Wp1, 32), FT_HALVES)));
     nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys
     const int tps = (int)ceil_div(ntiles, nsplit);
     nsplit = (int)ceil_div(ntiles, tps);
@@ -697,6 +719,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ca.strict = strict;
     ca.cmax = idx->cmax;
     ca.npow_c = npow_c;
+    ca.capped_kr = capped ? KR : 0;
     ca.npow_w = npow_w;
     ca.out_idx = out_idx ? out_idx + r0 * L : nullptr;
     ca.l1 = l1 ? l1 + r0 : nullptr;

@@ -432,3 +432,51 @@ def test_exact_fallback_split_path_large_nlist(oracle_mod):
         assert fb == Q.shape[0], f"expected every query uncertified, got {fb}"
         assert np.array_equal(pt, oracle_mod.probe(Q, cent, npb))
     idx.free()
+
+
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
+def test_parity_dsub4_padded_M(oracle_mod, scan):
+    """d/M = 4 (as BJ configs[2]) with M = 24 (not a multiple of 16: the LUT
+    has zero rows up to M_pad = 32, the code units are padded), AIR + SEIL."""
+    rng = np.random.default_rng(17)
+    means = rng.standard_normal((24, 96)).astype(np.float32)
+    X = (means[rng.integers(0, 24, 5000)] + 0.8 * rng.standard_normal((5000, 96))).astype(np.float32)
+    Q = (means[rng.integers(0, 24, 300)] + 0.8 * rng.standard_normal((300, 96))).astype(np.float32)
+    cent = oracle_mod.kmeans(X, 32, iters=4, seed=5)
+    cb = oracle_mod.pq_train(X, 24, iters=4, seed=6)
+    l1, l2 = oracle_mod.assign(X, cent, "air")
+    codes = oracle_mod.encode(X, cb)
+    idx = rb.Index.build(_t(X), 32, 24, centroids=_t(cent), codebook=_t(cb))
+    gl1, gl2, gcodes = [t.cpu().numpy() for t in idx.export_assignment()]
+    assert np.array_equal(gl1, l1) and np.array_equal(gl2, l2) and np.array_equal(gcodes, codes)
+    for k, nprobe, rf in ((10, 4, 10), (5, 12, 4)):
+        o = oracle_mod.search(X, l1, l2, codes, cent, cb, Q, k, nprobe, rf)
+        assert_search_equal(gpu_search(idx, Q, k, nprobe, rf, scan), o)
+    idx.free()
+
+
+def test_coarse_capped_lists_large_nprobe(oracle_mod):
+    """nlist 4,096 (16 column tiles) and nprobe 48 / 96: W + 1 > 32, so the
+    top-W epilogue keeps capped 32-entry register lists per (row, split, half)
+    and K2 certifies against the smallest full list's 32nd value. Probe sets
+    must equal the exact kernel's and O1 on a sample."""
+    rng = np.random.default_rng(9)
+    means = rng.standard_normal((512, 32)).astype(np.float32)
+    X = (means[rng.integers(0, 512, 60000)] + 0.5 * rng.standard_normal((60000, 32))).astype(np.float32)
+    Q = (means[rng.integers(0, 512, 2000)] + 0.5 * rng.standard_normal((2000, 32))).astype(np.float32)
+    cent = X[rng.choice(X.shape[0], 4096, replace=False)].copy()
+    cb = oracle_mod.pq_train(X[:20000], 8, iters=2, seed=1)
+    idx = rb.Index.build(_t(X), 4096, 8, centroids=_t(cent), codebook=_t(cb))
+    Qd = _t(Q)
+    sample = np.arange(0, Q.shape[0], 20)
+    for npb in (48, 96):
+        idx.set_coarse_mode("exact")
+        pe = idx.search_debug(Qd, 10, npb, 2)["probes"].cpu().numpy()
+        idx.set_coarse_mode("tensor")
+        idx.certify_fallbacks(reset=True)
+        pt = idx.search_debug(Qd, 10, npb, 2)["probes"].cpu().numpy()
+        fb = idx.certify_fallbacks(reset=True)
+        assert np.array_equal(pe, pt)
+        assert fb <= 0.05 * Q.shape[0], f"{fb} uncertified queries at nprobe {npb}"
+        assert np.array_equal(pt[sample], oracle_mod.probe(Q[sample], cent, npb))
+    idx.free()
