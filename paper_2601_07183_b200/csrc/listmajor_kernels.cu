@@ -281,8 +281,6 @@ struct LMArgs {
   void* S;
   int score_u32;
   int nlist;
-  int diag;  // timing diagnostics only (RAIRS_LM_DIAG): 1 no stores, 2 no expansion, 4 no MMA,
-            // 8 no tcgen05.st, 16 no tcgen05.ld
 };
 
 // D[tmem] (+)= A[tmem] x B[smem desc]  (A: 128 item rows x 32 K-bytes, 8 columns)
@@ -353,18 +351,6 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >=
   uint32_t r;
   asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
   return r;
-}
-
-// diag & 64: accumulate the cycles a role spends in a wait (printed by CTA 0)
-__device__ __forceinline__ void lm_wait(uint64_t* bar, uint32_t phase, bool prof,
-                                        unsigned long long& acc) {
-  if (!prof) {
-    mbar_wait(bar, phase);
-    return;
-  }
-  const long long t0 = clock64();
-  mbar_wait(bar, phase);
-  acc += (unsigned long long)(clock64() - t0);
 }
 
 template <int G>
@@ -449,9 +435,6 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const bool prof = (a.diag & 64) != 0 && blockIdx.x == 0;
-  unsigned long long t_wait = 0, t_wait2 = 0, t_setup = 0, n_tiles_done = 0;
-  const long long t_kernel0 = clock64();
   // chunks produced / consumed so far per generator group (same values in every
   // role).  Each group owns its own 4-stage half of the A ring, so a group is
   // never more than one phase ahead of the MMA on any of its stages (an
@@ -463,7 +446,6 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   uint32_t qt_ctr = 0;     // query tiles so far (bfull phase)
 
   for (;;) {
-    const long long t_s0 = clock64();
     if (tid == 0) sh_list = atomicAdd(a.list_counter, 1u);
     __syncthreads();
     const uint32_t l = sh_list;
@@ -508,7 +490,6 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
       }
       __syncthreads();
 
-      if (prof && lane == 0) t_setup += (unsigned long long)(clock64() - t_s0);
       if (warp < LM_GEN_WARPS) {
         // ---------------- generators (2 groups of 4: even / odd item tiles) ----------------
         const int quarter = warp & 3, grp = warp >> 2;  // grp < LM_GROUPS
@@ -545,7 +526,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
             // wait::st / arrive / MMA commit per pair
             const uint32_t pc = cc >> 1;                       // group pair index
             const int ps = grp * LM_GPAIRS + (int)(pc % LM_GPAIRS);
-            if (pc >= (uint32_t)LM_GPAIRS) lm_wait(&empty[ps], ((pc / LM_GPAIRS) - 1) & 1u, prof, t_wait);
+            if (pc >= (uint32_t)LM_GPAIRS) mbar_wait(&empty[ps], ((pc / LM_GPAIRS) - 1) & 1u);
             tc_fence_after();
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -553,15 +534,15 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
               uint32_t v[32];
 #pragma unroll
               for (int k = 0; k < 8; ++k) {  // one-hot of nibble n: byte n of 16 = 1
-                const uint32_t sh = (a.diag & 2) ? 0u : ((w32 >> (4 * k)) & 15u) << 3;
+                const uint32_t sh = ((w32 >> (4 * k)) & 15u) << 3;
                 v[4 * k + 0] = shl_clamp(1u, sh);
                 v[4 * k + 1] = shl_clamp(1u, sh - 32u);
                 v[4 * k + 2] = shl_clamp(1u, sh - 64u);
                 v[4 * k + 3] = shl_clamp(1u, sh - 96u);
               }
-              if (!(a.diag & 8)) tmem_st32(tq + (uint32_t)((2 * ps + h) * 32), v);
+              tmem_st32(tq + (uint32_t)((2 * ps + h) * 32), v);
             }
-            if (!(a.diag & 8)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[ps]);
@@ -577,22 +558,22 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
         {
           const uint32_t idesc =
               (2u << 4) | ((uint32_t)(Npad >> 3) << 17) | ((uint32_t)(LM_IT >> 4) << 24);
-          lm_wait(bfull, qt_ctr & 1u, prof, t_wait2);
+          mbar_wait(bfull, qt_ctr & 1u);
           tc_fence_after();
           uint32_t tc = tile_ctr;
           for (uint32_t t = 0; t < ntiles; ++t, ++tc) {
             const int grp = (int)(t % LM_GROUPS);
             uint32_t cc = gcnt_of(gcnt, grp) + (t / LM_GROUPS) * NCHUNK;
             const int acc = tc & 1;
-            if (tc >= 2) lm_wait(&tempty[acc], ((tc >> 1) - 1) & 1u, prof, t_wait2);
+            if (tc >= 2) mbar_wait(&tempty[acc], ((tc >> 1) - 1) & 1u);
             tc_fence_after();
             const uint32_t dt = tmem + LM_ACC_COL + (uint32_t)(acc * LM_QT);
             for (int c = 0; c < NCHUNK; c += 2, cc += 2) {
               const uint32_t pc = cc >> 1;
               const int ps = grp * LM_GPAIRS + (int)(pc % LM_GPAIRS);
-              lm_wait(&full[ps], (pc / LM_GPAIRS) & 1u, prof, t_wait);
+              mbar_wait(&full[ps], (pc / LM_GPAIRS) & 1u);
               tc_fence_after();
-              if (!(a.diag & 4)) {
+              {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   const uint64_t bd = umma_desc_sw128(sB + (size_t)(c + h) * Npad * 128);
@@ -629,18 +610,13 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           // sentinel (all ones) for a skipped reference (R9) / row padding, so the
           // selection can stream whole rows with 16-B loads
           const bool inrow = item < Nl8;
-          lm_wait(&tfull[acc], (tc >> 1) & 1u, prof, t_wait);
+          mbar_wait(&tfull[acc], (tc >> 1) & 1u);
           tc_fence_after();
           const uint64_t base = a.sbase[l] + (uint64_t)q0 * Nl8 + item;
           for (int cb = 16 * half; cb < Npad; cb += 32) {
             uint32_t v[16];
-            if (!(a.diag & 16)) {
-              tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + LM_ACC_COL + (uint32_t)(acc * LM_QT + cb), v);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0u;
-            }
-            if (inrow && !(a.diag & 1)) {
+            tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + LM_ACC_COL + (uint32_t)(acc * LM_QT + cb), v);
+            if (inrow) {
               const int jn = min(16, nq_tile - cb);
               const uint32_t okb = (uint32_t)(ok >> cb) & 0xFFFFu;
               if (a.score_u32) {
@@ -672,7 +648,6 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
       }
-      if (prof) n_tiles_done += ntiles;
 #pragma unroll
       for (int g = 0; g < G; ++g)  // tiles t = g mod G of this query tile
         gcnt[g] += ((ntiles + (uint32_t)(G - 1 - g)) / (uint32_t)G) * NCHUNK;
@@ -682,11 +657,6 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   }
   tc_fence_before();
   __syncthreads();
-  if (prof && lane == 0) {
-    const char* role = warp < LM_GEN_WARPS ? "gen" : (warp == LM_MMA_WARP ? "mma" : "epi");
-    printf("LMPROF cta0 warp %2d %s total %lld setup %llu wait %llu wait2 %llu tiles %llu\n", warp,
-           role, (long long)(clock64() - t_kernel0), t_setup, t_wait, t_wait2, n_tiles_done);
-  }
   if (warp == LM_MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem, LM_TMEM_COLS);
@@ -1044,20 +1014,11 @@ static cudaError_t launch_lm_tensor(const LMArgs& la, size_t tsm, cudaStream_t s
   return cudaGetLastError();
 }
 
-// pipeline shape (generator groups x stages per group); RAIRS_LM_SHAPE=0..3
-// selects one for experiments, the default is shape 0
+// pipeline shape: one generator group, 4 A stages (2 pair-stages), 2 CTAs/SM
+// (measured best of 1x4, 2x4, 4x2, 2x2 -- profiles/r01/SUMMARY.md)
 template <int NU>
 static cudaError_t launch_lm_tensor_shape(const LMArgs& la, size_t tsm, cudaStream_t s) {
-  static const int shape = [] {
-    const char* e = getenv("RAIRS_LM_SHAPE");
-    return e ? atoi(e) : 0;
-  }();
-  switch (shape) {
-    case 1: return launch_lm_tensor<NU, 2, 4>(la, tsm, s);   // 1 CTA/SM, 8 generator warps
-    case 2: return launch_lm_tensor<NU, 4, 2>(la, tsm, s);   // 1 CTA/SM, 16 generator warps
-    case 3: return launch_lm_tensor<NU, 2, 2>(la, tsm, s);   // 2 CTAs/SM, 8 generator warps
-    default: return launch_lm_tensor<NU, 1, 4>(la, tsm, s);  // 2 CTAs/SM, 4 generator warps
-  }
+  return launch_lm_tensor<NU, 1, 4>(la, tsm, s);
 }
 
 rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s) {
@@ -1158,13 +1119,6 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.S = S;
   la.score_u32 = score_u32;
   la.nlist = nlist;
-  {
-    static const int diag = [] {
-      const char* e = getenv("RAIRS_LM_DIAG");
-      return e ? atoi(e) : 0;
-    }();
-    la.diag = diag;
-  }
   const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 + (2 * 8 + 5) * 8 + 64;
   switch (idx->M_pad / 16) {
     case 1: LM_TRY(launch_lm_tensor_shape<1>(la, tsm, s)); break;
