@@ -311,6 +311,15 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # ---------------- AIR + SEIL vs single assignment (the paper's comparison) ----
+    vs_single = None
+    if world == 1 and args.compare_single and X is not None:
+        vs_single = compare_single(args, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream)
+        vs_single["air"] = {"nprobe": chosen, "recall": round(recall, 4),
+                            "qps": round(qps, 1), "dco_per_query": round(dco_total / nq, 1)}
+        vs_single["dco_ratio_air_over_single"] = round(
+            vs_single["air"]["dco_per_query"] / max(1.0, vs_single["single"]["dco_per_query"]), 3)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(idx, X, Q, spec, chosen)
@@ -347,6 +356,7 @@ def run_ours(args):
             "e2e": e2e, "gpu_launches": kernels,
             "coarse_uncertified_per_step": round(fallbacks / args.steps, 1),
             "latency_1q": lat,
+            "air_vs_single": vs_single,
             "clocks": clocks, "wall_s_timed_region": round(wall, 4),
             "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
             "index": {k2: info[k2] for k2 in ("n", "n_slots", "n_cells", "n_refs", "n_double",
@@ -357,6 +367,46 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def compare_single(args, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream):
+    """Single-assignment index from the SAME trained centroids/codebook: the
+    smallest swept nprobe reaching recall10@10 >= 0.95, its QPS (same timing
+    protocol, fewer steps) and DCO per query."""
+    import torch
+    import paper_2601_07183_b200 as rb
+    k, rf = spec.k, spec.refine_factor
+    cent, cb = idx.export_trained()
+    Xd = torch.from_numpy(X).to(Qd.device)
+    ids_ = rb.Index.build(Xd, spec.nlist, spec.M, assignment="single", centroids=cent, codebook=cb)
+    del Xd
+    chosen, rec = None, None
+    for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
+        ids, dists = ids_.search(Qd, k, npb, rf)
+        r = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], k)
+        chosen, rec = npb, r
+        if r >= 0.95:
+            break
+    _, _, dco = ids_.search(Qd, k, chosen, rf, return_dco=True)
+    for _ in range(3):
+        ids_.search(Qd, k, chosen, rf)
+    steps = max(3, args.steps // 2)
+    t = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ids_.search(Qd, k, chosen, rf)
+        e1.record(stream)
+        e1.synchronize()
+        t += e0.elapsed_time(e1)
+    nq = Qd.shape[0]
+    out = {"single": {"nprobe": chosen, "recall": round(rec, 4),
+                      "qps": round(nq * steps / (t / 1e3), 1),
+                      "dco_per_query": round(float(dco.sum().item()) / nq, 1)}}
+    ids_.free()
+    return out
 
 
 def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
@@ -448,6 +498,8 @@ def main():
     ap.add_argument("--assignment", default="AIR", choices=["AIR", "single"])
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--compare-single", type=int, default=1,
+                    help="also measure a single-assignment index on the same trained state")
     ap.add_argument("--latency-queries", type=int, default=200,
                     help="single-query searches timed for p50/p99 latency (0 = skip)")
     ap.add_argument("--gt-queries", type=int, default=0,
