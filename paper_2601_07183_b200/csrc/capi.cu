@@ -101,6 +101,9 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
+  for (auto& st : x->aux) if (st) cudaStreamDestroy(st);
+  for (auto& e : x->aux_ev) if (e) cudaEventDestroy(e);
+  delete x->aux_mu;
   for (auto& es : x->pending)
     for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
   for (auto e : x->pool) cudaEventDestroy(e);
@@ -185,21 +188,26 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   }
   ev.mark(1);
   int64_t nk = coarse_fused_ok(idx, nprobe) ? 3 : 1;  // topw + certify + exact fallback
+  bool refined = false;
   if (st == RAIRS_OK) {
     if (listmajor_ok(idx, nq, nprobe, bigK)) {
+      a.fused_refine = true;
+      a.ev_selected = ev.on ? ev.ev.e[2] : nullptr;
       st = launch_listmajor(idx, a, s);
-      nk += 6;  // count, scan, scatter, lut_tiles, tensor, select
+      const int halves = (nq >= 2 * LM_OVERLAP_MIN_Q && idx->aux[0]) ? 2 : 1;
+      nk += 5 + 2 * halves;  // count, scan, scatter, lut_tiles, tensor + (select, refine) x halves
+      refined = true;
     } else {
       st = launch_scan(idx, a, s);
       nk += 1;
+      ev.mark(2);
     }
   }
-  ev.mark(2);
   if (st == RAIRS_OK && (cand_ids || cand_scores)) {
     st = launch_split_keys(keys, nq * bigK, cand_ids, cand_scores, s);
     nk += 1;
   }
-  if (st == RAIRS_OK) {
+  if (st == RAIRS_OK && !refined) {
     st = launch_refine(idx, a, s);
     nk += 1;
   }

@@ -1,6 +1,7 @@
 // index.cuh -- device-resident RAIRS index (one shard) and kernel launchers.
 #pragma once
 
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -46,6 +47,10 @@ struct rairs_index_s {
   uint32_t* list_ids = nullptr;      // [sum N_l] global id of item i of list-task l
   int max_refs = 0;
   int64_t device_bytes = 0;
+  // two auxiliary streams + fork/join events (list-major select/refine overlap)
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t aux_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::mutex* aux_mu = nullptr;  // one search at a time enqueues on the aux streams
 
   // stage profiling (CUDA events on the search stream)
   bool prof = false;
@@ -110,6 +115,9 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s);
 bool listmajor_ok(const rairs_index_s* idx, int64_t nq, int nprobe, int bigK);
 struct SearchArgs;
 rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
+// batches of at least 2 x this many queries run select + refine as two
+// overlapped halves on the index's auxiliary streams
+constexpr int64_t LM_OVERLAP_MIN_Q = 2048;
 
 // ---- search-side launchers (search_kernels.cu) -----------------------------
 struct SearchArgs {
@@ -124,6 +132,11 @@ struct SearchArgs {
   float* lut_b;
   int64_t* out_ids;
   float* out_dists;
+  // list-major path: also run the refine (overlapped with the selection, in
+  // query halves on the index's two auxiliary streams); record ev_selected on
+  // the search stream once every query's candidates are final (stage timing)
+  bool fused_refine = false;
+  cudaEvent_t ev_selected = nullptr;
 };
 rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);

@@ -693,6 +693,7 @@ struct SelArgs {
   int shard_id, nshards;
   uint64_t* out_keys;
   int64_t* dco;
+  int64_t q0;  // first query of this launch (queries [q0, nq))
 };
 
 __device__ __forceinline__ uint32_t warp_bthr(const uint32_t* hist, uint32_t bigK) {
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
   const uint32_t bigK = (uint32_t)a.bigK;
   constexpr uint32_t SENT = U32 ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr int PER = U32 ? 4 : 8;  // scores per 16-B vector
-  for (int64_t q = (int64_t)blockIdx.x * SW_WARPS + warp; q < a.nq;
+  for (int64_t q = a.q0 + (int64_t)blockIdx.x * SW_WARPS + warp; q < a.nq;
        q += (int64_t)gridDim.x * SW_WARPS) {
     for (int i = lane; i < SW_NB; i += 32) hist[i] = 0u;
     __syncwarp();
@@ -1160,16 +1161,59 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.out_keys = sa.cand_keys;
   sl.dco = sa.dco;
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
-  // persistent: 4 CTAs per SM, warps loop over queries (no partial last wave)
-  const unsigned sgrid = (unsigned)std::min<int64_t>(ceil_div(nq, SW_WARPS), 148 * 4);
-  if (score_u32) {
-    LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    lm_select_kernel<true><<<sgrid, SW_WARPS * 32, ssm, s>>>(sl);
+  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  auto select_range = [&](int64_t q0, int64_t q1, cudaStream_t st) -> cudaError_t {
+    SelArgs sr = sl;
+    sr.q0 = q0;
+    sr.nq = q1;
+    // persistent: 4 CTAs per SM, warps loop over queries (no partial last wave)
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q1 - q0, SW_WARPS), 148 * 4));
+    if (score_u32) lm_select_kernel<true><<<g, SW_WARPS * 32, ssm, st>>>(sr);
+    else lm_select_kernel<false><<<g, SW_WARPS * 32, ssm, st>>>(sr);
+    return cudaGetLastError();
+  };
+  auto refine_range = [&](int64_t q0, int64_t q1, cudaStream_t st) -> rairs_status {
+    SearchArgs ra = sa;
+    ra.queries = sa.queries + q0 * idx->d;
+    ra.nq = q1 - q0;
+    ra.cand_keys = sa.cand_keys + q0 * bigK;
+    ra.out_ids = sa.out_ids + q0 * sa.k;
+    ra.out_dists = sa.out_dists + q0 * sa.k;
+    return launch_refine(idx, ra, st);
+  };
+  const bool overlap = sa.fused_refine && nq >= 2 * LM_OVERLAP_MIN_Q && idx->aux[0];
+  if (!overlap) {
+    LM_TRY(select_range(0, nq, s));
+    if (sa.ev_selected) LM_TRY(cudaEventRecord(sa.ev_selected, s));
+    if (sa.fused_refine) {
+      const rairs_status rs = refine_range(0, nq, s);
+      if (rs != RAIRS_OK) { cleanup(); return rs; }
+    }
   } else {
-    LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    lm_select_kernel<false><<<sgrid, SW_WARPS * 32, ssm, s>>>(sl);
+    // 4. + refine: two query halves on the auxiliary streams, so one half's
+    // selection overlaps the other's refine gather (both latency-bound)
+    std::lock_guard<std::mutex> lock(*idx->aux_mu);
+    cudaEvent_t* ev = const_cast<cudaEvent_t*>(idx->aux_ev);
+    const int64_t half = nq / 2;
+    const int64_t qb[3] = {0, half, nq};
+    LM_TRY(cudaEventRecord(ev[0], s));  // scores ready
+    for (int h = 0; h < 2; ++h) {
+      LM_TRY(cudaStreamWaitEvent(idx->aux[h], ev[0], 0));
+      LM_TRY(select_range(qb[h], qb[h + 1], idx->aux[h]));
+      LM_TRY(cudaEventRecord(ev[1 + h], idx->aux[h]));  // half h selected
+    }
+    for (int h = 0; h < 2; ++h) {
+      const rairs_status rs = refine_range(qb[h], qb[h + 1], idx->aux[h]);
+      if (rs != RAIRS_OK) { cleanup(); return rs; }
+      LM_TRY(cudaEventRecord(ev[3 + h], idx->aux[h]));  // half h refined
+    }
+    LM_TRY(cudaStreamWaitEvent(s, ev[1], 0));
+    LM_TRY(cudaStreamWaitEvent(s, ev[2], 0));
+    if (sa.ev_selected) LM_TRY(cudaEventRecord(sa.ev_selected, s));
+    LM_TRY(cudaStreamWaitEvent(s, ev[3], 0));
+    LM_TRY(cudaStreamWaitEvent(s, ev[4], 0));
   }
-  LM_TRY(cudaGetLastError());
   cleanup();
   return RAIRS_OK;
 #undef LM_TRY
@@ -1242,6 +1286,9 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
       idx->list_base, idx->nlist, idx->shard_id, idx->nshards, idx->list_ids);
   RAIRS_CHECK_LAUNCH();
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto& st : idx->aux) RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (auto& e : idx->aux_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  idx->aux_mu = new std::mutex();
   idx->device_bytes += (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4 +
                        (size_t)(idx->nlist + 1) * 8 + (size_t)base[idx->nlist] * 4;
   return RAIRS_OK;
