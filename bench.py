@@ -108,6 +108,17 @@ def recall_at_k(ids, gt_ids, gt_d64, dists, k):
     return float((hit | tie).float().sum().item()) / (ids.shape[0] * k)
 
 
+def spec_overrides(args):
+    """--k / --refine-factor (the paper's top-100 workload uses k 100 with
+    K_FACTOR 4)."""
+    ov = {}
+    if args.k:
+        ov["k"] = args.k
+    if args.refine_factor:
+        ov["refine_factor"] = args.refine_factor
+    return ov
+
+
 def build_workload(args, rank, world, dev):
     """Synthetic inputs + index. Host-drawn configs (c1-c3, c2pl) come from
     synth.make_dataset; the large BJ configs (c4: 10M x 96, c5: 100M x 128) are
@@ -116,7 +127,7 @@ def build_workload(args, rank, world, dev):
     import torch
     import paper_2601_07183_b200 as rb
     from synth import GPU_KINDS, get_config, make_dataset
-    spec = get_config(args.config)
+    spec = get_config(args.config, **spec_overrides(args))
     t0 = time.time()
     if spec.kind in GPU_KINDS:
         from synth.gpu_generators import make_dataset_torch
@@ -314,9 +325,17 @@ def run_ours(args):
     # ---------------- AIR + SEIL vs single assignment (the paper's comparison) ----
     vs_single = None
     if world == 1 and args.compare_single and X is not None:
-        vs_single = compare_single(args, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream)
+        steps = max(3, args.steps // 2)
+        vs_single = {name: compare_strategy(kw, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush,
+                                            stream, steps)
+                     for name, kw in STRATEGIES.items()}
         vs_single["air"] = {"nprobe": chosen, "recall": round(recall, 4),
-                            "qps": round(qps, 1), "dco_per_query": round(dco_total / nq, 1)}
+                            "qps": round(qps, 1), "dco_per_query": round(dco_total / nq, 1),
+                            "double_assigned_frac": round(idx.info()["n_double"] / max(1, spec.n), 4)}
+        for name in STRATEGIES:
+            if name != "single":
+                vs_single[f"dco_ratio_{name}_over_single"] = round(
+                    vs_single[name]["dco_per_query"] / max(1.0, vs_single["single"]["dco_per_query"]), 3)
         vs_single["dco_ratio_air_over_single"] = round(
             vs_single["air"]["dco_per_query"] / max(1.0, vs_single["single"]["dco_per_query"]), 3)
 
@@ -327,7 +346,7 @@ def run_ours(args):
     if rank == 0:
         info = idx.info()
         line = {
-            "metric": f"QPS at recall10@10>=0.95 ({spec.name}: {spec.n:,} x {spec.d}, nlist {spec.nlist}, "
+            "metric": f"QPS at recall{k}@{k}>=0.95 ({spec.name}: {spec.n:,} x {spec.d}, nlist {spec.nlist}, "
                       f"PQ {spec.M}x4b, AIR+SEIL, refine x{rf})",
             "value": round(qps, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
@@ -338,7 +357,7 @@ def run_ours(args):
                        "nprobe": chosen, "assignment": args.assignment + "+SEIL(cell-major)",
                        "parallelism": f"index sharded id mod {world}" if world > 1 else "1 GPU",
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
-            "recall10@10": round(recall, 4), "recall_sweep": sweep,
+            "recall%d@%d" % (k, k): round(recall, 4), "recall_sweep": sweep,
             "dco_per_query": round(dco_total / nq, 1),
             "dco_per_s": round(dco_total * args.steps / (t_ms / 1e3), 1),
             "stage_ms_per_step": {kk: round(v / args.steps, 4) for kk, v in prof["ms"].items()},
@@ -369,17 +388,29 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def compare_single(args, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream):
-    """Single-assignment index from the SAME trained centroids/codebook: the
-    smallest swept nprobe reaching recall10@10 >= 0.95, its QPS (same timing
-    protocol, fewer steps) and DCO per query."""
+# redundant-assignment strategies compared on the same trained state (SURVEY
+# §8(f) NEXT-2; the paper's Fig. 7b/c and ablation):
+# name -> Index.build keywords
+STRATEGIES = {
+    "single": {"assignment": "single"},                               # IVFPQfs
+    "naivera": {"assignment": "AIR", "lambda_": 0.0, "strict": True},
+    "soarl2": {"assignment": "SOAR", "lambda_": 1.0, "strict": True},
+    "srair": {"assignment": "AIR", "lambda_": 0.5, "strict": True},
+}
+
+
+def compare_strategy(kw, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream, steps):
+    """An index of another assignment strategy from the SAME trained
+    centroids/codebook: the smallest swept nprobe reaching recall >= 0.95, its
+    QPS (same timing protocol, fewer steps) and DCO per query."""
     import torch
     import paper_2601_07183_b200 as rb
     k, rf = spec.k, spec.refine_factor
     cent, cb = idx.export_trained()
     Xd = torch.from_numpy(X).to(Qd.device)
-    ids_ = rb.Index.build(Xd, spec.nlist, spec.M, assignment="single", centroids=cent, codebook=cb)
+    ids_ = rb.Index.build(Xd, spec.nlist, spec.M, centroids=cent, codebook=cb, **kw)
     del Xd
+    n_double = ids_.info()["n_double"]
     chosen, rec = None, None
     for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
         ids, dists = ids_.search(Qd, k, npb, rf)
@@ -390,7 +421,6 @@ def compare_single(args, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream)
     _, _, dco = ids_.search(Qd, k, chosen, rf, return_dco=True)
     for _ in range(3):
         ids_.search(Qd, k, chosen, rf)
-    steps = max(3, args.steps // 2)
     t = 0.0
     for _ in range(steps):
         flush.zero_()
@@ -402,11 +432,10 @@ def compare_single(args, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream)
         e1.synchronize()
         t += e0.elapsed_time(e1)
     nq = Qd.shape[0]
-    out = {"single": {"nprobe": chosen, "recall": round(rec, 4),
-                      "qps": round(nq * steps / (t / 1e3), 1),
-                      "dco_per_query": round(float(dco.sum().item()) / nq, 1)}}
     ids_.free()
-    return out
+    return {"nprobe": chosen, "recall": round(rec, 4), "qps": round(nq * steps / (t / 1e3), 1),
+            "dco_per_query": round(float(dco.sum().item()) / nq, 1),
+            "double_assigned_frac": round(n_double / max(1, X.shape[0]), 4)}
 
 
 def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
@@ -450,7 +479,7 @@ def run_reference(args):
         return
     import oracle
     from synth import get_config, make_dataset
-    spec = get_config(args.config)
+    spec = get_config(args.config, **spec_overrides(args))
     X, Q = make_dataset(spec)
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
@@ -497,9 +526,13 @@ def main():
     ap.add_argument("--config", default="c2pl")
     ap.add_argument("--assignment", default="AIR", choices=["AIR", "single"])
     ap.add_argument("--nprobe", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None,
+                    help="override the config's k (top-100 workload: --k 100 --refine-factor 4)")
+    ap.add_argument("--refine-factor", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--compare-single", type=int, default=1,
-                    help="also measure a single-assignment index on the same trained state")
+                    help="also measure single / NaiveRA / SOARL2 / SRAIR indexes on the same "
+                         "trained state (air_vs_single)")
     ap.add_argument("--latency-queries", type=int, default=200,
                     help="single-query searches timed for p50/p99 latency (0 = skip)")
     ap.add_argument("--gt-queries", type=int, default=0,

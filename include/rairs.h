@@ -51,7 +51,12 @@ typedef enum {
 
 typedef enum {
   RAIRS_ASSIGN_SINGLE = 0, /* each vector in its nearest list only (IVFPQfs) */
-  RAIRS_ASSIGN_AIR = 1     /* RAIR second list by the AIR metric (Alg. 3) */
+  RAIRS_ASSIGN_AIR = 1,    /* RAIR second list by the AIR metric (Alg. 3) */
+  RAIRS_ASSIGN_SOAR = 2    /* SOARL2 comparison strategy:
+                              Alg. 3 with loss ||r'||^2 + lambda*(r.r'/||r||)^2
+                              (Table 2); the term is 0 when ||r|| = 0.
+                              Use strict = 1 for the paper's always-two-lists
+                              SOARL2 (and lambda = 0, strict = 1 for NaiveRA). */
 } rairs_assign;
 
 typedef struct {
@@ -59,7 +64,7 @@ typedef struct {
   int32_t M;            /* PQ subquantizers; d % M == 0; d/M <= 8 */
   int32_t nbits;        /* must be 4 (16 sub-centroids) */
   int32_t assignment;   /* rairs_assign */
-  float lambda;         /* AIR lambda (0.5) */
+  float lambda;         /* AIR / SOAR lambda (AIR: P:1083-1084, 0.5) */
   int32_t n_cands;      /* N_CANDS (10); clamped to nlist */
   int32_t strict;       /* 0 = RAIR (non-strict), 1 = SRAIR */
   int32_t kmeans_iters; /* Lloyd iterations for training (default 25) */

@@ -91,12 +91,13 @@ def probe(queries, centroids, nprobe: int) -> np.ndarray:
 
 def assign(x, centroids, mode: str = "air", lam: float = 0.5, n_cands: int = 10,
            strict: bool = False):
-    """O4: (l1, l2) sorted pair per vector (Alg. 3)."""
+    """O4: (l1, l2) sorted pair per vector (Alg. 3); mode "soar" = SOARL2
+    (Table 2's SOAR loss in Alg. 3's place)."""
     xx, c = _f32(x), _f32(centroids)
     n = xx.shape[0]
     l1 = np.empty(n, np.int32)
     l2 = np.empty(n, np.int32)
-    m = {"single": 0, "air": 1}[mode]
+    m = {"single": 0, "air": 1, "soar": 2}[mode]
     _check(lib().oracle_assign(_ptr(xx), n, xx.shape[1], _ptr(c), c.shape[0], m, float(lam),
                                int(n_cands), int(bool(strict)), _ptr(l1), _ptr(l2)), "assign")
     return l1, l2

@@ -126,7 +126,12 @@ int oracle_probe(const float* q, int64_t nq, int d, const float* cent, int nlist
  *   listID1 = cand[0]; start = strict ? 1 : 0          (lines 9-10)
  *   listID2 = cand[first argmin loss[start..N_C-1]]    (line 11; ties -> nearer)
  *   return sorted pair                                  (line 12)
- * mode 0 = single assignment (l1 = l2 = nearest list). */
+ * mode 0 = single assignment (l1 = l2 = nearest list).
+ * mode 2 = SOARL2: the same steps with line 8's loss
+ *   replaced by Table 2's SOAR formula:
+ *   loss[i] = L2sqr(residual) + lambda * (InnerProd(residual0, residual) / ||residual0||)^2,
+ *   ||residual0|| = sqrt of the ordered fp64 sum of squares; the projection term
+ *   is 0 when ||residual0|| = 0 (then residual0 . residual = 0). */
 static void assign_one(const float* v, int d, const float* cent, int nlist, int mode,
                        double lambda, int n_cands, int strict, dist_id* scratch,
                        double* r0, double* r, int32_t* o1, int32_t* o2) {
@@ -139,6 +144,8 @@ static void assign_one(const float* v, int d, const float* cent, int nlist, int 
     if (mode == 0) { *o1 = c0; *o2 = c0; return; }
     const float* cen0 = cent + (int64_t)c0 * d;
     for (int t = 0; t < d; ++t) r0[t] = (double)cen0[t] - (double)v[t];
+    double rr = 0.0;
+    for (int t = 0; t < d; ++t) { double sq = r0[t] * r0[t]; rr = rr + sq; }
     int start = strict ? 1 : 0;
     int best = -1;
     double best_loss = 0.0;
@@ -148,8 +155,14 @@ static void assign_one(const float* v, int d, const float* cent, int nlist, int 
         double l2sqr = 0.0, ip = 0.0;
         for (int t = 0; t < d; ++t) { double sq = r[t] * r[t]; l2sqr = l2sqr + sq; }
         for (int t = 0; t < d; ++t) { double pr = r0[t] * r[t]; ip = ip + pr; }
-        double term = lambda * ip;
-        double loss = l2sqr + term;
+        double loss;
+        if (mode == 2) {
+            double proj = rr == 0.0 ? 0.0 : ip / sqrt(rr);
+            loss = rr == 0.0 ? l2sqr : l2sqr + lambda * (proj * proj);
+        } else {
+            double term = lambda * ip;
+            loss = l2sqr + term;
+        }
         if (best < 0 || loss < best_loss) { best = i; best_loss = loss; }
     }
     int c2 = (int)scratch[best].id;
@@ -160,9 +173,9 @@ static void assign_one(const float* v, int d, const float* cent, int nlist, int 
 int oracle_assign(const float* x, int64_t n, int d, const float* cent, int nlist,
                   int mode, double lambda, int n_cands, int strict,
                   int32_t* l1, int32_t* l2) {
-    if (nlist < 1 || d < 1 || (mode != 0 && mode != 1)) return OR_EINVAL;
+    if (nlist < 1 || d < 1 || mode < 0 || mode > 2) return OR_EINVAL;
     if (n_cands > nlist) n_cands = nlist;                 /* N_C = min(10, nlist) */
-    if (n_cands < 1 || (strict && n_cands < 2 && mode == 1)) return OR_EINVAL;
+    if (n_cands < 1 || (strict && n_cands < 2 && mode != 0)) return OR_EINVAL;
     int err = OR_OK;
 #pragma omp parallel
     {

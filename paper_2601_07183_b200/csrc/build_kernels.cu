@@ -191,14 +191,15 @@ __global__ void __launch_bounds__(PT) probe_exact_kernel(ProbeArgs a, ProbeSmem 
           const float* c0 = a.C + (int64_t)ids[0] * d;
           const float* ci = a.C + (int64_t)ids[lane] * d;
           const double* x = xs + r * d;
-          double ss = 0.0, ip = 0.0;
+          double ss = 0.0, ip = 0.0, rr = 0.0;
           for (int t = 0; t < d; ++t) {
             double r0t = __dsub_rn((double)c0[t], x[t]);
             double rit = __dsub_rn((double)ci[t], x[t]);
             ss = __dadd_rn(ss, __dmul_rn(rit, rit));
             ip = __dadd_rn(ip, __dmul_rn(r0t, rit));
+            rr = __dadd_rn(rr, __dmul_rn(r0t, r0t));
           }
-          loss = __dadd_rn(ss, __dmul_rn(a.lambda, ip));
+          loss = second_list_loss(a.mode, a.lambda, ss, ip, rr);
         }
         // first argmin over lanes (loss, lane)
         int best = ok ? lane : 0x7fffffff;
@@ -358,15 +359,16 @@ __global__ void __launch_bounds__(PX_T) probe_merge_kernel(ProbeArgs a,
         const float* c0 = a.C + (int64_t)ids[0] * a.d;
         const float* cj = a.C + (int64_t)ids[lane] * a.d;
         const float* xr = a.X + row * a.d;
-        double ss = 0.0, ip = 0.0;
+        double ss = 0.0, ip = 0.0, rr = 0.0;
         for (int t = 0; t < a.d; ++t) {
           const double x = (double)xr[t];
           const double r0t = __dsub_rn((double)c0[t], x);
           const double rjt = __dsub_rn((double)cj[t], x);
           ss = __dadd_rn(ss, __dmul_rn(rjt, rjt));
           ip = __dadd_rn(ip, __dmul_rn(r0t, rjt));
+          rr = __dadd_rn(rr, __dmul_rn(r0t, r0t));
         }
-        loss = __dadd_rn(ss, __dmul_rn(a.lambda, ip));
+        loss = second_list_loss(a.mode, a.lambda, ss, ip, rr);
       }
       int best = ok ? lane : 0x7fffffff;
 #pragma unroll
@@ -427,7 +429,7 @@ rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s) {
     set_error("probe_exact: bad L");
     return RAIRS_E_INVALID;
   }
-  if (a.mode == 1 && a.L > 32) {
+  if ((a.mode == 1 || a.mode == 3) && a.L > 32) {
     set_error("probe_exact: n_cands must be <= 32");
     return RAIRS_E_UNSUPPORTED;
   }

@@ -1,3 +1,4 @@
+#include <cmath>
 // capi.cu -- extern "C" entry points of librairs.so (see include/rairs.h).
 #include <cstdio>
 #include <cstring>
@@ -70,8 +71,9 @@ static rairs_status validate_params(const rairs_build_params* p, int64_t n, int3
     set_error("d/M > 8 is not supported");
     return RAIRS_E_UNSUPPORTED;
   }
-  if (p->assignment != RAIRS_ASSIGN_SINGLE && p->assignment != RAIRS_ASSIGN_AIR)
-    return invalid("assignment must be RAIRS_ASSIGN_SINGLE or RAIRS_ASSIGN_AIR");
+  if (p->assignment != RAIRS_ASSIGN_SINGLE && p->assignment != RAIRS_ASSIGN_AIR &&
+      p->assignment != RAIRS_ASSIGN_SOAR)
+    return invalid("assignment must be RAIRS_ASSIGN_SINGLE, RAIRS_ASSIGN_AIR or RAIRS_ASSIGN_SOAR");
   if (p->nshards < 1 || p->shard_id < 0 || p->shard_id >= p->nshards)
     return invalid("need 0 <= shard_id < nshards");
   if (n >= (1ll << 30)) {
@@ -82,7 +84,8 @@ static rairs_status validate_params(const rairs_build_params* p, int64_t n, int3
     set_error("global ids must fit in 32 bits");
     return RAIRS_E_UNSUPPORTED;
   }
-  if (p->assignment == RAIRS_ASSIGN_AIR) {
+  if (p->assignment != RAIRS_ASSIGN_SINGLE) {
+    if (!(p->lambda >= 0.0f) || !std::isfinite(p->lambda)) return invalid("lambda must be finite and >= 0");
     int nc = std::min(p->n_cands, p->nlist);
     if (nc < 1) return invalid("n_cands must be >= 1");
     if (nc > 32) {
@@ -342,8 +345,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   pa.d = d;
   pa.C = idx->centroids;
   pa.nl = p->nlist;
-  if (p->assignment == RAIRS_ASSIGN_AIR) {
-    pa.mode = 1;
+  if (p->assignment != RAIRS_ASSIGN_SINGLE) {
+    pa.mode = p->assignment == RAIRS_ASSIGN_SOAR ? 3 : 1;
     pa.L = std::min(p->n_cands, p->nlist);
     pa.lambda = (double)p->lambda;
     pa.strict = p->strict;

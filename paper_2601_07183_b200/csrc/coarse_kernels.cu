@@ -492,15 +492,16 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
       if (ok) {
         const float* c0 = a.C + (size_t)ci[0] * a.d;
         const float* cj = a.C + (size_t)ci[lane] * a.d;
-        double ss = 0.0, ip = 0.0;
+        double ss = 0.0, ip = 0.0, rr = 0.0;
         for (int t = 0; t < a.d; ++t) {
           const double x = (double)xr[t];
           const double r0t = __dsub_rn((double)c0[t], x);
           const double rjt = __dsub_rn((double)cj[t], x);
           ss = __dadd_rn(ss, __dmul_rn(rjt, rjt));
           ip = __dadd_rn(ip, __dmul_rn(r0t, rjt));
+          rr = __dadd_rn(rr, __dmul_rn(r0t, r0t));
         }
-        loss = __dadd_rn(ss, __dmul_rn(a.lambda, ip));
+        loss = second_list_loss(a.mode, a.lambda, ss, ip, rr);
       }
       int best = ok ? lane : 0x7fffffff;
 #pragma unroll

@@ -73,6 +73,22 @@ __device__ __forceinline__ double dsq_diff(float a, float b) {
 }
 
 // u64 bits of a non-negative double: integer order == numeric order.
+// Second-list loss of a redundant assignment (Table 2), fp64,
+// every operation rounded to nearest (O4):
+//   mode 1 AIR   : ||r'||^2 + lambda * r.r'                (Alg. 3 line 8)
+//   mode 3 SOARL2: ||r'||^2 + lambda * (r.r' / ||r||)^2
+// ss = ||r'||^2, ip = r.r', rr = ||r||^2 (ordered sums); SOAR's projection term
+// is 0 when ||r|| = 0 (x on the first centroid: r = 0, so r.r' = 0).
+__device__ __forceinline__ double second_list_loss(int mode, double lambda, double ss, double ip,
+                                                   double rr) {
+  if (mode == 3) {
+    if (rr == 0.0) return ss;
+    const double pr = __ddiv_rn(ip, __dsqrt_rn(rr));
+    return __dadd_rn(ss, __dmul_rn(lambda, __dmul_rn(pr, pr)));
+  }
+  return __dadd_rn(ss, __dmul_rn(lambda, ip));
+}
+
 __device__ __forceinline__ uint64_t dbits(double v) {
   return (uint64_t)__double_as_longlong(v);
 }

@@ -38,9 +38,10 @@ def make_params(nlist: int, M: int, nbits: int = 4, assignment: str = "AIR",
     lib().rairs_default_params(ctypes.byref(p), int(nlist), int(M))
     p.nbits = int(nbits)
     a = assignment.upper()
-    if a not in ("AIR", "SINGLE"):
-        raise ValueError("assignment must be 'AIR' or 'single'")
-    p.assignment = 1 if a == "AIR" else 0
+    modes = {"SINGLE": 0, "AIR": 1, "SOAR": 2, "SOARL2": 2}
+    if a not in modes:
+        raise ValueError("assignment must be 'AIR', 'single' or 'SOAR'")
+    p.assignment = modes[a]
     p.lambda_ = float(lambda_)
     p.n_cands = int(n_cands)
     p.strict = int(bool(strict))

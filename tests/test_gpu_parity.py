@@ -37,7 +37,7 @@ class Case:
     """Oracle-trained index of one config (CPU) + the GPU index built from it."""
 
     def __init__(self, oracle, name, n=None, nq=None, train_rows=20000, iters=6,
-                 assignment="air", strict=False):
+                 assignment="air", strict=False, lam=0.5):
         spec = get_config(name)
         self.spec = spec
         X, Q = make_dataset(spec, n=n, nq=nq)
@@ -45,14 +45,15 @@ class Case:
         rows = X[np.random.default_rng(5).permutation(X.shape[0])[:min(train_rows, X.shape[0])]]
         self.cent = oracle.kmeans(rows, spec.nlist, iters=iters, seed=11)
         self.cb = oracle.pq_train(rows, spec.M, iters=iters, seed=12)
-        self.l1, self.l2 = oracle.assign(X, self.cent, assignment, strict=strict)
+        self.l1, self.l2 = oracle.assign(X, self.cent, assignment, lam=lam, strict=strict)
         self.codes = oracle.encode(X, self.cb)
-        self.assignment, self.strict = assignment, strict
+        self.assignment, self.strict, self.lam = assignment, strict, lam
 
     def gpu_index(self, shard_id=0, nshards=1):
         rows = np.arange(shard_id, self.X.shape[0], nshards)
         return rb.Index.build(_t(self.X[rows]), self.spec.nlist, self.spec.M,
                               assignment=self.assignment.upper(), strict=self.strict,
+                              lambda_=self.lam,
                               centroids=_t(self.cent), codebook=_t(self.cb),
                               shard_id=shard_id, nshards=nshards)
 
@@ -141,6 +142,7 @@ SEARCH_CASES = [
     ("c0", 5, 4, 4), ("c0s", 5, 4, 4), ("c0s", 5, 16, 2), ("c0s", 1, 1, 1),
     ("c1", 10, 8, 4), ("c1", 10, 1, 4), ("c1", 10, 64, 4),
     ("c1s", 10, 8, 4), ("c1s", 10, 16, 10), ("c1s", 1, 3, 100), ("c1s", 100, 8, 1),
+    ("c1s", 100, 8, 4),   # top-100 workload: K_FACTOR 4, bigK 400
 ]
 
 
@@ -165,6 +167,20 @@ def test_search_parity_many_queries(oracle_mod, scan):
     assert_search_equal(gpu_search(idx, c.Q, 10, 16, 10, scan), o)
 
 
+@pytest.mark.parametrize("k,rf", [(10, 10), (100, 4)])
+def test_search_parity_overlapped_halves(oracle_mod, k, rf):
+    # >= 2 * LM_OVERLAP_MIN_Q queries: the list-major path selects and refines
+    # two query halves on the index's auxiliary streams (odd count: unequal halves)
+    c = case(oracle_mod, "c1s", nq=4503)
+    idx = c.gpu_index()
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, k, 8, rf)
+    assert_search_equal(gpu_search(idx, c.Q, k, 8, rf, "listmajor"), o)
+    # the plain search entry point (fused refine, no debug outputs) agrees too
+    idx.set_scan_mode("listmajor")
+    ids, dists = idx.search(_t(c.Q), k, 8, rf)
+    assert np.array_equal(ids.cpu().numpy(), o["ids"])
+
+
 def test_search_modes_single_and_strict(oracle_mod):
     for kw in ({"assignment": "single"}, {"assignment": "air", "strict": True}):
         c = case(oracle_mod, "c1s", **kw)
@@ -173,6 +189,23 @@ def test_search_modes_single_and_strict(oracle_mod):
         assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2)
         o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, 10, 8, 4)
         assert_search_equal(gpu_search(idx, c.Q, 10, 8, 4), o)
+
+
+@pytest.mark.parametrize("name,n", [("c1s", None), ("c2pl", 60000)])
+def test_soarl2_and_naivera_assignment(oracle_mod, name, n):
+    # NEXT-2 comparison strategies on the same kernels: SOARL2 (Table 2's SOAR loss,
+    # P:1100, strict) and NaiveRA (AIR with lambda 0, strict).
+    # c2pl (nlist 1024) builds through the tensor-core filter + certify path.
+    for kw in ({"assignment": "soar", "strict": True, "lam": 1.0},
+               {"assignment": "air", "strict": True, "lam": 0.0}):
+        c = case(oracle_mod, name, n=n, **kw)
+        idx = c.gpu_index()
+        l1, l2, _ = [t.cpu().numpy() for t in idx.export_assignment()]
+        assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2), kw
+        assert (l1 != l2).all()                       # strict: always two lists
+        o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q[:500], 10, 8, 4)
+        assert_search_equal(gpu_search(idx, c.Q[:500], 10, 8, 4), o)
+        idx.free()
 
 
 def test_exhaustive_reduction_equals_exact_knn(oracle_mod):

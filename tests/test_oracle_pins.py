@@ -155,6 +155,51 @@ def test_assign_exhaustive_argmin_and_rair_condition(oracle_mod):
             assert cond
 
 
+def test_assign_soar_closed_form(oracle_mod):
+    # SOARL2 (Table 2): loss = ||r'||^2 + lambda (r.r'/||r||)^2 prefers r'
+    # orthogonal to r; AIR prefers r' opposite to r.  x = 0, c0 = e1:
+    #   c1 = -1.2 e1 (opposite):   SOAR 1.44 + 1*1.44 = 2.88   AIR 1.44 - 0.5*1.2 = 0.84
+    #   c2 =  1.3 e2 (orthogonal): SOAR 1.69 + 0      = 1.69   AIR 1.69
+    #   c3 = (5, 5, 0, 0) far
+    C = np.zeros((4, 4), np.float32)
+    C[0, 0], C[1, 0], C[2, 1], C[3, :2] = 1.0, -1.2, 1.3, 5.0
+    x = np.zeros((1, 4), np.float32)
+    assert tuple(np.concatenate(oracle_mod.assign(x, C, "soar", 1.0, 10, strict=True))) == (0, 2)
+    assert tuple(np.concatenate(oracle_mod.assign(x, C, "air", 0.5, 10, strict=True))) == (0, 1)
+    # lambda = 0: SOAR is NaiveRA (2nd nearest)
+    assert tuple(np.concatenate(oracle_mod.assign(x, C, "soar", 0.0, 10, strict=True))) == (0, 1)
+    # non-strict: c0 itself scores (1 + lambda)||r||^2 = 2.0 > 1.69 -> still c2;
+    # moving c2 out to 1.5 e2 (2.25 > 2.0) makes c0 win (single assignment)
+    assert tuple(np.concatenate(oracle_mod.assign(x, C, "soar", 1.0, 10))) == (0, 2)
+    C2 = C.copy()
+    C2[2, 1] = 1.5                        # orthogonal candidate 2.25 > 2.0 of c0
+    assert tuple(np.concatenate(oracle_mod.assign(x, C2, "soar", 1.0, 10))) == (0, 0)
+    # x exactly on a centroid: ||r|| = 0, projection term 0 -> strict gives the
+    # nearest other list, non-strict stays single
+    assert tuple(np.concatenate(oracle_mod.assign(C[2:3], C, "soar", 1.0, 10, strict=True))) == (0, 2)
+    assert tuple(np.concatenate(oracle_mod.assign(C[2:3], C, "soar", 1.0, 10))) == (2, 2)
+
+
+def test_assign_soar_exhaustive_projection_argmin(oracle_mod):
+    # N_C = nlist: the SOAR second list minimises ||r'||^2 + lambda ||proj_r r'||^2
+    # over every other list (projection written as a vector, not as Table 2's ratio)
+    X, Q, C = rand_problem(16, n=400, nlist=9)
+    lam = 1.0
+    l1, l2 = oracle_mod.assign(X, C, "soar", lam, n_cands=9, strict=True)
+    D = ordered_d64(X[:, None, :], C[None, :, :])
+    for i in range(X.shape[0]):
+        order = np.lexsort((np.arange(C.shape[0]), D[i]))
+        c0 = int(order[0])
+        r = C[c0].astype(np.float64) - X[i].astype(np.float64)
+        R = C.astype(np.float64) - X[i].astype(np.float64)
+        proj = (R @ r / (r @ r))[:, None] * r[None, :]
+        loss = (R * R).sum(1) + lam * (proj * proj).sum(1)
+        loss[c0] = np.inf
+        other = int(l2[i]) if int(l1[i]) == c0 else int(l1[i])
+        assert other != c0 and c0 in (l1[i], l2[i])
+        assert loss[other] <= loss.min() * (1 + 1e-12)
+
+
 def test_assign_single_mode(oracle_mod):
     X, Q, C = rand_problem(7, n=200)
     l1, l2 = oracle_mod.assign(X, C, "single")
