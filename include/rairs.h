@@ -87,6 +87,7 @@ typedef struct {
   int32_t max_refs_per_list;
   int32_t shard_id, nshards;
   int64_t device_bytes; /* index memory on the device */
+  int64_t n_live;       /* rows not deleted (n counts every row ever inserted) */
 } rairs_index_info;
 
 /* ---- training (B1/B3; not part of the bit-exact contract) ----------------
@@ -115,6 +116,33 @@ rairs_status rairs_build_index(const float* base, int64_t n, int32_t d,
 
 rairs_status rairs_index_free(rairs_index_t idx);
 rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out);
+
+/* ---- updates ------------------------------------------
+ * Insert a batch (batched SeilInsert, Alg. 4): x is a dev
+ * [n_add x d] fp32 batch; its rows get local rows n .. n+n_add-1, i.e. global
+ * ids (n+i)*nshards + shard_id (first_id, host, optional, receives the first).
+ * Each row is assigned with the index's build parameters and trained state
+ * (Alg. 3, O4, bit-exact to a fresh build), and the cell-major layout, codes
+ * and list tables are rebuilt on the device (the paper appends blocks and
+ * reference entries per batch; the result -- U(q), scores, ids,
+ * DCO -- is the same as for an index built over all live rows at once).
+ * x is copied; the caller keeps ownership. Row storage grows by >= 1/8.
+ * Synchronises the device first: no search may run on this index concurrently.
+ * Errors: n_add < 0, x not a device pointer (INVALID); > 2^30 rows per shard or
+ * global ids >= 2^32 (UNSUPPORTED); OOM (the index is unchanged). */
+rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, int64_t* first_id,
+                       void* stream);
+
+/* Delete by global id: ids is a dev [n_ids] int64 array; ids this
+ * shard does not hold (id % nshards != shard_id, or beyond its rows) and ids
+ * already deleted are ignored. *n_removed (host, optional) = rows deleted now.
+ * Deleted rows leave the layout (no tombstone is ever scored: DCO, U(q) and
+ * results equal those of an index built over the remaining rows with their
+ * original ids); their raw rows stay in the refine store. Synchronises the
+ * device first: no search may run on this index concurrently.
+ * Errors: n_ids < 0, ids not a device pointer (INVALID). */
+rairs_status rairs_remove_ids(rairs_index_t idx, const int64_t* ids, int64_t n_ids,
+                              int64_t* n_removed, void* stream);
 
 /* ---- search (Alg. 2 RairsSearch, batched) --------------------------------
  * queries: dev [nq x d] fp32.  bigK = k*refine_factor.

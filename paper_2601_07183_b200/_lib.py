@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = [
     "rairs_export_assignment", "rairs_export_layout", "rairs_profile_enable",
     "rairs_profile_read", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
     "rairs_certify_fallbacks", "rairs_set_scan_mode", "rairs_profile_kernels",
-    "rairs_search_plan",
+    "rairs_search_plan", "rairs_add", "rairs_remove_ids",
 ]
 
 
@@ -47,7 +47,7 @@ class IndexInfo(ctypes.Structure):
     _fields_ = [("n", _I64), ("d", _I32), ("nlist", _I32), ("M", _I32), ("M_pad", _I32),
                 ("n_slots", _I64), ("n_cells", _I64), ("n_refs", _I64), ("n_double", _I64),
                 ("max_refs_per_list", _I32), ("shard_id", _I32), ("nshards", _I32),
-                ("device_bytes", _I64)]
+                ("device_bytes", _I64), ("n_live", _I64)]
 
 
 class RairsError(RuntimeError):
@@ -104,6 +104,8 @@ def lib() -> ctypes.CDLL:
         "rairs_set_scan_mode": [_P, _I32],
         "rairs_profile_kernels": [_P, _P, _I32],
         "rairs_search_plan": [_P, _I64, _I32, _I32, _I32, _P, _P],
+        "rairs_add": [_P, _P, _I64, _P, _P],
+        "rairs_remove_ids": [_P, _P, _I64, _P, _P],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

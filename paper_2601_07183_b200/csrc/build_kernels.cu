@@ -787,11 +787,15 @@ rairs_status train_pq(const float* X, int64_t n, int d, int M, int iters, uint64
 // [unit u = 16 subquantizers][lane][8 B], nibble i of unit u = subquantizer
 // 16u+i (bits 4i..4i+3).
 // ===========================================================================
+// cell-major sort key (l1, l2, row); deleted rows sort last (key ~0)
 __global__ void make_keys_kernel(const int32_t* __restrict__ l1, const int32_t* __restrict__ l2,
-                                 int64_t n, uint64_t* __restrict__ keys) {
+                                 const uint32_t* __restrict__ live_bits, int64_t n,
+                                 uint64_t* __restrict__ keys) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x)
-    keys[r] = ((uint64_t)l1[r] << 47) | ((uint64_t)l2[r] << 30) | (uint64_t)r;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = live_bits == nullptr || ((live_bits[r >> 5] >> (r & 31)) & 1u);
+    keys[r] = live ? (((uint64_t)l1[r] << 47) | ((uint64_t)l2[r] << 30) | (uint64_t)r) : ~0ull;
+  }
 }
 
 __global__ void list_bounds_kernel(const uint64_t* __restrict__ sk, int64_t n, int shift,
@@ -884,6 +888,17 @@ __global__ void refs_finalize_kernel(const uint64_t* __restrict__ rk_sorted,
 
 rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   const int64_t n = idx->n;
+  const int64_t n_live = idx->n_live;  // live rows: the first n_live sorted keys
+  // a rebuild (after rairs_add / rairs_remove_ids) replaces the previous layout
+  cudaFree(idx->own_off); cudaFree(idx->own_cnt); cudaFree(idx->codes); cudaFree(idx->slot_rows);
+  cudaFree(idx->ref_ptr); cudaFree(idx->ref_owner); cudaFree(idx->ref_start); cudaFree(idx->ref_cnt);
+  idx->own_off = idx->own_cnt = nullptr;
+  idx->codes = nullptr;
+  idx->slot_rows = nullptr;
+  idx->ref_ptr = idx->ref_start = idx->ref_cnt = nullptr;
+  idx->ref_owner = nullptr;
+  idx->device_bytes -= idx->layout_bytes;
+  idx->layout_bytes = 0;
   const int nlist = idx->nlist;
   const int NU = idx->M_pad / 16;
   uint64_t *keys = nullptr, *skeys = nullptr, *rk = nullptr, *rv = nullptr, *rk_s = nullptr,
@@ -903,7 +918,7 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   LY_TRY(cudaMalloc(&seg_s, nlist * sizeof(uint32_t)));
   LY_TRY(cudaMalloc(&seg_e, nlist * sizeof(uint32_t)));
   LY_TRY(cudaMalloc(&counters, 4 * sizeof(unsigned long long)));
-  make_keys_kernel<<<grid_for(n), 256, 0, s>>>(idx->l1, idx->l2, n, keys);
+  make_keys_kernel<<<grid_for(n), 256, 0, s>>>(idx->l1, idx->l2, idx->live_bits, n, keys);
   LY_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, skeys, (int64_t)n, 0, 64, s));
   LY_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys, skeys, keys, skeys, (int64_t)n, 0, 64, s));
   tmp_bytes = std::max(tmp_bytes, tb2);
@@ -911,7 +926,7 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   LY_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, skeys, (int64_t)n, 0, 64, s));
   LY_TRY(cudaMemsetAsync(seg_s, 0, nlist * sizeof(uint32_t), s));
   LY_TRY(cudaMemsetAsync(seg_e, 0, nlist * sizeof(uint32_t), s));
-  list_bounds_kernel<<<grid_for(n), 256, 0, s>>>(skeys, n, 47, 0x1FFFFu, seg_s, seg_e);
+  list_bounds_kernel<<<grid_for(n_live), 256, 0, s>>>(skeys, n_live, 47, 0x1FFFFu, seg_s, seg_e);
   std::vector<uint32_t> hs(nlist), he(nlist), hoff(nlist), hcnt(nlist);
   LY_TRY(cudaMemcpyAsync(hs.data(), seg_s, nlist * 4, cudaMemcpyDeviceToHost, s));
   LY_TRY(cudaMemcpyAsync(he.data(), seg_e, nlist * 4, cudaMemcpyDeviceToHost, s));
@@ -933,13 +948,13 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   LY_TRY(cudaMalloc(&idx->own_cnt, nlist * 4));
   LY_TRY(cudaMalloc(&idx->codes, code_bytes));
   LY_TRY(cudaMalloc(&idx->slot_rows, (size_t)std::max<int64_t>(off, 32) * 4));
-  idx->device_bytes += nlist * 8 + code_bytes + (size_t)std::max<int64_t>(off, 32) * 4;
+  idx->layout_bytes += nlist * 8 + code_bytes + (size_t)std::max<int64_t>(off, 32) * 4;
   LY_TRY(cudaMemcpyAsync(idx->own_off, hoff.data(), nlist * 4, cudaMemcpyHostToDevice, s));
   LY_TRY(cudaMemcpyAsync(idx->own_cnt, hcnt.data(), nlist * 4, cudaMemcpyHostToDevice, s));
   LY_TRY(cudaMemsetAsync(idx->codes, 0, code_bytes, s));
   LY_TRY(cudaMemsetAsync(idx->slot_rows, 0xFF, (size_t)std::max<int64_t>(off, 32) * 4, s));
-  fill_slots_kernel<<<grid_for(n * NU), 256, 0, s>>>(
-      skeys, n, idx->own_off, seg_s, idx->X, idx->d, idx->M, idx->dsub, NU, idx->codebook,
+  fill_slots_kernel<<<grid_for(n_live * NU), 256, 0, s>>>(
+      skeys, n_live, idx->own_off, seg_s, idx->X, idx->d, idx->M, idx->dsub, NU, idx->codebook,
       idx->slot_rows, reinterpret_cast<uint64_t*>(idx->codes));
   LY_TRY(cudaGetLastError());
 
@@ -949,7 +964,7 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   LY_TRY(cudaMalloc(&rk_s, n * sizeof(uint64_t)));
   LY_TRY(cudaMalloc(&rv_s, n * sizeof(uint64_t)));
   LY_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
-  cells_kernel<<<grid_for(n), 256, 0, s>>>(skeys, n, idx->own_off, seg_s, counters, rk, rv);
+  cells_kernel<<<grid_for(n_live), 256, 0, s>>>(skeys, n_live, idx->own_off, seg_s, counters, rk, rv);
   LY_TRY(cudaGetLastError());
   unsigned long long hcount[4];
   LY_TRY(cudaMemcpyAsync(hcount, counters, sizeof(hcount), cudaMemcpyDeviceToHost, s));
@@ -963,7 +978,7 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   LY_TRY(cudaMalloc(&idx->ref_owner, std::max<int64_t>(nr, 1) * 4));
   LY_TRY(cudaMalloc(&idx->ref_start, std::max<int64_t>(nr, 1) * 4));
   LY_TRY(cudaMalloc(&idx->ref_cnt, std::max<int64_t>(nr, 1) * 4));
-  idx->device_bytes += (nlist + 1) * 4 + std::max<int64_t>(nr, 1) * 12;
+  idx->layout_bytes += (nlist + 1) * 4 + std::max<int64_t>(nr, 1) * 12;
   idx->max_refs = 0;
   if (nr > 0) {
     LY_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, rk, rk_s, rv, rv_s, (int64_t)nr, 0, 34, s));
@@ -985,6 +1000,7 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   }
   LY_TRY(cudaMemcpyAsync(idx->ref_ptr, hptr.data(), (nlist + 1) * 4, cudaMemcpyHostToDevice, s));
   LY_TRY(cudaStreamSynchronize(s));
+  idx->device_bytes += idx->layout_bytes;
   cleanup();
   return RAIRS_OK;
 #undef LY_TRY

@@ -31,6 +31,10 @@ namespace rairs {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
+static inline unsigned grid_for(int64_t n, int bs = 256) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, 148 * 16));
+}
+
 static rairs_status invalid(const std::string& msg) {
   set_error(msg);
   return RAIRS_E_INVALID;
@@ -104,6 +108,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
+  cudaFree(x->live_bits);
   for (auto& st : x->aux) if (st) cudaStreamDestroy(st);
   for (auto& e : x->aux_ev) if (e) cudaEventDestroy(e);
   delete x->aux_mu;
@@ -285,6 +290,42 @@ rairs_status rairs_train(const float* base, int64_t n, int32_t d, const rairs_bu
   return RAIRS_OK;
 }
 
+// Alg. 3 RairAssign (AIR, SOARL2) or single assignment of local rows
+// [row0, row0 + cnt) of idx->X into idx->l1/l2, exact fp64 (O4). Tensor-core
+// filter + certified fp64 re-rank for nlist > 256 (same result as the exact kernel).
+static rairs_status assign_rows(rairs_index_s* idx, int64_t row0, int64_t cnt, cudaStream_t s) {
+  if (cnt <= 0) return RAIRS_OK;
+  const rairs_build_params* p = &idx->params;
+  ProbeArgs pa{};
+  pa.X = idx->X + row0 * idx->d;
+  pa.rows = cnt;
+  pa.d = idx->d;
+  pa.C = idx->centroids;
+  pa.nl = p->nlist;
+  if (p->assignment != RAIRS_ASSIGN_SINGLE) {
+    pa.mode = p->assignment == RAIRS_ASSIGN_SOAR ? 3 : 1;
+    pa.L = std::min(p->n_cands, p->nlist);
+    pa.lambda = (double)p->lambda;
+    pa.strict = p->strict;
+  } else {
+    pa.mode = 2;
+    pa.L = 1;
+  }
+  pa.l1 = idx->l1 + row0;
+  pa.l2 = idx->l2 + row0;
+  if (coarse_fused_ok(idx, pa.L) && idx->nlist > 256) {
+    unsigned* fb = nullptr;
+    RAIRS_CUDA_TRY(cudaMallocAsync(&fb, sizeof(unsigned), s));
+    RAIRS_CUDA_TRY(cudaMemsetAsync(fb, 0, sizeof(unsigned), s));
+    rairs_status st = launch_coarse_fused(idx, pa.X, cnt, pa.L, pa.mode, pa.lambda, pa.strict,
+                                          nullptr, pa.l1, pa.l2, fb, s);
+    cudaFreeAsync(fb, s);
+    if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "build: coarse assignment");
+    return st;
+  }
+  return launch_probe_exact(pa, s);
+}
+
 rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
                                       const float* centroids, const float* codebook,
                                       const rairs_build_params* p, void* stream,
@@ -310,6 +351,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   }
   cudaGetDevice(&idx->device);
   idx->n = n;
+  idx->n_live = n;
+  idx->cap_rows = n;
   idx->d = d;
   idx->nlist = p->nlist;
   idx->M = p->M;
@@ -338,36 +381,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   if (st != RAIRS_OK) return fail(st);
   B_TRY(cudaMalloc(&idx->certify_fallbacks, sizeof(unsigned)));
   B_TRY(cudaMemsetAsync(idx->certify_fallbacks, 0, sizeof(unsigned), s));
-  // Alg. 3 RairAssign (AIR) or single assignment, exact fp64 (O4)
-  ProbeArgs pa{};
-  pa.X = idx->X;
-  pa.rows = n;
-  pa.d = d;
-  pa.C = idx->centroids;
-  pa.nl = p->nlist;
-  if (p->assignment != RAIRS_ASSIGN_SINGLE) {
-    pa.mode = p->assignment == RAIRS_ASSIGN_SOAR ? 3 : 1;
-    pa.L = std::min(p->n_cands, p->nlist);
-    pa.lambda = (double)p->lambda;
-    pa.strict = p->strict;
-  } else {
-    pa.mode = 2;
-    pa.L = 1;
-  }
-  pa.l1 = idx->l1;
-  pa.l2 = idx->l2;
-  if (coarse_fused_ok(idx, pa.L) && idx->nlist > 256) {
-    // tensor-core filter + certified fp64 assignment (same result as the exact kernel)
-    unsigned* fb = nullptr;
-    B_TRY(cudaMallocAsync(&fb, sizeof(unsigned), s));
-    B_TRY(cudaMemsetAsync(fb, 0, sizeof(unsigned), s));
-    st = launch_coarse_fused(idx, idx->X, n, pa.L, pa.mode, pa.lambda, pa.strict, nullptr, idx->l1,
-                             idx->l2, fb, s);
-    cudaFreeAsync(fb, s);
-    if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "build: coarse assignment");
-  } else {
-    st = launch_probe_exact(pa, s);
-  }
+  // Alg. 3 RairAssign (AIR / SOARL2) or single assignment, exact fp64 (O4)
+  st = assign_rows(idx, 0, n, s);
   if (st != RAIRS_OK) return fail(st);
   // Alg. 4 SeilInsert (cell-major) + PQ encoding (O5) into the packed layout
   st = build_layout(idx, s);
@@ -424,7 +439,152 @@ rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out) {
   out->shard_id = idx->shard_id;
   out->nshards = idx->nshards;
   out->device_bytes = idx->device_bytes;
+  out->n_live = idx->n_live;
   return RAIRS_OK;
+}
+
+// ---- updates (NEXT-3; P:1393-1409 batched SeilInsert, P:1870-1880 delete) ----
+__global__ void live_init_kernel(uint32_t* __restrict__ bits, int64_t words, int64_t n) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = w * 32;
+    bits[w] = lo + 32 <= n ? 0xFFFFFFFFu : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
+  }
+}
+
+// clear the live bit of every listed global id this shard holds; count the
+// bits that were set (ids not held, out of range or already deleted are ignored)
+__global__ void remove_ids_kernel(const int64_t* __restrict__ ids, int64_t m, int shard, int G,
+                                  int64_t n, uint32_t* __restrict__ bits,
+                                  unsigned long long* __restrict__ removed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = ids[i];
+    if (id < 0 || id % G != shard) continue;
+    const int64_t r = id / G;
+    if (r >= n) continue;
+    const uint32_t bit = 1u << (r & 31);
+    const uint32_t old = atomicAnd(&bits[r >> 5], ~bit);
+    if (old & bit) atomicAdd(removed, 1ull);
+  }
+}
+
+__global__ void live_set_range_kernel(uint32_t* __restrict__ bits, int64_t r0, int64_t r1) {
+  for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1;
+       r += (int64_t)gridDim.x * blockDim.x)
+    atomicOr(&bits[r >> 5], 1u << (r & 31));
+}
+
+static rairs_status relayout(rairs_index_s* idx, cudaStream_t s) {
+  RAIRS_TRY(build_layout(idx, s));
+  RAIRS_TRY(listmajor_prepare(idx, s));
+  RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  return RAIRS_OK;
+}
+
+static rairs_status grow_rows(rairs_index_s* idx, int64_t need, cudaStream_t s) {
+  if (need <= idx->cap_rows) return RAIRS_OK;
+  // 1/8 headroom: repeated batches amortise the copy without doubling 100M-row stores
+  const int64_t cap = std::max<int64_t>(need, idx->cap_rows + idx->cap_rows / 8);
+  const int d = idx->d;
+  float* X = nullptr;
+  int32_t *l1 = nullptr, *l2 = nullptr;
+  uint32_t* bits = nullptr;
+  auto undo = [&](cudaError_t e) {
+    cudaFree(X); cudaFree(l1); cudaFree(l2); cudaFree(bits);
+    set_error(std::string("rairs_add: ") + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&X, (size_t)cap * d * 4)) != cudaSuccess) return undo(e);
+  if ((e = cudaMalloc(&l1, (size_t)cap * 4)) != cudaSuccess) return undo(e);
+  if ((e = cudaMalloc(&l2, (size_t)cap * 4)) != cudaSuccess) return undo(e);
+  if (idx->live_bits && (e = cudaMalloc(&bits, (size_t)(cap + 31) / 32 * 4)) != cudaSuccess) return undo(e);
+  cudaMemcpyAsync(X, idx->X, (size_t)idx->n * d * 4, cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(l1, idx->l1, (size_t)idx->n * 4, cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(l2, idx->l2, (size_t)idx->n * 4, cudaMemcpyDeviceToDevice, s);
+  if (bits) {
+    cudaMemsetAsync(bits, 0, (size_t)(cap + 31) / 32 * 4, s);
+    cudaMemcpyAsync(bits, idx->live_bits, (size_t)(idx->cap_rows + 31) / 32 * 4,
+                    cudaMemcpyDeviceToDevice, s);
+  }
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return undo(e);
+  cudaFree(idx->X); cudaFree(idx->l1); cudaFree(idx->l2); cudaFree(idx->live_bits);
+  idx->X = X; idx->l1 = l1; idx->l2 = l2; idx->live_bits = bits;
+  idx->device_bytes += (cap - idx->cap_rows) * ((int64_t)d * 4 + 8) +
+                       (bits ? ((cap + 31) / 32 - (idx->cap_rows + 31) / 32) * 4 : 0);
+  idx->cap_rows = cap;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, int64_t* first_id,
+                       void* stream) {
+  if (!idx) return invalid("index is NULL");
+  if (n_add < 0) return invalid("n_add must be >= 0");
+  if (n_add == 0) {
+    if (first_id) *first_id = idx->n * idx->nshards + idx->shard_id;
+    return RAIRS_OK;
+  }
+  REQUIRE_DEV(x, "x");
+  const int64_t n_new = idx->n + n_add;
+  if (n_new >= (1ll << 30)) {
+    set_error("more than 2^30 rows per shard is not supported");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  if (n_new * idx->nshards >= 0xFFFFFFFFll) {
+    set_error("global ids must fit in 32 bits");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  RAIRS_CUDA_TRY(cudaDeviceSynchronize());  // in-flight searches may read the old arrays
+  RAIRS_TRY(grow_rows(idx, n_new, s));
+  const int64_t r0 = idx->n;
+  RAIRS_CUDA_TRY(cudaMemcpyAsync(idx->X + r0 * idx->d, x, (size_t)n_add * idx->d * 4,
+                                 cudaMemcpyDeviceToDevice, s));
+  if (idx->live_bits) {
+    live_set_range_kernel<<<grid_for(n_add), 256, 0, s>>>(idx->live_bits, r0, n_new);
+    RAIRS_CHECK_LAUNCH();
+  }
+  // new rows: Alg. 3 assignment (lines 1-12) with the index's trained centroids
+  RAIRS_TRY(assign_rows(idx, r0, n_add, s));
+  idx->n = n_new;
+  idx->n_live += n_add;
+  // Alg. 4 for the batch: cells, references and codes re-laid out (cell-major)
+  RAIRS_TRY(relayout(idx, s));
+  if (first_id) *first_id = r0 * idx->nshards + idx->shard_id;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_remove_ids(rairs_index_t idx, const int64_t* ids, int64_t n_ids,
+                              int64_t* n_removed, void* stream) {
+  if (!idx) return invalid("index is NULL");
+  if (n_ids < 0) return invalid("n_ids must be >= 0");
+  if (n_removed) *n_removed = 0;
+  if (n_ids == 0) return RAIRS_OK;
+  REQUIRE_DEV(ids, "ids");
+  cudaStream_t s = (cudaStream_t)stream;
+  RAIRS_CUDA_TRY(cudaDeviceSynchronize());
+  const int64_t words = (idx->cap_rows + 31) / 32;
+  if (!idx->live_bits) {
+    RAIRS_CUDA_TRY(cudaMalloc(&idx->live_bits, (size_t)words * 4));
+    live_init_kernel<<<grid_for(words), 256, 0, s>>>(idx->live_bits, words, idx->n);
+    RAIRS_CHECK_LAUNCH();
+    idx->device_bytes += words * 4;
+  }
+  unsigned long long* cnt = nullptr;
+  RAIRS_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
+  RAIRS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+  remove_ids_kernel<<<grid_for(n_ids), 256, 0, s>>>(ids, n_ids, idx->shard_id, idx->nshards, idx->n,
+                                                    idx->live_bits, cnt);
+  RAIRS_CHECK_LAUNCH();
+  unsigned long long h = 0;
+  RAIRS_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(cnt, s);
+  RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (n_removed) *n_removed = (int64_t)h;
+  if (h == 0) return RAIRS_OK;
+  idx->n_live -= (int64_t)h;
+  return relayout(idx, s);
 }
 
 rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, int32_t k,

@@ -8,7 +8,12 @@
 
 struct rairs_index_s {
   int device = 0;
-  int64_t n = 0;            // local rows
+  int64_t n = 0;            // local rows (inserted so far, deleted ones included)
+  int64_t n_live = 0;       // rows not deleted (the ones the layout holds)
+  int64_t cap_rows = 0;     // allocated rows of X / l1 / l2
+  // deletion tombstones (NEXT-3): bit r of live_bits[r/32] = row r is live;
+  // NULL until the first rairs_remove_ids (then every row < n is live)
+  uint32_t* live_bits = nullptr;
   int d = 0, nlist = 0, M = 0, M_pad = 0, dsub = 0;
   int shard_id = 0, nshards = 1;
   rairs_build_params params{};
@@ -47,6 +52,7 @@ struct rairs_index_s {
   uint32_t* list_ids = nullptr;      // [sum N_l] global id of item i of list-task l
   int max_refs = 0;
   int64_t device_bytes = 0;
+  int64_t layout_bytes = 0, lm_bytes = 0;  // parts of device_bytes rebuilt by add/remove
   // two auxiliary streams + fork/join events (list-major select/refine overlap)
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t aux_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};

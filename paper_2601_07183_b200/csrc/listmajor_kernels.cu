@@ -1261,6 +1261,12 @@ __global__ void lm_ids_kernel(const uint32_t* __restrict__ own_off,
 }
 
 rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
+  // a rebuild (after rairs_add / rairs_remove_ids) replaces the previous tables
+  cudaFree(idx->list_items); cudaFree(idx->ref_item_off); cudaFree(idx->list_base); cudaFree(idx->list_ids);
+  idx->list_items = idx->ref_item_off = idx->list_ids = nullptr;
+  idx->list_base = nullptr;
+  idx->device_bytes -= idx->lm_bytes;
+  idx->lm_bytes = 0;
   RAIRS_CUDA_TRY(cudaMalloc(&idx->list_items, (size_t)idx->nlist * 4));
   RAIRS_CUDA_TRY(cudaMalloc(&idx->ref_item_off, (size_t)std::max<int64_t>(idx->n_refs, 1) * 4));
   lm_items_kernel<<<(idx->nlist + 255) / 256, 256, 0, s>>>(idx->own_cnt, idx->ref_ptr, idx->ref_cnt,
@@ -1286,11 +1292,14 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
       idx->list_base, idx->nlist, idx->shard_id, idx->nshards, idx->list_ids);
   RAIRS_CHECK_LAUNCH();
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
-  for (auto& st : idx->aux) RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  for (auto& e : idx->aux_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  idx->aux_mu = new std::mutex();
-  idx->device_bytes += (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4 +
-                       (size_t)(idx->nlist + 1) * 8 + (size_t)base[idx->nlist] * 4;
+  if (!idx->aux_mu) {
+    for (auto& st : idx->aux) RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : idx->aux_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    idx->aux_mu = new std::mutex();
+  }
+  idx->lm_bytes = (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4 +
+                  (size_t)(idx->nlist + 1) * 8 + (size_t)base[idx->nlist] * 4;
+  idx->device_bytes += idx->lm_bytes;
   return RAIRS_OK;
 }
 

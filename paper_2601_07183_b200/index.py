@@ -111,6 +111,28 @@ class Index:
         check(lib().rairs_index_get_info(self._h, ctypes.byref(inf)), "rairs_index_get_info")
         return {f: getattr(inf, f) for f, _ in IndexInfo._fields_}
 
+    # ---------------------------------------------------------- updates
+    def add(self, x: torch.Tensor) -> int:
+        """Insert a batch (rairs_add); returns the global id of its first row
+        (row i gets first_id + i * nshards)."""
+        xx = _dev_f32(x, "x")
+        if xx.shape[1] != self.d:
+            raise ValueError(f"x must be [n, {self.d}]")
+        first = ctypes.c_int64(0)
+        check(lib().rairs_add(self._h, _ptr(xx), xx.shape[0], ctypes.byref(first), _stream()),
+              "rairs_add")
+        self.n = self.info()["n"]
+        return int(first.value)
+
+    def remove_ids(self, ids: torch.Tensor) -> int:
+        """Delete rows by global id (rairs_remove_ids); returns how many this
+        shard held and deleted now."""
+        t = ids.to(device=self.device, dtype=torch.int64).contiguous()
+        removed = ctypes.c_int64(0)
+        check(lib().rairs_remove_ids(self._h, _ptr(t), t.numel(), ctypes.byref(removed),
+                                     _stream()), "rairs_remove_ids")
+        return int(removed.value)
+
     # ----------------------------------------------------------- search
     def search(self, queries: torch.Tensor, k: int, nprobe: int, refine_factor: int = 10,
                return_dco: bool = False, stream: Optional[torch.cuda.Stream] = None):
@@ -172,7 +194,7 @@ class Index:
     def export_assignment(self) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
         l1 = torch.empty((self.n,), dtype=torch.int32, device=self.device)
         l2 = torch.empty((self.n,), dtype=torch.int32, device=self.device)
-        codes = torch.empty((self.n, self.M), dtype=torch.uint8, device=self.device)
+        codes = torch.zeros((self.n, self.M), dtype=torch.uint8, device=self.device)  # deleted rows: 0
         check(lib().rairs_export_assignment(self._h, _ptr(l1), _ptr(l2), _ptr(codes), _stream()),
               "rairs_export_assignment")
         return l1, l2, codes

@@ -513,3 +513,91 @@ def test_coarse_capped_lists_large_nprobe(oracle_mod):
         assert fb <= 0.05 * Q.shape[0], f"{fb} uncertified queries at nprobe {npb}"
         assert np.array_equal(pt[sample], oracle_mod.probe(Q[sample], cent, npb))
     idx.free()
+
+
+# ------------------------------------------------------------ updates (NEXT-3)
+def _oracle_on_rows(oracle, c, rows, Q, k, nprobe, rf):
+    """Oracle search over the live subset X[rows] (same trained state), with
+    its row indices mapped back to the original ids. The map is increasing, so
+    every (s, id) / (delta, id) order is preserved."""
+    o = oracle.search(c.X[rows], c.l1[rows], c.l2[rows], c.codes[rows], c.cent, c.cb, Q,
+                      k, nprobe, rf)
+    ci = o["cand_ids"]
+    o["cand_ids"] = np.where(ci != U32, rows[np.minimum(ci, rows.size - 1)], U32).astype(np.uint32)
+    for key in ("ids", "shard_ids"):
+        ids = o[key]
+        o[key] = np.where(ids >= 0, rows[np.clip(ids, 0, rows.size - 1)], -1)
+    return o
+
+
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
+def test_insert_batches_equal_full_build(oracle_mod, scan):
+    # paper protocol shape (P:2286-2290): build on 80 % of the rows, then insert
+    # the rest in five batches; the index must equal a build over every row
+    c = case(oracle_mod, "c1s")
+    n = c.X.shape[0]
+    n0 = int(0.8 * n)
+    idx = rb.Index.build(_t(c.X[:n0]), c.spec.nlist, c.spec.M, assignment="AIR",
+                         centroids=_t(c.cent), codebook=_t(c.cb))
+    bounds = np.linspace(n0, n, 6).astype(int)
+    for b0, b1 in zip(bounds[:-1], bounds[1:]):
+        assert idx.add(_t(c.X[b0:b1])) == b0
+    info = idx.info()
+    assert info["n"] == n and info["n_live"] == n
+    l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
+    assert np.array_equal(l1, c.l1) and np.array_equal(l2, c.l2) and np.array_equal(codes, c.codes)
+    check_layout(idx, c.l1, c.l2)
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, 10, 8, 4)
+    assert_search_equal(gpu_search(idx, c.Q, 10, 8, 4, scan), o)
+    idx.free()
+
+
+@pytest.mark.parametrize("scan", ["simt", "listmajor"])
+def test_delete_then_insert_parity(oracle_mod, scan):
+    # deletes in three batches (with repeats, negative and out-of-range ids),
+    # then one insert: results equal the oracle over the live rows
+    c = case(oracle_mod, "c1s")
+    n = c.X.shape[0]
+    n0 = n - 1000
+    idx = rb.Index.build(_t(c.X[:n0]), c.spec.nlist, c.spec.M, assignment="AIR",
+                         centroids=_t(c.cent), codebook=_t(c.cb))
+    rng = np.random.default_rng(77)
+    dead = rng.choice(n0, size=n0 // 5, replace=False)
+    total = 0
+    for part in np.array_split(dead, 3):
+        extra = np.array([-1, n0 + 5000, int(part[0])], np.int64)   # ignored / repeated
+        total += idx.remove_ids(torch.from_numpy(np.concatenate([part, extra])))
+    assert total == dead.size
+    assert idx.remove_ids(torch.from_numpy(dead[:10])) == 0        # already deleted
+    assert idx.add(_t(c.X[n0:])) == n0
+    live = np.ones(n, bool)
+    live[dead] = False
+    rows = np.nonzero(live)[0]
+    info = idx.info()
+    assert info["n"] == n and info["n_live"] == rows.size
+    L = idx.export_layout()
+    stored = L["slot_rows"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(np.sort(stored[stored != U32]), rows)      # stored once, live only
+    o = _oracle_on_rows(oracle_mod, c, rows, c.Q, 10, 8, 4)
+    assert_search_equal(gpu_search(idx, c.Q, 10, 8, 4, scan), o)
+    idx.free()
+
+
+def test_sharded_insert_and_delete_ids(oracle_mod):
+    # shard s of G holds global ids = row * G + s; an insert continues that
+    # numbering and deletes ignore ids of other shards
+    c = case(oracle_mod, "c1s")
+    G, s = 2, 1
+    rows_all = np.arange(s, c.X.shape[0], G)
+    half = rows_all.size // 2
+    idx = rb.Index.build(_t(c.X[rows_all[:half]]), c.spec.nlist, c.spec.M, assignment="AIR",
+                         centroids=_t(c.cent), codebook=_t(c.cb), shard_id=s, nshards=G)
+    assert idx.add(_t(c.X[rows_all[half:]])) == half * G + s
+    ids = torch.arange(0, 200, dtype=torch.int64)                   # 100 ours, 100 not
+    assert idx.remove_ids(ids) == 100
+    # shard s's global ids are the original rows s, s+G, ...: compare with the
+    # oracle over its live rows (ids < 200 deleted), ids mapped back
+    live = rows_all[rows_all >= 200]
+    o = _oracle_on_rows(oracle_mod, c, live, c.Q[:300], 10, 8, 4)
+    assert_search_equal(gpu_search(idx, c.Q[:300], 10, 8, 4), o)
+    idx.free()
