@@ -339,6 +339,10 @@ def run_ours(args):
         vs_single["dco_ratio_air_over_single"] = round(
             vs_single["air"]["dco_per_query"] / max(1.0, vs_single["single"]["dco_per_query"]), 3)
 
+    updates = None
+    if world == 1 and args.updates and X is not None and spec.n <= 2_000_000:
+        updates = update_throughput(idx, X, spec, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(idx, X, Q, spec, chosen)
@@ -376,6 +380,7 @@ def run_ours(args):
             "coarse_uncertified_per_step": round(fallbacks / args.steps, 1),
             "latency_1q": lat,
             "air_vs_single": vs_single,
+            "updates": updates,
             "clocks": clocks, "wall_s_timed_region": round(wall, 4),
             "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
             "index": {k2: info[k2] for k2 in ("n", "n_slots", "n_cells", "n_refs", "n_double",
@@ -436,6 +441,44 @@ def compare_strategy(kw, idx, X, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream,
     return {"nprobe": chosen, "recall": round(rec, 4), "qps": round(nq * steps / (t / 1e3), 1),
             "dco_per_query": round(float(dco.sum().item()) / nq, 1),
             "double_assigned_frac": round(n_double / max(1, X.shape[0]), 4)}
+
+
+def update_throughput(idx, X, spec, dev):
+    """NEXT-3 side line, the paper's protocol: an index of 80 % of
+    the rows (same trained state) takes five insert batches of 4 % each, then
+    the full index loses five delete batches of 4 % each; rows per second of
+    rairs_add / rairs_remove_ids (assignment + device re-layout included),
+    for AIR+SEIL and for single assignment (the paper's IVFPQfs baseline)."""
+    import torch
+    import paper_2601_07183_b200 as rb
+    cent, cb = idx.export_trained()
+    n = X.shape[0]
+    n0, bs = int(0.8 * n), int(0.04 * n)
+    out = {"protocol": f"build {n0}, 5 inserts of {bs}; build {n}, 5 deletes of {bs} (P:2286-2292)"}
+    Xd = torch.from_numpy(X).to(dev)
+    perm = torch.from_numpy(np.random.default_rng(3).permutation(n)[:5 * bs]).to(dev)
+    for name, kw in (("air", {"assignment": "AIR"}), ("single", {"assignment": "single"})):
+        a = rb.Index.build(Xd[:n0], spec.nlist, spec.M, centroids=cent, codebook=cb, **kw)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for b in range(5):
+            a.add(Xd[n0 + b * bs:n0 + (b + 1) * bs])
+        torch.cuda.synchronize()
+        ins = 5 * bs / (time.perf_counter() - t0)
+        a.free()
+        a = rb.Index.build(Xd, spec.nlist, spec.M, centroids=cent, codebook=cb, **kw)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for b in range(5):
+            a.remove_ids(perm[b * bs:(b + 1) * bs])
+        torch.cuda.synchronize()
+        dele = 5 * bs / (time.perf_counter() - t0)
+        a.free()
+        out[name] = {"inserts_per_s": round(ins, 1), "deletes_per_s": round(dele, 1)}
+    del Xd
+    out["air_over_single"] = {k: round(out["air"][k] / out["single"][k], 3)
+                              for k in ("inserts_per_s", "deletes_per_s")}
+    return out
 
 
 def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
@@ -533,6 +576,8 @@ def main():
     ap.add_argument("--compare-single", type=int, default=1,
                     help="also measure single / NaiveRA / SOARL2 / SRAIR indexes on the same "
                          "trained state (air_vs_single)")
+    ap.add_argument("--updates", type=int, default=1,
+                    help="insert/delete throughput side line (paper protocol, n <= 2M)")
     ap.add_argument("--latency-queries", type=int, default=200,
                     help="single-query searches timed for p50/p99 latency (0 = skip)")
     ap.add_argument("--gt-queries", type=int, default=0,

@@ -46,13 +46,23 @@ def gather_shard_results(ids: torch.Tensor, dists: torch.Tensor,
     return torch.stack(li), torch.stack(ld)
 
 
+def batch_slice_for_rank(n_total: int, batch: int, shard_id: int, nshards: int) -> slice:
+    """Rows of an insert batch that shard `shard_id` keeps: batch row j gets
+    global id n_total + j and lives on shard (n_total + j) mod G, so shard s
+    takes rows j = (s - n_total) mod G, +G, ... -- which continues its local
+    numbering (local row r <-> global id r*G + s) without gaps."""
+    start = (shard_id - n_total) % nshards
+    return slice(start, batch, nshards)
+
+
 class ShardedIndex:
     """A RAIRS index sharded over the ranks of a process group."""
 
     def __init__(self, local_index, group=None,
-                 merge: Optional[Callable] = None):
+                 merge: Optional[Callable] = None, n_total: Optional[int] = None):
         self.local = local_index
         self.group = group
+        self.n_total = n_total
         if merge is None:
             from .index import merge_topk
             merge = merge_topk
@@ -77,7 +87,30 @@ class ShardedIndex:
         broadcast_trained(cent, cb, src=0, group=group)
         idx = Index.build(base_local, nlist, M, centroids=cent, codebook=cb,
                           shard_id=rank, nshards=G, **kw)
-        return ShardedIndex(idx, group=group)
+        return ShardedIndex(idx, group=group, n_total=n_total)
+
+    def add(self, x_batch: torch.Tensor) -> int:
+        """Insert a batch given in full on every rank (global ids n_total ..
+        n_total + batch - 1); each rank inserts its id-mod-G rows. Returns the
+        first global id of the batch."""
+        rank, G = dist.get_rank(self.group), dist.get_world_size(self.group)
+        first = self.n_total
+        sl = batch_slice_for_rank(first, x_batch.shape[0], rank, G)
+        local = x_batch[sl]
+        if local.shape[0] > 0:
+            got = self.local.add(local)
+            if got != first + sl.start:
+                raise RuntimeError(f"shard {rank}: local numbering out of step ({got} != {first + sl.start})")
+        self.n_total = first + x_batch.shape[0]
+        return first
+
+    def remove_ids(self, ids: torch.Tensor) -> int:
+        """Delete global ids (the same list on every rank); returns the total
+        deleted over all shards (one all_reduce)."""
+        n = torch.tensor([self.local.remove_ids(ids)], dtype=torch.int64,
+                         device=self.local.device if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(n, group=self.group)
+        return int(n.item())
 
     def search(self, queries: torch.Tensor, k: int, nprobe: int, refine_factor: int = 10):
         ids, dists = self.local.search(queries, k, nprobe, refine_factor)

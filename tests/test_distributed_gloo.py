@@ -87,3 +87,66 @@ def test_two_rank_gloo_merge_matches_oracle(oracle_mod):
         assert np.array_equal(rows, np.arange(r, X.shape[0], G))  # id mod G partition
     allrows = np.sort(np.concatenate([res[r][4] for r in range(G)]))
     assert np.array_equal(allrows, np.arange(X.shape[0]))
+
+
+class _FakeShard:
+    """Host stand-in for one shard's Index (the numbering contract of
+    rairs_add / rairs_remove_ids: local row r <-> global id r*G + s)."""
+
+    def __init__(self, s, G, n_local):
+        self.s, self.G, self.rows = s, G, [r * G + s for r in range(n_local)]
+        self.dead = set()
+        self.device = torch.device("cpu")
+
+    def add(self, x):
+        first = len(self.rows) * self.G + self.s
+        self.rows += [(len(self.rows) + j) * self.G + self.s for j in range(x.shape[0])]
+        self.kept = getattr(self, "kept", []) + x[:, 0].tolist()
+        return first
+
+    def remove_ids(self, ids):
+        held = {int(i) for i in ids.tolist() if i >= 0 and i % self.G == self.s and i in self.rows}
+        new = held - self.dead
+        self.dead |= new
+        return len(new)
+
+
+def _update_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2601_07183_b200.distributed import ShardedIndex, shard_rows
+        n0 = 11                                        # odd: shards start unequal
+        local = _FakeShard(rank, world, len(shard_rows(n0, rank, world)))
+        sh = ShardedIndex(local, n_total=n0, merge=lambda a, b: (a, b))
+        firsts = []
+        for size in (5, 4, 7):                         # batch row j carries id n_total + j
+            batch = torch.arange(sh.n_total, sh.n_total + size, dtype=torch.float32)[:, None]
+            firsts.append(sh.add(batch.repeat(1, 4)))
+        removed = sh.remove_ids(torch.tensor([0, 3, 3, 12, 26, 27, 99, -1]))
+        out_q.put((rank, firsts, sh.n_total, local.rows, local.kept, removed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_insert_delete_numbering():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_update_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    all_rows = []
+    for rank, firsts, n_total, rows, kept, removed in res:
+        assert firsts == [11, 16, 20] and n_total == 27
+        assert rows == list(range(rank, 27, world))    # id-mod-G shard, no gaps
+        assert all(int(v) % world == rank for v in kept)  # each rank kept its own ids
+        assert removed == 4                            # 0, 3, 12, 26 (3 repeated; 27, 99, -1 absent)
+        all_rows += rows
+    assert sorted(all_rows) == list(range(27))
