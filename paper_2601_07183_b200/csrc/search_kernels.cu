@@ -649,16 +649,18 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
   }
 }
 
-// K6 refine, staged variant (d = 4*D4 <= 128, bigK <= 128): a persistent CTA
-// walks queries.  Warp w gathers the rows w, w+8, ... of a query with one
-// coalesced 16-B-per-lane load per row (all of its rows in flight at once)
-// into registers; the NEXT query's rows are loaded while thread c runs
-// candidate c's serial fp64 sum (ascending t, O10 -- the same order and
-// rounding as refine_kernel) over the current query's padded shared tile.
-// The top-k by the unique key (bits(delta) << 32 | id) is found by rank
-// counting.
+// K6 refine, staged variant (d = 4*D4 <= 128, bigK <= 512): a persistent CTA
+// walks (query, chunk) units -- a query's candidates in chunks of 128 rows.
+// Warp w gathers the rows w, w+8, ... of a chunk with one coalesced
+// 16-B-per-lane load per row (all of its rows in flight at once) into
+// registers; the NEXT unit's rows are loaded while thread c runs candidate
+// c's serial fp64 sum (ascending t, O10 -- the same order and rounding as
+// refine_kernel) over the current chunk's padded shared tile.  After a
+// query's last chunk, the top-k by the unique key (bits(delta) << 32 | id) is
+// found by rank counting over its bigK keys.
 constexpr int RS_THREADS = 256;
 constexpr int RS_ROWS = 128;
+constexpr int RS_MAXK = 512;
 
 template <int D4>
 __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
@@ -666,17 +668,25 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     const float* __restrict__ queries, const float* __restrict__ X, int G,
     int64_t* __restrict__ out_ids, float* __restrict__ out_dists) {
   constexpr int D = 4 * D4, RSF = D + 4;  // tile row stride (floats): conflict-free float4 reads
-  extern __shared__ __align__(16) float tile[];  // [bigK rounded to 8][RSF]
+  extern __shared__ __align__(16) float tile[];  // [min(bigK, 128) rounded to 8][RSF]
   __shared__ double qs[D];
-  __shared__ uint64_t rk[RS_ROWS];
+  __shared__ uint64_t rk[RS_MAXK];
   __shared__ uint32_t gids[RS_ROWS];
   __shared__ uint32_t nvalid;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int myrow = warp + 8 * lane;  // lane j (< 16) fetches the key of row warp + 8j
-  // software pipeline: keys of query q + 2*grid and rows of query q + grid are
-  // in flight while query q is computed (the row loads never wait on a key load)
-  auto load_key = [&](int64_t q) -> uint64_t {
-    return (q < nq && lane < 16 && myrow < bigK) ? __ldg(keys + q * bigK + myrow) : kKeyInf;
+  const int nch = (bigK + RS_ROWS - 1) / RS_ROWS;
+  // software pipeline: keys of unit u + 2 and rows of unit u + 1 are in
+  // flight while unit u is computed (the row loads never wait on a key load)
+  auto load_key = [&](int64_t q, int c) -> uint64_t {
+    const int row = c * RS_ROWS + myrow;
+    return (q < nq && lane < 16 && row < bigK) ? __ldg(keys + q * bigK + row) : kKeyInf;
+  };
+  auto advance = [&](int64_t& q, int& c) {
+    if (++c == nch) {
+      c = 0;
+      q += gridDim.x;
+    }
   };
   uint32_t gid = 0xFFFFFFFFu;
   float4 v[16];
@@ -696,24 +706,34 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     }
   };
   int64_t q = blockIdx.x;
-  if (q < nq) fetch_rows(load_key(q));
-  uint64_t key_next = load_key(q + gridDim.x);
-  float qv = (q < nq && tid < D) ? __ldg(queries + q * D + tid) : 0.0f;  // query, one ahead
-  for (; q < nq; q += gridDim.x) {
+  int c = 0;
+  if (q < nq) fetch_rows(load_key(q, 0));
+  int64_t qn = q;
+  int cn = c;
+  advance(qn, cn);                                  // the unit after the current one
+  uint64_t key_next = load_key(qn, cn);
+  float qv = (q < nq && tid < D) ? __ldg(queries + q * D + tid) : 0.0f;  // next query to start
+  while (q < nq) {
+    const int crow = min(RS_ROWS, bigK - c * RS_ROWS);  // rows in this chunk
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (warp + 8 * j < bigK && lane < D4)
+      if (warp + 8 * j < crow && lane < D4)
         *reinterpret_cast<float4*>(tile + (warp + 8 * j) * RSF + 4 * lane) = v[j];
-    if (lane < 16 && myrow < bigK) gids[myrow] = gid;
-    if (tid < D) qs[tid] = (double)qv;
-    if (tid == 0) nvalid = 0;
-    __syncthreads();
-    if (q + gridDim.x < nq) {
-      fetch_rows(key_next);                        // rows of q + grid: in flight from here
-      key_next = load_key(q + 2 * (int64_t)gridDim.x);
-      if (tid < D) qv = __ldg(queries + (q + gridDim.x) * D + tid);
+    if (lane < 16 && myrow < crow) gids[myrow] = gid;
+    if (c == 0) {
+      if (tid < D) qs[tid] = (double)qv;
+      if (tid == 0) nvalid = 0;
     }
-    if (tid < bigK) {
+    __syncthreads();
+    int64_t q2 = qn;
+    int c2 = cn;
+    advance(q2, c2);
+    if (qn < nq) {
+      fetch_rows(key_next);                        // rows of the next unit: in flight from here
+      key_next = load_key(q2, c2);
+      if (cn == 0 && tid < D) qv = __ldg(queries + qn * D + tid);
+    }
+    if (tid < crow) {
       const uint32_t g = gids[tid];
       uint64_t out = kKeyInf;
       if (g != 0xFFFFFFFFu) {
@@ -731,33 +751,39 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
         out = ((uint64_t)__float_as_uint(__double2float_rn(acc)) << 32) | g;
         atomicAdd(&nvalid, 1u);
       }
-      rk[tid] = out;
+      rk[c * RS_ROWS + tid] = out;
     }
-    __syncthreads();
-    if (tid < bigK) {
-      const uint64_t kc = rk[tid];
-      if (kc != kKeyInf) {
-        int rank = 0;
+    __syncthreads();  // tile / gids free for the next unit; rk complete after the last chunk
+    if (c == nch - 1) {
+      for (int i = tid; i < bigK; i += RS_THREADS) {
+        const uint64_t kc = rk[i];
+        if (kc != kKeyInf) {
+          int rank = 0;
 #pragma unroll 8
-        for (int j = 0; j < bigK; ++j) rank += (rk[j] < kc) ? 1 : 0;
-        if (rank < k) {
-          out_ids[q * k + rank] = (int64_t)(uint32_t)(kc & 0xFFFFFFFFu);
-          out_dists[q * k + rank] = __uint_as_float((uint32_t)(kc >> 32));
+          for (int j = 0; j < bigK; ++j) rank += (rk[j] < kc) ? 1 : 0;
+          if (rank < k) {
+            out_ids[q * k + rank] = (int64_t)(uint32_t)(kc & 0xFFFFFFFFu);
+            out_dists[q * k + rank] = __uint_as_float((uint32_t)(kc >> 32));
+          }
         }
       }
+      for (int i = (int)nvalid + tid; i < k; i += RS_THREADS) {
+        out_ids[q * k + i] = -1;
+        out_dists[q * k + i] = __int_as_float(0x7f800000);
+      }
+      __syncthreads();  // rk / nvalid / qs free for the next query
     }
-    for (int i = (int)nvalid + tid; i < k; i += RS_THREADS) {
-      out_ids[q * k + i] = -1;
-      out_dists[q * k + i] = __int_as_float(0x7f800000);
-    }
-    __syncthreads();  // tile / gids / rk / nvalid free for the next query
+    q = qn;
+    c = cn;
+    qn = q2;
+    cn = c2;
   }
 }
 
 template <int D4>
 static rairs_status launch_refine_stage(const rairs_index_s* idx, const SearchArgs& a, int bigK,
                                         cudaStream_t s) {
-  const size_t smem = (size_t)round_up(bigK, 8) * (4 * D4 + 4) * 4;
+  const size_t smem = (size_t)round_up(std::min(bigK, RS_ROWS), 8) * (4 * D4 + 4) * 4;
   RAIRS_CUDA_TRY(cudaFuncSetAttribute(refine_stage_kernel<D4>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -775,7 +801,7 @@ rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaSt
   if (a.nq <= 0) return RAIRS_OK;
   {
     const int bigK = a.k * a.refine_factor;
-    if (bigK <= RS_ROWS) {
+    if (bigK <= RS_MAXK) {
       switch (idx->d) {
         case 32: return launch_refine_stage<8>(idx, a, bigK, s);
         case 64: return launch_refine_stage<16>(idx, a, bigK, s);
