@@ -200,6 +200,7 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   if (st == RAIRS_OK) {
     if (listmajor_ok(idx, nq, nprobe, bigK)) {
       a.fused_refine = true;
+      a.sorted_keys = cand_ids != nullptr || cand_scores != nullptr;
       a.ev_selected = ev.on ? ev.ev.e[2] : nullptr;
       st = launch_listmajor(idx, a, s);
       const int halves = (nq >= 2 * LM_OVERLAP_MIN_Q && idx->aux[0]) ? 2 : 1;

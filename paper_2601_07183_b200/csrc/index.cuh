@@ -143,6 +143,9 @@ struct SearchArgs {
   // the search stream once every query's candidates are final (stage timing)
   bool fused_refine = false;
   cudaEvent_t ev_selected = nullptr;
+  // candidate keys wanted in (s, id) order (debug outputs); otherwise each
+  // query's bigK keys may be written in any order (the refine ranks them)
+  bool sorted_keys = false;
 };
 rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);

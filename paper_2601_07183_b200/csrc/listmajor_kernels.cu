@@ -694,6 +694,7 @@ struct SelArgs {
   uint64_t* out_keys;
   int64_t* dco;
   int64_t q0;  // first query of this launch (queries [q0, nq))
+  int sorted_out;  // 1: write each query's bigK keys in (s, id) order (debug outputs)
 };
 
 __device__ __forceinline__ uint32_t warp_bthr(const uint32_t* hist, uint32_t bigK) {
@@ -756,6 +757,98 @@ __device__ void warp_sort_keys(uint64_t* a, int n) {
       __syncwarp();
     }
   }
+}
+
+// smallest bin b of a 256-bin histogram whose cumulative count reaches K
+// (K >= 1 and the total >= K); *below = the count of the bins before b
+__device__ __forceinline__ uint32_t warp_bsel256(const uint32_t* hist, uint32_t K, uint32_t* below) {
+  const int lane = lane_id();
+  uint32_t h[8], loc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { h[i] = hist[lane * 8 + i]; loc += h[i]; }
+  uint32_t inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  const unsigned hit = __ballot_sync(0xffffffffu, inc >= K);
+  const int hl = hit ? __ffs(hit) - 1 : 31;
+  uint32_t b = 255, run = inc - loc, bl = 0;
+  if (lane == hl) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (run + h[i] >= K) { b = lane * 8 + i; bl = run; break; }
+      run += h[i];
+    }
+  }
+  *below = __shfl_sync(0xffffffffu, bl, hl);
+  return __shfl_sync(0xffffffffu, b, hl);
+}
+
+// Exact top-K of n > K resolved keys (s << 32 | id), written UNORDERED to out:
+// a two-level radix select on s (s <= thr < 2^16): 256 bins of s >> sh, then
+// the exact s* inside the chosen bin; every key with s < s* is kept, and the
+// ties at s* by smallest id.  scratch: 512 u32 of shared memory.  Returns
+// false (nothing written) when more than 256 keys tie at s* -- the caller then
+// sorts everything.
+__device__ bool warp_select_unordered(const uint64_t* cand, uint32_t n, uint32_t K, uint32_t thr,
+                                      uint32_t* scratch, uint64_t* out) {
+  const int lane = lane_id();
+  const uint32_t sh = thr < 256u ? 0u : (uint32_t)(32 - __clz(thr)) - 8u;
+  for (int i = lane; i < 512; i += 32) scratch[i] = 0u;
+  __syncwarp();
+  for (uint32_t i = lane; i < n; i += 32) atomicAdd(&scratch[(uint32_t)(cand[i] >> 32) >> sh], 1u);
+  __syncwarp();
+  uint32_t below1;
+  const uint32_t b1 = warp_bsel256(scratch, K, &below1);
+  const uint32_t lo = b1 << sh, hi = lo + (1u << sh);   // scores of bin b1: [lo, hi)
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint32_t sc = (uint32_t)(cand[i] >> 32);
+    if (sc >= lo && sc < hi) atomicAdd(&scratch[256 + (sc - lo)], 1u);
+  }
+  __syncwarp();
+  uint32_t below2;
+  const uint32_t b2 = warp_bsel256(scratch + 256, K - below1, &below2);
+  const uint32_t sstar = lo + b2;
+  const uint32_t need = K - below1 - below2;       // ties at s* to keep (>= 1)
+  const uint32_t ties = scratch[256 + b2];
+  if (ties > 256u) return false;
+  __syncwarp();
+  // keys with s < s* (exactly K - need of them) + the ties, compacted
+  uint64_t* tie = reinterpret_cast<uint64_t*>(scratch);  // reuses the histograms
+  uint32_t nk = 0, nt = 0;
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint64_t v = i < n ? cand[i] : kKeyInf;
+    const uint32_t sc = (uint32_t)(v >> 32);
+    const bool keep = i < n && sc < sstar, tq = i < n && sc == sstar;
+    const unsigned bk = __ballot_sync(0xffffffffu, keep), bt = __ballot_sync(0xffffffffu, tq);
+    const unsigned below_me = (1u << lane) - 1u;
+    __syncwarp();
+    if (keep) out[nk + __popc(bk & below_me)] = v;
+    if (tq) tie[nt + __popc(bt & below_me)] = v;
+    nk += __popc(bk);
+    nt += __popc(bt);
+  }
+  __syncwarp();
+  if (nt == need) {
+    for (uint32_t j = lane; j < nt; j += 32) out[nk + j] = tie[j];
+  } else if (nt <= 32) {                           // rank the ties by id
+    const uint64_t v = (uint32_t)lane < nt ? tie[lane] : kKeyInf;
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < nt; ++j) rank += tie[j] < v ? 1u : 0u;
+    if ((uint32_t)lane < nt && rank < need) out[nk + rank] = v;
+  } else {
+    uint32_t np = 32;
+    while (np < nt) np <<= 1;
+    for (uint32_t j = nt + lane; j < np; j += 32) tie[j] = kKeyInf;
+    __syncwarp();
+    warp_sort_keys(tie, (int)np);
+    for (uint32_t j = lane; j < need; j += 32) out[nk + j] = tie[j];
+  }
+  __syncwarp();
+  return true;
 }
 
 // One WARP per query: exact top-bigK of the keys (s << 32 | id) over U(q).
@@ -962,7 +1055,18 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
         }
       }
     }
-    if (!exact) sel_resolve<U32>(a, q, cand, cnt);
+    if (!exact) {
+      sel_resolve<U32>(a, q, cand, cnt);
+      if (!a.sorted_out && cnt > bigK && thr < 65536u) {
+        // production: the refine needs the top-bigK SET only -- select it
+        // exactly without sorting every candidate
+        if (warp_select_unordered(cand, cnt, bigK, thr, hist, a.out_keys + q * a.bigK)) {
+          if (lane == 0 && a.dco) a.dco[q] = (int64_t)dco;
+          __syncwarp();
+          continue;
+        }
+      }
+    }
     cnt = warp_filter(cand, cnt, bstar, tau, a.hshift);
     int np = 2;
     while (np < (int)cnt) np <<= 1;
@@ -1160,6 +1264,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.nshards = idx->nshards;
   sl.out_keys = sa.cand_keys;
   sl.dco = sa.dco;
+  sl.sorted_out = sa.sorted_keys ? 1 : 0;
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
   LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
   LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));

@@ -73,6 +73,12 @@ def gpu_search(idx, Q, k, nprobe, rf, scan="auto"):
     out = idx.search_debug(_t(Q), k, nprobe, rf)
     torch.cuda.synchronize()
     r = {key: v.cpu().numpy() for key, v in out.items()}
+    # the plain entry point (no debug outputs: the list-major selection writes
+    # each query's top-bigK set unordered) must return the same results
+    ids, dists, dco = idx.search(_t(Q), k, nprobe, rf, return_dco=True)
+    assert np.array_equal(ids.cpu().numpy(), r["ids"]), "plain search ids differ from debug"
+    assert np.array_equal(dists.cpu().numpy(), r["dists"]), "plain search dists differ"
+    assert np.array_equal(dco.cpu().numpy(), r["dco"]), "plain search DCO differs"
     r["cand_ids"] = r["cand_ids"].view(np.uint32)
     r["cand_scores"] = r["cand_scores"].view(np.uint32)
     return r
