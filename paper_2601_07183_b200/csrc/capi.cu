@@ -111,6 +111,8 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->live_bits);
   for (auto& st : x->aux) if (st) cudaStreamDestroy(st);
   for (auto& e : x->aux_ev) if (e) cudaEventDestroy(e);
+  if (x->h2d) cudaStreamDestroy(x->h2d);
+  for (auto& e : x->h2d_ev) if (e) cudaEventDestroy(e);
   delete x->aux_mu;
   for (auto& es : x->pending)
     for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
@@ -147,7 +149,9 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
                                 int nprobe, int rf, int32_t* probes_out, uint8_t* lut_q,
                                 float* lut_a, float* lut_b, uint32_t* cand_ids,
                                 uint32_t* cand_scores, int64_t* dco, int64_t* out_ids,
-                                float* out_dists, cudaStream_t s) {
+                                float* out_dists, cudaStream_t s,
+                                const float* queries_host = nullptr) {
+  // queries_host != NULL: `queries` is a device buffer this call fills from it
   if (nq == 0) return RAIRS_OK;
   const int bigK = k * rf;
   int32_t* probes = probes_out;
@@ -179,9 +183,41 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   ev.mark(0);
   // coarse: P(q) = first nprobe lists by (D64, l)  (O1).  Tensor-core TF32
   // filter + exact fp64 certify (K1/K2), or the exact fp64 kernel directly.
-  if (coarse_fused_ok(idx, nprobe)) {
+  // Host queries: copied in chunks on the index's copy stream, the coarse
+  // stage of chunk h starting as soon as chunk h has landed.
+  static const int h2d_chunks = [] {
+    const char* e = getenv("RAIRS_H2D_CHUNKS");  // experiments only
+    return e ? std::max(1, std::min(H2D_CHUNKS, atoi(e))) : H2D_CHUNKS;
+  }();
+  const int hchunks = (queries_host && idx->h2d && coarse_fused_ok(idx, nprobe))
+                          ? (int)std::min<int64_t>(h2d_chunks, nq / H2D_MIN_ROWS) : 1;
+  int64_t nk = 0;
+  if (queries_host && hchunks <= 1) {
+    RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries), queries_host,
+                                   (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (hchunks > 1) {
+    std::lock_guard<std::mutex> lock(*idx->aux_mu);
+    RAIRS_CUDA_TRY(cudaEventRecord(idx->h2d_ev[0], s));  // workspaces allocated on s
+    RAIRS_CUDA_TRY(cudaStreamWaitEvent(idx->h2d, idx->h2d_ev[0], 0));
+    for (int h = 0; h < hchunks; ++h) {
+      const int64_t r0 = nq * h / hchunks, r1 = nq * (h + 1) / hchunks;
+      RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries) + r0 * idx->d,
+                                     queries_host + r0 * idx->d, (size_t)(r1 - r0) * idx->d * 4,
+                                     cudaMemcpyHostToDevice, idx->h2d));
+      RAIRS_CUDA_TRY(cudaEventRecord(idx->h2d_ev[1 + h], idx->h2d));
+    }
+    for (int h = 0; h < hchunks && st == RAIRS_OK; ++h) {
+      const int64_t r0 = nq * h / hchunks, r1 = nq * (h + 1) / hchunks;
+      RAIRS_CUDA_TRY(cudaStreamWaitEvent(s, idx->h2d_ev[1 + h], 0));
+      st = launch_coarse_fused(idx, queries + r0 * idx->d, r1 - r0, nprobe, 0, 0.0, 0,
+                               probes + r0 * nprobe, nullptr, nullptr, idx->certify_fallbacks, s);
+      nk += 3;
+    }
+  } else if (coarse_fused_ok(idx, nprobe)) {
     st = launch_coarse_fused(idx, queries, nq, nprobe, 0, 0.0, 0, probes, nullptr, nullptr,
                              idx->certify_fallbacks, s);
+    nk += 3;  // topw + certify + exact fallback
   } else {
     ProbeArgs pa{};
     pa.X = queries;
@@ -193,9 +229,9 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
     pa.mode = 0;
     pa.out_idx = probes;
     st = launch_probe_exact(pa, s);
+    nk += 1;
   }
   ev.mark(1);
-  int64_t nk = coarse_fused_ok(idx, nprobe) ? 3 : 1;  // topw + certify + exact fallback
   bool refined = false;
   if (st == RAIRS_OK) {
     if (listmajor_ok(idx, nq, nprobe, bigK)) {
@@ -615,9 +651,8 @@ rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int
   RAIRS_CUDA_TRY(cudaMallocAsync(&dq, qb, s));
   RAIRS_CUDA_TRY(cudaMallocAsync(&di, ib, s));
   RAIRS_CUDA_TRY(cudaMallocAsync(&dd, db, s));
-  RAIRS_CUDA_TRY(cudaMemcpyAsync(dq, queries_host, qb, cudaMemcpyHostToDevice, s));
   rairs_status st = search_impl(idx, dq, nq, k, nprobe, refine_factor, nullptr, nullptr, nullptr,
-                                nullptr, nullptr, nullptr, nullptr, di, dd, s);
+                                nullptr, nullptr, nullptr, nullptr, di, dd, s, queries_host);
   if (st == RAIRS_OK) {
     cudaMemcpyAsync(out_ids_host, di, ib, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(out_dists_host, dd, db, cudaMemcpyDeviceToHost, s);

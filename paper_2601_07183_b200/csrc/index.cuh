@@ -6,6 +6,12 @@
 
 #include "common.cuh"
 
+namespace rairs {
+// rairs_search_host: queries copied in up to H2D_CHUNKS chunks of >= H2D_MIN_ROWS
+constexpr int H2D_CHUNKS = 4;
+constexpr int64_t H2D_MIN_ROWS = 2048;
+}  // namespace rairs
+
 struct rairs_index_s {
   int device = 0;
   int64_t n = 0;            // local rows (inserted so far, deleted ones included)
@@ -57,6 +63,9 @@ struct rairs_index_s {
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t aux_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   std::mutex* aux_mu = nullptr;  // one search at a time enqueues on the aux streams
+  // host-query copy stream + events (rairs_search_host: chunked H2D / coarse overlap)
+  cudaStream_t h2d = nullptr;
+  cudaEvent_t h2d_ev[5] = {};
 
   // stage profiling (CUDA events on the search stream)
   bool prof = false;

@@ -1400,6 +1400,8 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
   if (!idx->aux_mu) {
     for (auto& st : idx->aux) RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     for (auto& e : idx->aux_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&idx->h2d, cudaStreamNonBlocking));
+    for (auto& e : idx->h2d_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     idx->aux_mu = new std::mutex();
   }
   idx->lm_bytes = (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4 +

@@ -607,3 +607,19 @@ def test_sharded_insert_and_delete_ids(oracle_mod):
     o = _oracle_on_rows(oracle_mod, c, live, c.Q[:300], 10, 8, 4)
     assert_search_equal(gpu_search(idx, c.Q[:300], 10, 8, 4), o)
     idx.free()
+
+
+def test_search_host_chunked_h2d(oracle_mod):
+    # rairs_search_host copies >= 4,096 host queries in chunks on the index's
+    # copy stream and runs the coarse stage chunk by chunk (tensor-core path,
+    # nlist 1024): same results as the device entry point, and as the oracle
+    c = case(oracle_mod, "c2pl", n=60000)
+    idx = c.gpu_index()
+    Q = c.Q[:9001]                                     # 4 chunks, ragged
+    ids, dists = idx.search(_t(Q), 10, 4, 10)
+    hi, hd = idx.search_host(Q, 10, 4, 10)
+    assert np.array_equal(ids.cpu().numpy(), hi) and np.array_equal(dists.cpu().numpy(), hd)
+    rows = np.r_[0:50, 2200:2300, 8950:9001]           # across the chunk borders
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, Q[rows], 10, 4, 10)
+    assert np.array_equal(hi[rows], o["ids"])
+    idx.free()

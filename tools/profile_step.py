@@ -22,7 +22,11 @@ idx = rb.build_index(torch.from_numpy(X).to(dev), spec.nlist, spec.M)
 idx.set_scan_mode(mode)
 Qd = torch.from_numpy(Q).to(dev)
 torch.cuda.synchronize()
-for _ in range(reps):
+for i in range(reps):
+    if i == reps - 1:
+        torch.cuda.nvtx.range_push("search")   # ncu --nvtx --nvtx-include "search/"
     ids, dists = idx.search(Qd, spec.k, npb, spec.refine_factor)
+    if i == reps - 1:
+        torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 print("profile_step OK", cfg, npb, mode, reps, ids.shape)
