@@ -3,7 +3,12 @@ bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of each kernel
 of the fast-scan stage (A3-A6) and their sum, which bench.py reports as the
 roofline `traffic` of that stage.
 
-  python tools/traffic_from_ncu.py <report.ncu-rep> <config> [out.json]
+  python tools/traffic_from_ncu.py <report.ncu-rep> <config> [out.json] [searches]
+
+`searches` = number of searches the report covers (default 1: an NVTX-filtered
+capture of one search, `tools/profile_step.py` + `ncu --nvtx --nvtx-include
+"search/"`); per-search bytes = the stage kernels' total / searches (a search
+may launch a kernel more than once, e.g. the selection in query halves).
 """
 import csv
 import json
@@ -18,6 +23,7 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 def main():
     rep, cfg = sys.argv[1], sys.argv[2]
     out = sys.argv[3] if len(sys.argv) > 3 else f"profiles/traffic_{cfg}.json"
+    searches = int(sys.argv[4]) if len(sys.argv) > 4 else 1
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
@@ -29,9 +35,10 @@ def main():
         name = r[ik].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
         b = (float(r[ir]) * UNIT.get(units[ir], 1) + float(r[iw]) * UNIT.get(units[iw], 1))
         per.setdefault(name, []).append((b, float(r[it])))
-    kern = {k: {"dram_bytes": sum(x[0] for x in v) / len(v), "duration": sum(x[1] for x in v) / len(v),
+    kern = {k: {"dram_bytes_per_search": sum(x[0] for x in v) / searches,
+                "duration_per_search": sum(x[1] for x in v) / searches,
                 "duration_unit": units[it], "launches": len(v)} for k, v in per.items()}
-    stage = sum(v["dram_bytes"] for k, v in kern.items() if k in STAGE)
+    stage = sum(v["dram_bytes_per_search"] for k, v in kern.items() if k in STAGE)
     json.dump({"config": cfg, "source": rep, "dram_bytes_per_launch": stage,
                "stage_kernels": [k for k in kern if k in STAGE], "kernels": kern},
               open(out, "w"), indent=1)
