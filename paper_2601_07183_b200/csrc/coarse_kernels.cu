@@ -621,7 +621,10 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   const int nl_tiles = (int)ceil_div(nl, FT_BN);
   const bool capped = Wp1 > 32 && nl_tiles >= 8;
   const bool reg = Wp1 <= 32 || capped;
-  const int KR = Wp1 <= 16 ? 16 : (Wp1 <= 24 ? 24 : 32);
+  // list length = W + 1 rounded up to an instantiated size: the insertion cost
+  // and the pass threshold (the KR-th kept value) both shrink with KR
+  const int KR = Wp1 <= 10 ? 10 : Wp1 <= 13 ? 13 : Wp1 <= 16 ? 16 : Wp1 <= 20 ? 20
+               : Wp1 <= 24 ? 24 : 32;
   const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
   const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
   const int nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
@@ -635,7 +638,13 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   if (!attr_set) {
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<0>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<10>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<13>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<20>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<24>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -688,8 +697,14 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ta.out_v = vals;
     ta.out_i = ids;
     const dim3 tgrid((unsigned)mtiles, (unsigned)nsplit);
-    if (reg && KR == 16)
+    if (reg && KR == 10)
+      coarse_topw_kernel<10><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    else if (reg && KR == 13)
+      coarse_topw_kernel<13><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    else if (reg && KR == 16)
       coarse_topw_kernel<16><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+    else if (reg && KR == 20)
+      coarse_topw_kernel<20><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
     else if (reg && KR == 24)
       coarse_topw_kernel<24><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
     else if (reg)

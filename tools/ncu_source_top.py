@@ -1,6 +1,7 @@
 """Summarise `ncu -i X --page source --csv --print-source=cuda,sass` per CUDA
 source line: share of executed instructions and of warp-stall samples."""
 import csv
+import os
 import subprocess
 import sys
 
@@ -27,7 +28,8 @@ def main():
     ti = sum(x[3] for x in recs) or 1
     ts = sum(x[4] for x in recs) or 1
     print(f"total warp-instructions executed: {ti:.3e}")
-    for f, ln, src, ins, st in sorted(recs, key=lambda x: -x[4])[:int(sys.argv[3]) if len(sys.argv) > 3 else 30]:
+    key = (lambda x: -x[3]) if os.environ.get("SORT_BY") == "inst" else (lambda x: -x[4])
+    for f, ln, src, ins, st in sorted(recs, key=key)[:int(sys.argv[3]) if len(sys.argv) > 3 else 30]:
         print(f"{f:20s}:{ln:<5d} inst {100*ins/ti:5.1f}%  stall {100*st/ts:5.1f}%  {src[:80]}")
 
 
