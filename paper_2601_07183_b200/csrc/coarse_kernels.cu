@@ -315,6 +315,31 @@ __device__ void warp_sort_u64(uint64_t* a, int n) {
   }
 }
 
+// a[0, n) holds n / run sorted (ascending) runs of length run (powers of 2):
+// merge them with the flip + half-cleaner network (log2(n/run) rounds instead
+// of a full bitonic sort)
+__device__ void warp_merge_runs(uint64_t* a, int run, int n) {
+  const int lane = lane_id();
+  for (int size = 2 * run; size <= n; size <<= 1) {
+    const int hs = size >> 1;
+    for (int i = lane; i < (n >> 1); i += 32) {  // flip: (j, size-1-j) of each block
+      const int b = i / hs, j = i - b * hs;
+      const int lo = b * size + j, hi = b * size + size - 1 - j;
+      const uint64_t x = a[lo], y = a[hi];
+      if (x > y) { a[lo] = y; a[hi] = x; }
+    }
+    __syncwarp();
+    for (int stride = size >> 2; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (n >> 1); i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const uint64_t x = a[lo], y = a[hi];
+        if (x > y) { a[lo] = y; a[hi] = x; }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __device__ void warp_sort_pairs2(uint64_t* k, uint32_t* id, int n) {
   const int lane = lane_id();
   for (int size = 2; size <= n; size <<= 1) {
@@ -347,6 +372,8 @@ struct CertArgs {
   double cmax;
   int npow_c, npow_w;
   int capped_kr;       // > 0: capped register lists of this length (see launcher)
+  int sorted_kr;       // > 0: the split lists are sorted, of this length (register path)
+  int run;             // their padded length in keys[] (power of 2)
   int32_t* out_idx;
   int32_t* l1;
   int32_t* l2;
@@ -374,16 +401,33 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
   const int tot = a.S * a.Wout;
   for (int64_t r = (int64_t)blockIdx.x * CT_WARPS + warp; r < a.rows;
        r += (int64_t)gridDim.x * CT_WARPS) {
-    for (int i = lane; i < a.npow_c; i += 32) {
-      uint64_t k = kKeyInf;
-      if (i < tot) {
-        const uint32_t id = a.ids[r * tot + i];
-        if (id != 0xFFFFFFFFu) k = ((uint64_t)ord_f32(a.vals[r * tot + i]) << 32) | id;
+    if (a.sorted_kr > 0) {
+      // register path: every (split, half) list is sorted by (g, l) -- merge
+      for (int i = lane; i < a.npow_c; i += 32) {
+        const int g = i / a.run, j = i - g * a.run;
+        uint64_t k = kKeyInf;
+        if (j < a.sorted_kr && g * a.sorted_kr < tot) {
+          const int e = g * a.sorted_kr + j;
+          const uint32_t id = a.ids[r * tot + e];
+          const float v = a.vals[r * tot + e];  // -0 as +0: the lists were built with float compares
+          if (id != 0xFFFFFFFFu) k = ((uint64_t)ord_f32(v == 0.0f ? 0.0f : v) << 32) | id;
+        }
+        keys[i] = k;
       }
-      keys[i] = k;
+      __syncwarp();
+      warp_merge_runs(keys, a.run, a.npow_c);
+    } else {
+      for (int i = lane; i < a.npow_c; i += 32) {
+        uint64_t k = kKeyInf;
+        if (i < tot) {
+          const uint32_t id = a.ids[r * tot + i];
+          if (id != 0xFFFFFFFFu) k = ((uint64_t)ord_f32(a.vals[r * tot + i]) << 32) | id;
+        }
+        keys[i] = k;
+      }
+      __syncwarp();
+      warp_sort_u64(keys, a.npow_c);
     }
-    __syncwarp();
-    warp_sort_u64(keys, a.npow_c);
     float gnext = all ? 0.0f : unord_f32((uint32_t)(keys[W] >> 32));
     if (!all && a.capped_kr > 0) {
       // bound from the capped lists: min over full lists of their largest kept value
@@ -665,7 +709,11 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys
     const int tps = (int)ceil_div(ntiles, nsplit);
     nsplit = (int)ceil_div(ntiles, tps);
-    const int npow_c = next_pow2(std::max(nsplit * Wout, 2));
+    // register path: nsplit * FT_HALVES sorted lists of KR, each padded to a
+    // power-of-2 run, merged in K2; shared-memory path: unsorted, fully sorted
+    const int run = next_pow2(KR);
+    const int npow_c = reg ? next_pow2(std::max(nsplit * FT_HALVES, 1) * run)
+                           : next_pow2(std::max(nsplit * Wout, 2));
     const size_t csmem = (size_t)CT_WARPS * ((size_t)npow_c * 8 + (size_t)npow_w * 12);
     if (csmem > 220 * 1024) {
       set_error("coarse certify: shared memory budget exceeded");
@@ -736,6 +784,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ca.cmax = idx->cmax;
     ca.npow_c = npow_c;
     ca.capped_kr = capped ? KR : 0;
+    ca.sorted_kr = reg ? KR : 0;
+    ca.run = run;
     ca.npow_w = npow_w;
     ca.out_idx = out_idx ? out_idx + r0 * L : nullptr;
     ca.l1 = l1 ? l1 + r0 : nullptr;
