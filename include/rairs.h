@@ -88,6 +88,7 @@ typedef struct {
   int32_t shard_id, nshards;
   int64_t device_bytes; /* index memory on the device */
   int64_t n_live;       /* rows not deleted (n counts every row ever inserted) */
+  int32_t has_ids;      /* 1: the index holds caller-supplied ids (see build) */
 } rairs_index_info;
 
 /* ---- training (B1/B3; not part of the bit-exact contract) ----------------
@@ -103,14 +104,20 @@ rairs_status rairs_train(const float* base, int64_t n, int32_t d,
  * [nlist x d]; codebook: dev [M x 16 x d/M].  Assignment (fp64, O4) and PQ
  * encoding (fp64, O5) are bit-exact functions of (base, centroids, codebook).
  * The raw rows are copied into the index (refine store).
- * Errors: n < 1, d < 1, nlist > n or > 65536, d % M, nbits != 4, n > 2^30. */
-rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
+ * ids: dev [n] int64 caller-supplied vector ids (SPEC's VectorSet ids),
+ * or NULL: then row r of shard s has id r * nshards + s.  Caller ids must be
+ * unique and in [0, 2^32 - 2]; they are what searches return and what
+ * rairs_remove_ids takes.  Ties in the exact distance are broken by the id
+ * returned; the candidate stage breaks score ties by insertion order (R5).
+ * Errors: n < 1, d < 1, nlist > n or > 65536, d % M, nbits != 4, n > 2^30;
+ * ids out of range or duplicated (INVALID, nothing allocated). */
+rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, const int64_t* ids,
                                       const float* centroids, const float* codebook,
                                       const rairs_build_params* p, void* stream,
                                       rairs_index_t* out);
 
-/* rairs_train + rairs_build_from_trained. */
-rairs_status rairs_build_index(const float* base, int64_t n, int32_t d,
+/* rairs_train + rairs_build_from_trained (ids: as above). */
+rairs_status rairs_build_index(const float* base, int64_t n, int32_t d, const int64_t* ids,
                                const rairs_build_params* p, void* stream,
                                rairs_index_t* out);
 
@@ -128,12 +135,16 @@ rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out);
  * DCO -- is the same as for an index built over all live rows at once).
  * x is copied; the caller keeps ownership. Row storage grows by >= 1/8.
  * Synchronises the device first: no search may run on this index concurrently.
- * Errors: n_add < 0, x not a device pointer (INVALID); > 2^30 rows per shard or
- * global ids >= 2^32 (UNSUPPORTED); OOM (the index is unchanged). */
-rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, int64_t* first_id,
-                       void* stream);
+ * ids: dev [n_add] int64 caller ids of the new rows -- required when the index
+ * was built with ids (unique, not yet held, in [0, 2^32 - 2]), NULL otherwise.
+ * Errors: n_add < 0, x not a device pointer, ids given / missing / invalid
+ * (INVALID); > 2^30 rows per shard or global ids >= 2^32 (UNSUPPORTED); OOM
+ * (the index is unchanged). */
+rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, const int64_t* ids,
+                       int64_t* first_id, void* stream);
 
-/* Delete by global id: ids is a dev [n_ids] int64 array; ids this
+/* Delete by id: ids is a dev [n_ids] int64 array of the ids the
+ * index returns (caller ids if it was built with them, else global ids); ids this
  * shard does not hold (id % nshards != shard_id, or beyond its rows) and ids
  * already deleted are ignored. *n_removed (host, optional) = rows deleted now.
  * Deleted rows leave the layout (no tombstone is ever scored: DCO, U(q) and

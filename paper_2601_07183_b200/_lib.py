@@ -47,7 +47,7 @@ class IndexInfo(ctypes.Structure):
     _fields_ = [("n", _I64), ("d", _I32), ("nlist", _I32), ("M", _I32), ("M_pad", _I32),
                 ("n_slots", _I64), ("n_cells", _I64), ("n_refs", _I64), ("n_double", _I64),
                 ("max_refs_per_list", _I32), ("shard_id", _I32), ("nshards", _I32),
-                ("device_bytes", _I64), ("n_live", _I64)]
+                ("device_bytes", _I64), ("n_live", _I64), ("has_ids", _I32)]
 
 
 class RairsError(RuntimeError):
@@ -85,8 +85,8 @@ def lib() -> ctypes.CDLL:
     PP = ctypes.POINTER(BuildParams)
     sigs = {
         "rairs_train": [_P, _I64, _I32, PP, _P, _P, _P],
-        "rairs_build_from_trained": [_P, _I64, _I32, _P, _P, PP, _P, ctypes.POINTER(_P)],
-        "rairs_build_index": [_P, _I64, _I32, PP, _P, ctypes.POINTER(_P)],
+        "rairs_build_from_trained": [_P, _I64, _I32, _P, _P, _P, PP, _P, ctypes.POINTER(_P)],
+        "rairs_build_index": [_P, _I64, _I32, _P, PP, _P, ctypes.POINTER(_P)],
         "rairs_index_free": [_P],
         "rairs_index_get_info": [_P, ctypes.POINTER(IndexInfo)],
         "rairs_search": [_P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],
@@ -104,7 +104,7 @@ def lib() -> ctypes.CDLL:
         "rairs_set_scan_mode": [_P, _I32],
         "rairs_profile_kernels": [_P, _P, _I32],
         "rairs_search_plan": [_P, _I64, _I32, _I32, _I32, _P, _P],
-        "rairs_add": [_P, _P, _I64, _P, _P],
+        "rairs_add": [_P, _P, _I64, _P, _P, _P],
         "rairs_remove_ids": [_P, _P, _I64, _P, _P],
     }
     for name, args in sigs.items():

@@ -109,6 +109,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
   cudaFree(x->live_bits);
+  cudaFree(x->labels); cudaFree(x->lab_sorted); cudaFree(x->lab_rows);
   for (auto& st : x->aux) if (st) cudaStreamDestroy(st);
   for (auto& e : x->aux_ev) if (e) cudaEventDestroy(e);
   if (x->h2d) cudaStreamDestroy(x->h2d);
@@ -363,7 +364,7 @@ static rairs_status assign_rows(rairs_index_s* idx, int64_t row0, int64_t cnt, c
   return launch_probe_exact(pa, s);
 }
 
-rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
+rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, const int64_t* ids,
                                       const float* centroids, const float* codebook,
                                       const rairs_build_params* p, void* stream,
                                       rairs_index_t* out) {
@@ -372,7 +373,9 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   REQUIRE_DEV(base, "base");
   REQUIRE_DEV(centroids, "centroids");
   REQUIRE_DEV(codebook, "codebook");
+  OPTIONAL_DEV(ids, "ids");
   cudaStream_t s = (cudaStream_t)stream;
+  if (ids) RAIRS_TRY(labels_validate(nullptr, ids, n, s));  // before any index state exists
   rairs_index_s* idx = new (std::nothrow) rairs_index_s();
   if (!idx) return RAIRS_E_OOM;
   {
@@ -414,6 +417,12 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   B_TRY(cudaMemcpyAsync(idx->centroids, centroids, (size_t)p->nlist * d * 4, cudaMemcpyDeviceToDevice, s));
   B_TRY(cudaMemcpyAsync(idx->codebook, codebook, cb_bytes, cudaMemcpyDeviceToDevice, s));
   B_TRY(cudaMemcpyAsync(idx->X, base, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, s));
+  if (ids) {
+    B_TRY(cudaMalloc(&idx->labels, (size_t)n * 4));
+    idx->device_bytes += n * 12;  // labels + the sorted (label, row) table
+    st = labels_store(idx, ids, 0, n, s);
+    if (st != RAIRS_OK) return fail(st);
+  }
   st = coarse_prepare(idx, s);
   if (st != RAIRS_OK) return fail(st);
   B_TRY(cudaMalloc(&idx->certify_fallbacks, sizeof(unsigned)));
@@ -432,11 +441,13 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d,
   return RAIRS_OK;
 }
 
-rairs_status rairs_build_index(const float* base, int64_t n, int32_t d,
+rairs_status rairs_build_index(const float* base, int64_t n, int32_t d, const int64_t* ids,
                                const rairs_build_params* p, void* stream, rairs_index_t* out) {
   RAIRS_TRY(validate_params(p, n, d));
   if (p->nlist > n) return invalid("nlist must be <= n");
   REQUIRE_DEV(base, "base");
+  OPTIONAL_DEV(ids, "ids");
+  if (ids) RAIRS_TRY(labels_validate(nullptr, ids, n, (cudaStream_t)stream));
   cudaStream_t s = (cudaStream_t)stream;
   float *c = nullptr, *cb = nullptr;
   RAIRS_CUDA_TRY(cudaMalloc(&c, (size_t)p->nlist * d * 4));
@@ -447,7 +458,7 @@ rairs_status rairs_build_index(const float* base, int64_t n, int32_t d,
     return RAIRS_E_OOM;
   }
   rairs_status st = rairs_train(base, n, d, p, stream, c, cb);
-  if (st == RAIRS_OK) st = rairs_build_from_trained(base, n, d, c, cb, p, stream, out);
+  if (st == RAIRS_OK) st = rairs_build_from_trained(base, n, d, ids, c, cb, p, stream, out);
   cudaStreamSynchronize(s);
   cudaFree(c);
   cudaFree(cb);
@@ -477,6 +488,7 @@ rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out) {
   out->nshards = idx->nshards;
   out->device_bytes = idx->device_bytes;
   out->n_live = idx->n_live;
+  out->has_ids = idx->labels != nullptr;
   return RAIRS_OK;
 }
 
@@ -537,6 +549,11 @@ static rairs_status grow_rows(rairs_index_s* idx, int64_t need, cudaStream_t s) 
   if ((e = cudaMalloc(&l1, (size_t)cap * 4)) != cudaSuccess) return undo(e);
   if ((e = cudaMalloc(&l2, (size_t)cap * 4)) != cudaSuccess) return undo(e);
   if (idx->live_bits && (e = cudaMalloc(&bits, (size_t)(cap + 31) / 32 * 4)) != cudaSuccess) return undo(e);
+  uint32_t* lab = nullptr;
+  if (idx->labels && (e = cudaMalloc(&lab, (size_t)cap * 4)) != cudaSuccess) {
+    cudaFree(lab);
+    return undo(e);
+  }
   cudaMemcpyAsync(X, idx->X, (size_t)idx->n * d * 4, cudaMemcpyDeviceToDevice, s);
   cudaMemcpyAsync(l1, idx->l1, (size_t)idx->n * 4, cudaMemcpyDeviceToDevice, s);
   cudaMemcpyAsync(l2, idx->l2, (size_t)idx->n * 4, cudaMemcpyDeviceToDevice, s);
@@ -545,17 +562,23 @@ static rairs_status grow_rows(rairs_index_s* idx, int64_t need, cudaStream_t s) 
     cudaMemcpyAsync(bits, idx->live_bits, (size_t)(idx->cap_rows + 31) / 32 * 4,
                     cudaMemcpyDeviceToDevice, s);
   }
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return undo(e);
+  if (lab) cudaMemcpyAsync(lab, idx->labels, (size_t)idx->n * 4, cudaMemcpyDeviceToDevice, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
+    cudaFree(lab);
+    return undo(e);
+  }
   cudaFree(idx->X); cudaFree(idx->l1); cudaFree(idx->l2); cudaFree(idx->live_bits);
-  idx->X = X; idx->l1 = l1; idx->l2 = l2; idx->live_bits = bits;
+  cudaFree(idx->labels);
+  idx->X = X; idx->l1 = l1; idx->l2 = l2; idx->live_bits = bits; idx->labels = lab;
+  if (lab) idx->device_bytes += (cap - idx->cap_rows) * 4;
   idx->device_bytes += (cap - idx->cap_rows) * ((int64_t)d * 4 + 8) +
                        (bits ? ((cap + 31) / 32 - (idx->cap_rows + 31) / 32) * 4 : 0);
   idx->cap_rows = cap;
   return RAIRS_OK;
 }
 
-rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, int64_t* first_id,
-                       void* stream) {
+rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, const int64_t* ids,
+                       int64_t* first_id, void* stream) {
   if (!idx) return invalid("index is NULL");
   if (n_add < 0) return invalid("n_add must be >= 0");
   if (n_add == 0) {
@@ -563,6 +586,11 @@ rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, int64_t
     return RAIRS_OK;
   }
   REQUIRE_DEV(x, "x");
+  OPTIONAL_DEV(ids, "ids");
+  if ((ids != nullptr) != (idx->labels != nullptr))
+    return invalid(idx->labels ? "this index holds caller ids: pass ids for the new rows"
+                               : "this index numbers its rows itself: ids must be NULL");
+  if (ids) RAIRS_TRY(labels_validate(idx, ids, n_add, (cudaStream_t)stream));
   const int64_t n_new = idx->n + n_add;
   if (n_new >= (1ll << 30)) {
     set_error("more than 2^30 rows per shard is not supported");
@@ -582,6 +610,7 @@ rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, int64_t
     live_set_range_kernel<<<grid_for(n_add), 256, 0, s>>>(idx->live_bits, r0, n_new);
     RAIRS_CHECK_LAUNCH();
   }
+  if (ids) RAIRS_TRY(labels_store(idx, ids, r0, n_add, s));
   // new rows: Alg. 3 assignment (lines 1-12) with the index's trained centroids
   RAIRS_TRY(assign_rows(idx, r0, n_add, s));
   idx->n = n_new;
@@ -609,11 +638,17 @@ rairs_status rairs_remove_ids(rairs_index_t idx, const int64_t* ids, int64_t n_i
     idx->device_bytes += words * 4;
   }
   unsigned long long* cnt = nullptr;
+  int64_t* gids = nullptr;
+  if (idx->labels) {  // caller ids -> internal global ids
+    RAIRS_CUDA_TRY(cudaMallocAsync(&gids, (size_t)n_ids * 8, s));
+    RAIRS_TRY(labels_to_gids(idx, ids, n_ids, gids, s));
+  }
   RAIRS_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
   RAIRS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
-  remove_ids_kernel<<<grid_for(n_ids), 256, 0, s>>>(ids, n_ids, idx->shard_id, idx->nshards, idx->n,
-                                                    idx->live_bits, cnt);
+  remove_ids_kernel<<<grid_for(n_ids), 256, 0, s>>>(gids ? gids : ids, n_ids, idx->shard_id,
+                                                    idx->nshards, idx->n, idx->live_bits, cnt);
   RAIRS_CHECK_LAUNCH();
+  if (gids) cudaFreeAsync(gids, s);
   unsigned long long h = 0;
   RAIRS_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
   cudaFreeAsync(cnt, s);

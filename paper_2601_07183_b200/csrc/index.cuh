@@ -20,6 +20,12 @@ struct rairs_index_s {
   // deletion tombstones (NEXT-3): bit r of live_bits[r/32] = row r is live;
   // NULL until the first rairs_remove_ids (then every row < n is live)
   uint32_t* live_bits = nullptr;
+  // caller-supplied ids (labels.cu): labels[r] of local row r (NULL: the
+  // internal global ids r * G + shard are the ids), and the sorted
+  // (label, row) table for deletes by label
+  uint32_t* labels = nullptr;
+  uint32_t* lab_sorted = nullptr;
+  uint32_t* lab_rows = nullptr;
   int d = 0, nlist = 0, M = 0, M_pad = 0, dsub = 0;
   int shard_id = 0, nshards = 1;
   rairs_build_params params{};
@@ -115,6 +121,15 @@ rairs_status export_codes(const rairs_index_s* idx, uint8_t* codes, cudaStream_t
 rairs_status export_layout64(const rairs_index_s* idx, int64_t* own_off, int64_t* own_cnt,
                              int64_t* ref_ptr, int32_t* ref_owner, int64_t* ref_start,
                              int64_t* ref_cnt, uint32_t* slot_rows, cudaStream_t s);
+
+// ---- caller-supplied ids (labels.cu) -------------------------------------------
+// every id in [0, 2^32 - 2], no duplicates, none already held by idx (idx may be NULL)
+rairs_status labels_validate(const rairs_index_s* idx, const int64_t* ids, int64_t m, cudaStream_t s);
+// labels[row0 .. row0+m) = ids, then rebuild the sorted (label, row) table
+rairs_status labels_store(rairs_index_s* idx, const int64_t* ids, int64_t row0, int64_t m, cudaStream_t s);
+// labels -> internal global ids (-1 if not held)
+rairs_status labels_to_gids(const rairs_index_s* idx, const int64_t* ids, int64_t m, int64_t* gids,
+                            cudaStream_t s);
 
 // ---- coarse stage (coarse_kernels.cu) ---------------------------------------
 rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s);

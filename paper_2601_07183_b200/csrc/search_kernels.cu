@@ -577,6 +577,7 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
                                                     int64_t nq, int bigK, int npow, int k,
                                                     const float* __restrict__ queries,
                                                     const float* __restrict__ X, int d, int G,
+                                                    const uint32_t* __restrict__ labels,
                                                     int64_t* __restrict__ out_ids,
                                                     float* __restrict__ out_dists) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
       uint64_t out = kKeyInf;
       if (key != kKeyInf) {
         const float dist = __double2float_rn(acc);
-        out = ((uint64_t)__float_as_uint(dist) << 32) | gid;
+        out = ((uint64_t)__float_as_uint(dist) << 32) | (labels ? labels[gid / (uint32_t)G] : gid);
       }
       if (c < npow) rk[c] = out;
     }
@@ -666,7 +667,8 @@ template <int D4>
 __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     const uint64_t* __restrict__ keys, int64_t nq, int bigK, int k,
     const float* __restrict__ queries, const float* __restrict__ X, int G,
-    int64_t* __restrict__ out_ids, float* __restrict__ out_dists) {
+    const uint32_t* __restrict__ labels, int64_t* __restrict__ out_ids,
+    float* __restrict__ out_dists) {
   constexpr int D = 4 * D4, RSF = D + 4;  // tile row stride (floats): conflict-free float4 reads
   extern __shared__ __align__(16) float tile[];  // [min(bigK, 128) rounded to 8][RSF]
   __shared__ double qs[D];
@@ -748,7 +750,8 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
           df = __dsub_rn(qs[4 * i + 2], (double)xv.z); acc = __dadd_rn(acc, __dmul_rn(df, df));
           df = __dsub_rn(qs[4 * i + 3], (double)xv.w); acc = __dadd_rn(acc, __dmul_rn(df, df));
         }
-        out = ((uint64_t)__float_as_uint(__double2float_rn(acc)) << 32) | g;
+        out = ((uint64_t)__float_as_uint(__double2float_rn(acc)) << 32) |
+              (labels ? labels[g / (uint32_t)G] : g);  // results carry the caller's ids
         atomicAdd(&nvalid, 1u);
       }
       rk[c * RS_ROWS + tid] = out;
@@ -791,8 +794,8 @@ static rairs_status launch_refine_stage(const rairs_index_s* idx, const SearchAr
                                                                RS_THREADS, smem));
   const int grid = (int)std::min<int64_t>(a.nq, (int64_t)148 * std::max(occ, 1));
   refine_stage_kernel<D4><<<grid, RS_THREADS, smem, s>>>(a.cand_keys, a.nq, bigK, a.k, a.queries,
-                                                          idx->X, idx->nshards, a.out_ids,
-                                                          a.out_dists);
+                                                          idx->X, idx->nshards, idx->labels,
+                                                          a.out_ids, a.out_dists);
   RAIRS_CHECK_LAUNCH();
   return RAIRS_OK;
 }
@@ -822,7 +825,7 @@ rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaSt
                                       (int)smem));
   const int grid = (int)std::min<int64_t>(a.nq, 1 << 30);
   refine_kernel<<<grid, RT, smem, s>>>(a.cand_keys, a.nq, bigK, npow, a.k, a.queries, idx->X,
-                                        idx->d, idx->nshards, a.out_ids, a.out_dists);
+                                        idx->d, idx->nshards, idx->labels, a.out_ids, a.out_dists);
   RAIRS_CHECK_LAUNCH();
   return RAIRS_OK;
 }

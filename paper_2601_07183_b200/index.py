@@ -21,6 +21,15 @@ def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
     return t.detach().to(torch.float32).contiguous()
 
 
+def _dev_ids(ids: Optional[torch.Tensor], n: int, device) -> Optional[torch.Tensor]:
+    if ids is None:
+        return None
+    t = torch.as_tensor(ids).to(device=device, dtype=torch.int64).contiguous()
+    if t.dim() != 1 or t.shape[0] != n:
+        raise ValueError(f"ids must be a 1-D tensor of {n} ids")
+    return t
+
+
 def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -79,18 +88,21 @@ class Index:
     @staticmethod
     def build(base: torch.Tensor, nlist: int, M: int, nbits: int = 4, assignment: str = "AIR",
               centroids: Optional[torch.Tensor] = None, codebook: Optional[torch.Tensor] = None,
-              **kw) -> "Index":
+              ids: Optional[torch.Tensor] = None, **kw) -> "Index":
+        """ids: optional [n] int64 caller ids (unique, in [0, 2^32 - 2]); searches
+        then return them and remove_ids takes them."""
         base = _dev_f32(base, "base")
         n, d = base.shape
         p = make_params(nlist, M, nbits=nbits, assignment=assignment, **kw)
         h = ctypes.c_void_p()
+        idt = _dev_ids(ids, n, base.device)
         if centroids is None and codebook is None:
-            check(lib().rairs_build_index(_ptr(base), n, d, ctypes.byref(p), _stream(),
+            check(lib().rairs_build_index(_ptr(base), n, d, _ptr(idt), ctypes.byref(p), _stream(),
                                           ctypes.byref(h)), "rairs_build_index")
         else:
             cent = _dev_f32(centroids, "centroids")
             cb = _dev_f32(codebook, "codebook")
-            check(lib().rairs_build_from_trained(_ptr(base), n, d, _ptr(cent), _ptr(cb),
+            check(lib().rairs_build_from_trained(_ptr(base), n, d, _ptr(idt), _ptr(cent), _ptr(cb),
                                                  ctypes.byref(p), _stream(), ctypes.byref(h)),
                   "rairs_build_from_trained")
         return Index(h, base.device)
@@ -112,15 +124,17 @@ class Index:
         return {f: getattr(inf, f) for f, _ in IndexInfo._fields_}
 
     # ---------------------------------------------------------- updates
-    def add(self, x: torch.Tensor) -> int:
+    def add(self, x: torch.Tensor, ids: Optional[torch.Tensor] = None) -> int:
         """Insert a batch (rairs_add); returns the global id of its first row
-        (row i gets first_id + i * nshards)."""
+        (row i gets first_id + i * nshards). ids: the new rows' caller ids,
+        required iff the index was built with ids."""
         xx = _dev_f32(x, "x")
         if xx.shape[1] != self.d:
             raise ValueError(f"x must be [n, {self.d}]")
+        idt = _dev_ids(ids, xx.shape[0], xx.device)
         first = ctypes.c_int64(0)
-        check(lib().rairs_add(self._h, _ptr(xx), xx.shape[0], ctypes.byref(first), _stream()),
-              "rairs_add")
+        check(lib().rairs_add(self._h, _ptr(xx), xx.shape[0], _ptr(idt), ctypes.byref(first),
+                              _stream()), "rairs_add")
         self.n = self.info()["n"]
         return int(first.value)
 

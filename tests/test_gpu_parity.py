@@ -623,3 +623,39 @@ def test_search_host_chunked_h2d(oracle_mod):
     o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, Q[rows], 10, 4, 10)
     assert np.array_equal(hi[rows], o["ids"])
     idx.free()
+
+
+def test_caller_ids(oracle_mod):
+    # SURVEY §8(b) `ids`: caller-supplied vector ids are returned by searches
+    # and taken by deletes; invalid ids are rejected before any mutation
+    c = case(oracle_mod, "c1s")
+    n = c.X.shape[0]
+    n0 = n - 500
+    rng = np.random.default_rng(9)
+    lab = rng.choice(2**32 - 1, size=n, replace=False).astype(np.int64)
+    idx = rb.Index.build(_t(c.X[:n0]), c.spec.nlist, c.spec.M, assignment="AIR",
+                         centroids=_t(c.cent), codebook=_t(c.cb), ids=_t(lab[:n0]))
+    assert idx.info()["has_ids"] == 1
+    with pytest.raises(rb.RairsError):                      # a held id
+        idx.add(_t(c.X[n0:]), ids=_t(np.r_[lab[n0:-1], lab[0]]))
+    with pytest.raises(rb.RairsError):                      # ids required
+        idx.add(_t(c.X[n0:]))
+    assert idx.info()["n"] == n0                            # unchanged
+    idx.add(_t(c.X[n0:]), ids=_t(lab[n0:]))
+    dead = rng.choice(n, size=n // 10, replace=False)
+    assert idx.remove_ids(torch.from_numpy(lab[dead])) == dead.size
+    unknown = np.setdiff1d(np.arange(n, dtype=np.int64), lab)
+    assert idx.remove_ids(torch.from_numpy(unknown)) == 0   # ids the index does not hold
+    live = np.ones(n, bool)
+    live[dead] = False
+    rows = np.nonzero(live)[0]
+    o = _oracle_on_rows(oracle_mod, c, rows, c.Q, 10, 8, 4)
+    ids, dists = idx.search(_t(c.Q), 10, 8, 4)
+    ids, dists = ids.cpu().numpy(), dists.cpu().numpy()
+    want = np.where(o["ids"] >= 0, lab[np.maximum(o["ids"], 0)], -1)
+    assert np.array_equal(ids, want) and np.array_equal(dists, o["dists"])
+    idx.free()
+    for bad in (np.r_[lab[:n0 - 1], lab[0]], np.r_[lab[:n0 - 1], -5], np.r_[lab[:n0 - 1], 2**32 - 1]):
+        with pytest.raises(rb.RairsError):
+            rb.Index.build(_t(c.X[:n0]), c.spec.nlist, c.spec.M, centroids=_t(c.cent),
+                           codebook=_t(c.cb), ids=_t(bad))
