@@ -223,6 +223,19 @@ rairs_status rairs_export_layout(rairs_index_t idx, int64_t* own_off, int64_t* o
 rairs_status rairs_set_coarse_mode(rairs_index_t idx, int32_t mode);
 rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t reset);
 
+/* Search statistics since the index was built or last reset (SURVEY §8(b)
+ * rairs_stats): searches and queries run, items scored (DCO, O12 / R17, summed
+ * over queries and shards' calls on this index), candidates refined (exact
+ * distances computed, A7), queries whose coarse stage fell back to the exact
+ * kernel, and stage times in ms (CUDA events; 0 unless rairs_profile_enable).
+ * Synchronises the device.  reset != 0 zeroes everything after reading. */
+typedef struct {
+  int64_t searches, queries;
+  int64_t dco_total, refine_total, certify_fallbacks;
+  double ms_coarse, ms_scan, ms_refine;
+} rairs_stats;
+rairs_status rairs_get_stats(rairs_index_t idx, rairs_stats* out, int32_t reset);
+
 /* ---- scan mode --------------------------------------------------------------
  * 0 = auto (list-major tensor-core scan when supported), 1 = query-major SIMT
  * fast scan (one CTA per query, shared-memory LUT lookups), 2 = list-major:

@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = [
     "rairs_export_assignment", "rairs_export_layout", "rairs_profile_enable",
     "rairs_profile_read", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
     "rairs_certify_fallbacks", "rairs_set_scan_mode", "rairs_profile_kernels",
-    "rairs_search_plan", "rairs_add", "rairs_remove_ids",
+    "rairs_search_plan", "rairs_add", "rairs_remove_ids", "rairs_get_stats",
 ]
 
 
@@ -48,6 +48,12 @@ class IndexInfo(ctypes.Structure):
                 ("n_slots", _I64), ("n_cells", _I64), ("n_refs", _I64), ("n_double", _I64),
                 ("max_refs_per_list", _I32), ("shard_id", _I32), ("nshards", _I32),
                 ("device_bytes", _I64), ("n_live", _I64), ("has_ids", _I32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("searches", _I64), ("queries", _I64), ("dco_total", _I64), ("refine_total", _I64),
+                ("certify_fallbacks", _I64), ("ms_coarse", ctypes.c_double),
+                ("ms_scan", ctypes.c_double), ("ms_refine", ctypes.c_double)]
 
 
 class RairsError(RuntimeError):
@@ -106,6 +112,7 @@ def lib() -> ctypes.CDLL:
         "rairs_search_plan": [_P, _I64, _I32, _I32, _I32, _P, _P],
         "rairs_add": [_P, _P, _I64, _P, _P, _P],
         "rairs_remove_ids": [_P, _P, _I64, _P, _P],
+        "rairs_get_stats": [_P, ctypes.POINTER(Stats), _I32],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

@@ -106,7 +106,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->centroids); cudaFree(x->codebook); cudaFree(x->X); cudaFree(x->l1); cudaFree(x->l2);
   cudaFree(x->codes); cudaFree(x->slot_rows); cudaFree(x->own_off); cudaFree(x->own_cnt);
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
-  cudaFree(x->cnorm); cudaFree(x->certify_fallbacks);
+  cudaFree(x->cnorm); cudaFree(x->certify_fallbacks); cudaFree(x->counters);
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
   cudaFree(x->live_bits);
   cudaFree(x->labels); cudaFree(x->lab_sorted); cudaFree(x->lab_rows);
@@ -178,6 +178,9 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   a.lut_b = lut_b;
   a.out_ids = out_ids;
   a.out_dists = out_dists;
+  a.counters = idx->counters;
+  idx->n_searches += 1;
+  idx->n_queries += nq;
 
   StageEvents ev(idx, s);
   rairs_status st = RAIRS_OK;
@@ -427,6 +430,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, c
   if (st != RAIRS_OK) return fail(st);
   B_TRY(cudaMalloc(&idx->certify_fallbacks, sizeof(unsigned)));
   B_TRY(cudaMemsetAsync(idx->certify_fallbacks, 0, sizeof(unsigned), s));
+  B_TRY(cudaMalloc(&idx->counters, 2 * sizeof(unsigned long long)));
+  B_TRY(cudaMemsetAsync(idx->counters, 0, 2 * sizeof(unsigned long long), s));
   // Alg. 3 RairAssign (AIR / SOARL2) or single assignment, exact fp64 (O4)
   st = assign_rows(idx, 0, n, s);
   if (st != RAIRS_OK) return fail(st);
@@ -821,6 +826,32 @@ rairs_status rairs_certify_fallbacks(rairs_index_t idx, int64_t* count, int32_t 
   RAIRS_CUDA_TRY(cudaMemcpy(&v, idx->certify_fallbacks, sizeof(unsigned), cudaMemcpyDeviceToHost));
   *count = v;
   if (reset) RAIRS_CUDA_TRY(cudaMemset(idx->certify_fallbacks, 0, sizeof(unsigned)));
+  return RAIRS_OK;
+}
+
+rairs_status rairs_get_stats(rairs_index_t idx, rairs_stats* out, int32_t reset) {
+  if (!idx || !out) return invalid("NULL argument");
+  RAIRS_CUDA_TRY(cudaDeviceSynchronize());
+  unsigned long long c[2] = {0, 0};
+  unsigned fb = 0;
+  RAIRS_CUDA_TRY(cudaMemcpy(c, idx->counters, sizeof(c), cudaMemcpyDeviceToHost));
+  RAIRS_CUDA_TRY(cudaMemcpy(&fb, idx->certify_fallbacks, sizeof(fb), cudaMemcpyDeviceToHost));
+  double ms[3] = {0, 0, 0};
+  RAIRS_TRY(rairs_profile_read(idx, ms, nullptr, 0));
+  out->searches = idx->n_searches;
+  out->queries = idx->n_queries;
+  out->dco_total = (int64_t)c[0];
+  out->refine_total = (int64_t)c[1];
+  out->certify_fallbacks = fb;
+  out->ms_coarse = ms[0];
+  out->ms_scan = ms[1];
+  out->ms_refine = ms[2];
+  if (reset) {
+    RAIRS_CUDA_TRY(cudaMemset(idx->counters, 0, sizeof(c)));
+    RAIRS_CUDA_TRY(cudaMemset(idx->certify_fallbacks, 0, sizeof(unsigned)));
+    RAIRS_TRY(rairs_profile_read(idx, nullptr, nullptr, 1));
+    idx->n_searches = idx->n_queries = 0;
+  }
   return RAIRS_OK;
 }
 

@@ -55,6 +55,10 @@ struct rairs_index_s {
   double cmax = 0.0;
   int coarse_mode = 0;
   unsigned* certify_fallbacks = nullptr;  // device counter
+  // rairs_get_stats: device counters [0] items scored (DCO), [1] candidates
+  // refined; host counters of searches and queries
+  unsigned long long* counters = nullptr;
+  int64_t n_searches = 0, n_queries = 0;
   // list-major scan (NEXT-1): mode 0 auto / 1 SIMT query-major / 2 list-major
   int scan_mode = 0;
   uint32_t* list_items = nullptr;    // [nlist] N_l = own_cnt + sum of ref_cnt
@@ -167,6 +171,7 @@ struct SearchArgs {
   // the search stream once every query's candidates are final (stage timing)
   bool fused_refine = false;
   cudaEvent_t ev_selected = nullptr;
+  unsigned long long* counters = nullptr;  // idx->counters (DCO, refined) or NULL
   // candidate keys wanted in (s, id) order (debug outputs); otherwise each
   // query's bigK keys may be written in any order (the refine ranks them)
   bool sorted_keys = false;

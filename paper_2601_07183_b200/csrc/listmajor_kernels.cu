@@ -695,6 +695,7 @@ struct SelArgs {
   int64_t* dco;
   int64_t q0;  // first query of this launch (queries [q0, nq))
   int sorted_out;  // 1: write each query's bigK keys in (s, id) order (debug outputs)
+  unsigned long long* dco_total;  // += DCO of every query (rairs_get_stats) or NULL
 };
 
 __device__ __forceinline__ uint32_t warp_bthr(const uint32_t* hist, uint32_t bigK) {
@@ -1062,6 +1063,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
         // exactly without sorting every candidate
         if (warp_select_unordered(cand, cnt, bigK, thr, hist, a.out_keys + q * a.bigK)) {
           if (lane == 0 && a.dco) a.dco[q] = (int64_t)dco;
+          if (lane == 0 && a.dco_total) atomicAdd(a.dco_total, (unsigned long long)dco);
           __syncwarp();
           continue;
         }
@@ -1076,6 +1078,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
     const uint32_t keep = min(cnt, bigK);
     for (int e = lane; e < a.bigK; e += 32) a.out_keys[q * a.bigK + e] = ((uint32_t)e < keep) ? cand[e] : kKeyInf;
     if (lane == 0 && a.dco) a.dco[q] = (int64_t)dco;
+    if (lane == 0 && a.dco_total) atomicAdd(a.dco_total, (unsigned long long)dco);
     __syncwarp();
   }
 }
@@ -1265,6 +1268,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.out_keys = sa.cand_keys;
   sl.dco = sa.dco;
   sl.sorted_out = sa.sorted_keys ? 1 : 0;
+  sl.dco_total = sa.counters;
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
   LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
   LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));

@@ -46,6 +46,7 @@ struct ScanParams {
   int nprobe, bigK, cap, hshift;
   uint64_t* out_keys;
   int64_t* dco;
+  unsigned long long* dco_total;
   uint8_t* lut_q;
   float* lut_a;
   float* lut_b;
@@ -471,6 +472,7 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
     for (int i = tid; i < p.bigK; i += ST)
       p.out_keys[q * p.bigK + i] = (i < keep) ? cand[i] : kKeyInf;
     if (tid == 0 && p.dco) p.dco[q] = (int64_t)dco_acc;
+    if (tid == 0 && p.dco_total) atomicAdd(p.dco_total, (unsigned long long)dco_acc);
     __syncthreads();
   }
 }
@@ -541,6 +543,7 @@ rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStre
   }
   p.out_keys = a.cand_keys;
   p.dco = a.dco;
+  p.dco_total = a.counters;
   p.lut_q = a.lut_q;
   p.lut_a = a.lut_a;
   p.lut_b = a.lut_b;
@@ -578,6 +581,7 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
                                                     const float* __restrict__ queries,
                                                     const float* __restrict__ X, int d, int G,
                                                     const uint32_t* __restrict__ labels,
+                                                    unsigned long long* __restrict__ refined,
                                                     int64_t* __restrict__ out_ids,
                                                     float* __restrict__ out_dists) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -631,6 +635,7 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
       if (key != kKeyInf) {
         const float dist = __double2float_rn(acc);
         out = ((uint64_t)__float_as_uint(dist) << 32) | (labels ? labels[gid / (uint32_t)G] : gid);
+        if (refined) atomicAdd(refined, 1ull);
       }
       if (c < npow) rk[c] = out;
     }
@@ -667,8 +672,8 @@ template <int D4>
 __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     const uint64_t* __restrict__ keys, int64_t nq, int bigK, int k,
     const float* __restrict__ queries, const float* __restrict__ X, int G,
-    const uint32_t* __restrict__ labels, int64_t* __restrict__ out_ids,
-    float* __restrict__ out_dists) {
+    const uint32_t* __restrict__ labels, unsigned long long* __restrict__ refined,
+    int64_t* __restrict__ out_ids, float* __restrict__ out_dists) {
   constexpr int D = 4 * D4, RSF = D + 4;  // tile row stride (floats): conflict-free float4 reads
   extern __shared__ __align__(16) float tile[];  // [min(bigK, 128) rounded to 8][RSF]
   __shared__ double qs[D];
@@ -774,6 +779,7 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
         out_ids[q * k + i] = -1;
         out_dists[q * k + i] = __int_as_float(0x7f800000);
       }
+      if (tid == 0 && refined) atomicAdd(refined, (unsigned long long)nvalid);
       __syncthreads();  // rk / nvalid / qs free for the next query
     }
     q = qn;
@@ -795,6 +801,7 @@ static rairs_status launch_refine_stage(const rairs_index_s* idx, const SearchAr
   const int grid = (int)std::min<int64_t>(a.nq, (int64_t)148 * std::max(occ, 1));
   refine_stage_kernel<D4><<<grid, RS_THREADS, smem, s>>>(a.cand_keys, a.nq, bigK, a.k, a.queries,
                                                           idx->X, idx->nshards, idx->labels,
+                                                          a.counters ? a.counters + 1 : nullptr,
                                                           a.out_ids, a.out_dists);
   RAIRS_CHECK_LAUNCH();
   return RAIRS_OK;
@@ -825,7 +832,8 @@ rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaSt
                                       (int)smem));
   const int grid = (int)std::min<int64_t>(a.nq, 1 << 30);
   refine_kernel<<<grid, RT, smem, s>>>(a.cand_keys, a.nq, bigK, npow, a.k, a.queries, idx->X,
-                                        idx->d, idx->nshards, idx->labels, a.out_ids, a.out_dists);
+                                        idx->d, idx->nshards, idx->labels,
+                                        a.counters ? a.counters + 1 : nullptr, a.out_ids, a.out_dists);
   RAIRS_CHECK_LAUNCH();
   return RAIRS_OK;
 }

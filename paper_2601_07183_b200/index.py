@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BuildParams, IndexInfo, check, lib
+from ._lib import BuildParams, IndexInfo, Stats, check, lib
 
 
 def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
@@ -146,6 +146,13 @@ class Index:
         check(lib().rairs_remove_ids(self._h, _ptr(t), t.numel(), ctypes.byref(removed),
                                      _stream()), "rairs_remove_ids")
         return int(removed.value)
+
+    def stats(self, reset: bool = False) -> Dict[str, float]:
+        """rairs_get_stats: searches, queries, DCO and refined totals, coarse
+        fallbacks, stage ms (synchronises the device)."""
+        st = Stats()
+        check(lib().rairs_get_stats(self._h, ctypes.byref(st), int(bool(reset))), "rairs_get_stats")
+        return {f: getattr(st, f) for f, _ in Stats._fields_}
 
     # ----------------------------------------------------------- search
     def search(self, queries: torch.Tensor, k: int, nprobe: int, refine_factor: int = 10,

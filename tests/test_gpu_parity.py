@@ -659,3 +659,21 @@ def test_caller_ids(oracle_mod):
         with pytest.raises(rb.RairsError):
             rb.Index.build(_t(c.X[:n0]), c.spec.nlist, c.spec.M, centroids=_t(c.cent),
                            codebook=_t(c.cb), ids=_t(bad))
+
+
+def test_search_stats(oracle_mod):
+    # rairs_get_stats (SURVEY §8(b) rairs_stats): DCO total = the per-query DCO
+    # sum, refined = the valid candidates, on both scan paths
+    c = case(oracle_mod, "c1s")
+    idx = c.gpu_index()
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, c.Q, 10, 8, 4)
+    idx.stats(reset=True)
+    for scan in ("simt", "listmajor"):
+        idx.set_scan_mode(scan)
+        idx.search(_t(c.Q), 10, 8, 4)
+    st = idx.stats(reset=True)
+    nq = c.Q.shape[0]
+    assert st["searches"] == 2 and st["queries"] == 2 * nq
+    assert st["dco_total"] == 2 * int(o["dco"].sum())
+    assert st["refine_total"] == 2 * int(np.minimum(o["dco"][:, 0], 40).sum())
+    assert idx.stats()["dco_total"] == 0
