@@ -110,7 +110,8 @@ rairs_status rairs_train(const float* base, int64_t n, int32_t d,
  * rairs_remove_ids takes.  Ties in the exact distance are broken by the id
  * returned; the candidate stage breaks score ties by insertion order (R5).
  * Errors: n < 1, d < 1, nlist > n or > 65536, d % M, nbits != 4, n > 2^30;
- * ids out of range or duplicated (INVALID, nothing allocated). */
+ * non-finite base values or ids out of range / duplicated (INVALID,
+ * checked on the device before anything is allocated). */
 rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, const int64_t* ids,
                                       const float* centroids, const float* codebook,
                                       const rairs_build_params* p, void* stream,
@@ -137,8 +138,8 @@ rairs_status rairs_index_get_info(rairs_index_t idx, rairs_index_info* out);
  * Synchronises the device first: no search may run on this index concurrently.
  * ids: dev [n_add] int64 caller ids of the new rows -- required when the index
  * was built with ids (unique, not yet held, in [0, 2^32 - 2]), NULL otherwise.
- * Errors: n_add < 0, x not a device pointer, ids given / missing / invalid
- * (INVALID); > 2^30 rows per shard or global ids >= 2^32 (UNSUPPORTED); OOM
+ * Errors: n_add < 0, x not a device pointer or non-finite, ids given / missing /
+ * invalid (INVALID); > 2^30 rows per shard or global ids >= 2^32 (UNSUPPORTED); OOM
  * (the index is unchanged). */
 rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, const int64_t* ids,
                        int64_t* first_id, void* stream);

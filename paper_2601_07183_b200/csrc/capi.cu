@@ -35,6 +35,43 @@ static inline unsigned grid_for(int64_t n, int bs = 256) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, 148 * 16));
 }
 
+__global__ void nonfinite_kernel(const float4* __restrict__ x, int64_t n4, unsigned* __restrict__ bad) {
+  unsigned c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = x[i];
+    c += !isfinite(v.x) + !isfinite(v.y) + !isfinite(v.z) + !isfinite(v.w);
+  }
+  if (c) atomicAdd(bad, c);
+}
+
+__global__ void nonfinite_tail_kernel(const float* __restrict__ x, int64_t n, unsigned* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) atomicAdd(bad, 1u);
+}
+
+// RAIRS_E_INVALID if any of the `count` floats at x (device) is NaN or +-inf
+static rairs_status check_finite(const float* x, int64_t count, const char* what, cudaStream_t s) {
+  unsigned* bad = nullptr;
+  RAIRS_CUDA_TRY(cudaMallocAsync(&bad, sizeof(unsigned), s));
+  RAIRS_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
+  const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int64_t n4 = al ? count / 4 : 0;
+  if (n4 > 0) nonfinite_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(x), n4, bad);
+  if (count - 4 * n4 > 0)
+    nonfinite_tail_kernel<<<grid_for(count - 4 * n4), 256, 0, s>>>(x + 4 * n4, count - 4 * n4, bad);
+  unsigned h = 0;
+  cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(bad, s);
+  RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h) {
+    set_error(std::string(what) + " holds non-finite values");
+    return RAIRS_E_INVALID;
+  }
+  return RAIRS_OK;
+}
+
 static rairs_status invalid(const std::string& msg) {
   set_error(msg);
   return RAIRS_E_INVALID;
@@ -378,7 +415,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, c
   REQUIRE_DEV(codebook, "codebook");
   OPTIONAL_DEV(ids, "ids");
   cudaStream_t s = (cudaStream_t)stream;
-  if (ids) RAIRS_TRY(labels_validate(nullptr, ids, n, s));  // before any index state exists
+  RAIRS_TRY(check_finite(base, n * d, "base", s));            // before any index state exists
+  if (ids) RAIRS_TRY(labels_validate(nullptr, ids, n, s));
   rairs_index_s* idx = new (std::nothrow) rairs_index_s();
   if (!idx) return RAIRS_E_OOM;
   {
@@ -595,6 +633,7 @@ rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, const i
   if ((ids != nullptr) != (idx->labels != nullptr))
     return invalid(idx->labels ? "this index holds caller ids: pass ids for the new rows"
                                : "this index numbers its rows itself: ids must be NULL");
+  RAIRS_TRY(check_finite(x, n_add * idx->d, "x", (cudaStream_t)stream));
   if (ids) RAIRS_TRY(labels_validate(idx, ids, n_add, (cudaStream_t)stream));
   const int64_t n_new = idx->n + n_add;
   if (n_new >= (1ll << 30)) {

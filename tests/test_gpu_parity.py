@@ -655,6 +655,15 @@ def test_caller_ids(oracle_mod):
     want = np.where(o["ids"] >= 0, lab[np.maximum(o["ids"], 0)], -1)
     assert np.array_equal(ids, want) and np.array_equal(dists, o["dists"])
     idx.free()
+    Xb = c.X[:n0].copy()
+    Xb[7, 3] = np.nan                                       # non-finite input
+    with pytest.raises(rb.RairsError):
+        rb.Index.build(_t(Xb), c.spec.nlist, c.spec.M, centroids=_t(c.cent), codebook=_t(c.cb))
+    idx = c.gpu_index()
+    with pytest.raises(rb.RairsError):
+        idx.add(_t(np.full((3, c.X.shape[1]), np.inf, np.float32)))
+    assert idx.info()["n"] == c.X.shape[0]
+    idx.free()
     for bad in (np.r_[lab[:n0 - 1], lab[0]], np.r_[lab[:n0 - 1], -5], np.r_[lab[:n0 - 1], 2**32 - 1]):
         with pytest.raises(rb.RairsError):
             rb.Index.build(_t(c.X[:n0]), c.spec.nlist, c.spec.M, centroids=_t(c.cent),
