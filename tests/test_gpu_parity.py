@@ -686,3 +686,34 @@ def test_search_stats(oracle_mod):
     assert st["dco_total"] == 2 * int(o["dco"].sum())
     assert st["refine_total"] == 2 * int(np.minimum(o["dco"][:, 0], 40).sum())
     assert idx.stats()["dco_total"] == 0
+
+
+def test_air_seil_direction_vs_single():
+    # SURVEY §8(c) "parity unpinned" directional checks:
+    # on the paper-like c2pl data, at the first swept nprobe reaching recall
+    # 10@10 >= 0.9, AIR + SEIL needs <= 0.95x single assignment's DCO and
+    # <= 0.7x its nprobe. Same trained state for both; 2,000 queries.
+    from synth import get_config, make_dataset
+    spec = get_config("c2pl")
+    X, Q = make_dataset(spec, nq=2000)
+    Xd, Qd = _t(X), _t(Q)
+    gt_ids, gt_d = rb.exact_knn(Xd, Qd, 10)
+    air = rb.build_index(Xd, spec.nlist, spec.M, assignment="AIR")
+    cent, cb = air.export_trained()
+    single = rb.Index.build(Xd, spec.nlist, spec.M, assignment="single", centroids=cent, codebook=cb)
+
+    def first(idx):
+        for npb in (1, 2, 3, 4, 5, 6, 8, 10, 12, 16):
+            ids, dists, dco = idx.search(Qd, 10, npb, 10, return_dco=True)
+            hit = (ids[:, :, None] == gt_ids[:, None, :]).any(-1)
+            tie = (dists == gt_d[:, 9:10].float()) & (ids >= 0)
+            rec = float((hit | tie).float().mean().item())
+            if rec >= 0.9:
+                return npb, float(dco.double().mean().item())
+        raise AssertionError("recall 0.9 not reached")
+
+    (pa, da), (ps, ds) = first(air), first(single)
+    assert da <= 0.95 * ds, (pa, da, ps, ds)
+    assert pa <= 0.7 * ps, (pa, ps)
+    air.free()
+    single.free()
