@@ -234,7 +234,9 @@ static rairs_status launch_probe_R(const ProbeArgs& a, cudaStream_t s) {
   RAIRS_CUDA_TRY(cudaFuncSetAttribute(probe_exact_kernel<R>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps.total));
   int64_t groups = ceil_div(a.rows, R);
-  int grid = (int)std::min<int64_t>(groups, 148 * 8);
+  // fallback mode (only_flagged): usually no row is flagged, so a small
+  // persistent grid just scans the flags (one resident wave, no launch tail)
+  int grid = (int)std::min<int64_t>(groups, a.only_flagged ? 148 * 2 : 148 * 8);
   if (grid < 1) return RAIRS_OK;
   probe_exact_kernel<R><<<grid, PT, ps.total, s>>>(a, ps);
   RAIRS_CHECK_LAUNCH();
