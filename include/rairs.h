@@ -168,10 +168,23 @@ rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, i
                           float* out_dists, int64_t* dco, void* stream);
 
 /* Same as rairs_search with HOST buffers: copies queries host->device, runs
- * the search, copies results device->host and synchronises `stream`. */
+ * the search, copies results device->host and synchronises `stream`.  For
+ * batches of >= 4,096 queries on the tensor-core coarse path the queries are
+ * copied in chunks on the index's copy stream and each chunk's coarse stage
+ * starts as soon as it lands.  Host buffers should be pinned (page-locked). */
 rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int64_t nq,
                                int32_t k, int32_t nprobe, int32_t refine_factor,
                                int64_t* out_ids_host, float* out_dists_host, void* stream);
+
+/* rairs_search_host without the final synchronisation: everything is
+ * enqueued (results land in the host buffers once `stream` has completed the
+ * call's work); queries_host and the outputs must stay valid and untouched
+ * until then.  Back-to-back calls on one stream overlap the next batch's
+ * host->device copy with the current batch's search.  Argument errors are
+ * reported synchronously; on an error the stream is synchronised. */
+rairs_status rairs_search_host_async(rairs_index_t idx, const float* queries_host, int64_t nq,
+                                     int32_t k, int32_t nprobe, int32_t refine_factor,
+                                     int64_t* out_ids_host, float* out_dists_host, void* stream);
 
 /* Per-stage outputs for parity tests (dev pointers, any may be NULL):
  * probes [nq x nprobe] i32 (O1); lut_q [nq x M x 16] u8, lut_a/lut_b [nq] f32

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = [
     "rairs_profile_read", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
     "rairs_certify_fallbacks", "rairs_set_scan_mode", "rairs_profile_kernels",
     "rairs_search_plan", "rairs_add", "rairs_remove_ids", "rairs_get_stats",
+    "rairs_search_host_async",
 ]
 
 
@@ -97,6 +98,7 @@ def lib() -> ctypes.CDLL:
         "rairs_index_get_info": [_P, ctypes.POINTER(IndexInfo)],
         "rairs_search": [_P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],
         "rairs_search_host": [_P, _P, _I64, _I32, _I32, _I32, _P, _P, _P],
+        "rairs_search_host_async": [_P, _P, _I64, _I32, _I32, _I32, _P, _P, _P],
         "rairs_search_debug": [_P, _P, _I64, _I32, _I32, _I32] + [_P] * 10,
         "rairs_merge_topk": [_P, _P, _I32, _I64, _I32, _P, _P, _P],
         "rairs_exact_knn": [_P, _I64, _I32, _P, _I64, _I32, _P, _P, _P],

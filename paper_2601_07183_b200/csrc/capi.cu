@@ -151,6 +151,9 @@ static void free_index(rairs_index_s* x) {
   for (auto& e : x->aux_ev) if (e) cudaEventDestroy(e);
   if (x->h2d) cudaStreamDestroy(x->h2d);
   for (auto& e : x->h2d_ev) if (e) cudaEventDestroy(e);
+  for (auto& e : x->hq_ev) if (e) cudaEventDestroy(e);
+  for (auto& b : x->hq_buf) cudaFree(b);
+  delete x->hq_mu;
   delete x->aux_mu;
   for (auto& es : x->pending)
     for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
@@ -182,6 +185,17 @@ struct StageEvents {
     if (on) idx->pending.push_back(ev);
   }
 };
+
+// rairs_search_host: host queries copied in this many chunks on the index's
+// copy stream (1 = one copy on the search stream)
+static int host_chunks(const rairs_index_s* idx, int64_t nq, int nprobe) {
+  static const int h2d_chunks = [] {
+    const char* e = getenv("RAIRS_H2D_CHUNKS");  // experiments only
+    return e ? std::max(1, std::min(H2D_CHUNKS, atoi(e))) : H2D_CHUNKS;
+  }();
+  if (!idx->h2d || !coarse_fused_ok(idx, nprobe)) return 1;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(h2d_chunks, nq / H2D_MIN_ROWS));
+}
 
 static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_t nq, int k,
                                 int nprobe, int rf, int32_t* probes_out, uint8_t* lut_q,
@@ -226,21 +240,16 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   // filter + exact fp64 certify (K1/K2), or the exact fp64 kernel directly.
   // Host queries: copied in chunks on the index's copy stream, the coarse
   // stage of chunk h starting as soon as chunk h has landed.
-  static const int h2d_chunks = [] {
-    const char* e = getenv("RAIRS_H2D_CHUNKS");  // experiments only
-    return e ? std::max(1, std::min(H2D_CHUNKS, atoi(e))) : H2D_CHUNKS;
-  }();
-  const int hchunks = (queries_host && idx->h2d && coarse_fused_ok(idx, nprobe))
-                          ? (int)std::min<int64_t>(h2d_chunks, nq / H2D_MIN_ROWS) : 1;
+  const int hchunks = queries_host ? host_chunks(idx, nq, nprobe) : 1;
   int64_t nk = 0;
   if (queries_host && hchunks <= 1) {
     RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries), queries_host,
                                    (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, s));
   }
   if (hchunks > 1) {
+    // `queries` was allocated on the copy stream (search_host_impl): the copies
+    // do not wait for earlier work on s, so they overlap the previous search
     std::lock_guard<std::mutex> lock(*idx->aux_mu);
-    RAIRS_CUDA_TRY(cudaEventRecord(idx->h2d_ev[0], s));  // workspaces allocated on s
-    RAIRS_CUDA_TRY(cudaStreamWaitEvent(idx->h2d, idx->h2d_ev[0], 0));
     for (int h = 0; h < hchunks; ++h) {
       const int64_t r0 = nq * h / hchunks, r1 = nq * (h + 1) / hchunks;
       RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries) + r0 * idx->d,
@@ -716,9 +725,10 @@ rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, i
                      nullptr, nullptr, nullptr, dco, out_ids, out_dists, (cudaStream_t)stream);
 }
 
-rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int64_t nq,
-                               int32_t k, int32_t nprobe, int32_t refine_factor,
-                               int64_t* out_ids_host, float* out_dists_host, void* stream) {
+static rairs_status search_host_impl(rairs_index_t idx, const float* queries_host, int64_t nq,
+                                     int32_t k, int32_t nprobe, int32_t refine_factor,
+                                     int64_t* out_ids_host, float* out_dists_host, void* stream,
+                                     bool sync) {
   RAIRS_TRY(validate_search(idx, nq, k, nprobe, refine_factor));
   if (nq == 0) return RAIRS_OK;
   if (!queries_host || !out_ids_host || !out_dists_host) return invalid("NULL host buffer");
@@ -727,20 +737,57 @@ rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int
   int64_t* di = nullptr;
   float* dd = nullptr;
   const size_t qb = (size_t)nq * idx->d * 4, ib = (size_t)nq * k * 8, db = (size_t)nq * k * 4;
-  RAIRS_CUDA_TRY(cudaMallocAsync(&dq, qb, s));
+  const bool chunked = host_chunks(idx, nq, nprobe) > 1;
+  std::unique_lock<std::mutex> lock;
+  int slot = -1;
+  if (chunked) {
+    // chunked copies run on the copy stream, into one of the index's two query
+    // buffers; it waits (on the device) until the search that last read the
+    // buffer has finished, never for the rest of the search stream
+    lock = std::unique_lock<std::mutex>(*idx->hq_mu);
+    slot = idx->hq_next;
+    idx->hq_next ^= 1;
+    if (idx->hq_cap[slot] < qb) {
+      RAIRS_CUDA_TRY(cudaDeviceSynchronize());
+      cudaFree(idx->hq_buf[slot]);
+      idx->hq_buf[slot] = nullptr;
+      idx->hq_cap[slot] = 0;
+      RAIRS_CUDA_TRY(cudaMalloc(&idx->hq_buf[slot], qb));
+      idx->hq_cap[slot] = qb;
+    }
+    RAIRS_CUDA_TRY(cudaStreamWaitEvent(idx->h2d, idx->hq_ev[slot], 0));
+    dq = idx->hq_buf[slot];
+  } else {
+    RAIRS_CUDA_TRY(cudaMallocAsync(&dq, qb, s));
+  }
   RAIRS_CUDA_TRY(cudaMallocAsync(&di, ib, s));
   RAIRS_CUDA_TRY(cudaMallocAsync(&dd, db, s));
   rairs_status st = search_impl(idx, dq, nq, k, nprobe, refine_factor, nullptr, nullptr, nullptr,
                                 nullptr, nullptr, nullptr, nullptr, di, dd, s, queries_host);
+  if (chunked) cudaEventRecord(idx->hq_ev[slot], s);  // the buffer is free again after this
   if (st == RAIRS_OK) {
     cudaMemcpyAsync(out_ids_host, di, ib, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(out_dists_host, dd, db, cudaMemcpyDeviceToHost, s);
   }
-  cudaFreeAsync(dq, s);
+  if (!chunked) cudaFreeAsync(dq, s);
   cudaFreeAsync(di, s);
   cudaFreeAsync(dd, s);
-  RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  if (sync || st != RAIRS_OK) RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
   return st;
+}
+
+rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int64_t nq,
+                               int32_t k, int32_t nprobe, int32_t refine_factor,
+                               int64_t* out_ids_host, float* out_dists_host, void* stream) {
+  return search_host_impl(idx, queries_host, nq, k, nprobe, refine_factor, out_ids_host,
+                          out_dists_host, stream, true);
+}
+
+rairs_status rairs_search_host_async(rairs_index_t idx, const float* queries_host, int64_t nq,
+                                     int32_t k, int32_t nprobe, int32_t refine_factor,
+                                     int64_t* out_ids_host, float* out_dists_host, void* stream) {
+  return search_host_impl(idx, queries_host, nq, k, nprobe, refine_factor, out_ids_host,
+                          out_dists_host, stream, false);
 }
 
 rairs_status rairs_search_debug(rairs_index_t idx, const float* queries, int64_t nq, int32_t k,

@@ -76,6 +76,14 @@ struct rairs_index_s {
   // host-query copy stream + events (rairs_search_host: chunked H2D / coarse overlap)
   cudaStream_t h2d = nullptr;
   cudaEvent_t h2d_ev[5] = {};
+  // two device query buffers for host searches, reused in turn: a buffer is
+  // refilled (on the copy stream) only after the search that read it is done
+  // (hq_ev, recorded on the search stream) -- no per-call allocation, no host sync
+  float* hq_buf[2] = {nullptr, nullptr};
+  size_t hq_cap[2] = {0, 0};
+  cudaEvent_t hq_ev[2] = {nullptr, nullptr};
+  int hq_next = 0;
+  std::mutex* hq_mu = nullptr;
 
   // stage profiling (CUDA events on the search stream)
   bool prof = false;

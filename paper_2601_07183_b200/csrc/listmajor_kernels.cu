@@ -1406,6 +1406,8 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
     for (auto& e : idx->aux_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&idx->h2d, cudaStreamNonBlocking));
     for (auto& e : idx->h2d_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : idx->hq_ev) RAIRS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    idx->hq_mu = new std::mutex();
     idx->aux_mu = new std::mutex();
   }
   idx->lm_bytes = (size_t)idx->nlist * 4 + (size_t)std::max<int64_t>(idx->n_refs, 1) * 4 +

@@ -182,6 +182,20 @@ class Index:
               "rairs_search_host")
         return ids, dists
 
+    def search_host_async(self, queries: np.ndarray, k: int, nprobe: int, refine_factor: int,
+                          out_ids: np.ndarray, out_dists: np.ndarray):
+        """rairs_search_host_async: enqueue H2D + search + D2H on the current
+        stream and return; the (pinned) host buffers are filled once the
+        stream reaches this point (synchronise it before reading them)."""
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        if not (out_ids.flags.c_contiguous and out_dists.flags.c_contiguous):
+            raise ValueError("output buffers must be C-contiguous")
+        check(lib().rairs_search_host_async(self._h, q.ctypes.data_as(ctypes.c_void_p), q.shape[0],
+                                            int(k), int(nprobe), int(refine_factor),
+                                            out_ids.ctypes.data_as(ctypes.c_void_p),
+                                            out_dists.ctypes.data_as(ctypes.c_void_p), _stream()),
+              "rairs_search_host_async")
+
     def search_debug(self, queries: torch.Tensor, k: int, nprobe: int,
                      refine_factor: int = 10) -> Dict[str, torch.Tensor]:
         q = _dev_f32(queries, "queries")

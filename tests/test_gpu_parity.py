@@ -619,6 +619,15 @@ def test_search_host_chunked_h2d(oracle_mod):
     ids, dists = idx.search(_t(Q), 10, 4, 10)
     hi, hd = idx.search_host(Q, 10, 4, 10)
     assert np.array_equal(ids.cpu().numpy(), hi) and np.array_equal(dists.cpu().numpy(), hd)
+    # the async entry point, twice back to back on one stream, then one sync
+    outs = [(torch.empty((Q.shape[0], 10), dtype=torch.int64).pin_memory().numpy(),
+             torch.empty((Q.shape[0], 10), dtype=torch.float32).pin_memory().numpy()) for _ in range(2)]
+    qh = torch.from_numpy(Q).pin_memory().numpy()
+    for o_i, o_d in outs:
+        idx.search_host_async(qh, 10, 4, 10, o_i, o_d)
+    torch.cuda.synchronize()
+    for o_i, o_d in outs:
+        assert np.array_equal(o_i, hi) and np.array_equal(o_d, hd)
     rows = np.r_[0:50, 2200:2300, 8950:9001]           # across the chunk borders
     o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, Q[rows], 10, 4, 10)
     assert np.array_equal(hi[rows], o["ids"])
