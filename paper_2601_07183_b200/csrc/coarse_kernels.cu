@@ -185,8 +185,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float g = __ldg(a.cnorm + col0 + c * 32 + j) - 2.0f * __uint_as_float(v[j]);
-          gbuf[j * (FT_BM * FT_HALVES) + warp * 32 + lane] = g;
-          if (g < thr) pass |= 1u << j;
+          if (g < thr) {  // only candidates are staged for the insertion loop
+            gbuf[j * (FT_BM * FT_HALVES) + warp * 32 + lane] = g;
+            pass |= 1u << j;
+          }
         }
         while (__any_sync(0xffffffffu, pass != 0)) {
           if (pass != 0) {

@@ -16,11 +16,19 @@ spec = get_config(cfg)
 npb = int(sys.argv[2]) if len(sys.argv) > 2 else spec.nprobe
 mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
-X, Q = make_dataset(spec)
 dev = torch.device("cuda:0")
-idx = rb.build_index(torch.from_numpy(X).to(dev), spec.nlist, spec.M)
+from synth import GPU_KINDS  # noqa: E402
+if spec.kind in GPU_KINDS:  # c4 / c5: drawn on the device
+    from synth.gpu_generators import make_dataset_torch
+    Xd, Qd = make_dataset_torch(spec, dev)
+    kw = dict(train_sample=64 * spec.nlist, kmeans_iters=10)
+else:
+    X, Q = make_dataset(spec)
+    Xd, Qd = torch.from_numpy(X).to(dev), torch.from_numpy(Q).to(dev)
+    kw = {}
+idx = rb.build_index(Xd, spec.nlist, spec.M, **kw)
+del Xd
 idx.set_scan_mode(mode)
-Qd = torch.from_numpy(Q).to(dev)
 torch.cuda.synchronize()
 for i in range(reps):
     if i == reps - 1:
