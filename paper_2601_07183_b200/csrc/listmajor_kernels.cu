@@ -154,7 +154,7 @@ __device__ __forceinline__ float lut_T(const float* qs, const float* smc, int m,
 }
 
 template <int DSUB, int MPL>
-__global__ void __launch_bounds__(LW * 32) lut_tiles_kernel(
+__global__ void __launch_bounds__(LW * 32, 3) lut_tiles_kernel(
     const float* __restrict__ queries, int64_t nq, int d, const float* __restrict__ cb, int M,
     int M_pad, const int32_t* __restrict__ probes, int nprobe,
     const uint32_t* __restrict__ qslot, const uint32_t* __restrict__ qcnt,
