@@ -668,6 +668,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
 // histogram-threshold top-bigK with warp-private state (no CTA barriers).
 constexpr int SW_WARPS = 8;
 constexpr int SW_NB = 512;
+constexpr int SEL_P1 = 4;  // 16-B loads in flight per lane in pass 1
 
 struct SelArgs {
   const int32_t* probes;
@@ -920,15 +921,15 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
       const uint4* rv = reinterpret_cast<const uint4*>(
           reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
       const uint32_t nv = Nl8 / PER;
-      for (uint32_t v0 = 0; v0 < nv; v0 += 64) {
-        uint4 x[2];
+      for (uint32_t v0 = 0; v0 < nv; v0 += 32 * SEL_P1) {
+        uint4 x[SEL_P1];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < SEL_P1; ++u) {
           const uint32_t vi = v0 + 32 * u + lane;
           x[u] = (vi < nv) ? __ldg(rv + vi) : make_uint4(~0u, ~0u, ~0u, ~0u);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < SEL_P1; ++u) {
           // histogram of the per-vector minima: a subset of U(q) (so the cut
           // stays valid) that holds almost every top item -- the bigK best
           // items rarely share a vector -- at one atomic per 8 (4) items
