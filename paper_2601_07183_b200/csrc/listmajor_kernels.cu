@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
 // histogram-threshold top-bigK with warp-private state (no CTA barriers).
 constexpr int SW_WARPS = 8;
 constexpr int SW_NB = 512;
-constexpr int SEL_P1 = 4;  // 16-B loads in flight per lane in pass 1
+constexpr int SEL_P1 = 8;  // 16-B loads in flight per lane in pass 1
 
 struct SelArgs {
   const int32_t* probes;
