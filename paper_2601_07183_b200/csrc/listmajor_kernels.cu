@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
 constexpr int SW_WARPS = 8;
 constexpr int SW_NB = 512;
 constexpr int SEL_P1 = 8;  // 16-B loads in flight per lane in pass 1
+constexpr int SEL_P2 = 2;  // ... in pass 2 (4 measured: no gain)
 
 struct SelArgs {
   const int32_t* probes;
@@ -959,15 +960,15 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
       const uint4* rv = reinterpret_cast<const uint4*>(
           reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
       const uint32_t nv = Nl8 / PER;
-      for (uint32_t v0 = 0; v0 < nv; v0 += 64) {
-        uint4 x[2];
+      for (uint32_t v0 = 0; v0 < nv; v0 += 32 * SEL_P2) {
+        uint4 x[SEL_P2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < SEL_P2; ++u) {
           const uint32_t vi = v0 + 32 * u + lane;
           x[u] = (vi < nv) ? __ldcs(rv + vi) : make_uint4(~0u, ~0u, ~0u, ~0u);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < SEL_P2; ++u) {
           const uint32_t w4[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
           uint32_t pm = 0;  // this lane's items with score <= thr (the sentinel never passes)
           if (U32) {
