@@ -904,12 +904,38 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
     for (int i = lane; i < SW_NB; i += 32) hist[i] = 0u;
     __syncwarp();
     const uint32_t* qb = a.qbits + (size_t)q * a.qwords;
+    // per-probe metadata: for nprobe <= 32 lane p resolves probe p once, all
+    // probes' dependent loads in flight together (the loops below shuffle it)
+    struct PMeta { uint32_t l, Nl8, r0, nref, own; uint64_t row; };
+    auto load_meta = [&](int p) {
+      PMeta m;
+      m.l = (uint32_t)a.probes[q * a.nprobe + p];
+      m.Nl8 = (a.list_items[m.l] + 7u) & ~7u;
+      m.r0 = a.ref_ptr[m.l];
+      m.nref = a.ref_ptr[m.l + 1] - m.r0;
+      m.own = a.own_cnt[m.l];
+      m.row = a.sbase[m.l] + (uint64_t)a.qslot[q * a.nprobe + p] * m.Nl8;
+      return m;
+    };
+    const bool lane_meta = a.nprobe <= 32;
+    PMeta mine{0, 0, 0, 0, 0, 0};
+    if (lane_meta && lane < a.nprobe) mine = load_meta(lane);
+    auto meta = [&](int p) {
+      if (!lane_meta) return load_meta(p);
+      PMeta m;
+      m.l = __shfl_sync(0xffffffffu, mine.l, p);
+      m.Nl8 = __shfl_sync(0xffffffffu, mine.Nl8, p);
+      m.r0 = __shfl_sync(0xffffffffu, mine.r0, p);
+      m.nref = __shfl_sync(0xffffffffu, mine.nref, p);
+      m.own = __shfl_sync(0xffffffffu, mine.own, p);
+      m.row = __shfl_sync(0xffffffffu, mine.row, p);
+      return m;
+    };
     // ---- pass 1: DCO and the score histogram
     uint32_t dco = 0;
     for (int p = 0; p < a.nprobe; ++p) {
-      const uint32_t l = (uint32_t)a.probes[q * a.nprobe + p];
-      const uint32_t Nl = a.list_items[l], Nl8 = (Nl + 7u) & ~7u;
-      const uint32_t r0 = a.ref_ptr[l], nref = a.ref_ptr[l + 1] - r0;
+      const PMeta pm_ = meta(p);
+      const uint32_t l = pm_.l, Nl8 = pm_.Nl8, r0 = pm_.r0, nref = pm_.nref;
       uint32_t c = 0;
       for (uint32_t j = lane; j < nref; j += 32) {
         const int o = a.ref_owner[r0 + j];
@@ -917,8 +943,9 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      dco += a.own_cnt[l] + c;
-      const uint64_t row = a.sbase[l] + (uint64_t)a.qslot[q * a.nprobe + p] * Nl8;
+      dco += pm_.own + c;
+      const uint64_t row = pm_.row;
+      (void)l;
       const uint4* rv = reinterpret_cast<const uint4*>(
           reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
       const uint32_t nv = Nl8 / PER;
@@ -953,9 +980,9 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
     bool exact = false;
     uint64_t tau = kKeyInf;
     for (int p = 0; p < a.nprobe; ++p) {
-      const uint32_t l = (uint32_t)a.probes[q * a.nprobe + p];
-      const uint32_t Nl = a.list_items[l], Nl8 = (Nl + 7u) & ~7u;
-      const uint64_t row = a.sbase[l] + (uint64_t)a.qslot[q * a.nprobe + p] * Nl8;
+      const PMeta pm_ = meta(p);
+      const uint32_t l = pm_.l, Nl8 = pm_.Nl8;
+      const uint64_t row = pm_.row;
       const uint32_t* lids = a.list_ids + a.list_base[l];
       const uint4* rv = reinterpret_cast<const uint4*>(
           reinterpret_cast<const unsigned char*>(a.S) + row * (U32 ? 4 : 2));
