@@ -145,6 +145,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->ref_ptr); cudaFree(x->ref_owner); cudaFree(x->ref_start); cudaFree(x->ref_cnt);
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks); cudaFree(x->counters);
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
+  cudaFree(x->lm_order);
   cudaFree(x->live_bits);
   cudaFree(x->labels); cudaFree(x->lab_sorted); cudaFree(x->lab_rows);
   for (auto& st : x->aux) if (st) cudaStreamDestroy(st);

@@ -281,6 +281,7 @@ struct LMArgs {
   void* S;
   int score_u32;
   int nlist;
+  const uint32_t* order;  // claim order: lists by descending N_l (longest first), or NULL
 };
 
 // D[tmem] (+)= A[tmem] x B[smem desc]  (A: 128 item rows x 32 K-bytes, 8 columns)
@@ -446,7 +447,10 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   uint32_t qt_ctr = 0;     // query tiles so far (bfull phase)
 
   for (;;) {
-    if (tid == 0) sh_list = atomicAdd(a.list_counter, 1u);
+    if (tid == 0) {  // longest list-tasks first: the persistent CTAs finish together
+      const uint32_t c = atomicAdd(a.list_counter, 1u);
+      sh_list = (c < (uint32_t)a.nlist && a.order) ? a.order[c] : c;
+    }
     __syncthreads();
     const uint32_t l = sh_list;
     __syncthreads();  // everyone has read sh_list before thread 0 may overwrite it
@@ -1256,6 +1260,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.S = S;
   la.score_u32 = score_u32;
   la.nlist = nlist;
+  la.order = idx->lm_order;
   const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 + (2 * 8 + 5) * 8 + 64;
   switch (idx->M_pad / 16) {
     case 1: LM_TRY(launch_lm_tensor_shape<1>(la, tsm, s)); break;
@@ -1416,6 +1421,17 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
                                  cudaMemcpyDeviceToHost, s));
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
   idx->max_list_items = 0;
+  {  // claim order of the list-major scan: descending N_l (ties by list id)
+    std::vector<uint32_t> ord(idx->nlist);
+    for (int l = 0; l < idx->nlist; ++l) ord[l] = (uint32_t)l;
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return h[x] > h[y]; });
+    cudaFree(idx->lm_order);
+    idx->lm_order = nullptr;
+    RAIRS_CUDA_TRY(cudaMalloc(&idx->lm_order, (size_t)idx->nlist * 4));
+    RAIRS_CUDA_TRY(cudaMemcpyAsync(idx->lm_order, ord.data(), (size_t)idx->nlist * 4,
+                                   cudaMemcpyHostToDevice, s));
+    RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   std::vector<uint64_t> base(idx->nlist + 1, 0);
   for (int l = 0; l < idx->nlist; ++l) {
     idx->max_list_items = std::max<int64_t>(idx->max_list_items, h[l]);
