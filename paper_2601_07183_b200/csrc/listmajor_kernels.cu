@@ -702,6 +702,7 @@ struct SelArgs {
   int64_t q0;  // first query of this launch (queries [q0, nq))
   int sorted_out;  // 1: write each query's bigK keys in (s, id) order (debug outputs)
   unsigned long long* dco_total;  // += DCO of every query (rairs_get_stats) or NULL
+  unsigned* qctr;                 // zeroed counter: warps claim queries q0 + atomicAdd (load balance)
 };
 
 __device__ __forceinline__ uint32_t warp_bthr(const uint32_t* hist, uint32_t bigK) {
@@ -903,8 +904,14 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
   const uint32_t bigK = (uint32_t)a.bigK;
   constexpr uint32_t SENT = U32 ? 0xFFFFFFFFu : 0xFFFFu;
   constexpr int PER = U32 ? 4 : 8;  // scores per 16-B vector
-  for (int64_t q = a.q0 + (int64_t)blockIdx.x * SW_WARPS + warp; q < a.nq;
-       q += (int64_t)gridDim.x * SW_WARPS) {
+  for (;;) {
+    // dynamic scheduling: a warp claims its next query when it is free, so the
+    // queries with the longest score rows do not pile up on a few warps
+    uint32_t claim = 0;
+    if (lane == 0) claim = atomicAdd(a.qctr, 1u);
+    const int64_t q = a.q0 + (int64_t)__shfl_sync(0xffffffffu, claim, 0);
+    if (q >= a.nq) break;
+    (void)warp;
     for (int i = lane; i < SW_NB; i += 32) hist[i] = 0u;
     __syncwarp();
     const uint32_t* qb = a.qbits + (size_t)q * a.qwords;
@@ -1306,10 +1313,12 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
   LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
   LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  int n_sel = 0;  // select launches so far: each gets its own zeroed counter in cnt's tail
   auto select_range = [&](int64_t q0, int64_t q1, cudaStream_t st) -> cudaError_t {
     SelArgs sr = sl;
     sr.q0 = q0;
     sr.nq = q1;
+    sr.qctr = cnt + nlist + 2 + (n_sel++);
     // persistent: 4 CTAs per SM, warps loop over queries (no partial last wave)
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q1 - q0, SW_WARPS), 148 * 4));
     if (score_u32) lm_select_kernel<true><<<g, SW_WARPS * 32, ssm, st>>>(sr);
