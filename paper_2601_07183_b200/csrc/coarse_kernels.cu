@@ -703,9 +703,12 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   for (int64_t r0 = 0; r0 < rows; r0 += CH) {
     const int64_t nr = std::min<int64_t>(CH, rows - r0);
     const int64_t mtiles = ceil_div(nr, FT_BM);
-    // column splits: enough CTAs to cover the SMs once (more splits only add
-    // per-CTA fixed cost and K2 merge work -- measured on c2pl)
-    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148, mtiles)));
+    // column splits: only when there are too few row tiles to occupy the GPU.
+    // A split restarts the top-W insertion (the first column tile pays most of
+    // it) and doubles the certify merge; measured on c2pl (4 column tiles) and
+    // c4 (64): one split per row tile beats covering every SM (coarse 0.120 ->
+    // 0.098 ms and 0.305 -> 0.265 ms for 79 row tiles)
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(64, mtiles)));
     if (capped)  // >= 4 capped lists per needed 32 candidates: a group rarely holds > 32 of them
       nsplit = std::max<int>(nsplit, (int)std::min<int64_t>(ntiles, ceil_div(4 * ceil_div(Wp1, 32), FT_HALVES)));
     nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys
