@@ -308,6 +308,36 @@ def run_ours(args):
                "sync_value": round(sync_v, 1),
                "sync_mode": "rairs_search_host per step (H2D + search + D2H + stream sync)"}
 
+    if world > 1:
+        # N GPUs: the sharded public API (ShardedIndex search = per-shard search +
+        # NCCL all_gather + K7 merge) with host buffers: every rank copies the
+        # batch in from pinned memory, rank 0 copies the merged result out
+        qh_t = torch.from_numpy(Q).pin_memory()
+        oi_t = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+        od_t = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+        def host_step():
+            Qd.copy_(qh_t, non_blocking=True)
+            ids_, dists_, _ = step(chosen)
+            if rank == 0:
+                oi_t.copy_(ids_, non_blocking=True)
+                od_t.copy_(dists_, non_blocking=True)
+        for _ in range(2):
+            host_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            host_step()
+        torch.cuda.synchronize()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(nq * args.steps / float(el.item()), 1), "unit": "queries/s",
+               "h2d_bytes_per_step": int(Q.nbytes) * world, "d2h_bytes_per_step": int(nq * k * 12),
+               "mode": "sharded public API per step: pinned H2D of the batch on every rank, "
+                       "search + all_gather + merge, D2H of the merged top-k on rank 0; "
+                       "wall clock, max over ranks"}
+
     # ---------------- one query at a time (paper's latency workload) ------------
     lat = None
     if world == 1 and args.latency_queries > 0:
