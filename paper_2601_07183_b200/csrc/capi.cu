@@ -1,5 +1,5 @@
-#include <cmath>
 // capi.cu -- extern "C" entry points of librairs.so (see include/rairs.h).
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <new>
