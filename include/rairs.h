@@ -168,10 +168,11 @@ rairs_status rairs_search(rairs_index_t idx, const float* queries, int64_t nq, i
                           float* out_dists, int64_t* dco, void* stream);
 
 /* Same as rairs_search with HOST buffers: copies queries host->device, runs
- * the search, copies results device->host and synchronises `stream`.  For
- * batches of >= 4,096 queries on the tensor-core coarse path the queries are
- * copied in chunks on the index's copy stream and each chunk's coarse stage
- * starts as soon as it lands.  Host buffers should be pinned (page-locked). */
+ * the search, copies results device->host and synchronises `stream`.  The
+ * queries are copied on the index's copy stream into one of two device
+ * buffers it reuses in turn (a buffer is refilled once the search that read
+ * it is done), so a call's copy can overlap the previous call's search.  Host
+ * buffers should be pinned (page-locked). */
 rairs_status rairs_search_host(rairs_index_t idx, const float* queries_host, int64_t nq,
                                int32_t k, int32_t nprobe, int32_t refine_factor,
                                int64_t* out_ids_host, float* out_dists_host, void* stream);

@@ -187,16 +187,12 @@ struct StageEvents {
   }
 };
 
-// rairs_search_host: host queries copied in this many chunks on the index's
-// copy stream (1 = one copy on the search stream)
-static int host_chunks(const rairs_index_s* idx, int64_t nq, int nprobe) {
-  static const int h2d_chunks = [] {
-    const char* e = getenv("RAIRS_H2D_CHUNKS");  // experiments only
-    return e ? std::max(1, std::min(H2D_CHUNKS, atoi(e))) : H2D_CHUNKS;
-  }();
-  if (!idx->h2d || !coarse_fused_ok(idx, nprobe)) return 1;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(h2d_chunks, nq / H2D_MIN_ROWS));
-}
+// rairs_search_host: 1 = the host queries are copied on the index's copy stream
+// (into its query-buffer ring, overlapping the previous search), 0 = no copy
+// stream, one copy on the search stream.  (Copying in 2-4 chunks with a coarse
+// launch per chunk was measured slower: the extra coarse launches cost more than
+// the earlier start.)
+static int host_chunks(const rairs_index_s* idx, int64_t, int) { return idx->h2d ? 1 : 0; }
 
 static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_t nq, int k,
                                 int nprobe, int rf, int32_t* probes_out, uint8_t* lut_q,
@@ -239,33 +235,22 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   ev.mark(0);
   // coarse: P(q) = first nprobe lists by (D64, l)  (O1).  Tensor-core TF32
   // filter + exact fp64 certify (K1/K2), or the exact fp64 kernel directly.
-  // Host queries: copied in chunks on the index's copy stream, the coarse
-  // stage of chunk h starting as soon as chunk h has landed.
-  const int hchunks = queries_host ? host_chunks(idx, nq, nprobe) : 1;
+  const int hchunks = queries_host ? host_chunks(idx, nq, nprobe) : 0;
   int64_t nk = 0;
-  if (queries_host && hchunks <= 1) {
+  if (queries_host && hchunks == 0) {
     RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries), queries_host,
                                    (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, s));
   }
-  if (hchunks > 1) {
-    // `queries` was allocated on the copy stream (search_host_impl): the copies
-    // do not wait for earlier work on s, so they overlap the previous search
+  if (hchunks == 1 && queries_host) {
+    // one copy on the copy stream (into the index's query-buffer ring): it
+    // overlaps the previous search; this search waits for it
     std::lock_guard<std::mutex> lock(*idx->aux_mu);
-    for (int h = 0; h < hchunks; ++h) {
-      const int64_t r0 = nq * h / hchunks, r1 = nq * (h + 1) / hchunks;
-      RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries) + r0 * idx->d,
-                                     queries_host + r0 * idx->d, (size_t)(r1 - r0) * idx->d * 4,
-                                     cudaMemcpyHostToDevice, idx->h2d));
-      RAIRS_CUDA_TRY(cudaEventRecord(idx->h2d_ev[1 + h], idx->h2d));
-    }
-    for (int h = 0; h < hchunks && st == RAIRS_OK; ++h) {
-      const int64_t r0 = nq * h / hchunks, r1 = nq * (h + 1) / hchunks;
-      RAIRS_CUDA_TRY(cudaStreamWaitEvent(s, idx->h2d_ev[1 + h], 0));
-      st = launch_coarse_fused(idx, queries + r0 * idx->d, r1 - r0, nprobe, 0, 0.0, 0,
-                               probes + r0 * nprobe, nullptr, nullptr, idx->certify_fallbacks, s);
-      nk += 3;
-    }
-  } else if (coarse_fused_ok(idx, nprobe)) {
+    RAIRS_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(queries), queries_host,
+                                   (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, idx->h2d));
+    RAIRS_CUDA_TRY(cudaEventRecord(idx->h2d_ev[1], idx->h2d));
+    RAIRS_CUDA_TRY(cudaStreamWaitEvent(s, idx->h2d_ev[1], 0));
+  }
+  if (coarse_fused_ok(idx, nprobe)) {
     st = launch_coarse_fused(idx, queries, nq, nprobe, 0, 0.0, 0, probes, nullptr, nullptr,
                              idx->certify_fallbacks, s);
     nk += 3;  // topw + certify + exact fallback
@@ -738,7 +723,7 @@ static rairs_status search_host_impl(rairs_index_t idx, const float* queries_hos
   int64_t* di = nullptr;
   float* dd = nullptr;
   const size_t qb = (size_t)nq * idx->d * 4, ib = (size_t)nq * k * 8, db = (size_t)nq * k * 4;
-  const bool chunked = host_chunks(idx, nq, nprobe) > 1;
+  const bool chunked = host_chunks(idx, nq, nprobe) >= 1;  // copies on the copy stream
   std::unique_lock<std::mutex> lock;
   int slot = -1;
   if (chunked) {

@@ -7,9 +7,6 @@
 #include "common.cuh"
 
 namespace rairs {
-// rairs_search_host: queries copied in up to H2D_CHUNKS chunks of >= H2D_MIN_ROWS
-constexpr int H2D_CHUNKS = 4;
-constexpr int64_t H2D_MIN_ROWS = 2048;
 }  // namespace rairs
 
 struct rairs_index_s {
@@ -76,7 +73,7 @@ struct rairs_index_s {
   std::mutex* aux_mu = nullptr;  // one search at a time enqueues on the aux streams
   // host-query copy stream + events (rairs_search_host: chunked H2D / coarse overlap)
   cudaStream_t h2d = nullptr;
-  cudaEvent_t h2d_ev[5] = {};
+  cudaEvent_t h2d_ev[2] = {};
   // two device query buffers for host searches, reused in turn: a buffer is
   // refilled (on the copy stream) only after the search that read it is done
   // (hq_ev, recorded on the search stream) -- no per-call allocation, no host sync

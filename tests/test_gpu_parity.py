@@ -609,13 +609,13 @@ def test_sharded_insert_and_delete_ids(oracle_mod):
     idx.free()
 
 
-def test_search_host_chunked_h2d(oracle_mod):
-    # rairs_search_host copies >= 4,096 host queries in chunks on the index's
-    # copy stream and runs the coarse stage chunk by chunk (tensor-core path,
+def test_search_host_copy_stream(oracle_mod):
+    # rairs_search_host(_async) copies the host queries on the index's copy
+    # stream into a two-slot device buffer ring (tensor-core coarse path,
     # nlist 1024): same results as the device entry point, and as the oracle
     c = case(oracle_mod, "c2pl", n=60000)
     idx = c.gpu_index()
-    Q = c.Q[:9001]                                     # 4 chunks, ragged
+    Q = c.Q[:9001]
     ids, dists = idx.search(_t(Q), 10, 4, 10)
     hi, hd = idx.search_host(Q, 10, 4, 10)
     assert np.array_equal(ids.cpu().numpy(), hi) and np.array_equal(dists.cpu().numpy(), hd)
@@ -628,7 +628,7 @@ def test_search_host_chunked_h2d(oracle_mod):
     torch.cuda.synchronize()
     for o_i, o_d in outs:
         assert np.array_equal(o_i, hi) and np.array_equal(o_d, hd)
-    rows = np.r_[0:50, 2200:2300, 8950:9001]           # across the chunk borders
+    rows = np.r_[0:50, 2200:2300, 8950:9001]
     o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, Q[rows], 10, 4, 10)
     assert np.array_equal(hi[rows], o["ids"])
     idx.free()
