@@ -276,10 +276,16 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
     const float* qv = p.queries + q * p.d;
 
     // ---------------- K3: LUT + uint8 quantisation (O2) ----------------
+    // the first 4 * ST entries' T stay in registers for the quantisation pass
+    float Tr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     for (int e0 = 0; e0 < M16; e0 += ST) {          // warp-uniform trip count
       const int e = e0 + tid;
       const bool act = e < M16;
       float T = act ? lut_T(qv, p.codebook, e >> 4, e & 15, p.dsub) : 0.0f;
+      const int kk = e0 / ST;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u == kk) Tr[u] = T;
       float lo = act ? T : __int_as_float(0x7f800000);
       float hi = act ? T : -__int_as_float(0x7f800000);
 #pragma unroll
@@ -322,7 +328,12 @@ __global__ void __launch_bounds__(ST, 4) scan_kernel(ScanParams p) {
       uint32_t v = 0;
       const int m = e >> 4;
       if (m < M && S > 0.0f) {
-        const float T = lut_T(qv, p.codebook, m, e & 15, p.dsub);
+        const int kk = (e - tid) / ST;
+        float T = 0.0f;  // the first pass's value (same function of the same inputs)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u == kk) T = Tr[u];
+        if (kk >= 4) T = lut_T(qv, p.codebook, m, e & 15, p.dsub);
         const float t2 = __fmul_rn(__fsub_rn(T, mn[m]), a);
         v = (uint32_t)min(255, __float2int_rn(t2));
       }
