@@ -348,12 +348,6 @@ __device__ __forceinline__ int lm_ref_of(const uint32_t* refoff, uint32_t nref, 
   return lo;
 }
 
-__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n) {  // n >= 32 -> 0
-  uint32_t r;
-  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
-  return r;
-}
-
 template <int G>
 __device__ __forceinline__ uint32_t gcnt_of(const uint32_t (&gc)[G], int g) {
   uint32_t v = gc[0];
@@ -418,8 +412,16 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   uint64_t* bfull = tempty + 2;         // LUT tile landed
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
   __shared__ uint32_t sh_list;
+  // one-hot rows of the 16 nibble values (16 B each): generation is one
+  // shared-memory load per nibble instead of ~9 ALU instructions
+  __shared__ __align__(16) uint4 onehot16[16];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < 16) {
+    const uint32_t b = 1u << (8 * (tid & 3));
+    const int w = tid >> 2;
+    onehot16[tid] = make_uint4(w == 0 ? b : 0u, w == 1 ? b : 0u, w == 2 ? b : 0u, w == 3 ? b : 0u);
+  }
   if (tid == 0) {
     for (int s = 0; s < LM_GROUPS * LM_GPAIRS; ++s) {
       mbar_init(&full[s], 4);  // the 4 lane-quarter warps of the tile's generator group
@@ -538,11 +540,11 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
               uint32_t v[32];
 #pragma unroll
               for (int k = 0; k < 8; ++k) {  // one-hot of nibble n: byte n of 16 = 1
-                const uint32_t sh = ((w32 >> (4 * k)) & 15u) << 3;
-                v[4 * k + 0] = shl_clamp(1u, sh);
-                v[4 * k + 1] = shl_clamp(1u, sh - 32u);
-                v[4 * k + 2] = shl_clamp(1u, sh - 64u);
-                v[4 * k + 3] = shl_clamp(1u, sh - 96u);
+                const uint4 o = onehot16[(w32 >> (4 * k)) & 15u];
+                v[4 * k + 0] = o.x;
+                v[4 * k + 1] = o.y;
+                v[4 * k + 2] = o.z;
+                v[4 * k + 3] = o.w;
               }
               tmem_st32(tq + (uint32_t)((2 * ps + h) * 32), v);
             }
