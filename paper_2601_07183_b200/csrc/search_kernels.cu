@@ -675,6 +675,14 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
 // refine_kernel) over the current chunk's padded shared tile.  After a
 // query's last chunk, the top-k by the unique key (bits(delta) << 32 | id) is
 // found by rank counting over its bigK keys.
+__device__ __forceinline__ float4 ldg_evict_first(const float4* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 constexpr int RS_THREADS = 256;
 constexpr int RS_ROWS = 128;
 constexpr int RS_MAXK = 512;
@@ -694,6 +702,10 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int myrow = warp + 8 * lane;  // lane j (< 16) fetches the key of row warp + 8j
   const int nch = (bigK + RS_ROWS - 1) / RS_ROWS;
+  // candidate rows are read once: evict them first from L2, so the gather does
+  // not push out the score rows the concurrent selection streams
+  uint64_t l2pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l2pol));
   // software pipeline: keys of unit u + 2 and rows of unit u + 1 are in
   // flight while unit u is computed (the row loads never wait on a key load)
   auto load_key = [&](int64_t q, int c) -> uint64_t {
@@ -720,7 +732,8 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
       const uint32_t g = __shfl_sync(0xffffffffu, gid, j);
       const uint32_t r = __shfl_sync(0xffffffffu, rowi, j);
       v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (g != 0xFFFFFFFFu && lane < D4) v[j] = __ldg(reinterpret_cast<const float4*>(X + (size_t)r * D) + lane);
+      if (g != 0xFFFFFFFFu && lane < D4)
+        v[j] = ldg_evict_first(reinterpret_cast<const float4*>(X + (size_t)r * D) + lane, l2pol);
     }
   };
   int64_t q = blockIdx.x;
