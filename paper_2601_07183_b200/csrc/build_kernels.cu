@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(PT) probe_exact_kernel(ProbeArgs a, ProbeSmem 
   const int d = a.d, L = a.L, cap = ps.bufcap;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
 
+  // fallback mode: only_flagged[rows] holds the number of flagged rows
+  if (a.only_flagged && a.flag_count && *(volatile const int32_t*)(a.only_flagged + a.rows) == 0) return;
   for (int64_t g = blockIdx.x; g * R < a.rows; g += gridDim.x) {
     const int64_t r0 = g * R;
     const int nr = (int)((a.rows - r0) < (int64_t)R ? (a.rows - r0) : (int64_t)R);

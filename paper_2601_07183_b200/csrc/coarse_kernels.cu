@@ -567,7 +567,10 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
     }
     if (lane == 0) {
       a.flags[r] = certified ? 0 : 1;
-      if (!certified) atomicAdd(a.nflag, 1u);
+      if (!certified) {
+        atomicAdd(a.nflag, 1u);
+        atomicAdd(a.flags + a.rows, 1);  // per-call count: the fallback exits at once when 0
+      }
     }
     __syncwarp();
   }
@@ -729,7 +732,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     int32_t* flags = nullptr;
     RAIRS_CUDA_TRY(cudaMallocAsync(&vals, (size_t)nr * nsplit * Wout * 4, s));
     RAIRS_CUDA_TRY(cudaMallocAsync(&ids, (size_t)nr * nsplit * Wout * 4, s));
-    RAIRS_CUDA_TRY(cudaMallocAsync(&flags, (size_t)nr * 4, s));
+    RAIRS_CUDA_TRY(cudaMallocAsync(&flags, (size_t)(nr + 1) * 4, s));
+    RAIRS_CUDA_TRY(cudaMemsetAsync(flags + nr, 0, 4, s));  // flagged-row count of this call
     const float* Xc = X + (size_t)r0 * d;
     CUtensorMap tmA, tmB;
     if (!make_tmap_f32(&tmA, Xc, nr, d, FT_BM) || !make_tmap_f32(&tmB, idx->centroids, nl, d, FT_BN)) {
@@ -825,6 +829,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     pa.l2 = ca.l2;
     pa.only_flagged = flags;
     rairs_status st = launch_probe_split(pa, flags, s);  // large nlist: split rows over CTAs
+    pa.flag_count = true;  // flags[nr]: rows the certify flagged (the split path may clear some)
     if (st == RAIRS_OK) st = launch_probe_exact(pa, s);   // remaining flagged rows
     if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "probe_exact fallback");
     cudaFreeAsync(vals, s);

@@ -117,6 +117,7 @@ struct ProbeArgs {
   int32_t* l1;         // modes 1/2
   int32_t* l2;
   const int32_t* only_flagged;  // mode 0: process only row groups with a flagged row
+  bool flag_count = false;      // only_flagged[rows] = number of flagged rows (0: exit at once)
 };
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s);
 // few flagged rows x many lists: split exact fallback (clears the flags it handles)
