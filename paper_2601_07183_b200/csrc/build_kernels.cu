@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(PT) probe_exact_kernel(ProbeArgs a, ProbeSmem 
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
 
   // fallback mode: only_flagged[rows] holds the number of flagged rows
+  if (a.flag_count) pdl_wait();  // launched with launch_pdl after the certify kernel
   if (a.only_flagged && a.flag_count && *(volatile const int32_t*)(a.only_flagged + a.rows) == 0) return;
   for (int64_t g = blockIdx.x; g * R < a.rows; g += gridDim.x) {
     const int64_t r0 = g * R;
@@ -240,8 +241,12 @@ static rairs_status launch_probe_R(const ProbeArgs& a, cudaStream_t s) {
   // persistent grid just scans the flags (one resident wave, no launch tail)
   int grid = (int)std::min<int64_t>(groups, a.only_flagged ? 148 * 2 : 148 * 8);
   if (grid < 1) return RAIRS_OK;
-  probe_exact_kernel<R><<<grid, PT, ps.total, s>>>(a, ps);
-  RAIRS_CHECK_LAUNCH();
+  if (a.flag_count) {
+    RAIRS_CUDA_TRY(launch_pdl(probe_exact_kernel<R>, dim3(grid), dim3(PT), ps.total, s, a, ps));
+  } else {
+    probe_exact_kernel<R><<<grid, PT, ps.total, s>>>(a, ps);
+    RAIRS_CHECK_LAUNCH();
+  }
   return RAIRS_OK;
 }
 

@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
@@ -392,6 +393,7 @@ struct CertArgs {
 __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
+  pdl_wait();  // the top-W lists of coarse_topw_kernel
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm) + (size_t)warp * a.npow_c;
   uint64_t* ck = reinterpret_cast<uint64_t*>(sm) + (size_t)CT_WARPS * a.npow_c + (size_t)warp * a.npow_w;
   uint32_t* ci = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm) +
@@ -574,6 +576,7 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
     }
     __syncwarp();
   }
+  pdl_trigger();
 }
 
 __global__ void cnorm_kernel(const float* __restrict__ C, int nlist, int npad, int d,
@@ -810,8 +813,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_certify_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem_all));
     const int cgrid = (int)std::min<int64_t>(ceil_div(nr, CT_WARPS), 148 * 16);
-    coarse_certify_kernel<<<cgrid, CT_THREADS, csmem_all, s>>>(ca);
-    RAIRS_CHECK_LAUNCH();
+    RAIRS_CUDA_TRY(launch_pdl(coarse_certify_kernel, dim3(cgrid), dim3(CT_THREADS), csmem_all, s, ca));
     RAIRS_DEBUG_POINT(s, "coarse_certify_kernel");
     // exact fp64 recomputation of the (rare) uncertified rows
     ProbeArgs pa{};

@@ -14,6 +14,34 @@
 
 namespace rairs {
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Kernels of one dependency chain on a stream are launched with the
+// programmatic-serialization attribute: the next kernel's CTAs are scheduled
+// (and run their prologue) while the previous grid drains; pdl_wait() then
+// blocks until the previous grid has completed and its writes are visible.
+// Every kernel launched with launch_pdl calls pdl_wait() before it reads
+// anything its predecessor wrote; pdl_trigger() lets the next grid launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+
 constexpr uint32_t kSlotPad = 0xFFFFFFFFu;   // padding slot marker in slot_rows
 constexpr int kBlk = 32;                     // items per code block (one warp)
 constexpr uint64_t kKeyInf = ~0ull;

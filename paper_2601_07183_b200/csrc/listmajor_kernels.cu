@@ -39,12 +39,14 @@ __global__ void lm_count_kernel(const int32_t* __restrict__ probes, int64_t tota
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nbits_words;
        w += (int64_t)gridDim.x * blockDim.x)
     qbits[w] = 0u;
+  pdl_trigger();
 }
 
 __global__ void lm_scatter_kernel(const int32_t* __restrict__ probes, int64_t total, int nprobe,
                                   const uint32_t* __restrict__ qptr,
                                   const uint32_t* __restrict__ qslot, uint32_t* __restrict__ list_q,
                                   uint32_t* __restrict__ qbits, int qwords) {
+  pdl_wait();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int l = probes[e];
@@ -52,6 +54,7 @@ __global__ void lm_scatter_kernel(const int32_t* __restrict__ probes, int64_t to
     list_q[qptr[l] + qslot[e]] = q;
     atomicOr(&qbits[(size_t)q * qwords + (l >> 5)], 1u << (l & 31));
   }
+  pdl_trigger();
 }
 
 // single CTA: exclusive scans over lists of |Q_l| (qptr), |Q_l|*N_l (score
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(SCN) lm_scan_kernel(const uint32_t* __restrict
   __shared__ uint64_t carry_s;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   if (tid == 0) { carry_q = 0; carry_t = 0; carry_s = 0; }
+  pdl_wait();
   __syncthreads();
   for (int base = 0; base < nlist; base += SCN) {
     const int l = base + tid;
@@ -128,6 +132,7 @@ __global__ void __launch_bounds__(SCN) lm_scan_kernel(const uint32_t* __restrict
     sbase[nlist] = carry_s;
     totals[0] = carry_t;
   }
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
@@ -167,6 +172,7 @@ __global__ void __launch_bounds__(LW * 32, 3) lut_tiles_kernel(
     const int m = e / (16 * DSUB), j = (e / DSUB) % 16, t = e % DSUB;
     smc[(j * DSUB + t) * M + m] = cb[e];
   }
+  pdl_wait();  // the grouping kernels' qslot / cnt / lrow (the codebook above is the index's)
   __syncthreads();
   float* mnw = smc + 16 * DSUB * M + warp * M;
   // MPL: subquantizers per lane (ceil(M_pad / 32) <= 4 on the list-major path)
@@ -251,6 +257,7 @@ __global__ void __launch_bounds__(LW * 32, 3) lut_tiles_kernel(
     }
     __syncwarp();  // mnw reuse
   }
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
@@ -435,6 +442,7 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == LM_MMA_WARP) tmem_alloc(tslot, LM_TMEM_COLS);
+  pdl_wait();  // LUT tiles and grouping of the previous kernels
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
@@ -1160,7 +1168,8 @@ static cudaError_t launch_lm_tensor(const LMArgs& la, size_t tsm, cudaStream_t s
   cudaError_t e = cudaFuncSetAttribute(lm_tensor_kernel<NU, G, GS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
   if (e != cudaSuccess) return e;
-  lm_tensor_kernel<NU, G, GS><<<148 * SH::CTAS_PER_SM, SH::THREADS, tsm, s>>>(la);
+  e = launch_pdl(lm_tensor_kernel<NU, G, GS>, dim3(148 * SH::CTAS_PER_SM), dim3(SH::THREADS), tsm, s, la);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1212,9 +1221,10 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   // 1. group (query, probe) pairs by list
   const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npairs, 256), 148 * 8));
   lm_count_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, cnt, qslot, qbits, nq * qwords);
-  lm_scan_kernel<<<1, SCN, 0, s>>>(cnt, idx->list_items, nlist, qptr, sbase, lrow, totals, QT,
-                                   LM_IT);
-  lm_scatter_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, nprobe, qptr, qslot, list_q, qbits, qwords);
+  LM_TRY(launch_pdl(lm_scan_kernel, dim3(1), dim3(SCN), 0, s, (const uint32_t*)cnt,
+                    (const uint32_t*)idx->list_items, nlist, qptr, sbase, lrow, totals, QT, LM_IT));
+  LM_TRY(launch_pdl(lm_scatter_kernel, dim3(g1), dim3(256), 0, s, (const int32_t*)sa.probes, npairs,
+                    nprobe, (const uint32_t*)qptr, (const uint32_t*)qslot, list_q, qbits, qwords));
   LM_TRY(cudaGetLastError());
   // 2. quantised LUTs (O2), one warp per query, written into the list-task tiles
   {
@@ -1223,10 +1233,10 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
 #define LUT_LAUNCH(DS, MP)                                                                   \
   LM_TRY(cudaFuncSetAttribute(lut_tiles_kernel<DS, MP>,                                      \
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));       \
-  lut_tiles_kernel<DS, MP><<<lgrid, LW * 32, lsm, s>>>(sa.queries, nq, idx->d, idx->codebook, \
-                                                      idx->M, idx->M_pad, sa.probes, nprobe,  \
-                                                      qslot, cnt, lrow, QT, tiles, sa.lut_a,   \
-                                                      sa.lut_b, sa.lut_q)
+  LM_TRY(launch_pdl(lut_tiles_kernel<DS, MP>, dim3(lgrid), dim3(LW * 32), lsm, s, sa.queries,  \
+                    nq, idx->d, (const float*)idx->codebook, idx->M, idx->M_pad, sa.probes,     \
+                    nprobe, (const uint32_t*)qslot, (const uint32_t*)cnt, (const uint32_t*)lrow, \
+                    QT, tiles, sa.lut_a, sa.lut_b, sa.lut_q))
 #define LUT_LAUNCH_D(DS)                                  \
   switch ((idx->M_pad + 31) / 32) {                        \
     case 1: LUT_LAUNCH(DS, 1); break;                      \
