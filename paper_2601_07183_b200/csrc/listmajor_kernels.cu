@@ -1207,7 +1207,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   };
 #define LM_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return _e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA; } } while (0)
   LM_TRY(cudaMallocAsync(&tiles, tile_bytes, s));
-  LM_TRY(cudaMallocAsync(&cnt, (size_t)(nlist + 1) * 4 + 16, s));
+  LM_TRY(cudaMallocAsync(&cnt, (size_t)(nlist + 2 + LM_NCH) * 4, s));
   LM_TRY(cudaMallocAsync(&qslot, (size_t)npairs * 4, s));
   LM_TRY(cudaMallocAsync(&qptr, (size_t)(nlist + 1) * 4, s));
   LM_TRY(cudaMallocAsync(&lrow, (size_t)(nlist + 1) * 4, s));
@@ -1216,7 +1216,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(cudaMallocAsync(&totals, 16, s));
   LM_TRY(cudaMallocAsync(&sbase, (size_t)(nlist + 1) * 8, s));
   LM_TRY(cudaMallocAsync(&S, std::max<size_t>(s_bytes, 16), s));
-  LM_TRY(cudaMemsetAsync(cnt, 0, (size_t)(nlist + 1) * 4 + 16, s));
+  LM_TRY(cudaMemsetAsync(cnt, 0, (size_t)(nlist + 2 + LM_NCH) * 4, s));
   unsigned* list_counter = cnt + nlist + 1;  // zeroed tail of cnt
   // 1. group (query, probe) pairs by list
   const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npairs, 256), 148 * 8));
@@ -1346,7 +1346,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
     ra.out_dists = sa.out_dists + q0 * sa.k;
     return launch_refine(idx, ra, st);
   };
-  const bool overlap = sa.fused_refine && nq >= 2 * LM_OVERLAP_MIN_Q && idx->aux[0];
+  const bool overlap = sa.fused_refine && nq >= LM_NCH * LM_OVERLAP_MIN_Q && idx->aux[0];
   if (!overlap) {
     LM_TRY(select_range(0, nq, s));
     if (sa.ev_selected) LM_TRY(cudaEventRecord(sa.ev_selected, s));
@@ -1355,28 +1355,27 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
       if (rs != RAIRS_OK) { cleanup(); return rs; }
     }
   } else {
-    // 4. + refine: two query halves on the auxiliary streams, so one half's
-    // selection overlaps the other's refine gather (both latency-bound)
+    // 4. + refine: LM_NCH query chunks, each selected then refined on its own
+    // auxiliary stream, so one chunk's selection overlaps another's refine
+    // gather (both latency-bound)
     std::lock_guard<std::mutex> lock(*idx->aux_mu);
     cudaEvent_t* ev = const_cast<cudaEvent_t*>(idx->aux_ev);
-    const int64_t half = nq / 2;
-    const int64_t qb[3] = {0, half, nq};
+    int64_t qb[LM_NCH + 1];
+    for (int h = 0; h <= LM_NCH; ++h) qb[h] = nq * h / LM_NCH;
     LM_TRY(cudaEventRecord(ev[0], s));  // scores ready
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < LM_NCH; ++h) {
       LM_TRY(cudaStreamWaitEvent(idx->aux[h], ev[0], 0));
       LM_TRY(select_range(qb[h], qb[h + 1], idx->aux[h]));
-      LM_TRY(cudaEventRecord(ev[1 + h], idx->aux[h]));  // half h selected
+      LM_TRY(cudaEventRecord(ev[1 + h], idx->aux[h]));  // chunk h selected
     }
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < LM_NCH; ++h) {
       const rairs_status rs = refine_range(qb[h], qb[h + 1], idx->aux[h]);
       if (rs != RAIRS_OK) { cleanup(); return rs; }
-      LM_TRY(cudaEventRecord(ev[3 + h], idx->aux[h]));  // half h refined
+      LM_TRY(cudaEventRecord(ev[1 + LM_NCH + h], idx->aux[h]));  // chunk h refined
     }
-    LM_TRY(cudaStreamWaitEvent(s, ev[1], 0));
-    LM_TRY(cudaStreamWaitEvent(s, ev[2], 0));
+    for (int h = 0; h < LM_NCH; ++h) LM_TRY(cudaStreamWaitEvent(s, ev[1 + h], 0));
     if (sa.ev_selected) LM_TRY(cudaEventRecord(sa.ev_selected, s));
-    LM_TRY(cudaStreamWaitEvent(s, ev[3], 0));
-    LM_TRY(cudaStreamWaitEvent(s, ev[4], 0));
+    for (int h = 0; h < LM_NCH; ++h) LM_TRY(cudaStreamWaitEvent(s, ev[1 + LM_NCH + h], 0));
   }
   cleanup();
   return RAIRS_OK;
