@@ -276,7 +276,7 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
       a.ev_selected = ev.on ? ev.ev.e[2] : nullptr;
       st = launch_listmajor(idx, a, s);
       const int chunks = (nq >= LM_NCH * LM_OVERLAP_MIN_Q && idx->aux[0]) ? LM_NCH : 1;
-      nk += 5 + 2 * chunks;  // count, scan, scatter, lut_tiles, tensor + (select, refine) x chunks
+      nk += 6 + 2 * chunks;  // zero, count, scan, scatter, lut_tiles, tensor + (select, refine) x chunks
       refined = true;
     } else {
       st = launch_scan(idx, a, s);

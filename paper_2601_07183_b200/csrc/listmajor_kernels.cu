@@ -29,9 +29,20 @@ namespace rairs {
 
 // ---------------------------------------------------------------------------
 // Grouping of (query, probe) pairs by list.
+// zeroes the list counters (a kernel, not a memset, so the chain from the
+// coarse stage to the scan stays programmatic-dependent-launch)
+__global__ void lm_zero_kernel(uint32_t* __restrict__ a, int64_t n) {
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = 0u;
+  pdl_trigger();
+}
+
 __global__ void lm_count_kernel(const int32_t* __restrict__ probes, int64_t total,
                                 uint32_t* __restrict__ cnt, uint32_t* __restrict__ qslot,
                                 uint32_t* __restrict__ qbits, int64_t nbits_words) {
+  pdl_wait();  // zeroed counters (lm_zero_kernel) and the probes of the coarse stage
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x)
     qslot[e] = atomicAdd(&cnt[probes[e]], 1u);
@@ -1216,11 +1227,13 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(cudaMallocAsync(&totals, 16, s));
   LM_TRY(cudaMallocAsync(&sbase, (size_t)(nlist + 1) * 8, s));
   LM_TRY(cudaMallocAsync(&S, std::max<size_t>(s_bytes, 16), s));
-  LM_TRY(cudaMemsetAsync(cnt, 0, (size_t)(nlist + 2 + LM_NCH) * 4, s));
+  LM_TRY(launch_pdl(lm_zero_kernel, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlist + 2 + LM_NCH, 256), 148))),
+                    dim3(256), 0, s, cnt, (int64_t)(nlist + 2 + LM_NCH)));
   unsigned* list_counter = cnt + nlist + 1;  // zeroed tail of cnt
   // 1. group (query, probe) pairs by list
   const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npairs, 256), 148 * 8));
-  lm_count_kernel<<<g1, 256, 0, s>>>(sa.probes, npairs, cnt, qslot, qbits, nq * qwords);
+  LM_TRY(launch_pdl(lm_count_kernel, dim3(g1), dim3(256), 0, s, (const int32_t*)sa.probes, npairs,
+                    cnt, qslot, qbits, (int64_t)(nq * qwords)));
   LM_TRY(launch_pdl(lm_scan_kernel, dim3(1), dim3(SCN), 0, s, (const uint32_t*)cnt,
                     (const uint32_t*)idx->list_items, nlist, qptr, sbase, lrow, totals, QT, LM_IT));
   LM_TRY(launch_pdl(lm_scatter_kernel, dim3(g1), dim3(256), 0, s, (const int32_t*)sa.probes, npairs,
