@@ -17,7 +17,11 @@ X, Q = make_dataset_torch(spec, torch.device("cuda"))
 idx = rb.build_index(X, spec.nlist, spec.M, train_sample=64 * spec.nlist, kmeans_iters=10)
 del X
 torch.cuda.empty_cache()
-for _ in range(reps):
+for i in range(reps):
+    if i == reps - 1:
+        torch.cuda.nvtx.range_push("search")   # ncu --nvtx --nvtx-include "search/"
     idx.search(Q, spec.k, 64, spec.refine_factor)
+    if i == reps - 1:
+        torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 print("ok", idx.info()["n_slots"])
