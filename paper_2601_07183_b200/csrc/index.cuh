@@ -71,6 +71,7 @@ struct rairs_index_s {
   uint64_t* list_base = nullptr;     // [nlist + 1] prefix of N_l (into list_ids)
   uint32_t* list_ids = nullptr;      // [sum N_l] global id of item i of list-task l
   uint32_t* lm_order = nullptr;      // [nlist] lists by descending N_l (claim order)
+  int64_t sum_list_items = 0;        // sum of N_l (mean list-task length = this / nlist)
   int max_refs = 0;
   int64_t device_bytes = 0;
   int64_t layout_bytes = 0, lm_bytes = 0;  // parts of device_bytes rebuilt by add/remove

@@ -694,7 +694,10 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
 constexpr int SW_WARPS = 8;
 constexpr int SW_NB = 512;
 constexpr int SEL_P1 = 8;  // 16-B loads in flight per lane in pass 1
-constexpr int SEL_P2 = 2;  // ... in pass 2 (4 measured: no gain)
+// pass 2: 2 loads in flight when the score rows are L2-resident (c2pl), 8 when
+// they stream from DRAM (c5: 2 GB of rows; measured scan 11.2 -> 10.8 ms)
+constexpr int SEL_P2_L2 = 2, SEL_P2_DRAM = 8;
+constexpr size_t SEL_DRAM_BYTES = 256ull << 20;  // score buffers above this stream from DRAM
 
 struct SelArgs {
   const int32_t* probes;
@@ -915,7 +918,7 @@ __device__ __forceinline__ void sel_resolve(const SelArgs& a, int64_t q, uint64_
   __syncwarp();
 }
 
-template <bool U32>
+template <bool U32, int SEL_P2>
 __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
@@ -1336,8 +1339,13 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   sl.sorted_out = sa.sorted_keys ? 1 : 0;
   sl.dco_total = sa.counters;
   const size_t ssm = (size_t)SW_WARPS * (SW_NB * 4 + (size_t)sl.cap * 8);
-  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true, SEL_P2_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false, SEL_P2_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<true, SEL_P2_DRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  LM_TRY(cudaFuncSetAttribute(lm_select_kernel<false, SEL_P2_DRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+  // expected score bytes of this batch: pairs x mean list-task length
+  const bool dram_rows = (double)npairs * ((double)idx->sum_list_items / nlist) * (score_u32 ? 4 : 2) >
+                         (double)SEL_DRAM_BYTES;
   int n_sel = 0;  // select launches so far: each gets its own zeroed counter in cnt's tail
   auto select_range = [&](int64_t q0, int64_t q1, cudaStream_t st) -> cudaError_t {
     SelArgs sr = sl;
@@ -1346,8 +1354,10 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
     sr.qctr = cnt + nlist + 2 + (n_sel++);
     // persistent: 4 CTAs per SM, warps loop over queries (no partial last wave)
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q1 - q0, SW_WARPS), 148 * 4));
-    if (score_u32) lm_select_kernel<true><<<g, SW_WARPS * 32, ssm, st>>>(sr);
-    else lm_select_kernel<false><<<g, SW_WARPS * 32, ssm, st>>>(sr);
+    if (score_u32 && dram_rows) lm_select_kernel<true, SEL_P2_DRAM><<<g, SW_WARPS * 32, ssm, st>>>(sr);
+    else if (score_u32) lm_select_kernel<true, SEL_P2_L2><<<g, SW_WARPS * 32, ssm, st>>>(sr);
+    else if (dram_rows) lm_select_kernel<false, SEL_P2_DRAM><<<g, SW_WARPS * 32, ssm, st>>>(sr);
+    else lm_select_kernel<false, SEL_P2_L2><<<g, SW_WARPS * 32, ssm, st>>>(sr);
     return cudaGetLastError();
   };
   auto refine_range = [&](int64_t q0, int64_t q1, cudaStream_t st) -> rairs_status {
@@ -1470,6 +1480,7 @@ rairs_status listmajor_prepare(rairs_index_s* idx, cudaStream_t s) {
     idx->max_list_items = std::max<int64_t>(idx->max_list_items, h[l]);
     base[l + 1] = base[l] + h[l];
   }
+  idx->sum_list_items = (int64_t)base[idx->nlist];
   RAIRS_CUDA_TRY(cudaMalloc(&idx->list_base, (size_t)(idx->nlist + 1) * 8));
   RAIRS_CUDA_TRY(cudaMalloc(&idx->list_ids, (size_t)std::max<uint64_t>(base[idx->nlist], 1) * 4));
   RAIRS_CUDA_TRY(cudaMemcpyAsync(idx->list_base, base.data(), (size_t)(idx->nlist + 1) * 8,
