@@ -465,19 +465,24 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
             if (i0 + u < Wc) reinterpret_cast<float4*>(cs)[(i0 + u) * rs4 + t4] = r[u];
         }
       }
+      // the row, widened to fp64 once (exact), after the staged candidate rows
+      double* xd = reinterpret_cast<double*>(cs + (size_t)Wc * rs4 * 4 + 2 * ((Wc * rs4 * 4) & 1));
+      for (int t = lane; t < a.d; t += 32) xd[t] = (double)xr[t];
       __syncwarp();
       for (int i = lane; i < a.npow_w; i += 32) {
         if (i < Wc) {
           const float4* c4 = reinterpret_cast<const float4*>(cs) + i * rs4;
-          const float4* x4 = reinterpret_cast<const float4*>(xr);
+          const double2* x2 = reinterpret_cast<const double2*>(xd);
           double acc = 0.0;
 #pragma unroll 4
           for (int t4 = 0; t4 < d4; ++t4) {
-            const float4 cv = c4[t4], xv = __ldg(x4 + t4);
-            acc = __dadd_rn(acc, dsq_diff(xv.x, cv.x));
-            acc = __dadd_rn(acc, dsq_diff(xv.y, cv.y));
-            acc = __dadd_rn(acc, dsq_diff(xv.z, cv.z));
-            acc = __dadd_rn(acc, dsq_diff(xv.w, cv.w));
+            const float4 cv = c4[t4];
+            const double2 xa = x2[2 * t4], xb = x2[2 * t4 + 1];
+            double df;
+            df = __dsub_rn(xa.x, (double)cv.x); acc = __dadd_rn(acc, __dmul_rn(df, df));
+            df = __dsub_rn(xa.y, (double)cv.y); acc = __dadd_rn(acc, __dmul_rn(df, df));
+            df = __dsub_rn(xb.x, (double)cv.z); acc = __dadd_rn(acc, __dmul_rn(df, df));
+            df = __dsub_rn(xb.y, (double)cv.w); acc = __dadd_rn(acc, __dmul_rn(df, df));
           }
           ck[i] = dbits(acc);
           ci[i] = (uint32_t)(keys[i] & 0xFFFFFFFFu);
@@ -805,7 +810,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ca.flags = flags;
     ca.nflag = nflag;
     // candidate-row staging (coalesced loads) when it fits next to the sort buffers
-    const size_t stage_warp = round_up((size_t)std::min(W, nl) * (d + 4) * 4, 16);
+    const size_t stage_warp = round_up((size_t)std::min(W, nl) * (d + 4) * 4, 16) + (size_t)d * 8 + 16;
     ca.stage_off = round_up(csmem, 16);
     ca.stage_warp = stage_warp;
     ca.stage_rows = ((d & 3) == 0 && ca.stage_off + CT_WARPS * stage_warp <= 160 * 1024) ? 1 : 0;
