@@ -187,30 +187,53 @@ __global__ void __launch_bounds__(LW * 32, 3) lut_tiles_kernel(
   __syncthreads();
   float* mnw = smc + 16 * DSUB * M + warp * M;
   // MPL: subquantizers per lane (ceil(M_pad / 32) <= 4 on the list-major path)
-  for (int64_t q = (int64_t)blockIdx.x * LW + warp; q < nq; q += (int64_t)gridDim.x * LW) {
-    const float* qv = queries + q * d;
-    // the destination of this query's row in each probed list-task's tile:
-    // lane p (< nprobe) resolves probe p once; the row loop reads it by shuffle
-    auto dst_of = [&](int p, uint64_t& base, uint32_t& npad, uint32_t& jqo) {
-      const int l = probes[q * nprobe + p];
-      const uint32_t j = qslot[q * nprobe + p], Ql = qcnt[l];
-      const uint32_t t = j / (uint32_t)QT;
-      jqo = j - t * (uint32_t)QT;
-      npad = (t < Ql / (uint32_t)QT) ? (uint32_t)QT : ((Ql - t * QT + 15u) & ~15u);
-      base = ((uint64_t)lrow[l] + (uint64_t)t * QT) * K;
-    };
-    uint64_t dst_base = 0;
-    uint32_t dst_npad = 0, dst_jq = 0;
-    if (lane < nprobe) dst_of(lane, dst_base, dst_npad, dst_jq);
+  // the destination of query q's row in each probed list-task's tile: lane p
+  // (< nprobe) resolves probe p; the row loop reads it by shuffle
+  auto dst_of = [&](int64_t q, int p, uint64_t& base, uint32_t& npad, uint32_t& jqo) {
+    const int l = probes[q * nprobe + p];
+    const uint32_t j = qslot[q * nprobe + p], Ql = qcnt[l];
+    const uint32_t t = j / (uint32_t)QT;
+    jqo = j - t * (uint32_t)QT;
+    npad = (t < Ql / (uint32_t)QT) ? (uint32_t)QT : ((Ql - t * QT + 15u) & ~15u);
+    base = ((uint64_t)lrow[l] + (uint64_t)t * QT) * K;
+  };
+  auto load_q = [&](int64_t q, float (&qs)[MPL][DSUB]) {
+#pragma unroll
+    for (int u = 0; u < MPL; ++u) {
+      const int m = lane + 32 * u;
+#pragma unroll
+      for (int t = 0; t < DSUB; ++t) qs[u][t] = (m < M) ? __ldg(queries + q * d + m * DSUB + t) : 0.0f;
+    }
+  };
+  const int64_t qstride = (int64_t)gridDim.x * LW;
+  int64_t q = (int64_t)blockIdx.x * LW + warp;
+  // the next query's values and destinations are loaded one query ahead
+  float qsn[MPL][DSUB];
+  uint64_t dbn = 0;
+  uint32_t dnn = 0, djn = 0;
+  if (q < nq) {
+    load_q(q, qsn);
+    if (lane < nprobe) dst_of(q, lane, dbn, dnn, djn);
+  }
+  for (; q < nq; q += qstride) {
+    float qsc[MPL][DSUB];
+#pragma unroll
+    for (int u = 0; u < MPL; ++u)
+#pragma unroll
+      for (int t = 0; t < DSUB; ++t) qsc[u][t] = qsn[u][t];
+    const uint64_t dst_base = dbn;
+    const uint32_t dst_npad = dnn, dst_jq = djn;
+    if (q + qstride < nq) {
+      load_q(q + qstride, qsn);
+      if (lane < nprobe) dst_of(q + qstride, lane, dbn, dnn, djn);
+    }
     float T[MPL][16];
     float S = 0.0f;
 #pragma unroll
     for (int u = 0; u < MPL; ++u) {  // pass 1: distances, per-subquantizer min and span
       const int m = lane + 32 * u;
       if (m < M) {
-        float qs[DSUB];
-#pragma unroll
-        for (int t = 0; t < DSUB; ++t) qs[t] = __ldg(qv + m * DSUB + t);
+        const float* qs = qsc[u];
         float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -258,7 +281,7 @@ __global__ void __launch_bounds__(LW * 32, 3) lut_tiles_kernel(
             npad = __shfl_sync(0xffffffffu, dst_npad, p);
             jq = __shfl_sync(0xffffffffu, dst_jq, p);
           } else {
-            dst_of(p, base, npad, jq);
+            dst_of(q, p, base, npad, jq);
           }
           if (m >= M_pad) continue;
           *reinterpret_cast<uint4*>(tiles + base + (size_t)c * npad * 128 + jq * 128 +
