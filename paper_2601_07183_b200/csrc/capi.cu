@@ -146,6 +146,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->cnorm); cudaFree(x->certify_fallbacks); cudaFree(x->counters);
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
   cudaFree(x->lm_order);
+  cudaFree(x->codes_g); cudaFree(x->cbT); cudaFree(x->fs_ctr);
   cudaFree(x->live_bits);
   cudaFree(x->labels); cudaFree(x->lab_sorted); cudaFree(x->lab_rows);
   for (auto& st : x->aux) if (st) cudaStreamDestroy(st);
@@ -279,7 +280,8 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
       nk += 6 + 2 * chunks;  // zero, count, scan, scatter, lut_tiles, tensor + (select, refine) x chunks
       refined = true;
     } else {
-      st = launch_scan(idx, a, s);
+      a.sorted_keys = cand_ids != nullptr || cand_scores != nullptr;
+      st = launch_fastscan(idx, a, s);
       nk += 1;
       ev.mark(2);
     }
@@ -473,6 +475,8 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, c
   if (st != RAIRS_OK) return fail(st);
   st = listmajor_prepare(idx, s);
   if (st != RAIRS_OK) return fail(st);
+  st = fastscan_prepare(idx, s);
+  if (st != RAIRS_OK) return fail(st);
   B_TRY(cudaStreamSynchronize(s));
 #undef B_TRY
   *out = idx;
@@ -565,6 +569,7 @@ __global__ void live_set_range_kernel(uint32_t* __restrict__ bits, int64_t r0, i
 static rairs_status relayout(rairs_index_s* idx, cudaStream_t s) {
   RAIRS_TRY(build_layout(idx, s));
   RAIRS_TRY(listmajor_prepare(idx, s));
+  RAIRS_TRY(fastscan_prepare(idx, s));
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
   return RAIRS_OK;
 }

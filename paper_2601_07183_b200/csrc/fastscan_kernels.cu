@@ -1,0 +1,788 @@
+// fastscan_kernels.cu -- query-major 4-bit fast scan with register LUTs (A3-A6).
+//
+// One WARP per query (queries claimed from an atomic counter by persistent
+// warps), fused:
+//   A3  ComputeLookupTable (LUT P:711-716) + uint8 quantisation (O2,
+//       R2/R3): lane per subquantizer, fp32 with explicit rounding, written
+//       to the warp's shared-memory LUT (16 B per subquantizer).
+//   A4  SEIL work list (Alg. 5, order-free rule R9): every probed
+//       list's owned range, plus each of its references (owner i -> list l)
+//       whose owner is NOT probed (binary search in the sorted probe set).
+//   A5  4-bit fast scan (PQFastScan P:729-737) on the GROUP layout: lane =
+//       one 8-item nibble group, so one 32-bit code word holds the 8 items'
+//       nibbles of ONE subquantizer m and the 16-entry LUT row of m sits in
+//       four registers.  Four items are looked up per `prmt` pair (entries
+//       0-7 and 8-15 of the row, selected by the low three nibble bits), a
+//       third `prmt` in sign-replicate mode turns bit 3 of each nibble into a
+//       byte mask that blends the two, and `dp4a` (fma pipe) adds each byte
+//       into its item's exact u32 sum (R4: no wrap, any M).  Codes stream as
+//       coalesced 16-B loads (a warp reads 512 contiguous-per-block bytes per
+//       instruction), nothing is staged: each byte is used by one lane.
+//   A6  top-bigK by the unique key (s << 32 | id) (rqueue P:1645, R5): items
+//       with s <= tau are appended to a warp buffer as pre-keys (s, slot); a
+//       full buffer is cut at the bigK-th SCORE by a radix select (ties kept,
+//       no id loads); at the end the survivors' ids are loaded and the exact
+//       top-bigK set is taken (ties at the cut score ranked by id).  Massive
+//       score ties switch the query to exact mode (resolved keys, sort + cut).
+// The candidate keys then go to the exact refine (search_kernels.cu).
+//
+// The group layout (`codes_g`, built from the cell-major layout by
+// fastscan_prepare): per 32-slot block of 16*M_pad bytes, [m4 = m/4][group g
+// = (slot/8)%4][4 words, m = 4 m4 + k]; word bits 4v..4v+3 = item slot%8 = v.
+#include <algorithm>
+#include <climits>
+
+#include "index.cuh"
+
+namespace rairs {
+
+constexpr int FS_RCAP = 64;      // ranges per scan batch (per warp)
+constexpr int FS_ROUND = 256;    // items appended per warp round at most (32 lanes x 8)
+constexpr int FS_MAXW = 8;       // warps per CTA (fewer when bigK needs more shared memory)
+constexpr int FS_SLOTS = 64;     // claim-counter slots (concurrent searches)
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint8_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// 8 lookups: items v = 0..7 of one nibble word w (subquantizer m, LUT row T)
+__device__ __forceinline__ void lookup8(const uint4& T, uint32_t w, uint32_t (&acc)[8]) {
+  const uint32_t x = w & 0x77777777u;          // low three bits of each nibble
+  const uint32_t xh = __umulhi(x, 0x10000u);   // x >> 16 (items 4-7), on the fma pipe
+  const uint32_t w4 = w << 4;
+  // byte i = 0xFF iff bit 3 of nibble i: sign-replicate the byte holding it at bit 7
+  const uint32_t m0 = prmt(w4, w, 0xD9C8u);
+  const uint32_t m1 = prmt(w4, w, 0xFBEAu);
+  const uint32_t lo0 = prmt(T.x, T.y, x), hi0 = prmt(T.z, T.w, x);
+  const uint32_t lo1 = prmt(T.x, T.y, xh), hi1 = prmt(T.z, T.w, xh);
+  const uint32_t r0 = (lo0 & ~m0) | (hi0 & m0);   // one LOP3
+  const uint32_t r1 = (lo1 & ~m1) | (hi1 & m1);
+  acc[0] = __dp4a(r0, 0x00000001u, acc[0]);
+  acc[1] = __dp4a(r0, 0x00000100u, acc[1]);
+  acc[2] = __dp4a(r0, 0x00010000u, acc[2]);
+  acc[3] = __dp4a(r0, 0x01000000u, acc[3]);
+  acc[4] = __dp4a(r1, 0x00000001u, acc[4]);
+  acc[5] = __dp4a(r1, 0x00000100u, acc[5]);
+  acc[6] = __dp4a(r1, 0x00010000u, acc[6]);
+  acc[7] = __dp4a(r1, 0x01000000u, acc[7]);
+}
+
+struct FsArgs {
+  const uint8_t* codes;        // group layout
+  const uint32_t* slot_rows;
+  const uint32_t* own_off;
+  const uint32_t* own_cnt;
+  const uint32_t* ref_ptr;
+  const int32_t* ref_owner;
+  const uint32_t* ref_start;
+  const uint32_t* ref_cnt;
+  const float* cbT;            // codebook transposed [16][dsub][M]
+  int d, M, M_pad, dsub, shard_id, nshards;
+  const float* queries;
+  int64_t nq;
+  const int32_t* probes;
+  int nprobe, npp2, bigK, cap, hbits;
+  uint64_t* out_keys;
+  int64_t* dco;
+  unsigned long long* dco_total;
+  uint8_t* lut_q;
+  float* lut_a;
+  float* lut_b;
+  int sorted_out;
+  unsigned* ctr;               // [2]: query claims, warps finished (self-resetting)
+  unsigned total_warps;
+  // per-warp shared memory carve-up (bytes)
+  int o_lut, o_cand, o_hist, o_ps, o_pre, o_r0, o_rs, o_rc, o_rg, warp_bytes;
+};
+
+// ---- warp helpers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// smallest bin b of a 256-bin histogram with cumulative count >= K (K >= 1,
+// total >= K); *below = the count of the bins before b
+__device__ __forceinline__ uint32_t fs_bsel256(const uint32_t* hist, uint32_t K, uint32_t* below) {
+  const int lane = lane_id();
+  uint32_t h[8], loc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { h[i] = hist[lane * 8 + i]; loc += h[i]; }
+  const uint32_t inc = warp_incl_scan(loc);
+  const unsigned hit = __ballot_sync(0xffffffffu, inc >= K);
+  const int hl = hit ? __ffs(hit) - 1 : 31;
+  uint32_t b = 255, run = inc - loc, bl = 0;
+  if (lane == hl) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (run + h[i] >= K) { b = lane * 8 + i; bl = run; break; }
+      run += h[i];
+    }
+  }
+  *below = __shfl_sync(0xffffffffu, bl, hl);
+  return __shfl_sync(0xffffffffu, b, hl);
+}
+
+// The K-th smallest SCORE (high 32 bits) of cand[0..n), K <= n: radix select
+// over 8-bit digits of s in [0, 2^hbits).  *below = #entries with s < s*.
+__device__ uint32_t fs_kth_score(const uint64_t* cand, uint32_t n, uint32_t K, int hbits,
+                                 uint32_t* hist, uint32_t* below_out) {
+  const int lane = lane_id();
+  uint32_t lo = 0, below = 0, need = K;
+  int w = hbits;
+  for (;;) {
+    const int sh = w > 8 ? w - 8 : 0;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+    __syncwarp();
+    const uint32_t span = 1u << w;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t s = (uint32_t)(cand[i] >> 32);
+      if (s >= lo && s - lo < span) atomicAdd(&hist[(s - lo) >> sh], 1u);
+    }
+    __syncwarp();
+    uint32_t bl;
+    const uint32_t b = fs_bsel256(hist, need, &bl);
+    __syncwarp();
+    below += bl;
+    need -= bl;
+    lo += b << sh;
+    if (sh == 0) break;
+    w = sh;
+  }
+  *below_out = below;
+  return lo;
+}
+
+// stable in-place compaction of cand[0..n) to the entries with score <= smax
+__device__ __forceinline__ uint32_t fs_keep_le(uint64_t* cand, uint32_t n, uint32_t smax) {
+  const int lane = lane_id();
+  uint32_t out = 0;
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint64_t v = i < n ? cand[i] : kKeyInf;
+    const bool k = i < n && (uint32_t)(v >> 32) <= smax;
+    const unsigned bal = __ballot_sync(0xffffffffu, k);
+    __syncwarp();
+    if (k) cand[out + __popc(bal & ((1u << lane) - 1u))] = v;
+    out += __popc(bal);
+  }
+  __syncwarp();
+  return out;
+}
+
+__device__ void fs_sort_u64(uint64_t* a, int n) {  // warp bitonic, n power of two
+  const int lane = lane_id();
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (n >> 1); i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == asc) { a[lo] = y; a[hi] = x; }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ void fs_sort_i32(int32_t* a, int n) {
+  const int lane = lane_id();
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (n >> 1); i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const int32_t x = a[lo], y = a[hi];
+        if ((x > y) == asc) { a[lo] = y; a[hi] = x; }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// pre-keys (s << 32 | slot) of cand[i0..n) -> keys (s << 32 | global id)
+__device__ __forceinline__ void fs_resolve(const FsArgs& a, uint64_t* cand, uint32_t i0, uint32_t n) {
+  const int lane = lane_id();
+  for (uint32_t b = i0; b < n; b += 128) {  // four independent loads in flight per lane
+    uint64_t v[4];
+    uint32_t row[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = b + u * 32 + lane;
+      v[u] = i < n ? cand[i] : 0ull;
+      row[u] = i < n ? __ldg(a.slot_rows + (uint32_t)v[u]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = b + u * 32 + lane;
+      if (i < n)
+        cand[i] = (v[u] & 0xFFFFFFFF00000000ull) |
+                  (uint64_t)(row[u] * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ bool fs_in_sorted(const int32_t* Ps, int npp2, int32_t x) {
+  int lo = 0;  // largest index with Ps[idx] <= x, by a power-of-two descent
+  for (int step = npp2 >> 1; step > 0; step >>= 1)
+    if (Ps[lo + step] <= x) lo += step;
+  return Ps[lo] == x;
+}
+
+// O2 row of subquantizer m: T[j] = sum_t (q_t - C[m][j][t])^2, fp32 RN, ascending t
+__device__ __forceinline__ void fs_lut_row(const float* __restrict__ qv, const float* __restrict__ cbT,
+                                           int m, int M, int dsub, float (&T)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) T[j] = 0.0f;
+  for (int t = 0; t < dsub; ++t) {
+    const float qt = __ldg(qv + m * dsub + t);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float diff = __fsub_rn(qt, __ldg(cbT + ((size_t)j * dsub + t) * M + m));
+      T[j] = __fadd_rn(T[j], __fmul_rn(diff, diff));
+    }
+  }
+}
+
+// scores of one 8-item group (lane task) over all M_pad subquantizers
+template <int M4T>
+__device__ __forceinline__ void fs_score_group(const uint8_t* __restrict__ gp, const uint4* lut,
+                                               int M4, uint32_t (&acc)[8]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) acc[v] = 0u;
+  if constexpr (M4T > 0) {
+    uint4 W[M4T];
+#pragma unroll
+    for (int c = 0; c < M4T; ++c) W[c] = ldg_nc_v4(gp + c * 64);
+#pragma unroll
+    for (int c = 0; c < M4T; ++c) {
+      lookup8(lut[4 * c + 0], W[c].x, acc);
+      lookup8(lut[4 * c + 1], W[c].y, acc);
+      lookup8(lut[4 * c + 2], W[c].z, acc);
+      lookup8(lut[4 * c + 3], W[c].w, acc);
+    }
+  } else {
+    constexpr int CH = 8;
+    for (int c0 = 0; c0 < M4; c0 += CH) {
+      uint4 W[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        W[c] = (c0 + c < M4) ? ldg_nc_v4(gp + (c0 + c) * 64) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        if (c0 + c < M4) {
+          const uint4* L = lut + 4 * (c0 + c);
+          lookup8(L[0], W[c].x, acc);
+          lookup8(L[1], W[c].y, acc);
+          lookup8(L[2], W[c].z, acc);
+          lookup8(L[3], W[c].w, acc);
+        }
+      }
+    }
+  }
+}
+
+template <int M4T>
+__global__ void __launch_bounds__(FS_MAXW * 32, 2) fs_scan_kernel(FsArgs a) {
+  extern __shared__ __align__(16) uint8_t fs_smem[];
+  const int lane = lane_id(), warp = warp_id();
+  uint8_t* wb = fs_smem + (size_t)warp * a.warp_bytes;
+  uint4* lut = reinterpret_cast<uint4*>(wb + a.o_lut);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(wb + a.o_cand);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(wb + a.o_hist);
+  int32_t* Ps = reinterpret_cast<int32_t*>(wb + a.o_ps);
+  uint32_t* pre = reinterpret_cast<uint32_t*>(wb + a.o_pre);
+  uint32_t* r0s = reinterpret_cast<uint32_t*>(wb + a.o_r0);
+  uint32_t* rs = reinterpret_cast<uint32_t*>(wb + a.o_rs);
+  uint32_t* rc = reinterpret_cast<uint32_t*>(wb + a.o_rc);
+  uint32_t* rg = reinterpret_cast<uint32_t*>(wb + a.o_rg);
+  const int M = a.M, M4 = M4T > 0 ? M4T : a.M_pad / 4;
+  const uint64_t blk_bytes = 16ull * (uint64_t)a.M_pad;
+  const int np = a.nprobe;
+  const uint32_t bigK = (uint32_t)a.bigK, cap = (uint32_t)a.cap;
+  const unsigned below_me = (1u << lane) - 1u;
+  pdl_wait();  // probes of the coarse stage
+
+  for (;;) {
+    uint32_t qq = 0;
+    if (lane == 0) qq = atomicAdd(&a.ctr[0], 1u);
+    qq = __shfl_sync(0xffffffffu, qq, 0);
+    if (qq >= (uint64_t)a.nq) break;
+    const int64_t q = qq;
+    const int32_t* pq = a.probes + q * np;
+
+    // ---- probe set: sorted copy (membership, R9) + per-probe reference prefix ----
+    for (int i = lane; i < a.npp2; i += 32) Ps[i] = i < np ? __ldg(pq + i) : INT_MAX;
+    __syncwarp();
+    if (a.npp2 > 1) fs_sort_i32(Ps, a.npp2);
+    uint32_t nrefs = 0;
+    for (int i0 = 0; i0 < np; i0 += 32) {
+      const int i = i0 + lane;
+      uint32_t nr = 0, r0 = 0;
+      if (i < np) {
+        const int l = __ldg(pq + i);
+        r0 = __ldg(a.ref_ptr + l);
+        nr = __ldg(a.ref_ptr + l + 1) - r0;
+      }
+      const uint32_t inc = warp_incl_scan(nr);
+      if (i < np) { pre[i] = nrefs + inc - nr; r0s[i] = r0; }
+      nrefs += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) pre[np] = nrefs;
+
+    // ---- A3: LUT + uint8 quantisation (O2) ----
+    const float* qv = a.queries + q * a.d;
+    float* mn = reinterpret_cast<float*>(cand);  // scratch until the scan starts
+    float spanmax = 0.0f;
+    for (int m = lane; m < M; m += 32) {
+      float T[16];
+      fs_lut_row(qv, a.cbT, m, M, a.dsub, T);
+      float lo = T[0], hi = T[0];
+#pragma unroll
+      for (int j = 1; j < 16; ++j) { lo = fminf(lo, T[j]); hi = fmaxf(hi, T[j]); }
+      mn[m] = lo;
+      spanmax = fmaxf(spanmax, __fsub_rn(hi, lo));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) spanmax = fmaxf(spanmax, __shfl_xor_sync(0xffffffffu, spanmax, o));
+    const float S = spanmax;
+    const float qa = S > 0.0f ? __fdiv_rn(255.0f, S) : 1.0f;
+    __syncwarp();
+    for (int m = lane; m < a.M_pad; m += 32) {
+      uint32_t wd[4] = {0u, 0u, 0u, 0u};
+      if (m < M && S > 0.0f) {
+        float T[16];
+        fs_lut_row(qv, a.cbT, m, M, a.dsub, T);
+        const float mnm = mn[m];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T[j], mnm), qa)));
+          wd[j >> 2] |= v << (8 * (j & 3));
+        }
+      }
+      const uint4 row = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      lut[m] = row;
+      if (a.lut_q && m < M) reinterpret_cast<uint4*>(a.lut_q + (q * M + m) * 16)[0] = row;
+    }
+    if (lane == 0) {
+      if (a.lut_a) a.lut_a[q] = qa;
+      if (a.lut_b) {
+        float b = 0.0f;
+        for (int m = 0; m < M; ++m) b = __fadd_rn(b, mn[m]);
+        a.lut_b[q] = b;
+      }
+    }
+    __syncwarp();
+
+    // ---- A4 + A5 + A6: work list, scan, threshold top-bigK ----
+    uint32_t n = 0;                 // buffered candidates
+    uint32_t tau = 0xFFFFFFFFu;     // items with s > tau cannot be in the top-bigK
+    bool exact = false;             // massive ties: buffer holds resolved keys
+    uint64_t tau_key = kKeyInf;     // exact mode: keys >= tau_key are dropped
+    uint32_t my_dco = 0;
+    uint32_t nr = 0;                // ranges in the batch
+
+    auto compact = [&]() {
+      if (!exact) {
+        uint32_t below;
+        const uint32_t s_star = fs_kth_score(cand, n, bigK, a.hbits, hist, &below);
+        n = fs_keep_le(cand, n, s_star);
+        tau = s_star;
+        if (n + FS_ROUND <= cap) return;
+        // more than cap - 256 items tie at s*: resolve, sort, cut to bigK
+        fs_resolve(a, cand, 0, n);
+        exact = true;
+      }
+      for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+      __syncwarp();
+      fs_sort_u64(cand, (int)cap);
+      n = bigK;
+      tau_key = cand[bigK - 1];
+      tau = (uint32_t)(tau_key >> 32);
+    };
+
+    auto scan_batch = [&]() {
+      // group prefix of the batch's ranges
+      uint32_t ng_tot = 0;
+      for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t g = 0;
+        if (r < nr) {
+          const uint32_t st = rs[r], c = rc[r];
+          g = ((st + c - 1) >> 3) - (st >> 3) + 1;
+          my_dco += c;
+        }
+        const uint32_t inc = warp_incl_scan(g);
+        if (r < nr) rg[r] = ng_tot + inc - g;
+        ng_tot += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) rg[nr] = ng_tot;
+      __syncwarp();
+      for (uint32_t t0 = 0; t0 < ng_tot; t0 += 32) {
+        if (n + FS_ROUND > cap) compact();
+        const uint32_t t = t0 + lane;
+        const bool act = t < ng_tot;
+        uint32_t acc[8];
+        uint32_t vmask = 0, gi = 0;
+        if (act) {
+          uint32_t lo = 0, hi = nr;  // largest r with rg[r] <= t
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (rg[mid] <= t) lo = mid; else hi = mid;
+          }
+          const uint32_t st = rs[lo], en = st + rc[lo];
+          gi = (st >> 3) + (t - rg[lo]);
+          const uint32_t g0 = gi * 8u;
+          const uint32_t a0 = st > g0 ? st - g0 : 0u;
+          const uint32_t a1 = min(en - g0, 8u);
+          vmask = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
+          fs_score_group<M4T>(a.codes + (uint64_t)(gi >> 2) * blk_bytes + (gi & 3) * 16, lut, M4, acc);
+        }
+        // append (pre-key) every valid item with s <= tau
+        uint32_t pm = 0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          if (((vmask >> v) & 1u) && acc[v] <= tau) pm |= 1u << v;
+        if (exact && pm) {  // massive-tie mode: exact keys, ids resolved now (rare)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            if ((pm >> v) & 1u) {
+              const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
+              const uint64_t key = ((uint64_t)acc[v] << 32) |
+                                   (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+              if (key >= tau_key) pm &= ~(1u << v);
+            }
+          }
+        }
+        const uint32_t c = __popc(pm);
+        const uint32_t inc = warp_incl_scan(c);
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (tot) {
+          uint32_t pos = n + inc - c;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            if ((pm >> v) & 1u) {
+              uint64_t key = ((uint64_t)acc[v] << 32) | (uint64_t)(gi * 8u + v);
+              if (exact) {
+                const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
+                key = (key & 0xFFFFFFFF00000000ull) |
+                      (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+              }
+              cand[pos++] = key;
+            }
+          }
+          n += tot;
+          __syncwarp();
+        }
+      }
+      nr = 0;
+      __syncwarp();
+    };
+
+    // sources: s < np -> owned range of probe s; s >= np -> reference s - np
+    const uint32_t nsrc = (uint32_t)np + nrefs;
+    for (uint32_t s0 = 0; s0 < nsrc; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      uint32_t st = 0, cnt = 0;
+      if (s < (uint32_t)np) {
+        const int l = __ldg(pq + s);
+        st = __ldg(a.own_off + l);
+        cnt = __ldg(a.own_cnt + l);
+      } else if (s < nsrc) {
+        const uint32_t e = s - (uint32_t)np;
+        int lo = 0, hi = np;  // probe of reference e: largest i with pre[i] <= e
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] <= e) lo = mid; else hi = mid;
+        }
+        const uint32_t j = r0s[lo] + (e - pre[lo]);
+        const int32_t o = __ldg(a.ref_owner + j);
+        if (!fs_in_sorted(Ps, a.npp2, o)) {  // R9: owner not probed -> scan the cell here
+          st = __ldg(a.ref_start + j);
+          cnt = __ldg(a.ref_cnt + j);
+        }
+      }
+      const bool has = cnt > 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, has);
+      if (has) {
+        const uint32_t p = nr + __popc(bal & below_me);
+        rs[p] = st;
+        rc[p] = cnt;
+      }
+      nr += __popc(bal);
+      __syncwarp();
+      if (nr > FS_RCAP - 32) scan_batch();
+    }
+    if (nr > 0) scan_batch();
+
+    // ---- exact top-bigK of the buffer ----
+    uint32_t keep = n;
+    if (exact) {
+      for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+      __syncwarp();
+      fs_sort_u64(cand, (int)cap);
+      keep = min(n, bigK);
+    } else if (n <= bigK) {
+      fs_resolve(a, cand, 0, n);
+      if (a.sorted_out && n > 1) {
+        int p2 = 1;
+        while (p2 < (int)n) p2 <<= 1;
+        for (uint32_t i = n + lane; i < (uint32_t)p2; i += 32) cand[i] = kKeyInf;
+        __syncwarp();
+        fs_sort_u64(cand, p2);
+      }
+    } else {
+      uint32_t below;
+      const uint32_t s_star = fs_kth_score(cand, n, bigK, a.hbits, hist, &below);
+      n = fs_keep_le(cand, n, s_star);  // the `below` keys with s < s*, and the ties at s*
+      fs_resolve(a, cand, 0, n);
+      const uint32_t need = bigK - below, nt = n - below;
+      keep = bigK;
+      if (nt > need) {  // rank the ties at s* by id (R5)
+        if (nt <= 128) {
+          uint64_t* tie = reinterpret_cast<uint64_t*>(hist);  // 128 keys of scratch
+          uint32_t nk = 0, ntt = 0;
+          for (uint32_t i0 = 0; i0 < n; i0 += 32) {  // stable partition: s < s* first
+            const uint32_t i = i0 + lane;
+            const uint64_t v = i < n ? cand[i] : kKeyInf;
+            const bool lt = i < n && (uint32_t)(v >> 32) < s_star;
+            const bool eq = i < n && !lt;
+            const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
+            __syncwarp();
+            if (lt) cand[nk + __popc(bl & below_me)] = v;
+            if (eq) tie[ntt + __popc(be & below_me)] = v;
+            nk += __popc(bl);
+            ntt += __popc(be);
+          }
+          __syncwarp();
+          for (uint32_t j = nt + lane; j < 128; j += 32) tie[j] = kKeyInf;
+          __syncwarp();
+          fs_sort_u64(tie, 128);
+          for (uint32_t j = lane; j < need; j += 32) cand[below + j] = tie[j];
+        } else {  // many ties: sort the whole (resolved) buffer
+          for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+          __syncwarp();
+          fs_sort_u64(cand, (int)cap);
+        }
+      }
+      __syncwarp();
+      if (a.sorted_out) {
+        int p2 = 1;
+        while (p2 < (int)keep) p2 <<= 1;
+        for (uint32_t i = keep + lane; i < (uint32_t)p2; i += 32) cand[i] = kKeyInf;
+        __syncwarp();
+        fs_sort_u64(cand, p2);
+      }
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? cand[i] : kKeyInf;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
+    if (lane == 0) {
+      if (a.dco) a.dco[q] = (int64_t)my_dco;
+      if (a.dco_total) atomicAdd(a.dco_total, (unsigned long long)my_dco);
+    }
+    __syncwarp();
+  }
+  // the last warp out resets the claim counters for the next launch on this slot
+  if (lane == 0) {
+    const unsigned done = atomicAdd(&a.ctr[1], 1u);
+    if (done == a.total_warps - 1) {
+      atomicExch(&a.ctr[0], 0u);
+      atomicExch(&a.ctr[1], 0u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// group layout from the cell-major layout (thread per (group, m4))
+__global__ void fs_regroup_kernel(const uint64_t* __restrict__ codes64, int64_t n_groups, int NU,
+                                  int M4, uint8_t* __restrict__ codes_g) {
+  const int64_t total = n_groups * M4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = e / M4;
+    const int m4 = (int)(e - gi * M4);
+    uint32_t wd[4] = {0u, 0u, 0u, 0u};
+    for (int v = 0; v < 8; ++v) {
+      const int64_t slot = gi * 8 + v;
+      const uint64_t w = codes64[((slot >> 5) * NU + (m4 >> 2)) * 32 + (slot & 31)];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int m = 4 * m4 + k;  // nibble (m & 15) of unit m >> 4
+        wd[k] |= (uint32_t)((w >> (4 * (m & 15))) & 0xFu) << (4 * v);
+      }
+    }
+    const int64_t blk = gi >> 2;
+    uint4* dst = reinterpret_cast<uint4*>(codes_g + blk * (int64_t)(16 * 4 * M4) + (int64_t)m4 * 64 +
+                                          (gi & 3) * 16);
+    *dst = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  }
+}
+
+__global__ void fs_transpose_cb_kernel(const float* __restrict__ cb, int M, int dsub,
+                                       float* __restrict__ cbT) {
+  const int total = M * 16 * dsub;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int m = e / (16 * dsub), j = (e / dsub) % 16, t = e % dsub;
+    cbT[((size_t)j * dsub + t) * M + m] = cb[e];
+  }
+}
+
+rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s) {
+  cudaFree(idx->codes_g);
+  idx->codes_g = nullptr;
+  idx->device_bytes -= idx->fs_bytes;
+  idx->fs_bytes = 0;
+  const int64_t slots = std::max<int64_t>(idx->n_slots, 32);
+  const size_t bytes = (size_t)slots * idx->M_pad / 2;
+  RAIRS_CUDA_TRY(cudaMalloc(&idx->codes_g, bytes));
+  const int M4 = idx->M_pad / 4;
+  const int64_t groups = slots / 8;
+  const int64_t total = groups * M4;
+  fs_regroup_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 32), 256, 0, s>>>(
+      reinterpret_cast<const uint64_t*>(idx->codes), groups, idx->M_pad / 16, M4, idx->codes_g);
+  RAIRS_CHECK_LAUNCH();
+  if (!idx->cbT) {
+    RAIRS_CUDA_TRY(cudaMalloc(&idx->cbT, (size_t)idx->M * 16 * idx->dsub * 4));
+    fs_transpose_cb_kernel<<<(unsigned)ceil_div(idx->M * 16 * idx->dsub, 256), 256, 0, s>>>(
+        idx->codebook, idx->M, idx->dsub, idx->cbT);
+    RAIRS_CHECK_LAUNCH();
+    RAIRS_CUDA_TRY(cudaMalloc(&idx->fs_ctr, FS_SLOTS * 2 * sizeof(unsigned)));
+    RAIRS_CUDA_TRY(cudaMemsetAsync(idx->fs_ctr, 0, FS_SLOTS * 2 * sizeof(unsigned), s));
+    idx->device_bytes += (size_t)idx->M * 16 * idx->dsub * 4 + FS_SLOTS * 8;
+  }
+  idx->fs_bytes = bytes;
+  idx->device_bytes += bytes;
+  return RAIRS_OK;
+}
+
+// ---------------------------------------------------------------------------
+static int fs_hbits(int M) {
+  int b = 1;
+  while (((int64_t)M * 255) >> b) ++b;
+  return b;
+}
+
+struct FsPlan {
+  FsArgs a;
+  int warps;
+  size_t smem;
+};
+
+static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPlan& pl) {
+  FsArgs& p = pl.a;
+  p = FsArgs{};
+  p.codes = idx->codes_g;
+  p.slot_rows = idx->slot_rows;
+  p.own_off = idx->own_off;
+  p.own_cnt = idx->own_cnt;
+  p.ref_ptr = idx->ref_ptr;
+  p.ref_owner = idx->ref_owner;
+  p.ref_start = idx->ref_start;
+  p.ref_cnt = idx->ref_cnt;
+  p.cbT = idx->cbT;
+  p.d = idx->d;
+  p.M = idx->M;
+  p.M_pad = idx->M_pad;
+  p.dsub = idx->dsub;
+  p.shard_id = idx->shard_id;
+  p.nshards = idx->nshards;
+  p.queries = sa.queries;
+  p.nq = sa.nq;
+  p.probes = sa.probes;
+  p.nprobe = sa.nprobe;
+  p.npp2 = next_pow2(sa.nprobe);
+  p.bigK = sa.k * sa.refine_factor;
+  p.cap = next_pow2(p.bigK + FS_ROUND + 64);
+  p.hbits = fs_hbits(idx->M);
+  p.out_keys = sa.cand_keys;
+  p.dco = sa.dco;
+  p.dco_total = sa.counters;
+  p.lut_q = sa.lut_q;
+  p.lut_a = sa.lut_a;
+  p.lut_b = sa.lut_b;
+  p.sorted_out = sa.sorted_keys ? 1 : 0;
+  int o = 0;
+  auto take = [&](int bytes, int align) {
+    o = (int)round_up(o, align);
+    const int at = o;
+    o += bytes;
+    return at;
+  };
+  p.o_lut = take(idx->M_pad * 16, 16);
+  p.o_cand = take(p.cap * 8, 16);
+  p.o_hist = take(256 * 4, 16);
+  p.o_ps = take(p.npp2 * 4, 16);
+  p.o_pre = take((p.nprobe + 1) * 4, 4);
+  p.o_r0 = take(p.nprobe * 4, 4);
+  p.o_rs = take(FS_RCAP * 4, 4);
+  p.o_rc = take(FS_RCAP * 4, 4);
+  p.o_rg = take((FS_RCAP + 1) * 4, 4);
+  p.warp_bytes = (int)round_up(o, 16);
+  if (p.cap * 8 < idx->M * 4) {
+    set_error("fast scan: candidate buffer smaller than the LUT scratch");
+    return RAIRS_E_INTERNAL;
+  }
+  pl.warps = std::min<int>(FS_MAXW, (200 * 1024) / p.warp_bytes);
+  if (pl.warps < 1) {
+    set_error("fast scan: k * refine_factor / nprobe exceed the shared-memory budget");
+    return RAIRS_E_UNSUPPORTED;
+  }
+  pl.smem = (size_t)pl.warps * p.warp_bytes;
+  return RAIRS_OK;
+}
+
+template <int M4T>
+static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<M4T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pl.smem));
+  int per_sm = 0;
+  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<M4T>,
+                                                               pl.warps * 32, pl.smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t need = ceil_div(pl.a.nq, pl.warps);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148LL * per_sm));
+  pl.a.total_warps = grid * (unsigned)pl.warps;
+  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<M4T>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
+  return RAIRS_OK;
+}
+
+rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s) {
+  if (sa.nq <= 0) return RAIRS_OK;
+  if (!idx->codes_g || !idx->fs_ctr) {
+    set_error("fast scan: group layout missing");
+    return RAIRS_E_INTERNAL;
+  }
+  FsPlan pl;
+  RAIRS_TRY(fs_plan(idx, sa, pl));
+  const unsigned slot = idx->fs_slot.fetch_add(1u) % FS_SLOTS;
+  pl.a.ctr = idx->fs_ctr + 2 * slot;
+  switch (idx->M_pad / 4) {
+    case 4: return fs_launch<4>(pl, s);
+    case 8: return fs_launch<8>(pl, s);
+    case 12: return fs_launch<12>(pl, s);
+    case 16: return fs_launch<16>(pl, s);
+    case 24: return fs_launch<24>(pl, s);
+    case 32: return fs_launch<32>(pl, s);
+    default: return fs_launch<0>(pl, s);
+  }
+}
+
+}  // namespace rairs

@@ -1,6 +1,7 @@
 // index.cuh -- device-resident RAIRS index (one shard) and kernel launchers.
 #pragma once
 
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -73,6 +74,14 @@ struct rairs_index_s {
   uint32_t* lm_order = nullptr;      // [nlist] lists by descending N_l (claim order)
   int64_t sum_list_items = 0;        // sum of N_l (mean list-task length = this / nlist)
   int max_refs = 0;
+  // query-major register-LUT fast scan (fastscan_kernels.cu): the codes again in
+  // the 8-item nibble-group layout, the codebook transposed [16][dsub][M], and
+  // self-resetting query-claim counters (one pair per concurrent search slot)
+  uint8_t* codes_g = nullptr;
+  float* cbT = nullptr;
+  unsigned* fs_ctr = nullptr;
+  std::atomic<unsigned> fs_slot{0};
+  int64_t fs_bytes = 0;
   int64_t device_bytes = 0;
   int64_t layout_bytes = 0, lm_bytes = 0;  // parts of device_bytes rebuilt by add/remove
   // two auxiliary streams + fork/join events (list-major select/refine overlap)
@@ -189,7 +198,9 @@ struct SearchArgs {
   // query's bigK keys may be written in any order (the refine ranks them)
   bool sorted_keys = false;
 };
-rairs_status launch_scan(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
+// query-major register-LUT fast scan (fastscan_kernels.cu): A3-A6 fused
+rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s);
+rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 rairs_status launch_merge(const int64_t* ids, const float* dists, int G, int64_t nq, int k,
                           int64_t* out_ids, float* out_dists, cudaStream_t s);
