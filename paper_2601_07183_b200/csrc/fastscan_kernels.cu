@@ -31,6 +31,7 @@
 // = (slot/8)%4][4 words, m = 4 m4 + k]; word bits 4v..4v+3 = item slot%8 = v.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "index.cuh"
 
@@ -52,6 +53,20 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const uint8_t* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
   return v;
 }
 
@@ -103,6 +118,8 @@ struct FsArgs {
   unsigned total_warps;
   // per-warp shared memory carve-up (bytes)
   int o_lut, o_cand, o_hist, o_ps, o_pre, o_r0, o_rs, o_rc, o_rg, warp_bytes;
+  int cb_smem;                 // bytes of the per-CTA codebook copy (0: read from global)
+  int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
 // ---- warp helpers -------------------------------------------------------------
@@ -138,13 +155,13 @@ __device__ __forceinline__ uint32_t fs_bsel256(const uint32_t* hist, uint32_t K,
   return __shfl_sync(0xffffffffu, b, hl);
 }
 
-// The K-th smallest SCORE (high 32 bits) of cand[0..n), K <= n: radix select
-// over 8-bit digits of s in [0, 2^hbits).  *below = #entries with s < s*.
-__device__ uint32_t fs_kth_score(const uint64_t* cand, uint32_t n, uint32_t K, int hbits,
-                                 uint32_t* hist, uint32_t* below_out) {
+// The K-th smallest SCORE (high 32 bits) among the entries of cand[0..n) whose
+// score lies in [lo, lo + 2^w) (K <= their count): radix select over 8-bit
+// digits.  *below_out = #entries in [lo, s*).  hist = 256 words of scratch.
+__device__ __noinline__ uint32_t fs_kth_score(const uint64_t* cand, uint32_t n, uint32_t K, uint32_t lo,
+                                              int w, uint32_t* hist, uint32_t* below_out) {
   const int lane = lane_id();
-  uint32_t lo = 0, below = 0, need = K;
-  int w = hbits;
+  uint32_t below = 0, need = K;
   for (;;) {
     const int sh = w > 8 ? w - 8 : 0;
     for (int i = lane; i < 256; i += 32) hist[i] = 0u;
@@ -169,7 +186,7 @@ __device__ uint32_t fs_kth_score(const uint64_t* cand, uint32_t n, uint32_t K, i
 }
 
 // stable in-place compaction of cand[0..n) to the entries with score <= smax
-__device__ __forceinline__ uint32_t fs_keep_le(uint64_t* cand, uint32_t n, uint32_t smax) {
+__device__ __noinline__ uint32_t fs_keep_le(uint64_t* cand, uint32_t n, uint32_t smax) {
   const int lane = lane_id();
   uint32_t out = 0;
   for (uint32_t i0 = 0; i0 < n; i0 += 32) {
@@ -185,7 +202,7 @@ __device__ __forceinline__ uint32_t fs_keep_le(uint64_t* cand, uint32_t n, uint3
   return out;
 }
 
-__device__ void fs_sort_u64(uint64_t* a, int n) {  // warp bitonic, n power of two
+__device__ __noinline__ void fs_sort_u64(uint64_t* a, int n) {  // warp bitonic, n power of two
   const int lane = lane_id();
   for (int size = 2; size <= n; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -216,7 +233,7 @@ __device__ void fs_sort_i32(int32_t* a, int n) {
 }
 
 // pre-keys (s << 32 | slot) of cand[i0..n) -> keys (s << 32 | global id)
-__device__ __forceinline__ void fs_resolve(const FsArgs& a, uint64_t* cand, uint32_t i0, uint32_t n) {
+__device__ __noinline__ void fs_resolve(const FsArgs& a, uint64_t* cand, uint32_t i0, uint32_t n) {
   const int lane = lane_id();
   for (uint32_t b = i0; b < n; b += 128) {  // four independent loads in flight per lane
     uint64_t v[4];
@@ -245,64 +262,338 @@ __device__ __forceinline__ bool fs_in_sorted(const int32_t* Ps, int npp2, int32_
   return Ps[lo] == x;
 }
 
-// O2 row of subquantizer m: T[j] = sum_t (q_t - C[m][j][t])^2, fp32 RN, ascending t
-__device__ __forceinline__ void fs_lut_row(const float* __restrict__ qv, const float* __restrict__ cbT,
-                                           int m, int M, int dsub, float (&T)[16]) {
+// The lane task of a scan round: one 8-item group of a range of the batch.
+struct FsTask {
+  const uint8_t* gp;   // the group's 16-B column at m4 = 0 (a valid dummy when idle)
+  uint32_t gi;         // group index (slot / 8)
+  uint32_t vmask;      // items of the group inside the range (0 when idle)
+};
+
+__device__ __forceinline__ FsTask fs_task(uint32_t t, uint32_t ng_tot, uint32_t nr, const uint32_t* rs,
+                                          const uint32_t* rc, const uint32_t* rg, const uint8_t* codes,
+                                          uint64_t blk_bytes) {
+  FsTask k{codes, 0u, 0u};
+  if (t < ng_tot) {
+    uint32_t lo = 0, hi = nr;  // largest r with rg[r] <= t
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (rg[mid] <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t st = rs[lo], en = st + rc[lo];
+    const uint32_t gi = (st >> 3) + (t - rg[lo]);
+    const uint32_t g0 = gi * 8u;
+    const uint32_t a0 = st > g0 ? st - g0 : 0u;
+    const uint32_t a1 = min(en - g0, 8u);
+    k.vmask = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
+    k.gi = gi;
+    k.gp = codes + (uint64_t)(gi >> 2) * blk_bytes + (gi & 3) * 16;
+  }
+  return k;
+}
+
+// The lane tasks of one round (tasks t0 .. t0+31) without a per-lane search:
+// r_lo = the range holding task t0; lane j looks at the start of range
+// r_lo + j, the boundaries that fall inside the round are OR-reduced into a
+// 32-bit mask, and lane L's range is r_lo + (boundaries at positions <= L).
+// On return r_lo holds the range of task t0 + 32 (the next round's).
+__device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uint32_t ng_tot, uint32_t nr,
+                                                const uint32_t* rs, const uint32_t* rc, const uint32_t* rg,
+                                                const uint8_t* codes, uint64_t blk_bytes) {
+  const int lane = lane_id();
+  const uint32_t j = r_lo + (uint32_t)lane;
+  uint32_t bit = 0, at32 = 0;
+  if (lane > 0 && j < nr) {
+    const uint32_t d = rg[j] - t0;  // >= 1: range r_lo holds t0
+    if (d < 32) bit = 1u << d;
+    at32 = d == 32 ? 1u : 0u;
+  }
+  const uint32_t bits = __reduce_or_sync(0xffffffffu, bit);
+  const uint32_t r = r_lo + __popc(bits & (0xFFFFFFFFu >> (31 - lane)));
+  const unsigned b32 = __ballot_sync(0xffffffffu, at32 != 0);
+  FsTask k{codes, 0u, 0u};
+  const uint32_t t = t0 + (uint32_t)lane;
+  if (t < ng_tot) {
+    const uint32_t st = rs[r], en = st + rc[r];
+    const uint32_t gi = (st >> 3) + (t - rg[r]);
+    const uint32_t g0 = gi * 8u;
+    const uint32_t a0 = st > g0 ? st - g0 : 0u;
+    const uint32_t a1 = min(en - g0, 8u);
+    k.vmask = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
+    k.gi = gi;
+    k.gp = codes + (uint64_t)(gi >> 2) * blk_bytes + (gi & 3) * 16;
+  }
+  r_lo += __popc(bits) + (b32 ? 1u : 0u);
+  return k;
+}
+
+// the final top-bigK of one query's buffer (cold: one copy, not inlined)
+__device__ __noinline__ uint32_t fs_finish(const FsArgs& a, uint64_t* cand, uint32_t* hist, uint32_t n,
+                                           bool exact, int hsh) {
+  const int lane = lane_id();
+  const unsigned below_me = (1u << lane) - 1u;
+  const uint32_t bigK = (uint32_t)a.bigK, cap = (uint32_t)a.cap;
+  uint32_t keep = n;
+  if (exact) {
+    for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+    __syncwarp();
+    fs_sort_u64(cand, (int)cap);
+    return min(n, bigK);
+  }
+  if (n <= bigK) {
+    fs_resolve(a, cand, 0, n);
+    keep = n;
+  } else {
+    // level 1 from the incremental histogram (exact counts of the buffered
+    // entries for every bin up to the threshold bin), then the score inside it
+    uint32_t below1, below2;
+    const uint32_t b1 = fs_bsel256(hist, bigK, &below1);
+    __syncwarp();
+    const uint32_t s_star = fs_kth_score(cand, n, bigK - below1, b1 << hsh, hsh, hist, &below2);
+    const uint32_t below = below1 + below2;
+    n = fs_keep_le(cand, n, s_star);  // the `below` keys with s < s*, and the ties at s*
+    fs_resolve(a, cand, 0, n);
+    const uint32_t need = bigK - below, nt = n - below;
+    keep = bigK;
+    if (nt > need) {  // rank the ties at s* by id (R5)
+      if (nt <= 128) {
+        uint64_t* tie = reinterpret_cast<uint64_t*>(hist);  // 128 keys of scratch
+        uint32_t nk = 0, ntt = 0;
+        for (uint32_t i0 = 0; i0 < n; i0 += 32) {  // stable partition: s < s* first
+          const uint32_t i = i0 + lane;
+          const uint64_t v = i < n ? cand[i] : kKeyInf;
+          const bool lt = i < n && (uint32_t)(v >> 32) < s_star;
+          const bool eq = i < n && !lt;
+          const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
+          __syncwarp();
+          if (lt) cand[nk + __popc(bl & below_me)] = v;
+          if (eq) tie[ntt + __popc(be & below_me)] = v;
+          nk += __popc(bl);
+          ntt += __popc(be);
+        }
+        __syncwarp();
+        if (nt <= 32) {  // rank by counting (keys are unique)
+          const uint64_t v = (uint32_t)lane < nt ? tie[lane] : kKeyInf;
+          uint32_t rank = 0;
+          for (uint32_t j = 0; j < nt; ++j) rank += tie[j] < v ? 1u : 0u;
+          __syncwarp();
+          if ((uint32_t)lane < nt && rank < need) cand[below + rank] = v;
+        } else {
+          for (uint32_t j = nt + lane; j < 128; j += 32) tie[j] = kKeyInf;
+          __syncwarp();
+          fs_sort_u64(tie, 128);
+          for (uint32_t j = lane; j < need; j += 32) cand[below + j] = tie[j];
+        }
+      } else {  // many ties: sort the whole (resolved) buffer
+        for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+        __syncwarp();
+        fs_sort_u64(cand, (int)cap);
+      }
+    }
+  }
+  __syncwarp();
+  if (a.sorted_out && keep > 1) {
+    int p2 = 1;
+    while (p2 < (int)keep) p2 <<= 1;
+    for (uint32_t i = keep + lane; i < (uint32_t)p2; i += 32) cand[i] = kKeyInf;
+    __syncwarp();
+    fs_sort_u64(cand, p2);
+  }
+  return keep;
+}
+
+// O2 row T[m][0..15] (fp32 RN, ascending t, no FMA); cb = codebook [16][dsub][M]
+__device__ __forceinline__ void fs_lut_row(const float* __restrict__ qv, const float* cb, int m, int M,
+                                           int dsub, float (&T)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) T[j] = 0.0f;
   for (int t = 0; t < dsub; ++t) {
     const float qt = __ldg(qv + m * dsub + t);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float diff = __fsub_rn(qt, __ldg(cbT + ((size_t)j * dsub + t) * M + m));
+      const float diff = __fsub_rn(qt, cb[((size_t)j * dsub + t) * M + m]);
       T[j] = __fadd_rn(T[j], __fmul_rn(diff, diff));
     }
   }
 }
 
-// scores of one 8-item group (lane task) over all M_pad subquantizers
-template <int M4T>
-__device__ __forceinline__ void fs_score_group(const uint8_t* __restrict__ gp, const uint4* lut,
-                                               int M4, uint32_t (&acc)[8]) {
+// The O2 LUT of one query into the warp's shared memory (+ debug outputs).
+// Lane per subquantizer; pass 1 computes T (kept in `scratch` as [16][M] when
+// it fits, else recomputed in pass 2), mn_m and the span; pass 2 quantises.
+__device__ __noinline__ void fs_build_lut(const FsArgs& a, int64_t q, uint4* lut, float* scratch,
+                                          const float* cb, bool keepT) {
+  const int lane = lane_id();
+  const int M = a.M;
+  const float* qv = a.queries + q * a.d;
+  float* Ts = scratch;                          // [16][M] when keepT
+  float* mn = scratch + (keepT ? 16 * M : 0);   // [M]
+  float spanmax = 0.0f;
+  for (int m = lane; m < M; m += 32) {
+    float T[16];
+    fs_lut_row(qv, cb, m, M, a.dsub, T);
+    float lo = T[0], hi = T[0];
 #pragma unroll
-  for (int v = 0; v < 8; ++v) acc[v] = 0u;
-  if constexpr (M4T > 0) {
-    uint4 W[M4T];
+    for (int j = 1; j < 16; ++j) { lo = fminf(lo, T[j]); hi = fmaxf(hi, T[j]); }
+    if (keepT) {
 #pragma unroll
-    for (int c = 0; c < M4T; ++c) W[c] = ldg_nc_v4(gp + c * 64);
-#pragma unroll
-    for (int c = 0; c < M4T; ++c) {
-      lookup8(lut[4 * c + 0], W[c].x, acc);
-      lookup8(lut[4 * c + 1], W[c].y, acc);
-      lookup8(lut[4 * c + 2], W[c].z, acc);
-      lookup8(lut[4 * c + 3], W[c].w, acc);
+      for (int j = 0; j < 16; ++j) Ts[j * M + m] = T[j];
     }
-  } else {
-    constexpr int CH = 8;
-    for (int c0 = 0; c0 < M4; c0 += CH) {
-      uint4 W[CH];
+    mn[m] = lo;
+    spanmax = fmaxf(spanmax, __fsub_rn(hi, lo));
+  }
 #pragma unroll
-      for (int c = 0; c < CH; ++c)
-        W[c] = (c0 + c < M4) ? ldg_nc_v4(gp + (c0 + c) * 64) : make_uint4(0, 0, 0, 0);
+  for (int o = 16; o > 0; o >>= 1) spanmax = fmaxf(spanmax, __shfl_xor_sync(0xffffffffu, spanmax, o));
+  const bool pos = spanmax > 0.0f;
+  const float qa = pos ? __fdiv_rn(255.0f, spanmax) : 1.0f;
+  __syncwarp();
+  for (int m = lane; m < a.M_pad; m += 32) {
+    uint32_t wd[4] = {0u, 0u, 0u, 0u};
+    if (m < M && pos) {
+      float T[16];
+      if (keepT) {
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        if (c0 + c < M4) {
-          const uint4* L = lut + 4 * (c0 + c);
-          lookup8(L[0], W[c].x, acc);
-          lookup8(L[1], W[c].y, acc);
-          lookup8(L[2], W[c].z, acc);
-          lookup8(L[3], W[c].w, acc);
-        }
+        for (int j = 0; j < 16; ++j) T[j] = Ts[j * M + m];
+      } else {
+        fs_lut_row(qv, cb, m, M, a.dsub, T);
       }
+      const float mnm = mn[m];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T[j], mnm), qa)));
+        wd[j >> 2] |= v << (8 * (j & 3));
+      }
+    }
+    const uint4 row = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    lut[m] = row;
+    if (a.lut_q && m < M) reinterpret_cast<uint4*>(a.lut_q + (q * M + m) * 16)[0] = row;
+  }
+  if (lane == 0) {
+    if (a.lut_a) a.lut_a[q] = qa;
+    if (a.lut_b) {
+      float b = 0.0f;
+      for (int m = 0; m < M; ++m) b = __fadd_rn(b, mn[m]);
+      a.lut_b[q] = b;
+    }
+  }
+  __syncwarp();
+}
+
+// A full buffer: drop the entries above the bin threshold; if still too full,
+// cut at the exact bigK-th score (ties kept, histogram rebuilt); if even that
+// leaves too many (massive ties), switch to exact mode: resolved keys, sorted,
+// cut to bigK.  Cold path.
+struct FsSel {
+  uint32_t n;        // buffered entries
+  uint32_t bthr;     // items whose bin (s >> hsh) exceeds bthr cannot be in the top-bigK
+  uint32_t tau;      // ... nor items with s > tau
+  uint32_t hcount;   // entries counted in hist (appended so far, minus those dropped)
+  uint32_t exact;    // massive-tie mode: the buffer holds resolved keys
+  uint64_t tau_key;  // exact mode: keys >= tau_key are dropped
+};
+
+__device__ __noinline__ void fs_compact(const FsArgs& a, uint64_t* cand, uint32_t* hist, int hsh,
+                                        FsSel& st) {
+  const int lane = lane_id();
+  const uint32_t bigK = (uint32_t)a.bigK, cap = (uint32_t)a.cap;
+  if (!st.exact) {
+    // (1) drop bins above bthr
+    uint32_t out = 0;
+    for (uint32_t i0 = 0; i0 < st.n; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint64_t v = i < st.n ? cand[i] : kKeyInf;
+      const uint32_t s = (uint32_t)(v >> 32);
+      const bool k = i < st.n && (s >> hsh) <= st.bthr && s <= st.tau;
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      __syncwarp();
+      if (k) cand[out + __popc(bal & ((1u << lane) - 1u))] = v;
+      out += __popc(bal);
+    }
+    __syncwarp();
+    st.n = out;
+    if (st.n + FS_ROUND <= cap) return;
+    // (2) exact bigK-th score, ties kept; rebuild the histogram
+    uint32_t below;
+    const uint32_t s_star = fs_kth_score(cand, st.n, bigK, 0u, a.hbits, hist, &below);
+    st.n = fs_keep_le(cand, st.n, s_star);
+    st.tau = s_star;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+    __syncwarp();
+    for (uint32_t i = lane; i < st.n; i += 32) atomicAdd(&hist[(uint32_t)(cand[i] >> 32) >> hsh], 1u);
+    __syncwarp();
+    st.hcount = st.n;
+    if (st.n + FS_ROUND <= cap) return;
+    fs_resolve(a, cand, 0, st.n);
+    st.exact = 1;
+  }
+  for (uint32_t i = st.n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+  __syncwarp();
+  fs_sort_u64(cand, (int)cap);
+  st.n = bigK;
+  st.tau_key = cand[bigK - 1];
+  st.tau = (uint32_t)(st.tau_key >> 32);
+}
+
+// lane's 8 scores -> pass mask: valid items that can still be in the top-bigK
+// (s <= lim = min(tau, the largest score of bin bthr))
+__device__ __forceinline__ uint32_t fs_pass(const uint32_t (&acc)[8], uint32_t vmask, uint32_t lim) {
+  uint32_t pm = 0;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) pm |= (acc[v] <= lim ? 1u : 0u) << v;
+  return pm & vmask;
+}
+
+// exact (massive-tie) mode: drop the items whose resolved key is >= tau_key
+__device__ __forceinline__ uint32_t fs_pass_exact(const FsArgs& a, const uint32_t (&accp)[8], uint32_t pm,
+                                                  uint32_t gi, uint64_t tau_key) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    if ((pm >> v) & 1u) {
+      const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
+      const uint64_t key = ((uint64_t)accp[v] << 32) |
+                           (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+      if (key >= tau_key) pm &= ~(1u << v);
+    }
+  }
+  return pm;
+}
+
+__device__ __forceinline__ void fs_put(const FsArgs& a, uint64_t* cand, uint32_t* hist, int hsh,
+                                       const uint32_t (&acc)[8], uint32_t pm, uint32_t gi, bool exact,
+                                       uint32_t& pos) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    if ((pm >> v) & 1u) {
+      uint64_t key;
+      if (!exact) {
+        key = ((uint64_t)acc[v] << 32) | (uint64_t)(gi * 8u + v);
+        atomicAdd(&hist[acc[v] >> hsh], 1u);
+      } else {
+        const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
+        key = ((uint64_t)acc[v] << 32) | (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+      }
+      cand[pos++] = key;
     }
   }
 }
 
-template <int M4T>
-__global__ void __launch_bounds__(FS_MAXW * 32, 2) fs_scan_kernel(FsArgs a) {
+// One warp per query; see the file header.  A round scores 64 groups: lane
+// tasks t0 + lane and t0 + 32 + lane (two independent chains per lane, one
+// LUT row load per subquantizer for both).  Each group keeps a ring of two
+// 16-B code loads in flight: consuming chunk c issues chunk c + 2, which past
+// the group's end is chunk 0/1 of the lane's NEXT round's group, so a round's
+// DRAM latency overlaps the previous round's lookups.
+template <int MINB>
+__global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
   extern __shared__ __align__(16) uint8_t fs_smem[];
   const int lane = lane_id(), warp = warp_id();
-  uint8_t* wb = fs_smem + (size_t)warp * a.warp_bytes;
+  // the transposed codebook, staged once per CTA when it fits (a.cb_smem bytes)
+  float* cbs = reinterpret_cast<float*>(fs_smem);
+  if (a.cb_smem) {
+    for (int i = threadIdx.x; i < a.cb_smem / 4; i += blockDim.x) cbs[i] = __ldg(a.cbT + i);
+    __syncthreads();
+  }
+  const float* cb = a.cb_smem ? cbs : a.cbT;
+  const bool keepT = (size_t)a.M * 17 * 4 <= (size_t)a.cap * 8;
+  uint8_t* wb = fs_smem + a.cb_smem + (size_t)warp * a.warp_bytes;
   uint4* lut = reinterpret_cast<uint4*>(wb + a.o_lut);
   uint64_t* cand = reinterpret_cast<uint64_t*>(wb + a.o_cand);
   uint32_t* hist = reinterpret_cast<uint32_t*>(wb + a.o_hist);
@@ -312,10 +603,11 @@ __global__ void __launch_bounds__(FS_MAXW * 32, 2) fs_scan_kernel(FsArgs a) {
   uint32_t* rs = reinterpret_cast<uint32_t*>(wb + a.o_rs);
   uint32_t* rc = reinterpret_cast<uint32_t*>(wb + a.o_rc);
   uint32_t* rg = reinterpret_cast<uint32_t*>(wb + a.o_rg);
-  const int M = a.M, M4 = M4T > 0 ? M4T : a.M_pad / 4;
+  const int M4 = a.M_pad / 4;  // a multiple of 4 (M_pad % 16 == 0)
   const uint64_t blk_bytes = 16ull * (uint64_t)a.M_pad;
   const int np = a.nprobe;
-  const uint32_t bigK = (uint32_t)a.bigK, cap = (uint32_t)a.cap;
+  const uint32_t cap = (uint32_t)a.cap, bigK = (uint32_t)a.bigK;
+  const int hsh = a.hbits > 8 ? a.hbits - 8 : 0;  // 256 score bins
   const unsigned below_me = (1u << lane) - 1u;
   pdl_wait();  // probes of the coarse stage
 
@@ -329,6 +621,7 @@ __global__ void __launch_bounds__(FS_MAXW * 32, 2) fs_scan_kernel(FsArgs a) {
 
     // ---- probe set: sorted copy (membership, R9) + per-probe reference prefix ----
     for (int i = lane; i < a.npp2; i += 32) Ps[i] = i < np ? __ldg(pq + i) : INT_MAX;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
     __syncwarp();
     if (a.npp2 > 1) fs_sort_i32(Ps, a.npp2);
     uint32_t nrefs = 0;
@@ -346,86 +639,58 @@ __global__ void __launch_bounds__(FS_MAXW * 32, 2) fs_scan_kernel(FsArgs a) {
     }
     if (lane == 0) pre[np] = nrefs;
 
-    // ---- A3: LUT + uint8 quantisation (O2) ----
-    const float* qv = a.queries + q * a.d;
-    float* mn = reinterpret_cast<float*>(cand);  // scratch until the scan starts
-    float spanmax = 0.0f;
-    for (int m = lane; m < M; m += 32) {
-      float T[16];
-      fs_lut_row(qv, a.cbT, m, M, a.dsub, T);
-      float lo = T[0], hi = T[0];
-#pragma unroll
-      for (int j = 1; j < 16; ++j) { lo = fminf(lo, T[j]); hi = fmaxf(hi, T[j]); }
-      mn[m] = lo;
-      spanmax = fmaxf(spanmax, __fsub_rn(hi, lo));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) spanmax = fmaxf(spanmax, __shfl_xor_sync(0xffffffffu, spanmax, o));
-    const float S = spanmax;
-    const float qa = S > 0.0f ? __fdiv_rn(255.0f, S) : 1.0f;
-    __syncwarp();
-    for (int m = lane; m < a.M_pad; m += 32) {
-      uint32_t wd[4] = {0u, 0u, 0u, 0u};
-      if (m < M && S > 0.0f) {
-        float T[16];
-        fs_lut_row(qv, a.cbT, m, M, a.dsub, T);
-        const float mnm = mn[m];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T[j], mnm), qa)));
-          wd[j >> 2] |= v << (8 * (j & 3));
-        }
-      }
-      const uint4 row = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-      lut[m] = row;
-      if (a.lut_q && m < M) reinterpret_cast<uint4*>(a.lut_q + (q * M + m) * 16)[0] = row;
-    }
-    if (lane == 0) {
-      if (a.lut_a) a.lut_a[q] = qa;
-      if (a.lut_b) {
-        float b = 0.0f;
-        for (int m = 0; m < M; ++m) b = __fadd_rn(b, mn[m]);
-        a.lut_b[q] = b;
-      }
-    }
-    __syncwarp();
+    // ---- A3: LUT + uint8 quantisation (O2); T / mn scratch in the candidate buffer ----
+    if (!(a.dbg & 2)) fs_build_lut(a, q, lut, reinterpret_cast<float*>(cand), cb, keepT);
 
-    // ---- A4 + A5 + A6: work list, scan, threshold top-bigK ----
-    uint32_t n = 0;                 // buffered candidates
-    uint32_t tau = 0xFFFFFFFFu;     // items with s > tau cannot be in the top-bigK
-    bool exact = false;             // massive ties: buffer holds resolved keys
-    uint64_t tau_key = kKeyInf;     // exact mode: keys >= tau_key are dropped
+    // ---- A4 + A5 + A6 ----
+    FsSel st{0u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, kKeyInf};
     uint32_t my_dco = 0;
-    uint32_t nr = 0;                // ranges in the batch
-
-    auto compact = [&]() {
-      if (!exact) {
-        uint32_t below;
-        const uint32_t s_star = fs_kth_score(cand, n, bigK, a.hbits, hist, &below);
-        n = fs_keep_le(cand, n, s_star);
-        tau = s_star;
-        if (n + FS_ROUND <= cap) return;
-        // more than cap - 256 items tie at s*: resolve, sort, cut to bigK
-        fs_resolve(a, cand, 0, n);
-        exact = true;
+    const uint32_t nsrc = (uint32_t)np + nrefs;
+    uint32_t s0 = 0;
+    for (;;) {
+      // (1) a batch of ranges: s < np -> owned range of probe s; else reference s - np
+      uint32_t nr = 0;
+      while (s0 < nsrc && nr <= FS_RCAP - 32) {
+        const uint32_t s = s0 + lane;
+        uint32_t st0 = 0, cnt = 0;
+        if (s < (uint32_t)np) {
+          const int l = __ldg(pq + s);
+          st0 = __ldg(a.own_off + l);
+          cnt = __ldg(a.own_cnt + l);
+        } else if (s < nsrc) {
+          const uint32_t e = s - (uint32_t)np;
+          int lo = 0, hi = np;  // probe of reference e: largest i with pre[i] <= e
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= e) lo = mid; else hi = mid;
+          }
+          const uint32_t j = r0s[lo] + (e - pre[lo]);
+          const int32_t o = __ldg(a.ref_owner + j);
+          if (!fs_in_sorted(Ps, a.npp2, o)) {  // R9: owner not probed -> scan the cell here
+            st0 = __ldg(a.ref_start + j);
+            cnt = __ldg(a.ref_cnt + j);
+          }
+        }
+        const bool has = cnt > 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (has) {
+          const uint32_t p = nr + __popc(bal & below_me);
+          rs[p] = st0;
+          rc[p] = cnt;
+        }
+        nr += __popc(bal);
+        s0 += 32;
       }
-      for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
+      if (nr == 0) break;
       __syncwarp();
-      fs_sort_u64(cand, (int)cap);
-      n = bigK;
-      tau_key = cand[bigK - 1];
-      tau = (uint32_t)(tau_key >> 32);
-    };
-
-    auto scan_batch = [&]() {
-      // group prefix of the batch's ranges
+      // (2) group prefix of the batch's ranges
       uint32_t ng_tot = 0;
       for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
         const uint32_t r = r0 + lane;
         uint32_t g = 0;
         if (r < nr) {
-          const uint32_t st = rs[r], c = rc[r];
-          g = ((st + c - 1) >> 3) - (st >> 3) + 1;
+          const uint32_t sr = rs[r], c = rc[r];
+          g = ((sr + c - 1) >> 3) - (sr >> 3) + 1;
           my_dco += c;
         }
         const uint32_t inc = warp_incl_scan(g);
@@ -434,163 +699,83 @@ __global__ void __launch_bounds__(FS_MAXW * 32, 2) fs_scan_kernel(FsArgs a) {
       }
       if (lane == 0) rg[nr] = ng_tot;
       __syncwarp();
-      for (uint32_t t0 = 0; t0 < ng_tot; t0 += 32) {
-        if (n + FS_ROUND > cap) compact();
-        const uint32_t t = t0 + lane;
-        const bool act = t < ng_tot;
+      // (3) rounds of 64 groups
+      uint32_t r_lo = 0;  // range holding the first task of the next round to map
+      FsTask A = fs_round_task(0u, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
+      // ring of four chunk slots (chunk c in slot c % 4), two loads in flight
+      // ahead of the chunk being consumed; slots are renamed by unrolling (no
+      // register copies): P = chunk c, Q = c + 1, U = c + 2, V = c + 3.  (A
+      // cp.async shared-memory ring measured 2x slower.)
+      uint4 P = ldg_nc_v4(A.gp), Q = ldg_nc_v4(A.gp + 64);
+      for (uint32_t t0 = 0; t0 < ((a.dbg & 1) ? 0u : ng_tot); t0 += 32) {
+        const FsTask nA = fs_round_task(t0 + 32, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
         uint32_t acc[8];
-        uint32_t vmask = 0, gi = 0;
-        if (act) {
-          uint32_t lo = 0, hi = nr;  // largest r with rg[r] <= t
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (rg[mid] <= t) lo = mid; else hi = mid;
-          }
-          const uint32_t st = rs[lo], en = st + rc[lo];
-          gi = (st >> 3) + (t - rg[lo]);
-          const uint32_t g0 = gi * 8u;
-          const uint32_t a0 = st > g0 ? st - g0 : 0u;
-          const uint32_t a1 = min(en - g0, 8u);
-          vmask = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
-          fs_score_group<M4T>(a.codes + (uint64_t)(gi >> 2) * blk_bytes + (gi & 3) * 16, lut, M4, acc);
-        }
-        // append (pre-key) every valid item with s <= tau
-        uint32_t pm = 0;
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          if (((vmask >> v) & 1u) && acc[v] <= tau) pm |= 1u << v;
-        if (exact && pm) {  // massive-tie mode: exact keys, ids resolved now (rare)
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            if ((pm >> v) & 1u) {
-              const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
-              const uint64_t key = ((uint64_t)acc[v] << 32) |
-                                   (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
-              if (key >= tau_key) pm &= ~(1u << v);
-            }
-          }
+        for (int v = 0; v < 8; ++v) acc[v] = 0u;
+#pragma unroll 1
+        for (int c = 0; c < M4; c += 4) {
+          const uint4* L = lut + 4 * c;
+          // chunks c+2, c+3 are always in this group (M4 % 4 == 0); c+4, c+5 are
+          // the next round's chunks 0, 1 when this is the group's last period
+          const uint4 U = ldg_nc_v4(A.gp + (c + 2) * 64);
+          lookup8(L[0], P.x, acc);
+          lookup8(L[1], P.y, acc);
+          lookup8(L[2], P.z, acc);
+          lookup8(L[3], P.w, acc);
+          const uint4 V = ldg_nc_v4(A.gp + (c + 3) * 64);
+          lookup8(L[4], Q.x, acc);
+          lookup8(L[5], Q.y, acc);
+          lookup8(L[6], Q.z, acc);
+          lookup8(L[7], Q.w, acc);
+          const uint8_t* f = c + 4 >= M4 ? nA.gp : A.gp + (c + 4) * 64;
+          P = ldg_nc_v4(f);
+          lookup8(L[8], U.x, acc);
+          lookup8(L[9], U.y, acc);
+          lookup8(L[10], U.z, acc);
+          lookup8(L[11], U.w, acc);
+          Q = ldg_nc_v4(f + 64);
+          lookup8(L[12], V.x, acc);
+          lookup8(L[13], V.y, acc);
+          lookup8(L[14], V.z, acc);
+          lookup8(L[15], V.w, acc);
         }
+        if (a.dbg & 8) {  // timing experiment: no selection (scores folded into the DCO sum)
+          uint32_t x = 0;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) x += acc[v];
+          my_dco += x & 1u;
+          A = nA;
+          continue;
+        }
+        if (st.n + FS_ROUND > cap) fs_compact(a, cand, hist, hsh, st);
+        // append (pre-key s << 32 | slot) every valid item that can be in the top-bigK
+        const uint32_t lim = min(st.tau, st.bthr >= (0xFFFFFFFFu >> hsh) ? 0xFFFFFFFFu
+                                                                          : ((st.bthr + 1u) << hsh) - 1u);
+        uint32_t pm = fs_pass(acc, A.vmask, lim);
+        if (st.exact && pm) pm = fs_pass_exact(a, acc, pm, A.gi, st.tau_key);
         const uint32_t c = __popc(pm);
         const uint32_t inc = warp_incl_scan(c);
         const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
         if (tot) {
-          uint32_t pos = n + inc - c;
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            if ((pm >> v) & 1u) {
-              uint64_t key = ((uint64_t)acc[v] << 32) | (uint64_t)(gi * 8u + v);
-              if (exact) {
-                const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
-                key = (key & 0xFFFFFFFF00000000ull) |
-                      (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
-              }
-              cand[pos++] = key;
+          uint32_t pos = st.n + inc - c;
+          fs_put(a, cand, hist, hsh, acc, pm, A.gi, st.exact, pos);
+          st.n += tot;
+          __syncwarp();
+          if (!st.exact) {
+            st.hcount += tot;
+            if (st.hcount >= bigK) {  // smallest bin whose cumulative count reaches bigK
+              uint32_t bl;
+              st.bthr = fs_bsel256(hist, bigK, &bl);
             }
           }
-          n += tot;
-          __syncwarp();
         }
+        A = nA;
       }
-      nr = 0;
       __syncwarp();
-    };
-
-    // sources: s < np -> owned range of probe s; s >= np -> reference s - np
-    const uint32_t nsrc = (uint32_t)np + nrefs;
-    for (uint32_t s0 = 0; s0 < nsrc; s0 += 32) {
-      const uint32_t s = s0 + lane;
-      uint32_t st = 0, cnt = 0;
-      if (s < (uint32_t)np) {
-        const int l = __ldg(pq + s);
-        st = __ldg(a.own_off + l);
-        cnt = __ldg(a.own_cnt + l);
-      } else if (s < nsrc) {
-        const uint32_t e = s - (uint32_t)np;
-        int lo = 0, hi = np;  // probe of reference e: largest i with pre[i] <= e
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (pre[mid] <= e) lo = mid; else hi = mid;
-        }
-        const uint32_t j = r0s[lo] + (e - pre[lo]);
-        const int32_t o = __ldg(a.ref_owner + j);
-        if (!fs_in_sorted(Ps, a.npp2, o)) {  // R9: owner not probed -> scan the cell here
-          st = __ldg(a.ref_start + j);
-          cnt = __ldg(a.ref_cnt + j);
-        }
-      }
-      const bool has = cnt > 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, has);
-      if (has) {
-        const uint32_t p = nr + __popc(bal & below_me);
-        rs[p] = st;
-        rc[p] = cnt;
-      }
-      nr += __popc(bal);
-      __syncwarp();
-      if (nr > FS_RCAP - 32) scan_batch();
     }
-    if (nr > 0) scan_batch();
 
     // ---- exact top-bigK of the buffer ----
-    uint32_t keep = n;
-    if (exact) {
-      for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
-      __syncwarp();
-      fs_sort_u64(cand, (int)cap);
-      keep = min(n, bigK);
-    } else if (n <= bigK) {
-      fs_resolve(a, cand, 0, n);
-      if (a.sorted_out && n > 1) {
-        int p2 = 1;
-        while (p2 < (int)n) p2 <<= 1;
-        for (uint32_t i = n + lane; i < (uint32_t)p2; i += 32) cand[i] = kKeyInf;
-        __syncwarp();
-        fs_sort_u64(cand, p2);
-      }
-    } else {
-      uint32_t below;
-      const uint32_t s_star = fs_kth_score(cand, n, bigK, a.hbits, hist, &below);
-      n = fs_keep_le(cand, n, s_star);  // the `below` keys with s < s*, and the ties at s*
-      fs_resolve(a, cand, 0, n);
-      const uint32_t need = bigK - below, nt = n - below;
-      keep = bigK;
-      if (nt > need) {  // rank the ties at s* by id (R5)
-        if (nt <= 128) {
-          uint64_t* tie = reinterpret_cast<uint64_t*>(hist);  // 128 keys of scratch
-          uint32_t nk = 0, ntt = 0;
-          for (uint32_t i0 = 0; i0 < n; i0 += 32) {  // stable partition: s < s* first
-            const uint32_t i = i0 + lane;
-            const uint64_t v = i < n ? cand[i] : kKeyInf;
-            const bool lt = i < n && (uint32_t)(v >> 32) < s_star;
-            const bool eq = i < n && !lt;
-            const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
-            __syncwarp();
-            if (lt) cand[nk + __popc(bl & below_me)] = v;
-            if (eq) tie[ntt + __popc(be & below_me)] = v;
-            nk += __popc(bl);
-            ntt += __popc(be);
-          }
-          __syncwarp();
-          for (uint32_t j = nt + lane; j < 128; j += 32) tie[j] = kKeyInf;
-          __syncwarp();
-          fs_sort_u64(tie, 128);
-          for (uint32_t j = lane; j < need; j += 32) cand[below + j] = tie[j];
-        } else {  // many ties: sort the whole (resolved) buffer
-          for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
-          __syncwarp();
-          fs_sort_u64(cand, (int)cap);
-        }
-      }
-      __syncwarp();
-      if (a.sorted_out) {
-        int p2 = 1;
-        while (p2 < (int)keep) p2 <<= 1;
-        for (uint32_t i = keep + lane; i < (uint32_t)p2; i += 32) cand[i] = kKeyInf;
-        __syncwarp();
-        fs_sort_u64(cand, p2);
-      }
-    }
-    __syncwarp();
+    const uint32_t keep = (a.dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh);
     for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? cand[i] : kKeyInf;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
@@ -674,6 +859,17 @@ rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// experiment switch (RAIRS_FS_VARIANT): 0 = 2 CTAs/SM (128 registers) with
+// 512-entry buffers, 1 = 3 CTAs/SM (80 registers), 2 = 2 CTAs/SM with 1024
+static int fs_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RAIRS_FS_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+static int fs_capmin() { return fs_variant() == 2 ? 1024 : 512; }
+
 static int fs_hbits(int M) {
   int b = 1;
   while (((int64_t)M * 255) >> b) ++b;
@@ -710,7 +906,7 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPl
   p.nprobe = sa.nprobe;
   p.npp2 = next_pow2(sa.nprobe);
   p.bigK = sa.k * sa.refine_factor;
-  p.cap = next_pow2(p.bigK + FS_ROUND + 64);
+  p.cap = std::max(fs_capmin(), next_pow2(p.bigK + FS_ROUND + 64));
   p.hbits = fs_hbits(idx->M);
   p.out_keys = sa.cand_keys;
   p.dco = sa.dco;
@@ -719,6 +915,10 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPl
   p.lut_a = sa.lut_a;
   p.lut_b = sa.lut_b;
   p.sorted_out = sa.sorted_keys ? 1 : 0;
+  {
+    const char* e = std::getenv("RAIRS_FS_DBG");
+    p.dbg = e ? std::atoi(e) : 0;
+  }
   int o = 0;
   auto take = [&](int bytes, int align) {
     o = (int)round_up(o, align);
@@ -736,31 +936,34 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPl
   p.o_rc = take(FS_RCAP * 4, 4);
   p.o_rg = take((FS_RCAP + 1) * 4, 4);
   p.warp_bytes = (int)round_up(o, 16);
-  if (p.cap * 8 < idx->M * 4) {
+  if (p.cap * 8 < idx->M * 4 + 16) {
     set_error("fast scan: candidate buffer smaller than the LUT scratch");
     return RAIRS_E_INTERNAL;
   }
-  pl.warps = std::min<int>(FS_MAXW, (200 * 1024) / p.warp_bytes);
+  const int cbb = idx->M * 16 * idx->dsub * 4;
+  p.cb_smem = cbb <= 16 * 1024 ? cbb : 0;
+  // 3 CTAs of 8 warps per SM fit 227 KB when a warp needs <= ~9 KB
+  pl.warps = std::min<int>(FS_MAXW, (200 * 1024 - p.cb_smem) / p.warp_bytes);
   if (pl.warps < 1) {
     set_error("fast scan: k * refine_factor / nprobe exceed the shared-memory budget");
     return RAIRS_E_UNSUPPORTED;
   }
-  pl.smem = (size_t)pl.warps * p.warp_bytes;
+  pl.smem = (size_t)p.cb_smem + (size_t)pl.warps * p.warp_bytes;
   return RAIRS_OK;
 }
 
-template <int M4T>
+template <int MINB>
 static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
-  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<M4T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pl.smem));
   int per_sm = 0;
-  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<M4T>,
+  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB>,
                                                                pl.warps * 32, pl.smem));
   per_sm = std::max(per_sm, 1);
   const int64_t need = ceil_div(pl.a.nq, pl.warps);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148LL * per_sm));
   pl.a.total_warps = grid * (unsigned)pl.warps;
-  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<M4T>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
+  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
   return RAIRS_OK;
 }
 
@@ -774,15 +977,7 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
   RAIRS_TRY(fs_plan(idx, sa, pl));
   const unsigned slot = idx->fs_slot.fetch_add(1u) % FS_SLOTS;
   pl.a.ctr = idx->fs_ctr + 2 * slot;
-  switch (idx->M_pad / 4) {
-    case 4: return fs_launch<4>(pl, s);
-    case 8: return fs_launch<8>(pl, s);
-    case 12: return fs_launch<12>(pl, s);
-    case 16: return fs_launch<16>(pl, s);
-    case 24: return fs_launch<24>(pl, s);
-    case 32: return fs_launch<32>(pl, s);
-    default: return fs_launch<0>(pl, s);
-  }
+  return fs_variant() == 1 ? fs_launch<3>(pl, s) : fs_launch<2>(pl, s);
 }
 
 }  // namespace rairs
