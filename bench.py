@@ -6,15 +6,21 @@ LUT + uint8 quantisation, SEIL work list, 4-bit fast scan, top-bigK, exact
 refine; plus the NCCL all_gather + top-k merge when N > 1) over one batch of
 10,000 synthetic queries with the index resident in HBM.
 
-Default workload: BASELINE.json configs[1] shape (1M x 128, nlist 1024, PQ
-M=64 x 4-bit, k=10, refine x10) drawn by the paper-like generator "c2pl"
-(DESIGN.md "Input recipe"), at the smallest swept nprobe whose recall10@10
->= 0.95 (BJ metric "QPS at recall10@10=0.95").
+Default workload: BASELINE.json configs[3] "c4" -- the largest BJ config
+that fits one B200 with its codes streaming from HBM (10M x 96, 16,384-cluster
+anisotropic Gaussian mixture drawn on the device, nlist 16,384, PQ M=48 x
+4-bit, AIR+SEIL, k=10, refine x10) -- at the smallest swept nprobe whose
+recall10@10 >= 0.95 (BJ metric "QPS at recall10@10=0.95").  Side lines: the
+same index at k=1 (BJ configs[3] asks for k=1 and k=10), single-query
+latency, and the AIR+SEIL vs single / NaiveRA / SOARL2 / SRAIR comparison.
+Other configs: --config c2pl | c2 | c3 | c5 | ...
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N > 1: launched by torch.distributed.run, one rank per GPU; the index is
-sharded by id mod N, every rank searches its shard, results are exchanged by
-one NCCL all_gather and merged (strong scaling: total work fixed).
+--gpus N > 1 without a torch.distributed environment re-launches this script
+under `python -m torch.distributed.run --nproc-per-node N` (one rank per GPU,
+NCCL); the index is sharded by id mod N, every rank searches its shard, the
+per-shard top-k are exchanged by one NCCL all_gather and merged by the K7
+kernel (strong scaling: total work fixed).
 """
 from __future__ import annotations
 
@@ -362,16 +368,8 @@ def run_ours(args):
     peak, peak_src = load_peaks()
     scan_mode = idx.scan_path(Q.shape[0], k, chosen, rf)
     scan_ms = prof["ms"]["scan"] / max(1, prof["launches"]["scan"])
-    scan_bytes = dco_local * (spec.M // 2)             # algorithmic code bytes per launch
-    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
-    traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tp):
-        try:
-            tj = json.load(open(tp))
-            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
-        except Exception:
-            traffic = None
+    roof = scan_roofline(idx, spec, scan_mode, dco_local, Qd, k, chosen, rf, scan_ms, peak, peak_src,
+                         args.config)
 
     # ---------------- AIR + SEIL vs single assignment (the paper's comparison) ----
     vs_single = None
@@ -390,13 +388,17 @@ def run_ours(args):
         vs_single["dco_ratio_air_over_single"] = round(
             vs_single["air"]["dco_per_query"] / max(1.0, vs_single["single"]["dco_per_query"]), 3)
 
+    k1 = None
+    if world == 1 and args.k1 and k > 1:
+        k1 = side_k1(idx, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream, args.steps)
+
     updates = None
     if world == 1 and args.updates and X is not None and spec.n <= 2_000_000:
         updates = update_throughput(idx, X, spec, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(idx, X, Q, spec, chosen)
+        cpu = cpu_baseline(spec, X, Q, chosen)
 
     if rank == 0:
         info = idx.info()
@@ -416,21 +418,12 @@ def run_ours(args):
             "dco_per_query": round(dco_total / nq, 1),
             "dco_per_s": round(dco_total * args.steps / (t_ms / 1e3), 1),
             "stage_ms_per_step": {kk: round(v / args.steps, 4) for kk, v in prof["ms"].items()},
-            "roofline": {"bound": "hbm",
-                         "kernel": ("fast-scan stage A3-A6: lut_tiles_kernel + list grouping + "
-                                    "lm_tensor_kernel (tcgen05 kind::i8 one-hot x LUT) + "
-                                    "lm_select_kernel" if scan_mode == "listmajor"
-                                    else "scan_kernel (LUT + SEIL work list + fast scan + top-bigK)"),
-                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "traffic_source": traffic_src, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": scan_bytes,
-                         "algorithmic_bytes_per_unit": f"M/2 = {spec.M // 2} B per DCO",
-                         "avg_launch_ms": round(scan_ms, 4)},
+            "roofline": roof,
             "e2e": e2e, "gpu_launches": kernels,
             "coarse_uncertified_per_step": round(fallbacks / args.steps, 1),
             "latency_1q": lat,
             "air_vs_single": vs_single,
+            "k1": k1,
             "updates": updates,
             "clocks": clocks, "wall_s_timed_region": round(wall, 4),
             "build_s": round(build_s, 2), "datagen_s": round(gen_s, 2),
@@ -442,6 +435,82 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def scan_roofline(idx, spec, scan_mode, dco_local, Qd, k, nprobe, rf, scan_ms, peak, peak_src, cfg):
+    """Roofline of the fast-scan stage (A3-A6), bytes it must read per launch:
+    * query-major register-LUT scan (fs_scan_kernel): every scored item's codes
+      are read once per query that scores it -- sum_q DCO(q) * M/2 (SURVEY §8(d));
+    * list-major tensor scan: each probed list-task's codes once per batch plus
+      the score rows it materialises (written once, read twice).
+    `traffic` is the stage's DRAM bytes per launch from an ncu capture
+    (profiles/traffic_<cfg>.json), and `frac_dram` = traffic / time / peak."""
+    import torch
+    M2 = spec.M // 2
+    if scan_mode == "listmajor":
+        plist = idx.probed_list_items(Qd, k, nprobe, rf) if hasattr(idx, "probed_list_items") else None
+        code_b = (plist * M2) if plist is not None else None
+        score_b = (dco_local * 2 * 3) if plist is not None else None  # u16 rows: 1 write + 2 reads
+        alg = (code_b + score_b) if plist is not None else dco_local * M2
+        kern = ("lut_tiles_kernel + list grouping + lm_tensor_kernel (tcgen05 kind::i8 one-hot x LUT)"
+                " + lm_select_kernel")
+        unit = "probed list-task codes once per batch + u16 score rows (1 write, 2 reads)"
+    else:
+        alg = dco_local * M2
+        kern = ("fs_scan_kernel (query-major: LUT + SEIL work list + register-LUT prmt/dp4a "
+                "fast scan + top-bigK, one warp per query)")
+        unit = f"M/2 = {M2} B per DCO (each scored item's codes, once per query)"
+    achieved = alg / (scan_ms / 1e3) / 1e9
+    traffic, traffic_src, frac_dram = None, None, None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            if tj.get("scan_path") in (None, scan_mode) and tj.get("nprobe") in (None, nprobe):
+                traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
+        except Exception:
+            traffic = None
+    if traffic:
+        frac_dram = round(traffic / (scan_ms / 1e3) / 1e9 / peak, 4)
+    return {"bound": "hbm", "kernel": kern, "scan_path": scan_mode,
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "frac_dram": frac_dram,
+            "traffic_source": traffic_src, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": int(alg), "algorithmic_bytes_per_unit": unit,
+            "avg_launch_ms": round(scan_ms, 4)}
+
+
+def side_k1(idx, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream, steps):
+    """BJ configs[3] asks for k=1 as well as k=10: the same index and protocol,
+    k = 1 with K_FACTOR 10, smallest swept nprobe with
+    recall1@1 >= 0.95, device-timed steps (L2 flushed between them)."""
+    import torch
+    rf = spec.refine_factor
+    chosen, rec, sweep = None, None, []
+    for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
+        ids, dists = idx.search(Qd, 1, npb, rf)
+        r = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], 1)
+        sweep.append({"nprobe": npb, "recall": round(r, 4)})
+        chosen, rec = npb, r
+        if r >= 0.95:
+            break
+    for _ in range(3):
+        idx.search(Qd, 1, chosen, rf)
+    t = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        idx.search(Qd, 1, chosen, rf)
+        e1.record(stream)
+        e1.synchronize()
+        t += e0.elapsed_time(e1)
+    nq = Qd.shape[0]
+    return {"metric": "QPS at recall1@1>=0.95", "k": 1, "refine_factor": rf, "nprobe": chosen,
+            "recall1@1": round(rec, 4), "recall_sweep": sweep,
+            "value": round(nq * steps / (t / 1e3), 1), "unit": "queries/s",
+            "ms_per_step": round(t / steps, 4)}
 
 
 # redundant-assignment strategies compared on the same trained state (SURVEY
@@ -532,38 +601,55 @@ def update_throughput(idx, X, spec, dev):
     return out
 
 
-def cpu_baseline(idx, X, Q, spec, nprobe, max_seconds=30.0):
-    """The CPU oracle (oracle/, plain C + OpenMP, never tuned) on the host cores:
-    oracle assignment + encode of the same base from the same trained state
-    (untimed), then oracle_search timed on a bounded query sample. For the
-    device-drawn 10M/100M configs the oracle's own assignment of every row would
-    take hours on the host, so its search runs on the index's exported
-    assignment and codes instead (bit-exact to the oracle's, as the parity tests
-    pin on c1-c2); only the search is timed either way."""
+ORACLE_MAX_ROWS = 1_000_000
+# the CUDA arm's measured recall-0.95 nprobe per config (the reference arm does no sweep)
+REF_NPROBE = {"c4": 2, "c2pl": 4}
+
+
+def oracle_sample_index(spec, X, iters=4, seed=11, n_full=None):
+    """The CPU oracle's own index (oracle/: k-means + PQ training, Alg. 3
+    assignment, O5 encode) of the workload, or of a bounded uniform sample of
+    it: configs above 1M rows keep their first 1M rows (i.i.d. draws, so a
+    uniform sample) and scale nlist by the same factor, which keeps the mean
+    list size -- hence the per-query scan work at a given nprobe -- of the full
+    workload.  Nothing here comes from the CUDA path."""
     import oracle
-    from synth import GPU_KINDS
+    n = X.shape[0] if n_full is None else n_full
+    if n > ORACLE_MAX_ROWS:
+        Xs = np.ascontiguousarray(X[:ORACLE_MAX_ROWS])
+        nlist = max(1, int(round(spec.nlist * ORACLE_MAX_ROWS / n)))
+        note = (f"uniform {ORACLE_MAX_ROWS:,}-row sample of the {n:,}-row base, nlist {nlist} "
+                f"(mean list size of the full config)")
+    else:
+        Xs, nlist, note = X, spec.nlist, f"full {n:,}-row base, nlist {spec.nlist}"
+    rows = Xs[np.random.default_rng(5).permutation(Xs.shape[0])[:min(Xs.shape[0], max(32768, 32 * nlist))]]
+    cent = oracle.kmeans(rows, nlist, iters=iters, seed=seed)
+    cb = oracle.pq_train(rows, spec.M, iters=iters, seed=seed + 1)
+    l1, l2 = oracle.assign(Xs, cent, "air")
+    codes = oracle.encode(Xs, cb)
+    return Xs, l1, l2, codes, cent, cb, nlist, note
+
+
+def cpu_baseline(spec, X, Q, nprobe, target_s=10.0):
+    """The CPU oracle (oracle/, plain C + OpenMP, never tuned) on the host
+    cores, on its own index of the same workload (oracle_sample_index; build
+    untimed), oracle_search timed on a bounded query sample (~10 s)."""
+    import oracle
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    cent, cb = [t.cpu().numpy() for t in idx.export_trained()]
-    if spec.kind in GPU_KINDS:
-        l1, l2, codes = [t.cpu().numpy() for t in idx.export_assignment()]
-        how = "index-exported assignment/codes"
-    else:
-        l1, l2 = oracle.assign(X, cent, "air")
-        codes = oracle.encode(X, cb)
-        how = "oracle assignment/encode from the same trained centroids/codebook"
-    sample = 100 if spec.n > 2_000_000 else 500
+    Xs, l1, l2, codes, cent, cb, nlist, note = oracle_sample_index(spec, X)
+    sample = 100
     t0 = time.perf_counter()
-    oracle.search(X, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
+    oracle.search(Xs, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
     dt = time.perf_counter() - t0
-    if dt < 5.0:   # grow the sample toward ~10 s of CPU work, bounded by the batch
-        sample = int(min(Q.shape[0], sample * max(1.0, 10.0 / max(dt, 1e-3))))
+    if dt < target_s / 2:   # grow the sample toward ~10 s of CPU work, bounded by the batch
+        sample = int(min(Q.shape[0], sample * max(1.0, target_s / max(dt, 1e-3))))
         t0 = time.perf_counter()
-        oracle.search(X, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
+        oracle.search(Xs, l1, l2, codes, cent, cb, Q[:sample], spec.k, nprobe, spec.refine_factor)
         dt = time.perf_counter() - t0
     return {"value": round(sample / dt, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {sample} of the {Q.shape[0]} queries, nprobe {nprobe}, "
-                      f"{how} (untimed)"}
+            "sample": f"first {sample} of the {Q.shape[0]} queries, nprobe {nprobe}, oracle index "
+                      f"of the {note} (built untimed)"}
 
 
 def run_reference(args):
@@ -572,25 +658,29 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    from synth import get_config, make_dataset
+    from synth import GPU_KINDS, get_config, make_dataset
     spec = get_config(args.config, **spec_overrides(args))
-    X, Q = make_dataset(spec)
+    if spec.kind in GPU_KINDS:   # the same seeded draw as the CUDA arm (input generation only)
+        import torch
+        from synth.gpu_generators import make_dataset_torch
+        dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+        Xd, Qd = make_dataset_torch(spec, dev, n=min(spec.n, ORACLE_MAX_ROWS))
+        X, Q = Xd.cpu().numpy(), Qd.cpu().numpy()
+        del Xd, Qd
+    else:
+        X, Q = make_dataset(spec)
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    rows = X[np.random.default_rng(5).permutation(X.shape[0])[:32768]]
-    cent = oracle.kmeans(rows, spec.nlist, iters=4, seed=11)
-    cb = oracle.pq_train(rows, spec.M, iters=4, seed=12)
-    l1, l2 = oracle.assign(X, cent, args.assignment.lower())
-    codes = oracle.encode(X, cb)
-    nprobe = args.nprobe or spec.nprobe
+    Xs, l1, l2, codes, cent, cb, nlist_s, note = oracle_sample_index(spec, X, n_full=spec.n)
+    nprobe = args.nprobe or REF_NPROBE.get(spec.name, spec.nprobe)
     sample = 1000
     for _ in range(args.warmup):
-        oracle.search(X, l1, l2, codes, cent, cb, Q[:64], spec.k, nprobe, spec.refine_factor)
+        oracle.search(Xs, l1, l2, codes, cent, cb, Q[:64], spec.k, nprobe, spec.refine_factor)
     times = []
     for i in range(args.steps):
         qs = Q[(i * sample) % Q.shape[0]:][:sample]
         t0 = time.perf_counter()
-        oracle.search(X, l1, l2, codes, cent, cb, qs, spec.k, nprobe, spec.refine_factor)
+        oracle.search(Xs, l1, l2, codes, cent, cb, qs, spec.k, nprobe, spec.refine_factor)
         times.append(time.perf_counter() - t0)
     v = sample * args.steps / sum(times)
     k = spec.k
@@ -607,10 +697,11 @@ def run_reference(args):
                        "nbits": 4, "k": spec.k, "refine_factor": spec.refine_factor,
                        "nprobe": nprobe, "assignment": args.assignment + "+SEIL(cell-major)",
                        "parallelism": f"CPU oracle, {cores} host threads",
-                       "queries_per_step": sample},
+                       "queries_per_step": sample, "oracle_index": note},
             "cpu_baseline": {"value": round(v, 2), "unit": "queries/s", "cores": cores,
                              "kind": "oracle",
-                             "sample": f"{sample} queries per step (bounded sample of the 10k batch)"},
+                             "sample": f"{sample} queries per step (bounded sample of the 10k batch) "
+                                       f"on the oracle index of the {note}"},
             "e2e": {"value": round(v, 2), "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -622,7 +713,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2pl")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--assignment", default="AIR", choices=["AIR", "single"])
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--k", type=int, default=None,
@@ -638,9 +729,21 @@ def main():
                     help="single-query searches timed for p50/p99 latency (0 = skip)")
     ap.add_argument("--gt-queries", type=int, default=0,
                     help="queries with exact ground truth for recall (0 = all)")
+    ap.add_argument("--k1", type=int, default=1,
+                    help="side line: the same index at k=1 (BJ configs[3]: k=1 and k=10)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (NCCL ranks)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+               "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:
