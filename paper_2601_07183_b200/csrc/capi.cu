@@ -281,7 +281,17 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
       refined = true;
     } else {
       a.sorted_keys = cand_ids != nullptr || cand_scores != nullptr;
-      st = launch_fastscan(idx, a, s);
+      uint4* luts = nullptr;
+      cudaError_t le = cudaMallocAsync(&luts, (size_t)nq * idx->M_pad * 16, s);
+      if (le != cudaSuccess) {
+        set_error(std::string("workspace: ") + cudaGetErrorString(le));
+        st = RAIRS_E_OOM;
+      } else {
+        a.luts = luts;
+        st = launch_fastscan(idx, a, s);
+        nk += 1;  // + the LUT kernel
+        cudaFreeAsync(luts, s);
+      }
       nk += 1;
       ev.mark(2);
     }

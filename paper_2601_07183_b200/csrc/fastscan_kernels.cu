@@ -70,6 +70,10 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // 8 lookups: items v = 0..7 of one nibble word w (subquantizer m, LUT row T)
 __device__ __forceinline__ void lookup8(const uint4& T, uint32_t w, uint32_t (&acc)[8]) {
   const uint32_t x = w & 0x77777777u;          // low three bits of each nibble
@@ -118,7 +122,8 @@ struct FsArgs {
   unsigned total_warps;
   // per-warp shared memory carve-up (bytes)
   int o_lut, o_cand, o_hist, o_ps, o_pre, o_r0, o_rs, o_rc, o_rg, warp_bytes;
-  int cb_smem;                 // bytes of the per-CTA codebook copy (0: read from global)
+  int cb_smem;                 // fs_lut_kernel: bytes of the per-CTA codebook copy (0: global)
+  const uint4* luts;           // [nq][M_pad] quantised LUT rows (fs_lut_kernel)
   int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
@@ -575,6 +580,31 @@ __device__ __forceinline__ void fs_put(const FsArgs& a, uint64_t* cand, uint32_t
   }
 }
 
+// A3 for every query of the batch, one warp per query (O2: lane per
+// subquantizer, fp32 RN, ascending t; see fs_build_lut), into luts[q][M_pad].
+// Needs only the queries, so under programmatic dependent launch it overlaps
+// the coarse stage; it waits for that stage (griddepcontrol.wait) only before
+// it exits, so its completion implies the probes are ready for the scan.
+constexpr int FL_WARPS = 8;
+__global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(FsArgs a, uint4* luts) {
+  extern __shared__ __align__(16) uint8_t fl_smem[];
+  const int lane = lane_id(), warp = warp_id();
+  float* cbs = reinterpret_cast<float*>(fl_smem);
+  if (a.cb_smem) {
+    for (int i = threadIdx.x; i < a.cb_smem / 4; i += blockDim.x) cbs[i] = __ldg(a.cbT + i);
+    __syncthreads();
+  }
+  const float* cb = a.cb_smem ? cbs : a.cbT;
+  const bool keepT = a.M * 17 <= 16 * 1024 / 4;  // [16][M] + [M] floats of scratch fit 16 KB
+  float* scratch = reinterpret_cast<float*>(fl_smem + a.cb_smem) + (size_t)warp * (keepT ? 17 * a.M : a.M);
+  for (int64_t q = (int64_t)blockIdx.x * FL_WARPS + warp; q < a.nq; q += (int64_t)gridDim.x * FL_WARPS) {
+    fs_build_lut(a, q, luts + q * a.M_pad, scratch, cb, keepT);
+    (void)lane;
+  }
+  pdl_wait();     // the coarse stage's probes are complete before this grid is
+  pdl_trigger();
+}
+
 // One warp per query; see the file header.  A round scores 64 groups: lane
 // tasks t0 + lane and t0 + 32 + lane (two independent chains per lane, one
 // LUT row load per subquantizer for both).  Each group keeps a ring of two
@@ -585,15 +615,7 @@ template <int MINB>
 __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
   extern __shared__ __align__(16) uint8_t fs_smem[];
   const int lane = lane_id(), warp = warp_id();
-  // the transposed codebook, staged once per CTA when it fits (a.cb_smem bytes)
-  float* cbs = reinterpret_cast<float*>(fs_smem);
-  if (a.cb_smem) {
-    for (int i = threadIdx.x; i < a.cb_smem / 4; i += blockDim.x) cbs[i] = __ldg(a.cbT + i);
-    __syncthreads();
-  }
-  const float* cb = a.cb_smem ? cbs : a.cbT;
-  const bool keepT = (size_t)a.M * 17 * 4 <= (size_t)a.cap * 8;
-  uint8_t* wb = fs_smem + a.cb_smem + (size_t)warp * a.warp_bytes;
+  uint8_t* wb = fs_smem + (size_t)warp * a.warp_bytes;
   uint4* lut = reinterpret_cast<uint4*>(wb + a.o_lut);
   uint64_t* cand = reinterpret_cast<uint64_t*>(wb + a.o_cand);
   uint32_t* hist = reinterpret_cast<uint32_t*>(wb + a.o_hist);
@@ -640,7 +662,11 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
     if (lane == 0) pre[np] = nrefs;
 
     // ---- A3: LUT + uint8 quantisation (O2); T / mn scratch in the candidate buffer ----
-    if (!(a.dbg & 2)) fs_build_lut(a, q, lut, reinterpret_cast<float*>(cand), cb, keepT);
+    {  // the query's LUT (fs_lut_kernel) into the warp's shared memory
+      const uint4* src_lut = a.luts + q * a.M_pad;
+      for (int m = lane; m < a.M_pad; m += 32) lut[m] = __ldg(src_lut + m);
+      __syncwarp();
+    }
 
     // ---- A4 + A5 + A6 ----
     FsSel st{0u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, kKeyInf};
@@ -702,42 +728,51 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
       // (3) rounds of 64 groups
       uint32_t r_lo = 0;  // range holding the first task of the next round to map
       FsTask A = fs_round_task(0u, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
-      // ring of four chunk slots (chunk c in slot c % 4), two loads in flight
-      // ahead of the chunk being consumed; slots are renamed by unrolling (no
-      // register copies): P = chunk c, Q = c + 1, U = c + 2, V = c + 3.  (A
-      // cp.async shared-memory ring measured 2x slower.)
+      // ring of four loop-carried chunk slots P, Q, U, V (chunk c in slot c % 4):
+      // three chunks in flight ahead of the one being consumed, no register
+      // copies.  (A cp.async shared-memory ring measured 2x slower.)
       uint4 P = ldg_nc_v4(A.gp), Q = ldg_nc_v4(A.gp + 64);
+      uint4 U = ldg_nc_v4(A.gp + 128), V = ldg_nc_v4(A.gp + 192);
       for (uint32_t t0 = 0; t0 < ((a.dbg & 1) ? 0u : ng_tot); t0 += 32) {
         const FsTask nA = fs_round_task(t0 + 32, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
+        // the next round's group into L2 now (one round ahead of its loads): the
+        // register ring alone covers L2 latency, not DRAM's
+        if (!(a.dbg & 16))
+          for (int c = 8; c < M4; c += 2) prefetch_l2(nA.gp + c * 64);
         uint32_t acc[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) acc[v] = 0u;
 #pragma unroll 1
         for (int c = 0; c < M4; c += 4) {
           const uint4* L = lut + 4 * c;
-          // chunks c+2, c+3 are always in this group (M4 % 4 == 0); c+4, c+5 are
-          // the next round's chunks 0, 1 when this is the group's last period
-          const uint4 U = ldg_nc_v4(A.gp + (c + 2) * 64);
+          // each slot is refilled right after it is consumed, with the chunk four
+          // ahead: c+4..c+7 of this group, or (at its end; M4 % 4 == 0) chunks
+          // 0..3 of the lane's next-round group
+          const uint8_t* f = c + 4 < M4 ? A.gp + (c + 4) * 64 : nA.gp;
+          if (a.dbg & 32) {  // timing experiment: no code loads (synthetic words)
+            P = make_uint4(c, c * 3u, c * 5u, c * 7u);
+            Q = P; U = P; V = P;
+          }
           lookup8(L[0], P.x, acc);
           lookup8(L[1], P.y, acc);
           lookup8(L[2], P.z, acc);
           lookup8(L[3], P.w, acc);
-          const uint4 V = ldg_nc_v4(A.gp + (c + 3) * 64);
+          if (!(a.dbg & 32)) P = ldg_nc_v4(f);
           lookup8(L[4], Q.x, acc);
           lookup8(L[5], Q.y, acc);
           lookup8(L[6], Q.z, acc);
           lookup8(L[7], Q.w, acc);
-          const uint8_t* f = c + 4 >= M4 ? nA.gp : A.gp + (c + 4) * 64;
-          P = ldg_nc_v4(f);
+          if (!(a.dbg & 32)) Q = ldg_nc_v4(f + 64);
           lookup8(L[8], U.x, acc);
           lookup8(L[9], U.y, acc);
           lookup8(L[10], U.z, acc);
           lookup8(L[11], U.w, acc);
-          Q = ldg_nc_v4(f + 64);
+          if (!(a.dbg & 32)) U = ldg_nc_v4(f + 128);
           lookup8(L[12], V.x, acc);
           lookup8(L[13], V.y, acc);
           lookup8(L[14], V.z, acc);
           lookup8(L[15], V.w, acc);
+          if (!(a.dbg & 32)) V = ldg_nc_v4(f + 192);
         }
         if (a.dbg & 8) {  // timing experiment: no selection (scores folded into the DCO sum)
           uint32_t x = 0;
@@ -942,13 +977,13 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPl
   }
   const int cbb = idx->M * 16 * idx->dsub * 4;
   p.cb_smem = cbb <= 16 * 1024 ? cbb : 0;
-  // 3 CTAs of 8 warps per SM fit 227 KB when a warp needs <= ~9 KB
-  pl.warps = std::min<int>(FS_MAXW, (200 * 1024 - p.cb_smem) / p.warp_bytes);
+  p.luts = sa.luts;
+  pl.warps = std::min<int>(FS_MAXW, (200 * 1024) / p.warp_bytes);
   if (pl.warps < 1) {
     set_error("fast scan: k * refine_factor / nprobe exceed the shared-memory budget");
     return RAIRS_E_UNSUPPORTED;
   }
-  pl.smem = (size_t)p.cb_smem + (size_t)pl.warps * p.warp_bytes;
+  pl.smem = (size_t)pl.warps * p.warp_bytes;
   return RAIRS_OK;
 }
 
@@ -969,14 +1004,23 @@ static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
 
 rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s) {
   if (sa.nq <= 0) return RAIRS_OK;
-  if (!idx->codes_g || !idx->fs_ctr) {
-    set_error("fast scan: group layout missing");
+  if (!idx->codes_g || !idx->fs_ctr || !sa.luts) {
+    set_error("fast scan: group layout or LUT workspace missing");
     return RAIRS_E_INTERNAL;
   }
   FsPlan pl;
   RAIRS_TRY(fs_plan(idx, sa, pl));
   const unsigned slot = idx->fs_slot.fetch_add(1u) % FS_SLOTS;
   pl.a.ctr = idx->fs_ctr + 2 * slot;
+  {  // A3 for the whole batch (overlaps the coarse stage's tail under PDL)
+    const bool keepT = idx->M * 17 <= 16 * 1024 / 4;
+    const size_t lsm = (size_t)pl.a.cb_smem + (size_t)FL_WARPS * (keepT ? 17 : 1) * idx->M * 4;
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lsm));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FL_WARPS), 148 * 8));
+    RAIRS_CUDA_TRY(launch_pdl(fs_lut_kernel, dim3(g), dim3(FL_WARPS * 32), lsm, s, pl.a,
+                              const_cast<uint4*>(sa.luts)));
+  }
   return fs_variant() == 1 ? fs_launch<3>(pl, s) : fs_launch<2>(pl, s);
 }
 

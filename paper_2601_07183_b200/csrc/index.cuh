@@ -197,6 +197,7 @@ struct SearchArgs {
   // candidate keys wanted in (s, id) order (debug outputs); otherwise each
   // query's bigK keys may be written in any order (the refine ranks them)
   bool sorted_keys = false;
+  const uint4* luts = nullptr;  // fast scan: [nq][M_pad] LUT rows workspace (16 B each)
 };
 // query-major register-LUT fast scan (fastscan_kernels.cu): A3-A6 fused
 rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s);
