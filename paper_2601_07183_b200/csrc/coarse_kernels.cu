@@ -18,6 +18,7 @@
 //     single assignment (build).  Results are always exactly O1 / O4.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -42,6 +43,8 @@ struct TopWArgs {
   int64_t rows;
   int nl, d, Wp1, nsplit, tiles_per_split, ntiles, nstage;
   const float* cnorm;  // [round_up(nl, 256)], +inf padding
+  int dbg;             // timing experiments (RAIRS_COARSE_DBG): 1 = no epilogue work
+  int a_res;           // the A tile (all K-chunks) stays resident in shared memory
   // output entries per (row, split): 32 on the register path (sorted), Wp1
   // on the shared-memory path (unsorted)
   float* out_v;        // [rows][nsplit][Wout]
@@ -75,8 +78,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
   const int S = a.nstage, Wp1 = a.Wp1;
+  const int nk = (a.d + FT_BK - 1) / FT_BK;
+  // a_res: the row tile's A (all nk K-chunks) is loaded ONCE and stays resident
+  // (every column tile of the CTA reuses it); the ring then carries B only
   uint8_t* sA = smem;
-  uint8_t* sB = smem + S * FT_A_BYTES;
+  uint8_t* sB = smem + (a.a_res ? nk : S) * FT_A_BYTES;
   float* lv = reinterpret_cast<float*>(sB + S * FT_B_BYTES);  // smem path only
   uint32_t* li = reinterpret_cast<uint32_t*>(lv + (KR > 0 ? 0 : Wp1 * FT_BM));
   // g staging: [32][128] on the shared-memory path (warps 0-3), [32][256] on the
@@ -86,14 +92,14 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* afull = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(afull + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m0 = (int64_t)blockIdx.x * FT_BM;
   const int split = blockIdx.y;
   const int t_begin = split * a.tiles_per_split;
   const int ntile = min(a.ntiles, t_begin + a.tiles_per_split) - t_begin;
-  const int nk = (a.d + FT_BK - 1) / FT_BK;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -104,6 +110,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       mbar_init(&tfull[k], 1);
       mbar_init(&tempty[k], FT_EPI_WARPS);
     }
+    mbar_init(afull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (KR == 0 && warp < 4) {  // smem path: column half 0 only (see launcher)
@@ -120,13 +127,21 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   if (warp == FT_PROD_WARP) {
     if (lane == 0 && ntile > 0) {  // TMA producer
       int it = 0;
+      if (a.a_res) {
+        mbar_expect_tx(afull, (uint32_t)nk * FT_A_BYTES);
+        for (int kc = 0; kc < nk; ++kc) tma_load_2d(sA + kc * FT_A_BYTES, &tmA, kc * FT_BK, (int)m0, afull);
+      }
       for (int t = 0; t < ntile; ++t) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % S;
           const uint32_t ph = (uint32_t)(it / S) & 1u;
           if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
-          mbar_expect_tx(&full[s], FT_A_BYTES + FT_B_BYTES);
-          tma_load_2d(sA + s * FT_A_BYTES, &tmA, kc * FT_BK, (int)m0, &full[s]);
+          if (a.a_res) {
+            mbar_expect_tx(&full[s], FT_B_BYTES);
+          } else {
+            mbar_expect_tx(&full[s], FT_A_BYTES + FT_B_BYTES);
+            tma_load_2d(sA + s * FT_A_BYTES, &tmA, kc * FT_BK, (int)m0, &full[s]);
+          }
           tma_load_2d(sB + s * FT_B_BYTES, &tmB, kc * FT_BK, (t_begin + t) * FT_BN, &full[s]);
         }
       }
@@ -135,6 +150,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   } else if (warp == FT_MMA_WARP) {
     if (lane == 0 && ntile > 0) {  // MMA issuer
       int it = 0;
+      if (a.a_res) mbar_wait(afull, 0u);
       for (int t = 0; t < ntile; ++t) {
         const int acc = t & 1;
         const uint32_t aph = (uint32_t)(t >> 1) & 1u;
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
           const uint32_t ph = (uint32_t)(it / S) & 1u;
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(sA + s * FT_A_BYTES);
+          const uint64_t ad = umma_desc_sw128(sA + (a.a_res ? kc : s) * FT_A_BYTES);
           const uint64_t bd = umma_desc_sw128(sB + s * FT_B_BYTES);
 #pragma unroll
           for (int k = 0; k < FT_BK / 8; ++k)  // K = 8 tf32 per MMA = 32 B = +2 desc units
@@ -177,16 +193,35 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int col0 = (t_begin + t) * FT_BN;
-      for (int c = half * (FT_BN / 32 / FT_HALVES); c < (half + 1) * (FT_BN / 32 / FT_HALVES); ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * FT_BN + c * 32), v);
-        uint32_t pass = 0;
+      // TMEM reads are the epilogue's bound (LDTM ~64 B/clk/SM): the next chunk's
+      // tcgen05.ld is in flight while this one is processed, and the
+      // accumulator is released as soon as the last chunk is in registers
+      auto process = [&](uint32_t (&v)[32], int c) {
+        if ((a.dbg & 1) && t > 0) return;  // timing experiment: MMA + TMA only after tile 0
+        // g = ||c||^2 - 2 q.c; ||c||^2 of the chunk's 32 columns by 8 broadcast
+        // 16-B loads; the chunk minimum decides (warp-wide) whether any value
+        // can enter a list -- the common case after the first tiles costs one
+        // FFMA + one FMNMX per value
+        const float4* cn4 = reinterpret_cast<const float4*>(a.cnorm + col0 + c * 32);
+        float g[32];
+        float gmin = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 cn = __ldg(cn4 + q4);
+          g[4 * q4 + 0] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 0]), cn.x);
+          g[4 * q4 + 1] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 1]), cn.y);
+          g[4 * q4 + 2] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 2]), cn.z);
+          g[4 * q4 + 3] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 3]), cn.w);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) gmin = fminf(gmin, g[j]);
         const float thr = rv[KR - 1];
+        if (!__any_sync(0xffffffffu, gmin < thr)) return;
+        uint32_t pass = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float g = __ldg(a.cnorm + col0 + c * 32 + j) - 2.0f * __uint_as_float(v[j]);
-          if (g < thr) {  // only candidates are staged for the insertion loop
-            gbuf[j * (FT_BM * FT_HALVES) + warp * 32 + lane] = g;
+          if (g[j] < thr) {  // only candidates are staged for the insertion loop
+            gbuf[j * (FT_BM * FT_HALVES) + warp * 32 + lane] = g[j];
             pass |= 1u << j;
           }
         }
@@ -208,10 +243,30 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
             }
           }
         }
+            };
+      constexpr int CPW = FT_BN / 32 / FT_HALVES;  // chunks per warp per tile (4)
+      static_assert(CPW % 2 == 0, "chunks come in pairs");
+      const int cb = half * CPW;
+      const uint32_t tbase = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * FT_BN);
+      uint32_t va[32], vb[32];
+      tmem_ld32_nowait(tbase + (uint32_t)(cb * 32), va);
+      tmem_wait_ld();
+#pragma unroll 1
+      for (int c = cb; c < cb + CPW; c += 2) {
+        tmem_ld32_nowait(tbase + (uint32_t)((c + 1) * 32), vb);
+        process(va, c);
+        tmem_wait_ld();
+        if (c + 2 < cb + CPW) {
+          tmem_ld32_nowait(tbase + (uint32_t)((c + 2) * 32), va);
+          process(vb, c + 1);
+          tmem_wait_ld();
+        } else {  // every chunk of this tile is in registers: release the accumulator
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          process(vb, c + 1);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     const int64_t row = m0 + rrow;
     if (row < a.rows) {
@@ -684,13 +739,23 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
                : Wp1 <= 24 ? 24 : 32;
   const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
   const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
-  const int nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
-  if (1024 + (size_t)nstage * (FT_A_BYTES + FT_B_BYTES) + lists_bytes + 256 > 227 * 1024) {
+  const int nkc = (int)ceil_div(d, FT_BK);
+  // A resident (loaded once per CTA) when it fits next to >= 3 B stages: the
+  // ring then moves 2/3 of the bytes per column tile (the TMA ingest bound)
+  const bool a_res = (size_t)nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2048 <= 227 * 1024;
+  int nstage;
+  if (a_res) {
+    nstage = (int)std::min<size_t>(6, (227 * 1024 - 2048 - lists_bytes - (size_t)nkc * FT_A_BYTES) / FT_B_BYTES);
+  } else {
+    nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
+  }
+  const size_t ring_bytes = a_res ? (size_t)nkc * FT_A_BYTES + (size_t)nstage * FT_B_BYTES
+                                  : (size_t)nstage * (FT_A_BYTES + FT_B_BYTES);
+  if (1024 + ring_bytes + lists_bytes + 256 > 227 * 1024) {
     set_error("coarse: shared memory budget exceeded");
     return RAIRS_E_UNSUPPORTED;
   }
-  const size_t smem = 1024 + (size_t)nstage * (FT_A_BYTES + FT_B_BYTES) + lists_bytes +
-                      (2 * nstage + 4) * 8 + 16;
+  const size_t smem = 1024 + ring_bytes + lists_bytes + (2 * nstage + 5) * 8 + 16;
   static bool attr_set = false;
   if (!attr_set) {
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<0>,
@@ -758,7 +823,12 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ta.tiles_per_split = tps;
     ta.ntiles = ntiles;
     ta.nstage = nstage;
+    ta.a_res = a_res ? 1 : 0;
     ta.cnorm = idx->cnorm;
+    {
+      const char* e = std::getenv("RAIRS_COARSE_DBG");
+      ta.dbg = e ? std::atoi(e) : 0;
+    }
     ta.out_v = vals;
     ta.out_i = ids;
     const dim3 tgrid((unsigned)mtiles, (unsigned)nsplit);

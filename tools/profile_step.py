@@ -29,6 +29,8 @@ else:
 idx = rb.build_index(Xd, spec.nlist, spec.M, **kw)
 del Xd
 idx.set_scan_mode(mode)
+if os.environ.get("COARSE_DBG"):  # timing experiments of the search's coarse kernel only
+    os.environ["RAIRS_COARSE_DBG"] = os.environ["COARSE_DBG"]
 torch.cuda.synchronize()
 for i in range(reps):
     if i == reps - 1:

@@ -25,6 +25,8 @@ else:
 idx = rb.build_index(Xd, spec.nlist, spec.M, **kw)
 del Xd
 mode = os.environ.get("SCAN_MODE", "auto")
+if os.environ.get("COARSE_DBG"):  # timing experiments of the search's coarse kernel only
+    os.environ["RAIRS_COARSE_DBG"] = os.environ["COARSE_DBG"]
 idx.set_scan_mode(mode)
 flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
 for _ in range(3):
