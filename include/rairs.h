@@ -199,8 +199,9 @@ rairs_status rairs_search_debug(rairs_index_t idx, const float* queries, int64_t
 
 /* ---- shard merge (K7) -----------------------------------------------------
  * ids/dists: dev [G x nq x k] (per-shard results, e.g. after an NCCL
- * all_gather).  Output: dev [nq x k], the first k of the union by (dist, id),
- * padded with (-1, +inf).  O11. */
+ * all_gather); ids are full 64-bit values (any id >= 0; negative = padding).
+ * Output: dev [nq x k], the first k of the union by (dist, id), padded with
+ * (-1, +inf).  O11.  G * k <= 16384 (UNSUPPORTED otherwise). */
 rairs_status rairs_merge_topk(const int64_t* ids, const float* dists, int32_t G, int64_t nq,
                               int32_t k, int64_t* out_ids, float* out_dists, void* stream);
 

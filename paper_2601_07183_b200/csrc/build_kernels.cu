@@ -895,19 +895,47 @@ __global__ void refs_finalize_kernel(const uint64_t* __restrict__ rk_sorted,
   }
 }
 
+// The previous layout of a rebuild (rairs_add / rairs_remove_ids) is kept until
+// the new one is complete: on any failure the index keeps its old layout.
+struct LayoutStash {
+  rairs_index_s* idx;
+  uint32_t *own_off, *own_cnt, *slot_rows, *ref_ptr, *ref_start, *ref_cnt;
+  int32_t* ref_owner;
+  uint8_t* codes;
+  int64_t n_slots, n_refs, n_cells, n_double, layout_bytes;
+  int max_refs;
+  bool committed = false;
+  explicit LayoutStash(rairs_index_s* x)
+      : idx(x), own_off(x->own_off), own_cnt(x->own_cnt), slot_rows(x->slot_rows),
+        ref_ptr(x->ref_ptr), ref_start(x->ref_start), ref_cnt(x->ref_cnt), ref_owner(x->ref_owner),
+        codes(x->codes), n_slots(x->n_slots), n_refs(x->n_refs), n_cells(x->n_cells),
+        n_double(x->n_double), layout_bytes(x->layout_bytes), max_refs(x->max_refs) {
+    x->own_off = x->own_cnt = x->slot_rows = x->ref_ptr = x->ref_start = x->ref_cnt = nullptr;
+    x->ref_owner = nullptr;
+    x->codes = nullptr;
+    x->layout_bytes = 0;
+  }
+  ~LayoutStash() {
+    if (committed) {  // the new layout is in place: release the old one
+      cudaFree(own_off); cudaFree(own_cnt); cudaFree(slot_rows); cudaFree(ref_ptr);
+      cudaFree(ref_start); cudaFree(ref_cnt); cudaFree(ref_owner); cudaFree(codes);
+      idx->device_bytes -= layout_bytes;
+      return;
+    }
+    // failure: free the partial new layout, restore the old one
+    cudaFree(idx->own_off); cudaFree(idx->own_cnt); cudaFree(idx->slot_rows); cudaFree(idx->ref_ptr);
+    cudaFree(idx->ref_start); cudaFree(idx->ref_cnt); cudaFree(idx->ref_owner); cudaFree(idx->codes);
+    idx->own_off = own_off; idx->own_cnt = own_cnt; idx->slot_rows = slot_rows; idx->ref_ptr = ref_ptr;
+    idx->ref_start = ref_start; idx->ref_cnt = ref_cnt; idx->ref_owner = ref_owner; idx->codes = codes;
+    idx->n_slots = n_slots; idx->n_refs = n_refs; idx->n_cells = n_cells; idx->n_double = n_double;
+    idx->layout_bytes = layout_bytes; idx->max_refs = max_refs;
+  }
+};
+
 rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   const int64_t n = idx->n;
   const int64_t n_live = idx->n_live;  // live rows: the first n_live sorted keys
-  // a rebuild (after rairs_add / rairs_remove_ids) replaces the previous layout
-  cudaFree(idx->own_off); cudaFree(idx->own_cnt); cudaFree(idx->codes); cudaFree(idx->slot_rows);
-  cudaFree(idx->ref_ptr); cudaFree(idx->ref_owner); cudaFree(idx->ref_start); cudaFree(idx->ref_cnt);
-  idx->own_off = idx->own_cnt = nullptr;
-  idx->codes = nullptr;
-  idx->slot_rows = nullptr;
-  idx->ref_ptr = idx->ref_start = idx->ref_cnt = nullptr;
-  idx->ref_owner = nullptr;
-  idx->device_bytes -= idx->layout_bytes;
-  idx->layout_bytes = 0;
+  LayoutStash stash(idx);
   const int nlist = idx->nlist;
   const int NU = idx->M_pad / 16;
   uint64_t *keys = nullptr, *skeys = nullptr, *rk = nullptr, *rv = nullptr, *rk_s = nullptr,
@@ -1010,6 +1038,7 @@ rairs_status build_layout(rairs_index_s* idx, cudaStream_t s) {
   LY_TRY(cudaMemcpyAsync(idx->ref_ptr, hptr.data(), (nlist + 1) * 4, cudaMemcpyHostToDevice, s));
   LY_TRY(cudaStreamSynchronize(s));
   idx->device_bytes += idx->layout_bytes;
+  stash.committed = true;
   cleanup();
   return RAIRS_OK;
 #undef LY_TRY

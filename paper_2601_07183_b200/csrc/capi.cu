@@ -171,6 +171,7 @@ struct StageEvents {
   bool on;
   StageEvents(rairs_index_s* i, cudaStream_t st) : idx(i), s(st), on(i->prof) {
     if (!on) return;
+    std::lock_guard<std::mutex> lock(idx->prof_mu);
     for (int k = 0; k < 4; ++k) {
       if (!idx->pool.empty()) {
         ev.e[k] = idx->pool.back();
@@ -184,7 +185,9 @@ struct StageEvents {
     if (on) cudaEventRecord(ev.e[k], s);
   }
   void commit() {
-    if (on) idx->pending.push_back(ev);
+    if (!on) return;
+    std::lock_guard<std::mutex> lock(idx->prof_mu);
+    idx->pending.push_back(ev);
   }
 };
 
@@ -427,14 +430,17 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, c
   rairs_index_s* idx = new (std::nothrow) rairs_index_s();
   if (!idx) return RAIRS_E_OOM;
   {
-    // search workspaces come from the stream-ordered pool: keep freed blocks
-    // cached instead of returning them to the driver at every sync
+    // search workspaces come from the stream-ordered pool: keep up to 4 GiB of
+    // freed blocks cached (per-search workspaces are reused without a driver
+    // round trip) instead of returning them at every sync; larger ones go back
     int dev = 0;
     cudaMemPool_t pool;
     cudaGetDevice(&dev);
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      uint64_t cur = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
+      uint64_t thr = 4ull << 30;
+      if (cur < thr) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
   cudaGetDevice(&idx->device);
@@ -664,13 +670,21 @@ rairs_status rairs_add(rairs_index_t idx, const float* x, int64_t n_add, const i
     live_set_range_kernel<<<grid_for(n_add), 256, 0, s>>>(idx->live_bits, r0, n_new);
     RAIRS_CHECK_LAUNCH();
   }
-  if (ids) RAIRS_TRY(labels_store(idx, ids, r0, n_add, s));
   // new rows: Alg. 3 assignment (lines 1-12) with the index's trained centroids
+  // (rows >= idx->n: nothing the index serves changes until the relayout)
   RAIRS_TRY(assign_rows(idx, r0, n_add, s));
   idx->n = n_new;
   idx->n_live += n_add;
-  // Alg. 4 for the batch: cells, references and codes re-laid out (cell-major)
-  RAIRS_TRY(relayout(idx, s));
+  // Alg. 4 for the batch: cells, references and codes re-laid out (cell-major);
+  // on failure the index keeps its previous rows and layout
+  const rairs_status rl = relayout(idx, s);
+  if (rl != RAIRS_OK) {
+    idx->n = r0;
+    idx->n_live -= n_add;
+    relayout(idx, s);  // the previous layout (kept, or rebuilt if a later table failed)
+    return rl;
+  }
+  if (ids) RAIRS_TRY(labels_store(idx, ids, r0, n_add, s));
   if (first_id) *first_id = r0 * idx->nshards + idx->shard_id;
   return RAIRS_OK;
 }
@@ -937,7 +951,8 @@ rairs_status rairs_get_stats(rairs_index_t idx, rairs_stats* out, int32_t reset)
     RAIRS_CUDA_TRY(cudaMemset(idx->counters, 0, sizeof(c)));
     RAIRS_CUDA_TRY(cudaMemset(idx->certify_fallbacks, 0, sizeof(unsigned)));
     RAIRS_TRY(rairs_profile_read(idx, nullptr, nullptr, 1));
-    idx->n_searches = idx->n_queries = 0;
+    idx->n_searches = 0;
+    idx->n_queries = 0;
   }
   return RAIRS_OK;
 }
@@ -953,7 +968,7 @@ rairs_status rairs_search_plan(rairs_index_t idx, int64_t nq, int32_t k, int32_t
 rairs_status rairs_profile_kernels(rairs_index_t idx, int64_t* kernels, int32_t reset) {
   if (!idx || !kernels) return invalid("NULL argument");
   *kernels = idx->kernels;
-  if (reset) idx->kernels = 0;
+  if (reset) idx->kernels.store(0);
   return RAIRS_OK;
 }
 
@@ -966,6 +981,7 @@ rairs_status rairs_profile_enable(rairs_index_t idx, int32_t on) {
 rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launches3,
                                 int32_t reset) {
   if (!idx) return invalid("index is NULL");
+  std::lock_guard<std::mutex> lock(idx->prof_mu);
   for (auto& es : idx->pending) {
     RAIRS_CUDA_TRY(cudaEventSynchronize(es.e[3]));
     for (int k = 0; k < 3; ++k) {

@@ -63,7 +63,8 @@ struct rairs_index_s {
   // rairs_get_stats: device counters [0] items scored (DCO), [1] candidates
   // refined; host counters of searches and queries
   unsigned long long* counters = nullptr;
-  int64_t n_searches = 0, n_queries = 0;
+  // host counters: searches may run concurrently on different streams (rairs.h)
+  std::atomic<int64_t> n_searches{0}, n_queries{0};
   // list-major scan (NEXT-1): mode 0 auto / 1 SIMT query-major / 2 list-major
   int scan_mode = 0;
   uint32_t* list_items = nullptr;    // [nlist] N_l = own_cnt + sum of ref_cnt
@@ -100,14 +101,16 @@ struct rairs_index_s {
   int hq_next = 0;
   std::mutex* hq_mu = nullptr;
 
-  // stage profiling (CUDA events on the search stream)
+  // stage profiling (CUDA events on the search stream); prof_mu guards the
+  // event vectors and sums (concurrent searches)
   bool prof = false;
   struct EvSet { cudaEvent_t e[4]; };
+  std::mutex prof_mu;
   std::vector<EvSet> pending;
   std::vector<cudaEvent_t> pool;
   double ms[3] = {0, 0, 0};
-  int64_t launches[3] = {0, 0, 0};
-  int64_t kernels = 0;  // kernels launched by searches (rairs_profile_kernels)
+  std::atomic<int64_t> launches[3] = {{0}, {0}, {0}};
+  std::atomic<int64_t> kernels{0};  // kernels launched by searches (rairs_profile_kernels)
 };
 
 namespace rairs {

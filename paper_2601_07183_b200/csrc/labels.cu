@@ -47,13 +47,30 @@ __device__ __forceinline__ int64_t label_find(const uint32_t* sorted, int64_t m,
   return (lo < m && sorted[lo] == v) ? lo : -1;
 }
 
-// bad[2] += new labels already held by the index
+// the (label, row) table keeps the labels of deleted rows (rows are never
+// reused): the row holding label v is the first LIVE one among its entries
+// (at most one is live -- a label is unique among live rows), or -1
+__device__ __forceinline__ int64_t label_find_live(const uint32_t* sorted, const uint32_t* rows,
+                                                   const uint32_t* live_bits, int64_t m, uint32_t v) {
+  int64_t p = label_find(sorted, m, v);
+  if (p < 0) return -1;
+  for (; p < m && sorted[p] == v; ++p) {
+    const uint32_t r = rows[p];
+    if (live_bits == nullptr || ((live_bits[r >> 5] >> (r & 31)) & 1u)) return p;
+  }
+  return -1;
+}
+
+// bad[2] += new labels already held by a live row of the index (a label whose
+// row was deleted may be added again)
 __global__ void label_clash_kernel(const uint32_t* __restrict__ keys, int64_t m,
-                                   const uint32_t* __restrict__ sorted, int64_t ns,
+                                   const uint32_t* __restrict__ sorted,
+                                   const uint32_t* __restrict__ rows,
+                                   const uint32_t* __restrict__ live_bits, int64_t ns,
                                    unsigned* __restrict__ bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
-    if (label_find(sorted, ns, keys[i]) >= 0) atomicAdd(bad, 1u);
+    if (label_find_live(sorted, rows, live_bits, ns, keys[i]) >= 0) atomicAdd(bad, 1u);
 }
 
 __global__ void iota_u32_kernel(uint32_t* __restrict__ a, int64_t m) {
@@ -86,7 +103,8 @@ rairs_status labels_validate(const rairs_index_s* idx, const int64_t* ids, int64
   label_dup_kernel<<<lgrid(m), 256, 0, s>>>(sorted, m, bad + 1);
   LB_TRY(cudaGetLastError());
   if (idx && idx->lab_sorted && idx->n > 0) {
-    label_clash_kernel<<<lgrid(m), 256, 0, s>>>(keys, m, idx->lab_sorted, idx->n, bad + 2);
+    label_clash_kernel<<<lgrid(m), 256, 0, s>>>(keys, m, idx->lab_sorted, idx->lab_rows,
+                                                idx->live_bits, idx->n, bad + 2);
     LB_TRY(cudaGetLastError());
   }
   unsigned h[3] = {0, 0, 0};
@@ -150,14 +168,15 @@ rairs_status labels_store(rairs_index_s* idx, const int64_t* ids, int64_t row0, 
 // hold the label)
 __global__ void label_rows_kernel(const int64_t* __restrict__ ids, int64_t m,
                                   const uint32_t* __restrict__ sorted,
-                                  const uint32_t* __restrict__ rows, int64_t n, int G, int shard,
+                                  const uint32_t* __restrict__ rows,
+                                  const uint32_t* __restrict__ live_bits, int64_t n, int G, int shard,
                                   int64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = ids[i];
     int64_t r = -1;
     if (v >= 0 && v <= (int64_t)kMaxLabel) {
-      const int64_t p = label_find(sorted, n, (uint32_t)v);
+      const int64_t p = label_find_live(sorted, rows, live_bits, n, (uint32_t)v);
       if (p >= 0) r = (int64_t)rows[p] * G + shard;
     }
     out[i] = r;
@@ -167,8 +186,8 @@ __global__ void label_rows_kernel(const int64_t* __restrict__ ids, int64_t m,
 rairs_status labels_to_gids(const rairs_index_s* idx, const int64_t* ids, int64_t m,
                             int64_t* gids_out, cudaStream_t s) {
   if (m <= 0) return RAIRS_OK;
-  label_rows_kernel<<<lgrid(m), 256, 0, s>>>(ids, m, idx->lab_sorted, idx->lab_rows, idx->n,
-                                             idx->nshards, idx->shard_id, gids_out);
+  label_rows_kernel<<<lgrid(m), 256, 0, s>>>(ids, m, idx->lab_sorted, idx->lab_rows, idx->live_bits,
+                                             idx->n, idx->nshards, idx->shard_id, gids_out);
   RAIRS_CHECK_LAUNCH();
   return RAIRS_OK;
 }

@@ -1252,7 +1252,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(cudaMallocAsync(&qbits, (size_t)nq * qwords * 4, s));
   LM_TRY(cudaMallocAsync(&totals, 16, s));
   LM_TRY(cudaMallocAsync(&sbase, (size_t)(nlist + 1) * 8, s));
-  LM_TRY(cudaMallocAsync(&S, std::max<size_t>(s_bytes, 16), s));
+
   LM_TRY(launch_pdl(lm_zero_kernel, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlist + 2 + LM_NCH, 256), 148))),
                     dim3(256), 0, s, cnt, (int64_t)(nlist + 2 + LM_NCH)));
   unsigned* list_counter = cnt + nlist + 1;  // zeroed tail of cnt
@@ -1265,6 +1265,19 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   LM_TRY(launch_pdl(lm_scatter_kernel, dim3(g1), dim3(256), 0, s, (const int32_t*)sa.probes, npairs,
                     nprobe, (const uint32_t*)qptr, (const uint32_t*)qslot, list_q, qbits, qwords));
   LM_TRY(cudaGetLastError());
+  // the score rows: the worst-case bound (every pair x the largest list-task)
+  // when it is small, else the exact total sum_l |Q_l| * round8(N_l) read back
+  // from the scan (one host synchronisation; multi-GB batches only)
+  {
+    size_t bytes = s_bytes;
+    if (s_bytes > (512ull << 20)) {
+      uint64_t tot = 0;
+      LM_TRY(cudaMemcpyAsync(&tot, sbase + nlist, 8, cudaMemcpyDeviceToHost, s));
+      LM_TRY(cudaStreamSynchronize(s));
+      bytes = (size_t)tot * (score_u32 ? 4 : 2);
+    }
+    LM_TRY(cudaMallocAsync(&S, std::max<size_t>(bytes, 16), s));
+  }
   // 2. quantised LUTs (O2), one warp per query, written into the list-task tiles
   {
     const size_t lsm = ((size_t)16 * idx->dsub * idx->M + (size_t)LW * idx->M) * 4;

@@ -6,6 +6,7 @@
 //       top-k by (fp32 distance, id), one CTA per query.
 //   K7  shard merge (O11).
 #include <algorithm>
+#include <climits>
 
 #include "index.cuh"
 #include "tc_helpers.cuh"
@@ -300,29 +301,48 @@ rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaSt
 
 // ---------------------------------------------------------------------------
 // K7 merge of G per-shard top-k lists: first k by (dist, id) (O11).
+// K7: the first k of the G per-shard lists by (fp32 distance, 64-bit id);
+// entries with id < 0 (padding) sort last.  The distance is ordered by its
+// bits (squared distances are >= 0, +inf last); ids keep all 64 bits.
 __global__ void merge_kernel(const int64_t* __restrict__ ids, const float* __restrict__ dists,
                              int G, int64_t nq, int k, int npow, int64_t* __restrict__ out_ids,
                              float* __restrict__ out_dists) {
   extern __shared__ __align__(16) unsigned char sm[];
-  uint64_t* key = reinterpret_cast<uint64_t*>(sm);
+  int64_t* kid = reinterpret_cast<int64_t*>(sm);
+  uint32_t* kd = reinterpret_cast<uint32_t*>(kid + npow);
   for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
     for (int e = threadIdx.x; e < npow; e += blockDim.x) {
-      uint64_t v = kKeyInf;
+      uint32_t d = 0xFFFFFFFFu;
+      int64_t id = INT64_MAX;
       if (e < G * k) {
         const int g = e / k, j = e - g * k;
-        const int64_t id = ids[((int64_t)g * nq + q) * k + j];
-        const float dd = dists[((int64_t)g * nq + q) * k + j];
-        if (id >= 0) v = ((uint64_t)__float_as_uint(dd) << 32) | (uint64_t)(uint32_t)id;
+        const int64_t v = ids[((int64_t)g * nq + q) * k + j];
+        if (v >= 0) {
+          id = v;
+          d = __float_as_uint(dists[((int64_t)g * nq + q) * k + j]);
+        }
       }
-      key[e] = v;
+      kid[e] = id;
+      kd[e] = d;
     }
     __syncthreads();
-    cta_bitonic_sort_u64(key, npow);
+    for (int size = 2; size <= npow; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < (npow >> 1); i += blockDim.x) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const uint32_t da = kd[lo], db = kd[hi];
+          const int64_t ia = kid[lo], ib = kid[hi];
+          const bool gt = da > db || (da == db && ia > ib);
+          if (gt == asc) { kd[lo] = db; kd[hi] = da; kid[lo] = ib; kid[hi] = ia; }
+        }
+        __syncthreads();
+      }
+    }
     for (int i = threadIdx.x; i < k; i += blockDim.x) {
-      const uint64_t v = key[i];
-      out_ids[q * k + i] = (v != kKeyInf) ? (int64_t)(uint32_t)(v & 0xFFFFFFFFu) : -1;
-      out_dists[q * k + i] = (v != kKeyInf) ? __uint_as_float((uint32_t)(v >> 32))
-                                            : __int_as_float(0x7f800000);
+      const bool ok = kid[i] != INT64_MAX;
+      out_ids[q * k + i] = ok ? kid[i] : -1;
+      out_dists[q * k + i] = ok ? __uint_as_float(kd[i]) : __int_as_float(0x7f800000);
     }
     __syncthreads();
   }
@@ -332,7 +352,7 @@ rairs_status launch_merge(const int64_t* ids, const float* dists, int G, int64_t
                           int64_t* out_ids, float* out_dists, cudaStream_t s) {
   if (nq <= 0) return RAIRS_OK;
   const int npow = next_pow2(std::max(G * k, 2));
-  const size_t smem = (size_t)npow * 8;
+  const size_t smem = (size_t)npow * 12;
   if (smem > 200 * 1024) {
     set_error("merge: G*k too large");
     return RAIRS_E_UNSUPPORTED;

@@ -155,6 +155,32 @@ def test_assign_exhaustive_argmin_and_rair_condition(oracle_mod):
             assert cond
 
 
+def test_assign_candidates_truncated_to_n_cands(oracle_mod):
+    """Alg. 3 line 2 takes the second list only among the N_C
+    nearest centroids (N_CANDS = 10).  Hand geometry (2-d, x = 0,
+    lambda = 0.5): c_0 = (1, 0) is nearest; ten more centroids on the same side
+    at distance 1.1 (r_i . r_0 = 1.1 cos(theta_i) > 0, so loss_i =
+    1.21 + 0.55 cos(theta_i)); one centroid at (-1.2, 0), 12th nearest, has
+    loss 1.44 - 0.6 = 0.84 -- the smallest of all, but outside the first 10.
+    Closed forms: with N_C = 10 the pair is (0, argmin over the ten = the one
+    at the largest angle); with N_C = 12 it is (0, the far centroid)."""
+    thetas = np.linspace(-1.2, 1.2, 10)   # radians, all |theta| < pi/2
+    same = np.stack([1.1 * np.cos(thetas), 1.1 * np.sin(thetas)], 1)
+    cent = np.concatenate([[[1.0, 0.0]], same, [[-1.2, 0.0]]]).astype(np.float32)
+    x = np.zeros((1, 2), np.float32)
+    # ranks by distance: c_0 (1.0), the ten (1.1 each, ties broken by list id), far (1.2)
+    d = (cent.astype(np.float64) ** 2).sum(1)
+    assert np.argsort(d, kind="stable")[-1] == 11
+    loss = d + 0.5 * (cent.astype(np.float64) @ cent[0].astype(np.float64))
+    first10 = np.argsort(d, kind="stable")[:10]
+    exp10 = first10[np.argmin(loss[first10])]
+    assert exp10 != 0 and exp10 != 11 and loss[11] < loss[exp10]
+    l1, l2 = oracle_mod.assign(x, cent, "air", lam=0.5, n_cands=10)
+    assert (int(l1[0]), int(l2[0])) == tuple(sorted((0, int(exp10))))
+    l1, l2 = oracle_mod.assign(x, cent, "air", lam=0.5, n_cands=12)
+    assert (int(l1[0]), int(l2[0])) == (0, 11)
+
+
 def test_assign_soar_closed_form(oracle_mod):
     # SOARL2 (Table 2, P:1100): loss = ||r'||^2 + lambda (r.r'/||r||)^2 prefers r'
     # orthogonal to r; AIR (P:1062) prefers r' opposite to r.  x = 0, c0 = e1:
