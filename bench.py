@@ -191,10 +191,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # RAIRS_BENCH_BACKEND=gloo + RAIRS_BENCH_ONE_GPU=1: a functional run of the
+    # N-rank path with every rank on cuda:0 (NCCL refuses two ranks per device);
+    # timings of such a run are not scaling numbers
+    backend = os.environ.get("RAIRS_BENCH_BACKEND", "nccl")
+    gpu = 0 if os.environ.get("RAIRS_BENCH_ONE_GPU") == "1" else local_rank
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local_rank)
+        torch.cuda.set_device(gpu)
+        dist.init_process_group(backend)
+    dev = torch.device("cuda", gpu)
     spec, X, Q, Qd, idx, gen_s, build_s, gt_ids, gt_d64, nq_gt = build_workload(args, rank, world, dev)
     k, rf = spec.k, spec.refine_factor
 
@@ -227,7 +232,7 @@ def run_ours(args):
     dco_local = int(dco.sum().item())
     dco_total = dco_local
     if world > 1:
-        t = torch.tensor([dco_local], dtype=torch.int64, device=dev)
+        t = torch.tensor([dco_local], dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t)
         dco_total = int(t.item())
 
@@ -243,7 +248,7 @@ def run_ours(args):
     idx.profile_read(reset=True)
     idx.kernels_launched(reset=True)
     idx.certify_fallbacks(reset=True)
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(gpu)
     clk.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -268,7 +273,7 @@ def run_ours(args):
     fallbacks = idx.certify_fallbacks(reset=True)
     t_ms = float(sum(step_ms))
     if world > 1:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
     nq = Q.shape[0]
@@ -336,7 +341,8 @@ def run_ours(args):
             flush.zero_()
             host_step()
         torch.cuda.synchronize()
-        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                          device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e2e = {"value": round(nq * args.steps / float(el.item()), 1), "unit": "queries/s",
                "h2d_bytes_per_step": int(Q.nbytes) * world, "d2h_bytes_per_step": int(nq * k * 12),

@@ -21,10 +21,20 @@ def shard_rows(n: int, shard_id: int, nshards: int) -> torch.Tensor:
     return torch.arange(shard_id, n, nshards, dtype=torch.int64)
 
 
+def _via_host(t: torch.Tensor, group) -> bool:
+    """gloo collectives run on host tensors (device tensors are staged)."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
 def broadcast_trained(centroids: torch.Tensor, codebook: torch.Tensor, src: int = 0,
                       group=None) -> Tuple[torch.Tensor, torch.Tensor]:
-    dist.broadcast(centroids, src=src, group=group)
-    dist.broadcast(codebook, src=src, group=group)
+    for t in (centroids, codebook):
+        if _via_host(t, group):
+            h = t.cpu()
+            dist.broadcast(h, src=src, group=group)
+            t.copy_(h)
+        else:
+            dist.broadcast(t, src=src, group=group)
     return centroids, codebook
 
 
@@ -39,11 +49,13 @@ def gather_shard_results(ids: torch.Tensor, dists: torch.Tensor,
         dist.all_gather_into_tensor(all_ids, ids.contiguous(), group=group)
         dist.all_gather_into_tensor(all_d, dists.contiguous(), group=group)
         return all_ids, all_d
-    li = [torch.empty_like(ids) for _ in range(G)]
-    ld = [torch.empty_like(dists) for _ in range(G)]
-    dist.all_gather(li, ids.contiguous(), group=group)
-    dist.all_gather(ld, dists.contiguous(), group=group)
-    return torch.stack(li), torch.stack(ld)
+    dev = ids.device
+    hi, hd = ids.contiguous().cpu(), dists.contiguous().cpu()   # gloo: host staging
+    li = [torch.empty_like(hi) for _ in range(G)]
+    ld = [torch.empty_like(hd) for _ in range(G)]
+    dist.all_gather(li, hi, group=group)
+    dist.all_gather(ld, hd, group=group)
+    return torch.stack(li).to(dev), torch.stack(ld).to(dev)
 
 
 def batch_slice_for_rank(n_total: int, batch: int, shard_id: int, nshards: int) -> slice:
@@ -67,6 +79,21 @@ class ShardedIndex:
             from .index import merge_topk
             merge = merge_topk
         self.merge = merge
+
+    @staticmethod
+    def from_trained(base_local: torch.Tensor, n_total: int, centroids: torch.Tensor,
+                     codebook: torch.Tensor, group=None, **kw) -> "ShardedIndex":
+        """This rank's shard built from a trained state held by rank 0
+        (broadcast first), e.g. an oracle-trained one in the parity tests."""
+        from .index import Index
+        rank, G = dist.get_rank(group), dist.get_world_size(group)
+        cent = centroids.to(base_local.device).contiguous().clone()
+        cb = codebook.to(base_local.device).contiguous().clone()
+        broadcast_trained(cent, cb, src=0, group=group)
+        nlist, M = cent.shape[0], cb.shape[0]
+        idx = Index.build(base_local, nlist, M, centroids=cent, codebook=cb,
+                          shard_id=rank, nshards=G, **kw)
+        return ShardedIndex(idx, group=group, n_total=n_total)
 
     @staticmethod
     def build(base_local: torch.Tensor, n_total: int, nlist: int, M: int,
