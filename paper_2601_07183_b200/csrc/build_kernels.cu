@@ -415,10 +415,10 @@ rairs_status launch_probe_split(const ProbeArgs& a, int32_t* flags, cudaStream_t
   uint64_t* tk = nullptr;
   auto cleanup = [&]() { cudaFreeAsync(list, s); cudaFreeAsync(count, s); cudaFreeAsync(tk, s); cudaFreeAsync(ti, s); };
 #define PX_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return RAIRS_E_CUDA; } } while (0)
-  PX_TRY(cudaMallocAsync(&list, PX_CAP * 4, s));
-  PX_TRY(cudaMallocAsync(&count, 4, s));
-  PX_TRY(cudaMallocAsync(&tk, (size_t)PX_CAP * PX_S * a.L * 8, s));
-  PX_TRY(cudaMallocAsync(&ti, (size_t)PX_CAP * PX_S * a.L * 4, s));
+  PX_TRY(ws_malloc(&list, PX_CAP * 4, s));
+  PX_TRY(ws_malloc(&count, 4, s));
+  PX_TRY(ws_malloc(&tk, (size_t)PX_CAP * PX_S * a.L * 8, s));
+  PX_TRY(ws_malloc(&ti, (size_t)PX_CAP * PX_S * a.L * 4, s));
   PX_TRY(cudaMemsetAsync(count, 0, 4, s));
   flag_compact_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.rows, 256), 148 * 32)), 256, 0, s>>>(
       a.only_flagged, a.rows, list, count);

@@ -29,6 +29,32 @@ rairs_status debug_sync_point(cudaStream_t s, const char* what) {
 namespace rairs {
 
 static thread_local std::string g_err;
+
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) {
+        pools[dev] = nullptr;
+        return e;
+      }
+      uint64_t thr = ~0ull;  // keep freed blocks (the pool is the library's)
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pools[dev], s);
+}
 void set_error(const std::string& msg) { g_err = msg; }
 
 static inline unsigned grid_for(int64_t n, int bs = 256) {
@@ -54,7 +80,7 @@ __global__ void nonfinite_tail_kernel(const float* __restrict__ x, int64_t n, un
 // RAIRS_E_INVALID if any of the `count` floats at x (device) is NaN or +-inf
 static rairs_status check_finite(const float* x, int64_t count, const char* what, cudaStream_t s) {
   unsigned* bad = nullptr;
-  RAIRS_CUDA_TRY(cudaMallocAsync(&bad, sizeof(unsigned), s));
+  RAIRS_CUDA_TRY(ws_malloc(&bad, sizeof(unsigned), s));
   RAIRS_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
   const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const int64_t n4 = al ? count / 4 : 0;
@@ -209,8 +235,8 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   const int bigK = k * rf;
   int32_t* probes = probes_out;
   uint64_t* keys = nullptr;
-  if (!probes) RAIRS_CUDA_TRY(cudaMallocAsync(&probes, (size_t)nq * nprobe * 4, s));
-  cudaError_t e = cudaMallocAsync(&keys, (size_t)nq * bigK * 8, s);
+  if (!probes) RAIRS_CUDA_TRY(ws_malloc(&probes, (size_t)nq * nprobe * 4, s));
+  cudaError_t e = ws_malloc(&keys, (size_t)nq * bigK * 8, s);
   if (e != cudaSuccess) {
     if (!probes_out) cudaFreeAsync(probes, s);
     set_error(std::string("workspace: ") + cudaGetErrorString(e));
@@ -285,7 +311,7 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
     } else {
       a.sorted_keys = cand_ids != nullptr || cand_scores != nullptr;
       uint4* luts = nullptr;
-      cudaError_t le = cudaMallocAsync(&luts, (size_t)nq * idx->M_pad * 16, s);
+      cudaError_t le = ws_malloc(&luts, (size_t)nq * idx->M_pad * 16, s);
       if (le != cudaSuccess) {
         set_error(std::string("workspace: ") + cudaGetErrorString(le));
         st = RAIRS_E_OOM;
@@ -403,7 +429,7 @@ static rairs_status assign_rows(rairs_index_s* idx, int64_t row0, int64_t cnt, c
   pa.l2 = idx->l2 + row0;
   if (coarse_fused_ok(idx, pa.L) && idx->nlist > 256) {
     unsigned* fb = nullptr;
-    RAIRS_CUDA_TRY(cudaMallocAsync(&fb, sizeof(unsigned), s));
+    RAIRS_CUDA_TRY(ws_malloc(&fb, sizeof(unsigned), s));
     RAIRS_CUDA_TRY(cudaMemsetAsync(fb, 0, sizeof(unsigned), s));
     rairs_status st = launch_coarse_fused(idx, pa.X, cnt, pa.L, pa.mode, pa.lambda, pa.strict,
                                           nullptr, pa.l1, pa.l2, fb, s);
@@ -430,18 +456,7 @@ rairs_status rairs_build_from_trained(const float* base, int64_t n, int32_t d, c
   rairs_index_s* idx = new (std::nothrow) rairs_index_s();
   if (!idx) return RAIRS_E_OOM;
   {
-    // search workspaces come from the stream-ordered pool: keep up to 4 GiB of
-    // freed blocks cached (per-search workspaces are reused without a driver
-    // round trip) instead of returning them at every sync; larger ones go back
-    int dev = 0;
-    cudaMemPool_t pool;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t cur = 0;
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
-      uint64_t thr = 4ull << 30;
-      if (cur < thr) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    // (search workspaces: the library's own stream-ordered pool, ws_malloc)
   }
   cudaGetDevice(&idx->device);
   idx->n = n;
@@ -708,10 +723,10 @@ rairs_status rairs_remove_ids(rairs_index_t idx, const int64_t* ids, int64_t n_i
   unsigned long long* cnt = nullptr;
   int64_t* gids = nullptr;
   if (idx->labels) {  // caller ids -> internal global ids
-    RAIRS_CUDA_TRY(cudaMallocAsync(&gids, (size_t)n_ids * 8, s));
+    RAIRS_CUDA_TRY(ws_malloc(&gids, (size_t)n_ids * 8, s));
     RAIRS_TRY(labels_to_gids(idx, ids, n_ids, gids, s));
   }
-  RAIRS_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
+  RAIRS_CUDA_TRY(ws_malloc(&cnt, sizeof(unsigned long long), s));
   RAIRS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
   remove_ids_kernel<<<grid_for(n_ids), 256, 0, s>>>(gids ? gids : ids, n_ids, idx->shard_id,
                                                     idx->nshards, idx->n, idx->live_bits, cnt);
@@ -773,10 +788,10 @@ static rairs_status search_host_impl(rairs_index_t idx, const float* queries_hos
     RAIRS_CUDA_TRY(cudaStreamWaitEvent(idx->h2d, idx->hq_ev[slot], 0));
     dq = idx->hq_buf[slot];
   } else {
-    RAIRS_CUDA_TRY(cudaMallocAsync(&dq, qb, s));
+    RAIRS_CUDA_TRY(ws_malloc(&dq, qb, s));
   }
-  RAIRS_CUDA_TRY(cudaMallocAsync(&di, ib, s));
-  RAIRS_CUDA_TRY(cudaMallocAsync(&dd, db, s));
+  RAIRS_CUDA_TRY(ws_malloc(&di, ib, s));
+  RAIRS_CUDA_TRY(ws_malloc(&dd, db, s));
   rairs_status st = search_impl(idx, dq, nq, k, nprobe, refine_factor, nullptr, nullptr, nullptr,
                                 nullptr, nullptr, nullptr, nullptr, di, dd, s, queries_host);
   if (chunked) cudaEventRecord(idx->hq_ev[slot], s);  // the buffer is free again after this

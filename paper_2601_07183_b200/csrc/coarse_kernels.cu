@@ -688,7 +688,7 @@ rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s) {
   const int npad = (int)round_up(idx->nlist, FT_BN);
   RAIRS_CUDA_TRY(cudaMalloc(&idx->cnorm, (size_t)npad * 4));
   double* dmax = nullptr;
-  RAIRS_CUDA_TRY(cudaMallocAsync(&dmax, 8, s));
+  RAIRS_CUDA_TRY(ws_malloc(&dmax, 8, s));
   RAIRS_CUDA_TRY(cudaMemsetAsync(dmax, 0, 8, s));
   cnorm_kernel<<<(npad + 255) / 256, 256, 0, s>>>(idx->centroids, idx->nlist, npad, idx->d,
                                                   idx->cnorm, dmax);
@@ -803,9 +803,9 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     float* vals = nullptr;
     uint32_t* ids = nullptr;
     int32_t* flags = nullptr;
-    RAIRS_CUDA_TRY(cudaMallocAsync(&vals, (size_t)nr * nsplit * Wout * 4, s));
-    RAIRS_CUDA_TRY(cudaMallocAsync(&ids, (size_t)nr * nsplit * Wout * 4, s));
-    RAIRS_CUDA_TRY(cudaMallocAsync(&flags, (size_t)(nr + 1) * 4, s));
+    RAIRS_CUDA_TRY(ws_malloc(&vals, (size_t)nr * nsplit * Wout * 4, s));
+    RAIRS_CUDA_TRY(ws_malloc(&ids, (size_t)nr * nsplit * Wout * 4, s));
+    RAIRS_CUDA_TRY(ws_malloc(&flags, (size_t)(nr + 1) * 4, s));
     RAIRS_CUDA_TRY(cudaMemsetAsync(flags + nr, 0, 4, s));  // flagged-row count of this call
     const float* Xc = X + (size_t)r0 * d;
     CUtensorMap tmA, tmB;

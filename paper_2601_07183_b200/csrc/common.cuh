@@ -79,6 +79,17 @@ struct Status {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Stream-ordered workspaces come from the library's own memory pool (one per
+// device, created on first use), which keeps freed blocks cached: a search's
+// multi-GB workspace (list-major score rows of a 100M batch) is reused by the
+// next search without a driver round trip, and the caller's default pool is
+// left untouched.
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s);
+template <typename T>
+inline cudaError_t ws_malloc(T** p, size_t bytes, cudaStream_t s) {
+  return ws_malloc(reinterpret_cast<void**>(p), bytes, s);
+}
+
 // RAIRS_DEBUG_SYNC=1: synchronise after the named launch and report a fault
 // there (debugging aid for large builds; off by default, no effect on results)
 bool debug_sync_enabled();

@@ -124,6 +124,14 @@ struct FsArgs {
   int o_lut, o_cand, o_hist, o_ps, o_pre, o_r0, o_rs, o_rc, o_rg, warp_bytes;
   int cb_smem;                 // fs_lut_kernel: bytes of the per-CTA codebook copy (0: global)
   const uint4* luts;           // [nq][M_pad] quantised LUT rows (fs_lut_kernel)
+  int pstride;                 // probes row stride (>= nprobe: a prefix of each probe list)
+  const uint32_t* qlist;       // optional: scan only queries qlist[0 .. *qcount)
+  const uint32_t* qcount;
+  // threshold mode (list-major fused path): with nprobe = 1 the scanned items
+  // are the members of the query's nearest list, a subset of U(q), so their
+  // bigK-th smallest score bounds the query's bigK-th from above; written to
+  // tau_out[q] (0xFFFFFFFF if the list has fewer than bigK items), no keys
+  uint32_t* tau_out;
   int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
@@ -637,9 +645,11 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
     uint32_t qq = 0;
     if (lane == 0) qq = atomicAdd(&a.ctr[0], 1u);
     qq = __shfl_sync(0xffffffffu, qq, 0);
-    if (qq >= (uint64_t)a.nq) break;
-    const int64_t q = qq;
-    const int32_t* pq = a.probes + q * np;
+    // a query subset (a.qlist / *a.qcount: the list-major path's overflowed
+    // queries) or every query
+    if (a.qlist ? qq >= *a.qcount : qq >= (uint64_t)a.nq) break;
+    const int64_t q = a.qlist ? (int64_t)a.qlist[qq] : (int64_t)qq;
+    const int32_t* pq = a.probes + q * a.pstride;
 
     // ---- probe set: sorted copy (membership, R9) + per-probe reference prefix ----
     for (int i = lane; i < a.npp2; i += 32) Ps[i] = i < np ? __ldg(pq + i) : INT_MAX;
@@ -811,7 +821,15 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
 
     // ---- exact top-bigK of the buffer ----
     const uint32_t keep = (a.dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh);
-    for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? cand[i] : kKeyInf;
+    if (a.tau_out) {  // threshold mode: the bigK-th smallest score (an upper bound, see FsArgs)
+      uint32_t mx = 0;
+      for (uint32_t i = lane; i < keep; i += 32) mx = max(mx, (uint32_t)(cand[i] >> 32));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) a.tau_out[q] = keep == bigK ? mx : 0xFFFFFFFFu;
+    } else {
+      for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? cand[i] : kKeyInf;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
     if (lane == 0) {
@@ -917,7 +935,7 @@ struct FsPlan {
   size_t smem;
 };
 
-static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPlan& pl) {
+static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, const FsExtra& ex, FsPlan& pl) {
   FsArgs& p = pl.a;
   p = FsArgs{};
   p.codes = idx->codes_g;
@@ -938,14 +956,18 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, FsPl
   p.queries = sa.queries;
   p.nq = sa.nq;
   p.probes = sa.probes;
-  p.nprobe = sa.nprobe;
-  p.npp2 = next_pow2(sa.nprobe);
+  p.nprobe = ex.nprobe_eff > 0 ? ex.nprobe_eff : sa.nprobe;
+  p.pstride = sa.nprobe;
+  p.npp2 = next_pow2(p.nprobe);
+  p.qlist = ex.qlist;
+  p.qcount = ex.qcount;
+  p.tau_out = ex.tau_out;
   p.bigK = sa.k * sa.refine_factor;
   p.cap = std::max(fs_capmin(), next_pow2(p.bigK + FS_ROUND + 64));
   p.hbits = fs_hbits(idx->M);
   p.out_keys = sa.cand_keys;
-  p.dco = sa.dco;
-  p.dco_total = sa.counters;
+  p.dco = ex.tau_out ? nullptr : sa.dco;
+  p.dco_total = ex.tau_out ? nullptr : sa.counters;
   p.lut_q = sa.lut_q;
   p.lut_a = sa.lut_a;
   p.lut_b = sa.lut_b;
@@ -1002,17 +1024,18 @@ static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
   return RAIRS_OK;
 }
 
-rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s) {
+rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStream_t s,
+                             const FsExtra& ex) {
   if (sa.nq <= 0) return RAIRS_OK;
   if (!idx->codes_g || !idx->fs_ctr || !sa.luts) {
     set_error("fast scan: group layout or LUT workspace missing");
     return RAIRS_E_INTERNAL;
   }
   FsPlan pl;
-  RAIRS_TRY(fs_plan(idx, sa, pl));
+  RAIRS_TRY(fs_plan(idx, sa, ex, pl));
   const unsigned slot = idx->fs_slot.fetch_add(1u) % FS_SLOTS;
   pl.a.ctr = idx->fs_ctr + 2 * slot;
-  {  // A3 for the whole batch (overlaps the coarse stage's tail under PDL)
+  if (!ex.luts_ready) {  // A3 for the whole batch (overlaps the coarse stage's tail under PDL)
     const bool keepT = idx->M * 17 <= 16 * 1024 / 4;
     const size_t lsm = (size_t)pl.a.cb_smem + (size_t)FL_WARPS * (keepT ? 17 : 1) * idx->M * 4;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -204,7 +204,15 @@ struct SearchArgs {
 };
 // query-major register-LUT fast scan (fastscan_kernels.cu): A3-A6 fused
 rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s);
-rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
+struct FsExtra {
+  int nprobe_eff = 0;                 // > 0: scan only the first nprobe_eff probes of each row
+  const uint32_t* qlist = nullptr;    // scan only queries qlist[0 .. *qcount) (device)
+  const uint32_t* qcount = nullptr;
+  uint32_t* tau_out = nullptr;        // threshold mode (see FsArgs::tau_out)
+  bool luts_ready = false;            // a.luts already holds every query's LUT
+};
+rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s,
+                             const FsExtra& ex = FsExtra{});
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
 rairs_status launch_merge(const int64_t* ids, const float* dists, int G, int64_t nq, int k,
                           int64_t* out_ids, float* out_dists, cudaStream_t s);

@@ -91,14 +91,14 @@ rairs_status labels_validate(const rairs_index_s* idx, const int64_t* ids, int64
     return st;
   };
 #define LB_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); return done(_e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA); } } while (0)
-  LB_TRY(cudaMallocAsync(&keys, (size_t)m * 4, s));
-  LB_TRY(cudaMallocAsync(&sorted, (size_t)m * 4, s));
-  LB_TRY(cudaMallocAsync(&bad, 3 * sizeof(unsigned), s));
+  LB_TRY(ws_malloc(&keys, (size_t)m * 4, s));
+  LB_TRY(ws_malloc(&sorted, (size_t)m * 4, s));
+  LB_TRY(ws_malloc(&bad, 3 * sizeof(unsigned), s));
   LB_TRY(cudaMemsetAsync(bad, 0, 3 * sizeof(unsigned), s));
   label_range_kernel<<<lgrid(m), 256, 0, s>>>(ids, m, keys, bad);
   LB_TRY(cudaGetLastError());
   LB_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, m, 0, 32, s));
-  LB_TRY(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), s));
+  LB_TRY(ws_malloc(&tmp, std::max<size_t>(tb, 16), s));
   LB_TRY(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, m, 0, 32, s));
   label_dup_kernel<<<lgrid(m), 256, 0, s>>>(sorted, m, bad + 1);
   LB_TRY(cudaGetLastError());
@@ -150,12 +150,12 @@ rairs_status labels_store(rairs_index_s* idx, const int64_t* ids, int64_t row0, 
   size_t tb = 0;
   RAIRS_CUDA_TRY(cudaMalloc(&idx->lab_sorted, (size_t)std::max<int64_t>(n, 1) * 4));
   RAIRS_CUDA_TRY(cudaMalloc(&idx->lab_rows, (size_t)std::max<int64_t>(n, 1) * 4));
-  RAIRS_CUDA_TRY(cudaMallocAsync(&rows_in, (size_t)std::max<int64_t>(n, 1) * 4, s));
+  RAIRS_CUDA_TRY(ws_malloc(&rows_in, (size_t)std::max<int64_t>(n, 1) * 4, s));
   iota_u32_kernel<<<lgrid(n), 256, 0, s>>>(rows_in, n);
   RAIRS_CHECK_LAUNCH();
   RAIRS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, idx->labels, idx->lab_sorted, rows_in,
                                                  idx->lab_rows, n, 0, 32, s));
-  RAIRS_CUDA_TRY(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), s));
+  RAIRS_CUDA_TRY(ws_malloc(&tmp, std::max<size_t>(tb, 16), s));
   RAIRS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, idx->labels, idx->lab_sorted, rows_in,
                                                  idx->lab_rows, n, 0, 32, s));
   cudaFreeAsync(tmp, s);

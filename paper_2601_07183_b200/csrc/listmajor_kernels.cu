@@ -323,6 +323,14 @@ struct LMArgs {
   int score_u32;
   int nlist;
   const uint32_t* order;  // claim order: lists by descending N_l (longest first), or NULL
+  // fused mode (no score rows): an item joins query q's candidates iff its score
+  // is <= tau[q] (an upper bound of q's bigK-th score, fs_scan threshold mode);
+  // entries (s << 39 | list << 22 | item) go to fcand[q][0 .. fcap), fcnt[q] counts
+  int fused;
+  const uint32_t* tau;
+  uint64_t* fcand;
+  uint32_t* fcnt;
+  int fcap;
 };
 
 // D[tmem] (+)= A[tmem] x B[smem desc]  (A: 128 item rows x 32 K-bytes, 8 columns)
@@ -445,8 +453,9 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
   uint32_t* refoff = reinterpret_cast<uint32_t*>(owners + LM_MAXREF);   // [LM_MAXREF+1]
   uint32_t* skipT = refoff + LM_MAXREF + 1;  // [LM_MAXREF][2]: queries skipping ref j
   uint32_t* qid = skipT + LM_MAXREF * 2;     // [LM_QT]
+  uint32_t* qtau = qid + LM_QT;              // [LM_QT] fused mode: tau of the tile's queries
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(qid + LM_QT) + 7) & ~(uintptr_t)7);  // [LM_STAGES]
+      (reinterpret_cast<uintptr_t>(qtau + LM_QT) + 7) & ~(uintptr_t)7);  // [LM_STAGES]
   uint64_t* empty = full + LM_STAGES;
   uint64_t* tfull = empty + LM_STAGES;  // [2]
   uint64_t* tempty = tfull + 2;         // [2]
@@ -521,7 +530,11 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
         bulk_g2s(sB, a.tiles + ((size_t)a.lrow[l] + q0) * a.K, bytes, bfull);
       }
       for (uint32_t j = tid; j < nref * 2; j += LM_WS_THREADS) skipT[j] = 0u;
-      if (tid < LM_QT) qid[tid] = (tid < nq_tile) ? a.list_q[a.qptr[l] + q0 + tid] : 0xFFFFFFFFu;
+      if (tid < LM_QT) {
+        const uint32_t qq = (tid < nq_tile) ? a.list_q[a.qptr[l] + q0 + tid] : 0xFFFFFFFFu;
+        qid[tid] = qq;
+        if (a.fused) qtau[tid] = (tid < nq_tile) ? a.tau[qq] : 0u;
+      }
       __syncthreads();
       // ref j (owner o) of this list is NOT scanned for query q iff o is probed by q (R9)
       if (tid < nq_tile) {
@@ -660,11 +673,32 @@ __global__ void __launch_bounds__(LMShape<G, GS>::THREADS, LMShape<G, GS>::CTAS_
           const bool inrow = item < Nl8;
           mbar_wait(&tfull[acc], (tc >> 1) & 1u);
           tc_fence_after();
-          const uint64_t base = a.sbase[l] + (uint64_t)q0 * Nl8 + item;
+          const uint64_t base = a.fused ? 0ull : a.sbase[l] + (uint64_t)q0 * Nl8 + item;
           for (int cb = 16 * half; cb < Npad; cb += 32) {
             uint32_t v[16];
             tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + LM_ACC_COL + (uint32_t)(acc * LM_QT + cb), v);
-            if (inrow) {
+            if (a.fused) {
+              // threshold filter: 16 compares; the (rare) passing (item, query)
+              // pairs are appended one atomic each
+              const int jn = min(16, nq_tile - cb);
+              uint32_t pm = 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) pm |= (v[j] <= qtau[cb + j] ? 1u : 0u) << j;
+              pm &= ((uint32_t)(ok >> cb) & 0xFFFFu) & ((1u << jn) - 1u);
+              if (__any_sync(0xffffffffu, pm != 0)) {
+                const uint64_t key_lo = ((uint64_t)l << 22) | (uint64_t)item;
+                while (pm) {
+                  const int j = __ffs(pm) - 1;
+                  pm &= pm - 1;
+                  uint32_t sv = v[0];
+#pragma unroll
+                  for (int jj = 1; jj < 16; ++jj) sv = (jj == j) ? v[jj] : sv;
+                  const uint32_t qq = qid[cb + j];
+                  const uint32_t pos = atomicAdd(&a.fcnt[qq], 1u);
+                  if (pos < (uint32_t)a.fcap) a.fcand[(size_t)qq * a.fcap + pos] = ((uint64_t)sv << 39) | key_lo;
+                }
+              }
+            } else if (inrow) {
               const int jn = min(16, nq_tile - cb);
               const uint32_t okb = (uint32_t)(ok >> cb) & 0xFFFFu;
               if (a.score_u32) {
@@ -1171,6 +1205,93 @@ __global__ void __launch_bounds__(SW_WARPS * 32, 4) lm_select_kernel(SelArgs a) 
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Fused mode, per query (one WARP per query): the candidates the tensor
+// epilogue appended (every item of U(q) with s <= tau[q], a superset of the
+// top-bigK), their ids resolved and sorted by the unique key (s << 32 | id);
+// the first bigK are the query's candidates (O9).  DCO from the layout tables
+// and the probe bitmap (R9, R17).  Queries whose buffer overflowed are listed
+// for the query-major kernel.
+constexpr int FIN_WARPS = 4;
+struct FinArgs {
+  const int32_t* probes;
+  int nprobe;
+  const uint32_t* qbits;
+  int qwords;
+  const uint32_t* own_cnt;
+  const uint32_t* ref_ptr;
+  const int32_t* ref_owner;
+  const uint32_t* ref_cnt;
+  const uint64_t* list_base;
+  const uint32_t* list_ids;
+  const uint64_t* fcand;
+  const uint32_t* fcnt;
+  int fcap;
+  int64_t nq;
+  int bigK;
+  uint64_t* out_keys;
+  int64_t* dco;
+  unsigned long long* dco_total;
+  uint32_t* ovf;
+  uint32_t* novf;
+  unsigned* qctr;
+};
+
+__global__ void __launch_bounds__(FIN_WARPS * 32) lm_final_kernel(FinArgs a) {
+  extern __shared__ __align__(16) uint64_t fin_sm[];
+  const int lane = lane_id(), warp = warp_id();
+  uint64_t* buf = fin_sm + (size_t)warp * a.fcap;
+  pdl_wait();  // the tensor kernel's candidates
+  for (;;) {
+    uint32_t qi = 0;
+    if (lane == 0) qi = atomicAdd(a.qctr, 1u);
+    qi = __shfl_sync(0xffffffffu, qi, 0);
+    if (qi >= (uint64_t)a.nq) break;
+    const int64_t q = qi;
+    const uint32_t n = a.fcnt[q];
+    if (n > (uint32_t)a.fcap) {  // overflow: the query-major kernel redoes this query
+      if (lane == 0) a.ovf[atomicAdd(a.novf, 1u)] = (uint32_t)q;
+      continue;
+    }
+    // DCO = owned + non-skipped referenced items (R9: owner probed -> skipped)
+    const uint32_t* qb = a.qbits + (size_t)q * a.qwords;
+    uint32_t dco = 0;
+    for (int p = 0; p < a.nprobe; ++p) {
+      const int l = a.probes[q * a.nprobe + p];
+      const uint32_t r0 = a.ref_ptr[l], r1 = a.ref_ptr[l + 1];
+      uint32_t c = 0;
+      for (uint32_t j = r0 + lane; j < r1; j += 32) {
+        const int o = a.ref_owner[j];
+        if (!((qb[o >> 5] >> (o & 31)) & 1u)) c += a.ref_cnt[j];
+      }
+      dco += c + (lane == 0 ? a.own_cnt[l] : 0u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dco += __shfl_xor_sync(0xffffffffu, dco, o);
+    // resolve (s, list, item) -> (s << 32 | global id)
+    const uint64_t* src = a.fcand + (size_t)q * a.fcap;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint64_t v = src[i];
+      const uint32_t s = (uint32_t)(v >> 39), l = (uint32_t)(v >> 22) & 0x1FFFFu;
+      const uint32_t item = (uint32_t)v & 0x3FFFFFu;
+      buf[i] = ((uint64_t)s << 32) | a.list_ids[a.list_base[l] + item];
+    }
+    int p2 = 2;
+    while (p2 < (int)n) p2 <<= 1;
+    for (int i = (int)n + lane; i < p2; i += 32) buf[i] = kKeyInf;
+    __syncwarp();
+    warp_sort_keys(buf, p2);
+    const uint32_t keep = min(n, (uint32_t)a.bigK);
+    for (int i = lane; i < a.bigK; i += 32) a.out_keys[q * a.bigK + i] = ((uint32_t)i < keep) ? buf[i] : kKeyInf;
+    if (lane == 0) {
+      if (a.dco) a.dco[q] = (int64_t)dco;
+      if (a.dco_total) atomicAdd(a.dco_total, (unsigned long long)dco);
+    }
+    __syncwarp();
+  }
+  pdl_trigger();
+}
+
 static int sel_cap(int bigK) { return next_pow2(2 * bigK + 64); }
 
 static int lm_qt(int K) {  // queries per LUT tile: QT x K <= LM_B_MAX, multiple of 16, <= 64
@@ -1214,6 +1335,13 @@ static cudaError_t launch_lm_tensor(const LMArgs& la, size_t tsm, cudaStream_t s
 // (measured best of 1x4, 2x4, 4x2, 2x2 -- profiles/r01/SUMMARY.md)
 template <int NU>
 static cudaError_t launch_lm_tensor_shape(const LMArgs& la, size_t tsm, cudaStream_t s) {
+  // RAIRS_LM_SHAPE=22: two generator groups of 2 stages (16 generator warps per
+  // SM) -- an experiment for generator-bound batches (few queries per list)
+  static const int shape = [] {
+    const char* e = std::getenv("RAIRS_LM_SHAPE");
+    return e ? std::atoi(e) : 14;
+  }();
+  if (shape == 22) return launch_lm_tensor<NU, 2, 2>(la, tsm, s);
   return launch_lm_tensor<NU, 1, 4>(la, tsm, s);
 }
 
@@ -1237,21 +1365,32 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   const size_t s_bytes = s_elems * (score_u32 ? 4 : 2);
   // LUT tiles: every (query, probe) row, plus <= 15 padding rows per list
   const size_t tile_bytes = ((size_t)npairs + 15 * (size_t)nlist) * K;
+  // fused mode (no score rows): large batches whose rows would stream from DRAM
+  // (RAIRS_LM_FUSED=0/1 overrides)
+  const double exp_rows = (double)npairs * ((double)idx->sum_list_items / nlist) * (score_u32 ? 4 : 2);
+  bool fused = exp_rows > (double)SEL_DRAM_BYTES;
+  if (const char* e = std::getenv("RAIRS_LM_FUSED")) fused = std::atoi(e) != 0;
+  const int fcap = std::max(2048, next_pow2(8 * bigK));
+  uint4* luts = nullptr;
+  uint32_t *tau = nullptr, *fcnt = nullptr, *ovf = nullptr;
+  uint64_t* fcand = nullptr;
   auto cleanup = [&]() {
     cudaFreeAsync(tiles, s); cudaFreeAsync(cnt, s); cudaFreeAsync(qslot, s); cudaFreeAsync(qptr, s);
     cudaFreeAsync(lrow, s); cudaFreeAsync(list_q, s); cudaFreeAsync(qbits, s);
     cudaFreeAsync(totals, s); cudaFreeAsync(sbase, s); cudaFreeAsync(S, s);
+    cudaFreeAsync(luts, s); cudaFreeAsync(tau, s); cudaFreeAsync(fcnt, s); cudaFreeAsync(ovf, s);
+    cudaFreeAsync(fcand, s);
   };
 #define LM_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return _e == cudaErrorMemoryAllocation ? RAIRS_E_OOM : RAIRS_E_CUDA; } } while (0)
-  LM_TRY(cudaMallocAsync(&tiles, tile_bytes, s));
-  LM_TRY(cudaMallocAsync(&cnt, (size_t)(nlist + 2 + LM_NCH) * 4, s));
-  LM_TRY(cudaMallocAsync(&qslot, (size_t)npairs * 4, s));
-  LM_TRY(cudaMallocAsync(&qptr, (size_t)(nlist + 1) * 4, s));
-  LM_TRY(cudaMallocAsync(&lrow, (size_t)(nlist + 1) * 4, s));
-  LM_TRY(cudaMallocAsync(&list_q, (size_t)npairs * 4, s));
-  LM_TRY(cudaMallocAsync(&qbits, (size_t)nq * qwords * 4, s));
-  LM_TRY(cudaMallocAsync(&totals, 16, s));
-  LM_TRY(cudaMallocAsync(&sbase, (size_t)(nlist + 1) * 8, s));
+  LM_TRY(ws_malloc(&tiles, tile_bytes, s));
+  LM_TRY(ws_malloc(&cnt, (size_t)(nlist + 2 + LM_NCH) * 4, s));
+  LM_TRY(ws_malloc(&qslot, (size_t)npairs * 4, s));
+  LM_TRY(ws_malloc(&qptr, (size_t)(nlist + 1) * 4, s));
+  LM_TRY(ws_malloc(&lrow, (size_t)(nlist + 1) * 4, s));
+  LM_TRY(ws_malloc(&list_q, (size_t)npairs * 4, s));
+  LM_TRY(ws_malloc(&qbits, (size_t)nq * qwords * 4, s));
+  LM_TRY(ws_malloc(&totals, 16, s));
+  LM_TRY(ws_malloc(&sbase, (size_t)(nlist + 1) * 8, s));
 
   LM_TRY(launch_pdl(lm_zero_kernel, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nlist + 2 + LM_NCH, 256), 148))),
                     dim3(256), 0, s, cnt, (int64_t)(nlist + 2 + LM_NCH)));
@@ -1268,7 +1407,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   // the score rows: the worst-case bound (every pair x the largest list-task)
   // when it is small, else the exact total sum_l |Q_l| * round8(N_l) read back
   // from the scan (one host synchronisation; multi-GB batches only)
-  {
+  if (!fused) {
     size_t bytes = s_bytes;
     if (s_bytes > (512ull << 20)) {
       uint64_t tot = 0;
@@ -1276,7 +1415,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
       LM_TRY(cudaStreamSynchronize(s));
       bytes = (size_t)tot * (score_u32 ? 4 : 2);
     }
-    LM_TRY(cudaMallocAsync(&S, std::max<size_t>(bytes, 16), s));
+    LM_TRY(ws_malloc(&S, std::max<size_t>(bytes, 16), s));
   }
   // 2. quantised LUTs (O2), one warp per query, written into the list-task tiles
   {
@@ -1308,8 +1447,34 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
 #undef LUT_LAUNCH
     LM_TRY(cudaGetLastError());
   }
+  if (fused) {
+    // 3f. per-query bound tau[q]: the bigK-th smallest score over the members
+    // of q's nearest list (query-major kernel, first probe only) -- a subset of
+    // U(q), so no item of the top-bigK scores above it
+    LM_TRY(ws_malloc(&luts, (size_t)nq * idx->M_pad * 16, s));
+    LM_TRY(ws_malloc(&tau, (size_t)nq * 4, s));
+    LM_TRY(ws_malloc(&fcnt, (size_t)(nq + 1) * 4, s));
+    LM_TRY(ws_malloc(&ovf, (size_t)nq * 4, s));
+    LM_TRY(ws_malloc(&fcand, (size_t)nq * fcap * 8, s));
+    SearchArgs ta = sa;
+    ta.luts = luts;
+    FsExtra ex;
+    ex.nprobe_eff = 1;
+    ex.tau_out = tau;
+    {
+      const rairs_status rs = launch_fastscan(const_cast<rairs_index_s*>(idx), ta, s, ex);
+      if (rs != RAIRS_OK) { cleanup(); return rs; }
+    }
+    LM_TRY(launch_pdl(lm_zero_kernel, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nq + 1, 256), 148))),
+                      dim3(256), 0, s, fcnt, (int64_t)(nq + 1)));
+  }
   // 3. tensor-core scores, one list at a time
   LMArgs la{};
+  la.fused = fused ? 1 : 0;
+  la.tau = tau;
+  la.fcand = fcand;
+  la.fcnt = fcnt;
+  la.fcap = fcap;
   la.codes64 = reinterpret_cast<const uint64_t*>(idx->codes);
   la.own_off = idx->own_off;
   la.own_cnt = idx->own_cnt;
@@ -1332,7 +1497,7 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.score_u32 = score_u32;
   la.nlist = nlist;
   la.order = idx->lm_order;
-  const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 4 + (2 * 8 + 5) * 8 + 64;
+  const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 8 + (2 * 8 + 5) * 8 + 64;
   switch (idx->M_pad / 16) {
     case 1: LM_TRY(launch_lm_tensor_shape<1>(la, tsm, s)); break;
     case 2: LM_TRY(launch_lm_tensor_shape<2>(la, tsm, s)); break;
@@ -1341,6 +1506,54 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
     case 6: LM_TRY(launch_lm_tensor_shape<6>(la, tsm, s)); break;
     case 8: LM_TRY(launch_lm_tensor_shape<8>(la, tsm, s)); break;
     default: cleanup(); set_error("list-major: unsupported M"); return RAIRS_E_INTERNAL;
+  }
+  if (fused) {
+    // 4f. candidates -> exact top-bigK per query; overflowed queries (more than
+    // fcap items at or below their bound) are redone by the query-major kernel
+    FinArgs fa{};
+    fa.probes = sa.probes;
+    fa.nprobe = nprobe;
+    fa.qbits = qbits;
+    fa.qwords = qwords;
+    fa.own_cnt = idx->own_cnt;
+    fa.ref_ptr = idx->ref_ptr;
+    fa.ref_owner = idx->ref_owner;
+    fa.ref_cnt = idx->ref_cnt;
+    fa.list_base = idx->list_base;
+    fa.list_ids = idx->list_ids;
+    fa.fcand = fcand;
+    fa.fcnt = fcnt;
+    fa.fcap = fcap;
+    fa.nq = nq;
+    fa.bigK = bigK;
+    fa.out_keys = sa.cand_keys;
+    fa.dco = sa.dco;
+    fa.dco_total = sa.counters;
+    fa.ovf = ovf;
+    fa.novf = fcnt + nq;
+    fa.qctr = cnt + nlist + 2;
+    const size_t fsm = (size_t)FIN_WARPS * fcap * 8;
+    LM_TRY(cudaFuncSetAttribute(lm_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    const unsigned fg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nq, FIN_WARPS), 148 * 8));
+    LM_TRY(launch_pdl(lm_final_kernel, dim3(fg), dim3(FIN_WARPS * 32), fsm, s, fa));
+    SearchArgs fb = sa;
+    fb.luts = luts;
+    FsExtra ex;
+    ex.qlist = ovf;
+    ex.qcount = fcnt + nq;
+    ex.luts_ready = true;
+    {
+      const rairs_status rs = launch_fastscan(const_cast<rairs_index_s*>(idx), fb, s, ex);
+      if (rs != RAIRS_OK) { cleanup(); return rs; }
+    }
+    if (sa.ev_selected) LM_TRY(cudaEventRecord(sa.ev_selected, s));
+    if (sa.fused_refine) {
+      SearchArgs ra = sa;
+      const rairs_status rs = launch_refine(idx, ra, s);
+      if (rs != RAIRS_OK) { cleanup(); return rs; }
+    }
+    cleanup();
+    return RAIRS_OK;
   }
   // 4. per-query selection (warp per query)
   SelArgs sl{};
