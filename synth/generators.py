@@ -74,9 +74,23 @@ CONFIGS = {
                      1.0, 4, 16384, note="BJ configs[3]"),
     "c5": ConfigSpec("c5", 100_000_000, 128, 10_000, 65536, 64, 10, 64, 10, "gauss_gpu",
                      0.25, 5, 65536, note="BJ configs[4] (one 10k batch of the 100k queries)"),
+    # paper-like variants of the device-drawn / high-d configs (SURVEY §8(d) "-pl"):
+    # rank-16 clusters, natural clusters = nlist/16; sigma frozen from
+    # tools/calibrate_pl.py on 1M-row samples (profiles/calibration_<config>.jsonl):
+    #   c4pl sigma 2.0: AIR double-assigns 42.9 %, single recall10@10 at nprobe 1 = 0.56,
+    #        AIR reaches 0.95 at nprobe 3 (DCO 2.6k) vs single at nprobe 5 (0.967)
+    #   c5pl sigma 1.0: 47.6 %, single 0.47, AIR 0.95 at nprobe 4 (DCO 8.8k) vs single at 6
+    #   c3pl sigma 0.016 (~0.6/sqrt(d) per dimension, as c3): 40.4 %, single 0.37,
+    #        AIR 0.95 at nprobe 6 (DCO 1.95k) vs single at 8
+    "c4pl": ConfigSpec("c4pl", 10_000_000, 96, 10_000, 16384, 48, 10, 3, 10, "aniso_lowrank_gpu",
+                       2.0, 4, 1024, rank=16, note="paper-like c4"),
+    "c5pl": ConfigSpec("c5pl", 100_000_000, 128, 10_000, 65536, 64, 10, 4, 10, "lowrank_gpu",
+                       1.0, 5, 4096, rank=16, note="paper-like c5"),
+    "c3pl": ConfigSpec("c3pl", 1_000_000, 1536, 10_000, 4096, 384, 10, 6, 10, "sphere_lowrank_gpu",
+                       0.016, 3, 256, rank=16, note="paper-like c3"),
 }
 
-GPU_KINDS = ("aniso", "gauss_gpu")
+GPU_KINDS = ("aniso", "gauss_gpu", "lowrank_gpu", "aniso_lowrank_gpu", "sphere_lowrank_gpu")
 
 
 def get_config(name: str, **overrides) -> ConfigSpec:

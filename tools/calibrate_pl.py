@@ -15,21 +15,32 @@ import torch  # noqa: E402
 
 import paper_2601_07183_b200 as rb  # noqa: E402
 from bench import NPROBE_SWEEP, recall_at_k  # noqa: E402
-from synth import get_config, make_dataset  # noqa: E402
+from synth import GPU_KINDS, get_config, make_dataset  # noqa: E402
 
 
 def main():
     base = sys.argv[1] if len(sys.argv) > 1 else "c2pl"
     grid = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [[24, 64], [48, 64], [64, 64], [48, 16], [96, 16]]
     dev = torch.device("cuda:0")
+    nmax = int(os.environ.get("CAL_N", "1000000"))   # calibrate on a <= 1M-row sample
     for sigma, nat in grid:
-        spec = get_config(base, sigma=float(sigma), nclusters=int(nat))
+        spec0 = get_config(base)
+        n = min(spec0.n, nmax)
+        scale = n / spec0.n
+        nlist = max(16, int(round(spec0.nlist * scale)))
+        spec = get_config(base, sigma=float(sigma), nclusters=max(1, int(round(nat * scale))),
+                          n=n, nlist=nlist)
         t0 = time.time()
-        X, Q = make_dataset(spec)
-        Xd, Qd = torch.from_numpy(X).to(dev), torch.from_numpy(Q).to(dev)
+        if spec.kind in GPU_KINDS:
+            from synth.gpu_generators import make_dataset_torch
+            Xd, Qd = make_dataset_torch(spec, dev)
+        else:
+            X, Q = make_dataset(spec)
+            Xd, Qd = torch.from_numpy(X).to(dev), torch.from_numpy(Q).to(dev)
         gt, gd = rb.exact_knn(Xd, Qd, spec.k)
         cent, cb = rb.train(Xd, spec.nlist, spec.M)
-        row = {"config": base, "sigma": sigma, "natural_clusters": nat}
+        row = {"config": base, "sigma": sigma, "natural_clusters": nat, "n": n, "nlist": nlist,
+               "natural_clusters_sample": spec.nclusters}
         for mode in ("AIR", "single"):
             idx = rb.Index.build(Xd, spec.nlist, spec.M, assignment=mode, centroids=cent, codebook=cb)
             info = idx.info()
