@@ -21,9 +21,8 @@ namespace rairs {
 // conflict-free column reads); each thread then extends its own row's serial
 // fp64 sum over the tile, so the summation order stays ascending in t.
 constexpr int RT = 128;
-constexpr int RDC = 128;           // dims per tile
-constexpr int RSTRIDE = RDC + 1;
 
+template <int RDC>  // dims per tile (the row stride RDC + 1 keeps column reads conflict-free)
 __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__ keys,
                                                     int64_t nq, int bigK, int npow, int k,
                                                     const float* __restrict__ queries,
@@ -32,6 +31,7 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
                                                     unsigned long long* __restrict__ refined,
                                                     int64_t* __restrict__ out_ids,
                                                     float* __restrict__ out_dists) {
+  constexpr int RSTRIDE = RDC + 1;
   extern __shared__ __align__(16) unsigned char sm[];
   uint64_t* rk = reinterpret_cast<uint64_t*>(sm);
   double* qs = reinterpret_cast<double*>(sm + (size_t)npow * 8);
@@ -51,10 +51,11 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
         const int dc = min(RDC, d - t0);
         // warp w gathers rows [32w, 32w+32): 8 rows x 4 coalesced 128-B loads in
         // flight per lane before the shared-memory stores
-        for (int rb = 0; rb < 32; rb += 8) {
-          float v[8][RDC / 32];
+        constexpr int RB = (32 * 32 / RDC) < 32 ? (32 * 32 / RDC) : 32;  // rows per batch: 32 loads in flight
+        for (int rb = 0; rb < 32; rb += RB) {
+          float v[RB][RDC / 32];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < RB; ++i) {
             const uint32_t row = rows[warp * 32 + rb + i];
             const float* src = X + (size_t)(row == 0xFFFFFFFFu ? 0u : row) * d + t0;
 #pragma unroll
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(RT) refine_kernel(const uint64_t* __restrict__
             }
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < RB; ++i)
 #pragma unroll
             for (int j = 0; j < RDC / 32; ++j)
               tile[(warp * 32 + rb + i) * RSTRIDE + lane + 32 * j] = v[i][j];
@@ -268,6 +269,199 @@ static rairs_status launch_refine_stage(const rairs_index_s* idx, const SearchAr
   return RAIRS_OK;
 }
 
+// K6 for long rows (d > 128): the generic kernel's gather/sum alternation,
+// double-buffered -- chunk c+1's 32 rows x 32 dims are in flight (32 loads per
+// lane) while every thread extends its candidate's ordered fp64 sum over chunk
+// c from shared memory (O10: ascending t, one rounding to fp32 at the end).
+__global__ void __launch_bounds__(RT) refine_long_kernel(const uint64_t* __restrict__ keys,
+                                                         int64_t nq, int bigK, int npow, int k,
+                                                         const float* __restrict__ queries,
+                                                         const float* __restrict__ X, int d, int G,
+                                                         const uint32_t* __restrict__ labels,
+                                                         unsigned long long* __restrict__ refined,
+                                                         int64_t* __restrict__ out_ids,
+                                                         float* __restrict__ out_dists) {
+  constexpr int S = 33;  // row stride of a 32-dim tile (conflict-free column reads)
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint64_t* rk = reinterpret_cast<uint64_t*>(sm);
+  float* qs = reinterpret_cast<float*>(sm + (size_t)npow * 8);
+  float* tile = qs + ((d + 3) & ~3);                       // [2][RT][S]
+  uint32_t* rows = reinterpret_cast<uint32_t*>(tile + 2 * RT * S);
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const int nch = (d + 31) / 32;
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    for (int t = tid; t < d; t += RT) qs[t] = queries[q * d + t];
+    for (int c0 = 0; c0 < npow; c0 += RT) {
+      const int c = c0 + tid;
+      const uint64_t key = (c < bigK) ? keys[q * bigK + c] : kKeyInf;
+      const uint32_t gid = (uint32_t)(key & 0xFFFFFFFFu);
+      rows[tid] = (key != kKeyInf) ? gid / (uint32_t)G : 0xFFFFFFFFu;
+      __syncthreads();
+      float v[32];
+      auto gather = [&](int ch) {
+        const int t = ch * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t row = rows[warp * 32 + i];
+          v[i] = (row != 0xFFFFFFFFu && t < d) ? __ldg(X + (size_t)row * d + t) : 0.0f;
+        }
+      };
+      gather(0);
+      double acc = 0.0;
+      for (int ch = 0; ch < nch; ++ch) {
+        float* tb = tile + (ch & 1) * RT * S;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tb[(warp * 32 + i) * S + lane] = v[i];
+        __syncthreads();
+        if (ch + 1 < nch) gather(ch + 1);
+        if (key != kKeyInf) {
+          const float* myrow = tb + tid * S;
+          const int dc = min(32, d - ch * 32);
+          for (int t = 0; t < dc; ++t) {
+            const double df = __dsub_rn((double)qs[ch * 32 + t], (double)myrow[t]);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+          }
+        }
+      }
+      uint64_t out = kKeyInf;
+      if (key != kKeyInf) {
+        const float dist = __double2float_rn(acc);
+        out = ((uint64_t)__float_as_uint(dist) << 32) | (labels ? labels[gid / (uint32_t)G] : gid);
+        if (refined) atomicAdd(refined, 1ull);
+      }
+      __syncthreads();  // every thread is done with both tiles and rows[]
+      if (c < npow) rk[c] = out;
+    }
+    __syncthreads();
+    cta_bitonic_sort_u64(rk, npow);
+    for (int i = tid; i < k; i += RT) {
+      const uint64_t v2 = (i < npow) ? rk[i] : kKeyInf;
+      out_ids[q * k + i] = v2 != kKeyInf ? (int64_t)(uint32_t)(v2 & 0xFFFFFFFFu) : -1;
+      out_dists[q * k + i] = v2 != kKeyInf ? __uint_as_float((uint32_t)(v2 >> 32)) : __int_as_float(0x7f800000);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6 for long rows (d > 128, d % 4 == 0; c3: 6 KB per row): one THREAD per
+// candidate streams its own row with eight 16-B loads in flight (no shared
+// tile, so ~64 warps per SM keep the gather busy) and extends the fp64
+// ordered sum in ascending t (O10); its key (bits(delta) << 32 | id) goes to
+// dk[].  Then a warp per query keeps the first k by key.
+constexpr int RL_T = 256;
+__global__ void __launch_bounds__(RL_T) refine_rows_kernel(const uint64_t* __restrict__ keys,
+                                                           int64_t total, int bigK,
+                                                           const float* __restrict__ queries,
+                                                           const float* __restrict__ X, int d, int G,
+                                                           const uint32_t* __restrict__ labels,
+                                                           unsigned long long* __restrict__ refined,
+                                                           uint64_t* __restrict__ dk) {
+  pdl_wait();
+  uint32_t nref = 0;
+  for (int64_t i = blockIdx.x * (int64_t)RL_T + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * RL_T) {
+    const uint64_t key = keys[i];
+    uint64_t out = kKeyInf;
+    if (key != kKeyInf) {
+      const uint32_t gid = (uint32_t)(key & 0xFFFFFFFFu);
+      const float4* xr = reinterpret_cast<const float4*>(X + (size_t)(gid / (uint32_t)G) * d);
+      const float4* qr = reinterpret_cast<const float4*>(queries + (i / bigK) * d);
+      double acc = 0.0;
+      const int n4 = d / 4;
+      for (int c0 = 0; c0 < n4; c0 += 8) {
+        float4 xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          xv[u] = (c0 + u < n4) ? __ldcs(xr + c0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (c0 + u < n4) {
+            const float4 qv = __ldg(qr + c0 + u);
+            double df = __dsub_rn((double)qv.x, (double)xv[u].x);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+            df = __dsub_rn((double)qv.y, (double)xv[u].y);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+            df = __dsub_rn((double)qv.z, (double)xv[u].z);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+            df = __dsub_rn((double)qv.w, (double)xv[u].w);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+          }
+        }
+      }
+      const float dist = __double2float_rn(acc);
+      out = ((uint64_t)__float_as_uint(dist) << 32) | (labels ? labels[gid / (uint32_t)G] : gid);
+      ++nref;
+    }
+    dk[i] = out;
+  }
+  if (refined) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nref += __shfl_xor_sync(0xffffffffu, nref, o);
+    if ((threadIdx.x & 31) == 0 && nref) atomicAdd(refined, (unsigned long long)nref);
+  }
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(128) refine_topk_kernel(const uint64_t* __restrict__ dk, int64_t nq,
+                                                          int bigK, int npow, int k,
+                                                          int64_t* __restrict__ out_ids,
+                                                          float* __restrict__ out_dists) {
+  extern __shared__ __align__(16) uint64_t rt_sm[];
+  const int lane = lane_id(), warp = warp_id();
+  uint64_t* buf = rt_sm + (size_t)warp * npow;
+  pdl_wait();
+  for (int64_t q = (int64_t)blockIdx.x * 4 + warp; q < nq; q += (int64_t)gridDim.x * 4) {
+    for (int i = lane; i < npow; i += 32) buf[i] = i < bigK ? dk[q * bigK + i] : kKeyInf;
+    __syncwarp();
+    for (int size = 2; size <= npow; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < (npow >> 1); i += 32) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const uint64_t x = buf[lo], y = buf[hi];
+          if ((x > y) == asc) { buf[lo] = y; buf[hi] = x; }
+        }
+        __syncwarp();
+      }
+    }
+    for (int i = lane; i < k; i += 32) {
+      const uint64_t v = i < npow ? buf[i] : kKeyInf;
+      out_ids[q * k + i] = v != kKeyInf ? (int64_t)(uint32_t)(v & 0xFFFFFFFFu) : -1;
+      out_dists[q * k + i] = v != kKeyInf ? __uint_as_float((uint32_t)(v >> 32)) : __int_as_float(0x7f800000);
+    }
+    __syncwarp();
+  }
+}
+
+static rairs_status launch_refine_rows(const rairs_index_s* idx, const SearchArgs& a, int bigK,
+                                       cudaStream_t s) {
+  const int64_t total = a.nq * bigK;
+  uint64_t* dk = nullptr;
+  RAIRS_CUDA_TRY(ws_malloc(&dk, (size_t)total * 8, s));
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, RL_T), 148 * 8));
+  cudaError_t e = launch_pdl(refine_rows_kernel, dim3(g), dim3(RL_T), 0, s, (const uint64_t*)a.cand_keys,
+                             total, bigK, a.queries, (const float*)idx->X, idx->d, idx->nshards,
+                             (const uint32_t*)idx->labels,
+                             a.counters ? a.counters + 1 : (unsigned long long*)nullptr, dk);
+  if (e == cudaSuccess) {
+    const int npow = next_pow2(std::max(bigK, 2));
+    const size_t smem = (size_t)4 * npow * 8;
+    e = cudaFuncSetAttribute(refine_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.nq, 4), 148 * 16));
+      e = launch_pdl(refine_topk_kernel, dim3(g2), dim3(128), smem, s, (const uint64_t*)dk, a.nq, bigK,
+                     npow, a.k, a.out_ids, a.out_dists);
+    }
+  }
+  cudaFreeAsync(dk, s);
+  if (e != cudaSuccess) {
+    set_error(std::string("refine (long rows): ") + cudaGetErrorString(e));
+    return RAIRS_E_CUDA;
+  }
+  return RAIRS_OK;
+}
+
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s) {
   if (a.nq <= 0) return RAIRS_OK;
   {
@@ -283,18 +477,33 @@ rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaSt
     }
   }
   const int bigK = a.k * a.refine_factor;
+  // (thread-per-row streaming, launch_refine_rows, measured 4x slower on c3pl: uncoalesced)
+  if (std::getenv("RAIRS_REFINE_ROWS") && (idx->d & 3) == 0 && bigK <= 2048)
+    return launch_refine_rows(idx, a, bigK, s);
   const int npow = next_pow2(std::max(bigK, 2));
-  const size_t smem = (size_t)npow * 8 + (size_t)idx->d * 8 + (size_t)RT * RSTRIDE * 4 + RT * 4;
+  // narrower tiles for long rows: ~3x smaller shared footprint, more CTAs per SM
+  // overlap one CTA's gather with another's serial fp64 sums
+  const int rdc = (idx->d > 128 && !std::getenv("RAIRS_REFINE_RDC128")) ? 32 : 128;
+  const size_t smem = (size_t)npow * 8 + (size_t)idx->d * 8 + (size_t)RT * (rdc + 1) * 4 + RT * 4;
   if (smem > 220 * 1024) {
     set_error("refine: shared memory budget exceeded");
     return RAIRS_E_UNSUPPORTED;
   }
-  RAIRS_CUDA_TRY(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
   const int grid = (int)std::min<int64_t>(a.nq, 1 << 30);
-  refine_kernel<<<grid, RT, smem, s>>>(a.cand_keys, a.nq, bigK, npow, a.k, a.queries, idx->X,
-                                        idx->d, idx->nshards, idx->labels,
-                                        a.counters ? a.counters + 1 : nullptr, a.out_ids, a.out_dists);
+  if (rdc == 32) {
+    const size_t lsm = (size_t)npow * 8 + (size_t)((idx->d + 3) & ~3) * 4 + (size_t)2 * RT * 33 * 4 + RT * 4;
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(refine_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)lsm));
+    refine_long_kernel<<<grid, RT, lsm, s>>>(a.cand_keys, a.nq, bigK, npow, a.k, a.queries, idx->X,
+                                             idx->d, idx->nshards, idx->labels,
+                                             a.counters ? a.counters + 1 : nullptr, a.out_ids, a.out_dists);
+  } else {
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(refine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    refine_kernel<128><<<grid, RT, smem, s>>>(a.cand_keys, a.nq, bigK, npow, a.k, a.queries, idx->X,
+                                              idx->d, idx->nshards, idx->labels,
+                                              a.counters ? a.counters + 1 : nullptr, a.out_ids, a.out_dists);
+  }
   RAIRS_CHECK_LAUNCH();
   return RAIRS_OK;
 }
