@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(PX_T) probe_split_kernel(ProbeArgs a,
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm);
   uint32_t* ids = reinterpret_cast<uint32_t*>(keys + npow);
   double* xs = reinterpret_cast<double*>(ids + npow + (npow & 1));
+  float* tile = reinterpret_cast<float*>(xs + a.d);  // [PX_T][33]
   const int64_t n = min(*count, (uint32_t)PX_CAP);
   for (int64_t w = blockIdx.x; w < n * PX_S; w += gridDim.x) {
     const int64_t i = w / PX_S;
@@ -306,19 +307,36 @@ __global__ void __launch_bounds__(PX_T) probe_split_kernel(ProbeArgs a,
     for (int t = threadIdx.x; t < a.d; t += PX_T) xs[t] = (double)a.X[r * a.d + t];
     __syncthreads();
     const int64_t l0 = (int64_t)sp * per;
-    for (int e = threadIdx.x; e < npow; e += PX_T) {
+    // PX_T centroids per pass; their rows staged 32 dims at a time in a padded
+    // shared tile (warp w loads rows 32w.. coalesced, lane = dimension, 32
+    // loads in flight), then thread e extends centroid e's ordered fp64 sum
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (int e0 = 0; e0 < npow; e0 += PX_T) {
+      const int e = e0 + threadIdx.x;
       const int64_t l = l0 + e;
-      uint64_t key = kKeyInf;
-      if (e < per && l < a.nl) {
-        const float* c = a.C + l * a.d;
-        double acc = 0.0;
-        for (int t = 0; t < a.d; ++t) {  // ascending t, fp64 ordered (O1)
-          const double df = __dsub_rn(xs[t], (double)__ldg(c + t));
-          acc = __dadd_rn(acc, __dmul_rn(df, df));
+      const bool valid = e < per && l < a.nl;
+      double acc = 0.0;
+      for (int t0 = 0; t0 < a.d; t0 += 32) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int ee = e0 + wp * 32 + i;
+          const int64_t rl = l0 + ee;
+          v[i] = (ee < per && rl < a.nl && t0 + lane < a.d) ? __ldg(a.C + rl * a.d + t0 + lane) : 0.0f;
         }
-        key = dbits(acc);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tile[(wp * 32 + i) * 33 + lane] = v[i];
+        __syncthreads();
+        if (valid) {
+          const int dc = min(32, a.d - t0);
+          for (int t = 0; t < dc; ++t) {  // ascending t, fp64 ordered (O1)
+            const double df = __dsub_rn(xs[t0 + t], (double)tile[threadIdx.x * 33 + t]);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+          }
+        }
+        __syncthreads();
       }
-      keys[e] = key;
+      keys[e] = valid ? dbits(acc) : kKeyInf;
       ids[e] = (uint32_t)l;
     }
     __syncthreads();
@@ -408,7 +426,7 @@ rairs_status launch_probe_split(const ProbeArgs& a, int32_t* flags, cudaStream_t
   const int per = (int)ceil_div(a.nl, PX_S);
   const int npow_s = next_pow2(std::max(per, a.L));
   const int npow_m = next_pow2(PX_S * a.L);
-  const size_t sm_s = (size_t)npow_s * 12 + 8 + (size_t)a.d * 8;
+  const size_t sm_s = (size_t)npow_s * 12 + 8 + (size_t)a.d * 8 + (size_t)PX_T * 33 * 4;
   const size_t sm_m = (size_t)npow_m * 12 + 8;
   if (sm_s > 200 * 1024 || sm_m > 200 * 1024) return RAIRS_OK;
   uint32_t *list = nullptr, *count = nullptr, *ti = nullptr;

@@ -785,6 +785,10 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     // c4 (64): one split per row tile beats covering every SM (coarse 0.120 ->
     // 0.098 ms and 0.305 -> 0.265 ms for 79 row tiles)
     int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(64, mtiles)));
+    // long rows (d >= 512, c3: 1536): a tile's MMA (K = d) dwarfs the top-W
+    // insertion a split restarts, so spread the column tiles over >= 4 CTAs
+    // per SM (the grid of row tiles alone leaves SMs idle: 79 of 148 at 10k rows)
+    if (d >= 512) nsplit = std::max<int>(nsplit, (int)std::min<int64_t>(ntiles, ceil_div(4 * 148, mtiles)));
     if (capped)  // >= 4 capped lists per needed 32 candidates: a group rarely holds > 32 of them
       nsplit = std::max<int>(nsplit, (int)std::min<int64_t>(ntiles, ceil_div(4 * ceil_div(Wp1, 32), FT_HALVES)));
     nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys

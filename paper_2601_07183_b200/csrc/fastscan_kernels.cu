@@ -998,7 +998,7 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
     return RAIRS_E_INTERNAL;
   }
   const int cbb = idx->M * 16 * idx->dsub * 4;
-  p.cb_smem = cbb <= 16 * 1024 ? cbb : 0;
+  p.cb_smem = cbb <= 160 * 1024 ? cbb : 0;  // fs_lut_kernel stages it (c3: 96 KB)
   p.luts = sa.luts;
   pl.warps = std::min<int>(FS_MAXW, (200 * 1024) / p.warp_bytes);
   if (pl.warps < 1) {
@@ -1040,7 +1040,11 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     const size_t lsm = (size_t)pl.a.cb_smem + (size_t)FL_WARPS * (keepT ? 17 : 1) * idx->M * 4;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)lsm));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FL_WARPS), 148 * 8));
+    // persistent: each CTA stages the codebook once for many queries
+    int per_sm = 1;
+    RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_lut_kernel, FL_WARPS * 32, lsm));
+    per_sm = std::max(1, std::min(per_sm, 8));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FL_WARPS), 148LL * per_sm));
     RAIRS_CUDA_TRY(launch_pdl(fs_lut_kernel, dim3(g), dim3(FL_WARPS * 32), lsm, s, pl.a,
                               const_cast<uint4*>(sa.luts)));
   }
