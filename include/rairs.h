@@ -253,8 +253,10 @@ typedef struct {
 rairs_status rairs_get_stats(rairs_index_t idx, rairs_stats* out, int32_t reset);
 
 /* ---- scan mode --------------------------------------------------------------
- * 0 = auto (list-major tensor-core scan when supported), 1 = query-major SIMT
- * fast scan (one CTA per query, shared-memory LUT lookups), 2 = list-major:
+ * 0 = auto (list-major when the batch probes each list >= 3 times on average
+ * and its limits hold, else query-major), 1 = query-major fast scan (one warp
+ * per query: LUT rows in registers, prmt lookups, dp4a sums over an 8-item
+ * nibble-group code layout, SEIL range list, exact top-bigK), 2 = list-major:
  * (query, probe) pairs grouped by list, scores of each list's items for all its
  * queries as one exact u8 x u8 -> s32 tcgen05 contraction of one-hot codes and
  * quantised LUTs (the paper's query-batch cache optimisation).
@@ -270,6 +272,12 @@ rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode);
 rairs_status rairs_profile_enable(rairs_index_t idx, int32_t on);
 rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launches3,
                                 int32_t reset);
+/* The dominant scan kernel's own device time (fs_scan_kernel on the
+ * query-major path, lm_tensor_kernel on the list-major one) from events
+ * recorded right around its launch while profiling is enabled: accumulated
+ * milliseconds (*ms) and launches (*launches) since the last reset. */
+rairs_status rairs_profile_read_kernel(rairs_index_t idx, double* ms, int64_t* launches,
+                                       int32_t reset);
 /* Number of CUDA kernels the library launched for searches on this index
  * since the last reset (host-side count, always on): *kernels receives it;
  * reset != 0 zeroes the counter. RAIRS_E_INVALID on NULL arguments. */

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "rairs_index_free", "rairs_index_get_info", "rairs_search", "rairs_search_host",
     "rairs_search_debug", "rairs_merge_topk", "rairs_exact_knn", "rairs_export_trained",
     "rairs_export_assignment", "rairs_export_layout", "rairs_profile_enable",
-    "rairs_profile_read", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
+    "rairs_profile_read", "rairs_profile_read_kernel", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
     "rairs_certify_fallbacks", "rairs_set_scan_mode", "rairs_profile_kernels",
     "rairs_search_plan", "rairs_add", "rairs_remove_ids", "rairs_get_stats",
     "rairs_search_host_async",
@@ -107,6 +107,7 @@ def lib() -> ctypes.CDLL:
         "rairs_export_layout": [_P] * 9,
         "rairs_profile_enable": [_P, _I32],
         "rairs_profile_read": [_P, _P, _P, _I32],
+        "rairs_profile_read_kernel": [_P, _P, _P, _I32],
         "rairs_set_coarse_mode": [_P, _I32],
         "rairs_certify_fallbacks": [_P, _P, _I32],
         "rairs_set_scan_mode": [_P, _I32],

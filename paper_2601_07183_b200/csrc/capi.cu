@@ -2,6 +2,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 
@@ -184,7 +185,7 @@ static void free_index(rairs_index_s* x) {
   delete x->hq_mu;
   delete x->aux_mu;
   for (auto& es : x->pending)
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(es.e[i]);
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(es.e[i]);
   for (auto e : x->pool) cudaEventDestroy(e);
   delete x;
 }
@@ -198,7 +199,7 @@ struct StageEvents {
   StageEvents(rairs_index_s* i, cudaStream_t st) : idx(i), s(st), on(i->prof) {
     if (!on) return;
     std::lock_guard<std::mutex> lock(idx->prof_mu);
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 6; ++k) {
       if (!idx->pool.empty()) {
         ev.e[k] = idx->pool.back();
         idx->pool.pop_back();
@@ -261,6 +262,11 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
   idx->n_queries += nq;
 
   StageEvents ev(idx, s);
+  if (ev.on) {
+    a.kev[0] = ev.ev.e[4];
+    a.kev[1] = ev.ev.e[5];
+    a.kev_used = &ev.ev.kern;
+  }
   rairs_status st = RAIRS_OK;
   ev.mark(0);
   // coarse: P(q) = first nprobe lists by (D64, l)  (O1).  Tensor-core TF32
@@ -311,16 +317,31 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
     } else {
       a.sorted_keys = cand_ids != nullptr || cand_scores != nullptr;
       uint4* luts = nullptr;
+      uint64_t* dbuf = nullptr;
+      uint32_t* dn = nullptr;
+      // the exact top-bigK in a separate pass (RAIRS_FS_DEFER=0: in the scan kernel)
+      static const bool defer = [] {
+        const char* e = std::getenv("RAIRS_FS_DEFER");
+        return e ? std::atoi(e) != 0 : true;
+      }();
+      const size_t dcap = (size_t)fastscan_cap(bigK);
       cudaError_t le = ws_malloc(&luts, (size_t)nq * idx->M_pad * 16, s);
+      if (le == cudaSuccess && defer) le = ws_malloc(&dbuf, (size_t)nq * dcap * 8, s);
+      if (le == cudaSuccess && defer) le = ws_malloc(&dn, (size_t)nq * 4, s);
       if (le != cudaSuccess) {
         set_error(std::string("workspace: ") + cudaGetErrorString(le));
         st = RAIRS_E_OOM;
       } else {
         a.luts = luts;
-        st = launch_fastscan(idx, a, s);
-        nk += 1;  // + the LUT kernel
-        cudaFreeAsync(luts, s);
+        FsExtra ex;
+        ex.defer_buf = dbuf;
+        ex.defer_n = dn;
+        st = launch_fastscan(idx, a, s, ex);
+        nk += defer ? 2 : 1;  // + the LUT kernel (+ the finish kernel)
       }
+      cudaFreeAsync(luts, s);
+      cudaFreeAsync(dbuf, s);
+      cudaFreeAsync(dn, s);
       nk += 1;
       ev.mark(2);
     }
@@ -1004,7 +1025,13 @@ rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launche
       RAIRS_CUDA_TRY(cudaEventElapsedTime(&ms, es.e[k], es.e[k + 1]));
       idx->ms[k] += ms;
     }
-    for (int k = 0; k < 4; ++k) idx->pool.push_back(es.e[k]);
+    if (es.kern) {
+      float ms = 0.0f;
+      RAIRS_CUDA_TRY(cudaEventElapsedTime(&ms, es.e[4], es.e[5]));
+      idx->ms_kern += ms;
+      idx->kern_launches += 1;
+    }
+    for (int k = 0; k < 6; ++k) idx->pool.push_back(es.e[k]);
   }
   idx->pending.clear();
   for (int k = 0; k < 3; ++k) {
@@ -1016,6 +1043,20 @@ rairs_status rairs_profile_read(rairs_index_t idx, double* ms3, int64_t* launche
       idx->ms[k] = 0;
       idx->launches[k] = 0;
     }
+  }
+  return RAIRS_OK;
+}
+
+rairs_status rairs_profile_read_kernel(rairs_index_t idx, double* ms, int64_t* launches,
+                                       int32_t reset) {
+  if (!idx) return invalid("index is NULL");
+  RAIRS_TRY(rairs_profile_read(idx, nullptr, nullptr, 0));  // drain pending events
+  std::lock_guard<std::mutex> lock(idx->prof_mu);
+  if (ms) *ms = idx->ms_kern;
+  if (launches) *launches = idx->kern_launches;
+  if (reset) {
+    idx->ms_kern = 0;
+    idx->kern_launches = 0;
   }
   return RAIRS_OK;
 }

@@ -789,6 +789,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     // insertion a split restarts, so spread the column tiles over >= 4 CTAs
     // per SM (the grid of row tiles alone leaves SMs idle: 79 of 148 at 10k rows)
     if (d >= 512) nsplit = std::max<int>(nsplit, (int)std::min<int64_t>(ntiles, ceil_div(4 * 148, mtiles)));
+    if (const char* e = std::getenv("RAIRS_COARSE_NSPLIT")) nsplit = std::max(1, std::min<int>(ntiles, std::atoi(e)));
     if (capped)  // >= 4 capped lists per needed 32 candidates: a group rarely holds > 32 of them
       nsplit = std::max<int>(nsplit, (int)std::min<int64_t>(ntiles, ceil_div(4 * ceil_div(Wp1, 32), FT_HALVES)));
     nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys

@@ -132,6 +132,11 @@ struct FsArgs {
   // bigK-th smallest score bounds the query's bigK-th from above; written to
   // tau_out[q] (0xFFFFFFFF if the list has fewer than bigK items), no keys
   uint32_t* tau_out;
+  // deferred finish: the scan kernel leaves each query's buffer (cap entries,
+  // n | exact << 31 in defer_n) to fs_finish_kernel, a separate high-occupancy
+  // pass, instead of selecting in place
+  uint64_t* defer_buf;
+  uint32_t* defer_n;
   int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
@@ -588,6 +593,39 @@ __device__ __forceinline__ void fs_put(const FsArgs& a, uint64_t* cand, uint32_t
   }
 }
 
+// The deferred exact top-bigK: one warp per query over the buffer the scan
+// left (pre-keys with an s <= bin-threshold filter, or resolved keys in
+// massive-tie mode): histogram of its scores, then fs_finish (exact bigK-th
+// score, ids, ties by id).  Runs at high occupancy, apart from the lookups.
+constexpr int FF_WARPS = 8;
+__global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(FsArgs a) {
+  extern __shared__ __align__(16) uint8_t ff_smem[];
+  const int lane = lane_id(), warp = warp_id();
+  const uint32_t cap = (uint32_t)a.cap, bigK = (uint32_t)a.bigK;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(ff_smem + (size_t)warp * (cap * 8 + 1024));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(cand + cap);
+  const int hsh = a.hbits > 8 ? a.hbits - 8 : 0;
+  pdl_wait();  // the scan kernel's buffers
+  for (int64_t q = (int64_t)blockIdx.x * FF_WARPS + warp; q < a.nq; q += (int64_t)gridDim.x * FF_WARPS) {
+    const uint32_t nx = a.defer_n[q];
+    const uint32_t n = nx & 0x7FFFFFFFu;
+    const bool exact = (nx >> 31) != 0;
+    const uint64_t* src = a.defer_buf + (size_t)q * cap;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint64_t v = src[i];
+      cand[i] = v;
+      if (!exact) atomicAdd(&hist[(uint32_t)(v >> 32) >> hsh], 1u);
+    }
+    __syncwarp();
+    const uint32_t keep = fs_finish(a, cand, hist, n, exact, hsh);
+    for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? cand[i] : kKeyInf;
+    __syncwarp();
+  }
+  pdl_trigger();
+}
+
 // A3 for every query of the batch, one warp per query (O2: lane per
 // subquantizer, fp32 RN, ascending t; see fs_build_lut), into luts[q][M_pad].
 // Needs only the queries, so under programmatic dependent launch it overlaps
@@ -819,7 +857,20 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
       __syncwarp();
     }
 
-    // ---- exact top-bigK of the buffer ----
+    // ---- exact top-bigK of the buffer (here, or deferred to fs_finish_kernel) ----
+    if (a.defer_buf) {
+      uint64_t* dst = a.defer_buf + (size_t)q * cap;
+      for (uint32_t i = lane; i < st.n; i += 32) dst[i] = cand[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
+      if (lane == 0) {
+        a.defer_n[q] = st.n | (st.exact ? 0x80000000u : 0u);
+        if (a.dco) a.dco[q] = (int64_t)my_dco;
+        if (a.dco_total) atomicAdd(a.dco_total, (unsigned long long)my_dco);
+      }
+      __syncwarp();
+      continue;
+    }
     const uint32_t keep = (a.dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh);
     if (a.tau_out) {  // threshold mode: the bigK-th smallest score (an upper bound, see FsArgs)
       uint32_t mx = 0;
@@ -923,6 +974,8 @@ static int fs_variant() {
 }
 static int fs_capmin() { return fs_variant() == 2 ? 1024 : 512; }
 
+int fastscan_cap(int bigK);
+
 static int fs_hbits(int M) {
   int b = 1;
   while (((int64_t)M * 255) >> b) ++b;
@@ -962,8 +1015,10 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   p.qlist = ex.qlist;
   p.qcount = ex.qcount;
   p.tau_out = ex.tau_out;
+  p.defer_buf = ex.defer_buf;
+  p.defer_n = ex.defer_n;
   p.bigK = sa.k * sa.refine_factor;
-  p.cap = std::max(fs_capmin(), next_pow2(p.bigK + FS_ROUND + 64));
+  p.cap = fastscan_cap(p.bigK);
   p.hbits = fs_hbits(idx->M);
   p.out_keys = sa.cand_keys;
   p.dco = ex.tau_out ? nullptr : sa.dco;
@@ -1048,7 +1103,23 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     RAIRS_CUDA_TRY(launch_pdl(fs_lut_kernel, dim3(g), dim3(FL_WARPS * 32), lsm, s, pl.a,
                               const_cast<uint4*>(sa.luts)));
   }
-  return fs_variant() == 1 ? fs_launch<3>(pl, s) : fs_launch<2>(pl, s);
+  const bool kev = sa.kev[0] && sa.kev_used && !ex.tau_out && !ex.qlist;
+  if (kev) RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[0], s));
+  RAIRS_TRY(fs_variant() == 1 ? fs_launch<3>(pl, s) : fs_launch<2>(pl, s));
+  if (kev) {
+    RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[1], s));
+    *sa.kev_used = true;
+  }
+  if (pl.a.defer_buf) {
+    const size_t fsm = (size_t)FF_WARPS * ((size_t)pl.a.cap * 8 + 1024);
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)fsm));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FF_WARPS), 148 * 8));
+    RAIRS_CUDA_TRY(launch_pdl(fs_finish_kernel, dim3(g), dim3(FF_WARPS * 32), fsm, s, pl.a));
+  }
+  return RAIRS_OK;
 }
+
+int fastscan_cap(int bigK) { return std::max(fs_capmin(), next_pow2(bigK + FS_ROUND + 64)); }
 
 }  // namespace rairs

@@ -104,11 +104,13 @@ struct rairs_index_s {
   // stage profiling (CUDA events on the search stream); prof_mu guards the
   // event vectors and sums (concurrent searches)
   bool prof = false;
-  struct EvSet { cudaEvent_t e[4]; };
+  struct EvSet { cudaEvent_t e[6]; bool kern = false; };  // e[4..5]: the dominant scan kernel
   std::mutex prof_mu;
   std::vector<EvSet> pending;
   std::vector<cudaEvent_t> pool;
   double ms[3] = {0, 0, 0};
+  double ms_kern = 0;
+  int64_t kern_launches = 0;
   std::atomic<int64_t> launches[3] = {{0}, {0}, {0}};
   std::atomic<int64_t> kernels{0};  // kernels launched by searches (rairs_profile_kernels)
 };
@@ -201,6 +203,10 @@ struct SearchArgs {
   // query's bigK keys may be written in any order (the refine ranks them)
   bool sorted_keys = false;
   const uint4* luts = nullptr;  // fast scan: [nq][M_pad] LUT rows workspace (16 B each)
+  // profiling: events recorded right around the dominant scan kernel's launch
+  // (fs_scan_kernel / lm_tensor_kernel); *kev_used set when recorded
+  cudaEvent_t kev[2] = {nullptr, nullptr};
+  bool* kev_used = nullptr;
 };
 // query-major register-LUT fast scan (fastscan_kernels.cu): A3-A6 fused
 rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s);
@@ -210,7 +216,10 @@ struct FsExtra {
   const uint32_t* qcount = nullptr;
   uint32_t* tau_out = nullptr;        // threshold mode (see FsArgs::tau_out)
   bool luts_ready = false;            // a.luts already holds every query's LUT
+  uint64_t* defer_buf = nullptr;      // deferred finish workspace [nq][fastscan_cap(bigK)]
+  uint32_t* defer_n = nullptr;        // [nq]
 };
+int fastscan_cap(int bigK);
 rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s,
                              const FsExtra& ex = FsExtra{});
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);

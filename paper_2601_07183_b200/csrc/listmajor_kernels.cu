@@ -1498,6 +1498,8 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
   la.nlist = nlist;
   la.order = idx->lm_order;
   const size_t tsm = 1024 + LM_B_MAX + LM_MAXREF * 4 * 4 + 8 + LM_QT * 8 + (2 * 8 + 5) * 8 + 64;
+  const bool kev = sa.kev[0] && sa.kev_used;
+  if (kev) LM_TRY(cudaEventRecord(sa.kev[0], s));
   switch (idx->M_pad / 16) {
     case 1: LM_TRY(launch_lm_tensor_shape<1>(la, tsm, s)); break;
     case 2: LM_TRY(launch_lm_tensor_shape<2>(la, tsm, s)); break;
@@ -1506,6 +1508,10 @@ rairs_status launch_listmajor(const rairs_index_s* idx, const SearchArgs& sa, cu
     case 6: LM_TRY(launch_lm_tensor_shape<6>(la, tsm, s)); break;
     case 8: LM_TRY(launch_lm_tensor_shape<8>(la, tsm, s)); break;
     default: cleanup(); set_error("list-major: unsupported M"); return RAIRS_E_INTERNAL;
+  }
+  if (kev) {
+    LM_TRY(cudaEventRecord(sa.kev[1], s));
+    *sa.kev_used = true;
   }
   if (fused) {
     // 4f. candidates -> exact top-bigK per query; overflowed queries (more than

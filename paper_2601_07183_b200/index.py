@@ -286,6 +286,14 @@ class Index:
         return {"ms": {"coarse": ms[0], "scan": ms[1], "refine": ms[2]},
                 "launches": {"coarse": nl[0], "scan": nl[1], "refine": nl[2]}}
 
+    def profile_read_kernel(self, reset: bool = True) -> Dict[str, float]:
+        """The dominant scan kernel's own time (ms) and launches (profiling on)."""
+        ms = ctypes.c_double()
+        nl = ctypes.c_int64()
+        check(lib().rairs_profile_read_kernel(self._h, ctypes.byref(ms), ctypes.byref(nl),
+                                              int(bool(reset))), "rairs_profile_read_kernel")
+        return {"ms": ms.value, "launches": nl.value}
+
     def scan_path(self, nq: int, k: int, nprobe: int, refine_factor: int) -> str:
         """'listmajor' or 'simt': the scan kernels a search of nq queries uses."""
         sp = ctypes.c_int32()
