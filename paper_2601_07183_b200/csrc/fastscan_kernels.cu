@@ -606,7 +606,8 @@ __global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(FsArgs a) {
   uint32_t* hist = reinterpret_cast<uint32_t*>(cand + cap);
   const int hsh = a.hbits > 8 ? a.hbits - 8 : 0;
   pdl_wait();  // the scan kernel's buffers
-  for (int64_t q = (int64_t)blockIdx.x * FF_WARPS + warp; q < a.nq; q += (int64_t)gridDim.x * FF_WARPS) {
+  const int nw = blockDim.x >> 5;
+  for (int64_t q = (int64_t)blockIdx.x * nw + warp; q < a.nq; q += (int64_t)gridDim.x * nw) {
     const uint32_t nx = a.defer_n[q];
     const uint32_t n = nx & 0x7FFFFFFFu;
     const bool exact = (nx >> 31) != 0;
@@ -1111,11 +1112,13 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     *sa.kev_used = true;
   }
   if (pl.a.defer_buf) {
-    const size_t fsm = (size_t)FF_WARPS * ((size_t)pl.a.cap * 8 + 1024);
+    const size_t per = (size_t)pl.a.cap * 8 + 1024;
+    const int nw = (int)std::max<size_t>(1, std::min<size_t>(FF_WARPS, (200 * 1024) / per));
+    const size_t fsm = (size_t)nw * per;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)fsm));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FF_WARPS), 148 * 8));
-    RAIRS_CUDA_TRY(launch_pdl(fs_finish_kernel, dim3(g), dim3(FF_WARPS * 32), fsm, s, pl.a));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, nw), 148 * 8));
+    RAIRS_CUDA_TRY(launch_pdl(fs_finish_kernel, dim3(g), dim3(nw * 32), fsm, s, pl.a));
   }
   return RAIRS_OK;
 }
