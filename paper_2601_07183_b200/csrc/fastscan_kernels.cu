@@ -38,9 +38,15 @@
 namespace rairs {
 
 constexpr int FS_RCAP = 64;      // ranges per scan batch (per warp)
-constexpr int FS_ROUND = 256;    // items appended per warp round at most (32 lanes x 8)
 constexpr int FS_MAXW = 8;       // warps per CTA (fewer when bigK needs more shared memory)
 constexpr int FS_SLOTS = 64;     // claim-counter slots (concurrent searches)
+// RAIRS_FS_DBG timing experiments (skip rounds / selection / loads) are only
+// compiled in with -DRAIRS_FS_TIMING; the product kernel has no such branches.
+#ifdef RAIRS_FS_TIMING
+constexpr bool kFsTiming = true;
+#else
+constexpr bool kFsTiming = false;
+#endif
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -137,6 +143,7 @@ struct FsArgs {
   // pass, instead of selecting in place
   uint64_t* defer_buf;
   uint32_t* defer_n;
+  int pf_lo;                   // first chunk of the next round's groups prefetched into L2
   int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
@@ -508,8 +515,8 @@ struct FsSel {
   uint64_t tau_key;  // exact mode: keys >= tau_key are dropped
 };
 
-__device__ __noinline__ void fs_compact(const FsArgs& a, uint64_t* cand, uint32_t* hist, int hsh,
-                                        FsSel& st) {
+__device__ __noinline__ FsSel fs_compact(const FsArgs& a, uint64_t* cand, uint32_t* hist, int hsh,
+                                         FsSel st, uint32_t round) {
   const int lane = lane_id();
   const uint32_t bigK = (uint32_t)a.bigK, cap = (uint32_t)a.cap;
   if (!st.exact) {
@@ -527,7 +534,7 @@ __device__ __noinline__ void fs_compact(const FsArgs& a, uint64_t* cand, uint32_
     }
     __syncwarp();
     st.n = out;
-    if (st.n + FS_ROUND <= cap) return;
+    if (st.n + round <= cap) return st;
     // (2) exact bigK-th score, ties kept; rebuild the histogram
     uint32_t below;
     const uint32_t s_star = fs_kth_score(cand, st.n, bigK, 0u, a.hbits, hist, &below);
@@ -538,7 +545,7 @@ __device__ __noinline__ void fs_compact(const FsArgs& a, uint64_t* cand, uint32_
     for (uint32_t i = lane; i < st.n; i += 32) atomicAdd(&hist[(uint32_t)(cand[i] >> 32) >> hsh], 1u);
     __syncwarp();
     st.hcount = st.n;
-    if (st.n + FS_ROUND <= cap) return;
+    if (st.n + round <= cap) return st;
     fs_resolve(a, cand, 0, st.n);
     st.exact = 1;
   }
@@ -548,6 +555,7 @@ __device__ __noinline__ void fs_compact(const FsArgs& a, uint64_t* cand, uint32_
   st.n = bigK;
   st.tau_key = cand[bigK - 1];
   st.tau = (uint32_t)(st.tau_key >> 32);
+  return st;
 }
 
 // lane's 8 scores -> pass mask: valid items that can still be in the top-bigK
@@ -658,8 +666,11 @@ __global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(FsArgs a, uint4* 
 // 16-B code loads in flight: consuming chunk c issues chunk c + 2, which past
 // the group's end is chunk 0/1 of the lane's NEXT round's group, so a round's
 // DRAM latency overlaps the previous round's lookups.
-template <int MINB>
-__global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
+template <int MINB, int GPL, int NW>
+__global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
+  constexpr int D = 4 / GPL;                 // ring slots per group
+  constexpr uint32_t FS_ROUND = 256u * GPL;  // items appended per round at most
+  const int dbg = kFsTiming ? a.dbg : 0;
   extern __shared__ __align__(16) uint8_t fs_smem[];
   const int lane = lane_id(), warp = warp_id();
   uint8_t* wb = fs_smem + (size_t)warp * a.warp_bytes;
@@ -774,86 +785,103 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
       }
       if (lane == 0) rg[nr] = ng_tot;
       __syncwarp();
-      // (3) rounds of 64 groups
+      // (3) rounds of 32 * GPL groups: lane tasks t0 + 32 g + lane, g < GPL
       uint32_t r_lo = 0;  // range holding the first task of the next round to map
-      FsTask A = fs_round_task(0u, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
-      // ring of four loop-carried chunk slots P, Q, U, V (chunk c in slot c % 4):
-      // three chunks in flight ahead of the one being consumed, no register
-      // copies.  (A cp.async shared-memory ring measured 2x slower.)
-      uint4 P = ldg_nc_v4(A.gp), Q = ldg_nc_v4(A.gp + 64);
-      uint4 U = ldg_nc_v4(A.gp + 128), V = ldg_nc_v4(A.gp + 192);
-      for (uint32_t t0 = 0; t0 < ((a.dbg & 1) ? 0u : ng_tot); t0 += 32) {
-        const FsTask nA = fs_round_task(t0 + 32, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
-        // the next round's group into L2 now (one round ahead of its loads): the
-        // register ring alone covers L2 latency, not DRAM's
-        if (!(a.dbg & 16))
-          for (int c = 8; c < M4; c += 2) prefetch_l2(nA.gp + c * 64);
-        uint32_t acc[8];
+      FsTask A[GPL];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[v] = 0u;
+      for (int g = 0; g < GPL; ++g) A[g] = fs_round_task(32u * g, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
+      // per group a ring of D loop-carried chunk slots (chunk c in slot c % D),
+      // each refilled right after it is consumed with the chunk D ahead (past
+      // the group's end: chunk c % D of the lane's next-round group), so the
+      // ring holds GPL * D = 4 16-B loads in flight and no register copies.
+      // (A cp.async shared-memory ring measured 2x slower.)
+      uint4 R[GPL][D];
+#pragma unroll
+      for (int g = 0; g < GPL; ++g)
+#pragma unroll
+        for (int s = 0; s < D; ++s) R[g][s] = ldg_nc_v4(A[g].gp + s * 64);
+      for (uint32_t t0 = 0; t0 < ((dbg & 1) ? 0u : ng_tot); t0 += 32u * GPL) {
+        FsTask nA[GPL];
+#pragma unroll
+        for (int g = 0; g < GPL; ++g)
+          nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
+        // the next round's groups into L2 now (one round ahead of their loads):
+        // the register ring alone covers L2 latency, not DRAM's
+        if (!(dbg & 16))
+#pragma unroll
+          for (int g = 0; g < GPL; ++g)
+            for (int c = a.pf_lo; c < M4; c += 2) prefetch_l2(nA[g].gp + c * 64);
+        uint32_t acc[GPL][8];
+#pragma unroll
+        for (int g = 0; g < GPL; ++g)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) acc[g][v] = 0u;
 #pragma unroll 1
-        for (int c = 0; c < M4; c += 4) {
+        for (int c = 0; c < M4; c += D) {
           const uint4* L = lut + 4 * c;
-          // each slot is refilled right after it is consumed, with the chunk four
-          // ahead: c+4..c+7 of this group, or (at its end; M4 % 4 == 0) chunks
-          // 0..3 of the lane's next-round group
-          const uint8_t* f = c + 4 < M4 ? A.gp + (c + 4) * 64 : nA.gp;
-          if (a.dbg & 32) {  // timing experiment: no code loads (synthetic words)
-            P = make_uint4(c, c * 3u, c * 5u, c * 7u);
-            Q = P; U = P; V = P;
-          }
-          lookup8(L[0], P.x, acc);
-          lookup8(L[1], P.y, acc);
-          lookup8(L[2], P.z, acc);
-          lookup8(L[3], P.w, acc);
-          if (!(a.dbg & 32)) P = ldg_nc_v4(f);
-          lookup8(L[4], Q.x, acc);
-          lookup8(L[5], Q.y, acc);
-          lookup8(L[6], Q.z, acc);
-          lookup8(L[7], Q.w, acc);
-          if (!(a.dbg & 32)) Q = ldg_nc_v4(f + 64);
-          lookup8(L[8], U.x, acc);
-          lookup8(L[9], U.y, acc);
-          lookup8(L[10], U.z, acc);
-          lookup8(L[11], U.w, acc);
-          if (!(a.dbg & 32)) U = ldg_nc_v4(f + 128);
-          lookup8(L[12], V.x, acc);
-          lookup8(L[13], V.y, acc);
-          lookup8(L[14], V.z, acc);
-          lookup8(L[15], V.w, acc);
-          if (!(a.dbg & 32)) V = ldg_nc_v4(f + 192);
-        }
-        if (a.dbg & 8) {  // timing experiment: no selection (scores folded into the DCO sum)
-          uint32_t x = 0;
 #pragma unroll
-          for (int v = 0; v < 8; ++v) x += acc[v];
-          my_dco += x & 1u;
-          A = nA;
-          continue;
-        }
-        if (st.n + FS_ROUND > cap) fs_compact(a, cand, hist, hsh, st);
-        // append (pre-key s << 32 | slot) every valid item that can be in the top-bigK
-        const uint32_t lim = min(st.tau, st.bthr >= (0xFFFFFFFFu >> hsh) ? 0xFFFFFFFFu
-                                                                          : ((st.bthr + 1u) << hsh) - 1u);
-        uint32_t pm = fs_pass(acc, A.vmask, lim);
-        if (st.exact && pm) pm = fs_pass_exact(a, acc, pm, A.gi, st.tau_key);
-        const uint32_t c = __popc(pm);
-        const uint32_t inc = warp_incl_scan(c);
-        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-        if (tot) {
-          uint32_t pos = st.n + inc - c;
-          fs_put(a, cand, hist, hsh, acc, pm, A.gi, st.exact, pos);
-          st.n += tot;
-          __syncwarp();
-          if (!st.exact) {
-            st.hcount += tot;
-            if (st.hcount >= bigK) {  // smallest bin whose cumulative count reaches bigK
-              uint32_t bl;
-              st.bthr = fs_bsel256(hist, bigK, &bl);
+          for (int s = 0; s < D; ++s) {
+#pragma unroll
+            for (int g = 0; g < GPL; ++g) {
+              // M4 % D == 0: chunk c + D + s of this group, or chunk s of the next
+              const uint8_t* f = c + D < M4 ? A[g].gp + (c + D + s) * 64 : nA[g].gp + s * 64;
+              if (dbg & 32) R[g][s] = make_uint4(c, c * 3u, c * 5u, c * 7u);  // timing: no code loads
+              lookup8(L[4 * s + 0], R[g][s].x, acc[g]);
+              lookup8(L[4 * s + 1], R[g][s].y, acc[g]);
+              lookup8(L[4 * s + 2], R[g][s].z, acc[g]);
+              lookup8(L[4 * s + 3], R[g][s].w, acc[g]);
+              if (!(dbg & 32)) R[g][s] = ldg_nc_v4(f);
             }
           }
         }
-        A = nA;
+        if (dbg & 8) {  // timing experiment: no selection (scores folded into the DCO sum)
+          uint32_t x = 0;
+#pragma unroll
+          for (int g = 0; g < GPL; ++g)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) x += acc[g][v];
+          my_dco += x & 1u;
+#pragma unroll
+          for (int g = 0; g < GPL; ++g) A[g] = nA[g];
+          continue;
+        }
+        if (st.n + FS_ROUND > cap) st = fs_compact(a, cand, hist, hsh, st, FS_ROUND);
+        // append (pre-key s << 32 | slot) every valid item that can be in the top-bigK
+        const uint32_t lim = min(st.tau, st.bthr >= (0xFFFFFFFFu >> hsh) ? 0xFFFFFFFFu
+                                                                          : ((st.bthr + 1u) << hsh) - 1u);
+        // cheap first test: no score of the lane's groups (valid or not) <= lim
+        uint32_t mn = acc[0][0];
+#pragma unroll
+        for (int g = 0; g < GPL; ++g)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) mn = min(mn, acc[g][v]);
+        if (__any_sync(0xffffffffu, mn <= lim)) {
+          uint32_t pm[GPL], c = 0;
+#pragma unroll
+          for (int g = 0; g < GPL; ++g) {
+            pm[g] = mn <= lim ? fs_pass(acc[g], A[g].vmask, lim) : 0u;
+            if (st.exact && pm[g]) pm[g] = fs_pass_exact(a, acc[g], pm[g], A[g].gi, st.tau_key);
+            c += __popc(pm[g]);
+          }
+          if (__any_sync(0xffffffffu, c != 0u)) {
+            const uint32_t inc = warp_incl_scan(c);
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            uint32_t pos = st.n + inc - c;
+#pragma unroll
+            for (int g = 0; g < GPL; ++g) fs_put(a, cand, hist, hsh, acc[g], pm[g], A[g].gi, st.exact, pos);
+            st.n += tot;
+            __syncwarp();
+            if (!st.exact) {
+              st.hcount += tot;
+              if (st.hcount >= bigK) {  // smallest bin whose cumulative count reaches bigK
+                uint32_t bl;
+                st.bthr = fs_bsel256(hist, bigK, &bl);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < GPL; ++g) A[g] = nA[g];
       }
       __syncwarp();
     }
@@ -872,7 +900,7 @@ __global__ void __launch_bounds__(FS_MAXW * 32, MINB) fs_scan_kernel(FsArgs a) {
       __syncwarp();
       continue;
     }
-    const uint32_t keep = (a.dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh);
+    const uint32_t keep = (dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh);
     if (a.tau_out) {  // threshold mode: the bigK-th smallest score (an upper bound, see FsArgs)
       uint32_t mx = 0;
       for (uint32_t i = lane; i < keep; i += 32) mx = max(mx, (uint32_t)(cand[i] >> 32));
@@ -964,8 +992,10 @@ rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// experiment switch (RAIRS_FS_VARIANT): 0 = 2 CTAs/SM (128 registers) with
-// 512-entry buffers, 1 = 3 CTAs/SM (80 registers), 2 = 2 CTAs/SM with 1024
+// experiment switch (RAIRS_FS_VARIANT): 0 = one group per lane per round,
+// 2 CTAs/SM (128 registers); 1 = 3 CTAs/SM (80 registers, spills); 2 = two
+// groups per lane per round (shared LUT rows; ptxas sinks the ring refills to
+// the end of the iteration, so the loads stall: measured 7 % slower)
 static int fs_variant() {
   static const int v = [] {
     const char* e = std::getenv("RAIRS_FS_VARIANT");
@@ -973,7 +1003,7 @@ static int fs_variant() {
   }();
   return v;
 }
-static int fs_capmin() { return fs_variant() == 2 ? 1024 : 512; }
+static int fs_round_items() { return fs_variant() == 2 ? 512 : 256; }
 
 int fastscan_cap(int bigK);
 
@@ -1031,6 +1061,8 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   {
     const char* e = std::getenv("RAIRS_FS_DBG");
     p.dbg = e ? std::atoi(e) : 0;
+    const char* pf = std::getenv("RAIRS_FS_PF");
+    p.pf_lo = pf ? std::atoi(pf) : 0;
   }
   int o = 0;
   auto take = [&](int bytes, int align) {
@@ -1065,18 +1097,20 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   return RAIRS_OK;
 }
 
-template <int MINB>
+template <int MINB, int GPL, int NW>
 static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
-  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  pl.warps = std::min(pl.warps, NW);
+  pl.smem = (size_t)pl.warps * pl.a.warp_bytes;
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB, GPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pl.smem));
   int per_sm = 0;
-  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB>,
+  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB, GPL, NW>,
                                                                pl.warps * 32, pl.smem));
   per_sm = std::max(per_sm, 1);
   const int64_t need = ceil_div(pl.a.nq, pl.warps);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148LL * per_sm));
   pl.a.total_warps = grid * (unsigned)pl.warps;
-  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
+  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB, GPL, NW>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
   return RAIRS_OK;
 }
 
@@ -1106,7 +1140,11 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
   }
   const bool kev = sa.kev[0] && sa.kev_used && !ex.tau_out && !ex.qlist;
   if (kev) RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[0], s));
-  RAIRS_TRY(fs_variant() == 1 ? fs_launch<3>(pl, s) : fs_launch<2>(pl, s));
+  switch (fs_variant()) {
+    case 1: RAIRS_TRY((fs_launch<3, 1, 8>(pl, s))); break;
+    case 2: RAIRS_TRY((fs_launch<2, 2, 8>(pl, s))); break;
+    default: RAIRS_TRY((fs_launch<2, 1, 8>(pl, s))); break;
+  }
   if (kev) {
     RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[1], s));
     *sa.kev_used = true;
@@ -1123,6 +1161,6 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
   return RAIRS_OK;
 }
 
-int fastscan_cap(int bigK) { return std::max(fs_capmin(), next_pow2(bigK + FS_ROUND + 64)); }
+int fastscan_cap(int bigK) { return std::max(512, next_pow2(bigK + fs_round_items() + 64)); }
 
 }  // namespace rairs
