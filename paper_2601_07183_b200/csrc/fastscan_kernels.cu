@@ -143,7 +143,6 @@ struct FsArgs {
   // pass, instead of selecting in place
   uint64_t* defer_buf;
   uint32_t* defer_n;
-  int pf_lo;                   // first chunk of the next round's groups prefetched into L2
   int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
@@ -325,16 +324,23 @@ __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uin
                                                 const uint32_t* rs, const uint32_t* rc, const uint32_t* rg,
                                                 const uint8_t* codes, uint64_t blk_bytes) {
   const int lane = lane_id();
-  const uint32_t j = r_lo + (uint32_t)lane;
-  uint32_t bit = 0, at32 = 0;
-  if (lane > 0 && j < nr) {
-    const uint32_t d = rg[j] - t0;  // >= 1: range r_lo holds t0
-    if (d < 32) bit = 1u << d;
-    at32 = d == 32 ? 1u : 0u;
+  uint32_t r, adv;
+  const uint32_t e = r_lo + 1 <= nr ? rg[r_lo + 1] : 0xFFFFFFFFu;  // end of range r_lo
+  if (e >= t0 + 32u) {  // the whole round inside range r_lo (warp-uniform)
+    r = r_lo;
+    adv = e == t0 + 32u ? 1u : 0u;
+  } else {
+    const uint32_t j = r_lo + (uint32_t)lane;
+    uint32_t bit = 0, at32 = 0;
+    if (lane > 0 && j < nr) {
+      const uint32_t d = rg[j] - t0;  // >= 1: range r_lo holds t0
+      if (d < 32) bit = 1u << d;
+      at32 = d == 32 ? 1u : 0u;
+    }
+    const uint32_t bits = __reduce_or_sync(0xffffffffu, bit);
+    r = r_lo + __popc(bits & (0xFFFFFFFFu >> (31 - lane)));
+    adv = __popc(bits) + (__ballot_sync(0xffffffffu, at32 != 0) ? 1u : 0u);
   }
-  const uint32_t bits = __reduce_or_sync(0xffffffffu, bit);
-  const uint32_t r = r_lo + __popc(bits & (0xFFFFFFFFu >> (31 - lane)));
-  const unsigned b32 = __ballot_sync(0xffffffffu, at32 != 0);
   FsTask k{codes, 0u, 0u};
   const uint32_t t = t0 + (uint32_t)lane;
   if (t < ng_tot) {
@@ -347,7 +353,7 @@ __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uin
     k.gi = gi;
     k.gp = codes + (uint64_t)(gi >> 2) * blk_bytes + (gi & 3) * 16;
   }
-  r_lo += __popc(bits) + (b32 ? 1u : 0u);
+  r_lo += adv;
   return k;
 }
 
@@ -805,12 +811,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
 #pragma unroll
         for (int g = 0; g < GPL; ++g)
           nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
-        // the next round's groups into L2 now (one round ahead of their loads):
-        // the register ring alone covers L2 latency, not DRAM's
-        if (!(dbg & 16))
-#pragma unroll
-          for (int g = 0; g < GPL; ++g)
-            for (int c = a.pf_lo; c < M4; c += 2) prefetch_l2(nA[g].gp + c * 64);
         uint32_t acc[GPL][8];
 #pragma unroll
         for (int g = 0; g < GPL; ++g)
@@ -819,6 +819,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
 #pragma unroll 1
         for (int c = 0; c < M4; c += D) {
           const uint4* L = lut + 4 * c;
+          // the same chunks of the next round's groups into L2 (one round ahead
+          // of their loads: the register ring alone covers L2 latency, not
+          // DRAM's); a 128-B line holds two chunks of four groups
+          if (!(dbg & 16))
+#pragma unroll
+            for (int g = 0; g < GPL; ++g)
+#pragma unroll
+              for (int s = 0; s < D; s += 2) prefetch_l2(nA[g].gp + (c + s) * 64);
 #pragma unroll
           for (int s = 0; s < D; ++s) {
 #pragma unroll
@@ -1061,8 +1069,6 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   {
     const char* e = std::getenv("RAIRS_FS_DBG");
     p.dbg = e ? std::atoi(e) : 0;
-    const char* pf = std::getenv("RAIRS_FS_PF");
-    p.pf_lo = pf ? std::atoi(pf) : 0;
   }
   int o = 0;
   auto take = [&](int bytes, int align) {
