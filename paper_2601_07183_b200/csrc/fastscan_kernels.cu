@@ -161,9 +161,10 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
 // total >= K); *below = the count of the bins before b
 __device__ __forceinline__ uint32_t fs_bsel256(const uint32_t* hist, uint32_t K, uint32_t* below) {
   const int lane = lane_id();
-  uint32_t h[8], loc = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) { h[i] = hist[lane * 8 + i]; loc += h[i]; }
+  const uint4 h0 = reinterpret_cast<const uint4*>(hist)[lane * 2];  // hist is 16-B aligned
+  const uint4 h1 = reinterpret_cast<const uint4*>(hist)[lane * 2 + 1];
+  const uint32_t h[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  const uint32_t loc = (h0.x + h0.y) + (h0.z + h0.w) + (h1.x + h1.y) + (h1.z + h1.w);
   const uint32_t inc = warp_incl_scan(loc);
   const unsigned hit = __ballot_sync(0xffffffffu, inc >= K);
   const int hl = hit ? __ffs(hit) - 1 : 31;
@@ -518,6 +519,7 @@ struct FsSel {
   uint32_t tau;      // ... nor items with s > tau
   uint32_t hcount;   // entries counted in hist (appended so far, minus those dropped)
   uint32_t exact;    // massive-tie mode: the buffer holds resolved keys
+  uint32_t hlast;    // hcount at the last bin-threshold refresh
   uint64_t tau_key;  // exact mode: keys >= tau_key are dropped
 };
 
@@ -551,6 +553,7 @@ __device__ __noinline__ FsSel fs_compact(const FsArgs& a, uint64_t* cand, uint32
     for (uint32_t i = lane; i < st.n; i += 32) atomicAdd(&hist[(uint32_t)(cand[i] >> 32) >> hsh], 1u);
     __syncwarp();
     st.hcount = st.n;
+    st.hlast = 0u;
     if (st.n + round <= cap) return st;
     fs_resolve(a, cand, 0, st.n);
     st.exact = 1;
@@ -591,20 +594,40 @@ __device__ __forceinline__ uint32_t fs_pass_exact(const FsArgs& a, const uint32_
 __device__ __forceinline__ void fs_put(const FsArgs& a, uint64_t* cand, uint32_t* hist, int hsh,
                                        const uint32_t (&acc)[8], uint32_t pm, uint32_t gi, bool exact,
                                        uint32_t& pos) {
+  if (!exact) {  // warp-uniform; predicated stores, no branches
 #pragma unroll
-  for (int v = 0; v < 8; ++v) {
-    if ((pm >> v) & 1u) {
-      uint64_t key;
-      if (!exact) {
-        key = ((uint64_t)acc[v] << 32) | (uint64_t)(gi * 8u + v);
+    for (int v = 0; v < 8; ++v) {
+      const bool on = (pm >> v) & 1u;
+      if (on) {
         atomicAdd(&hist[acc[v] >> hsh], 1u);
-      } else {
-        const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
-        key = ((uint64_t)acc[v] << 32) | (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+        cand[pos] = ((uint64_t)acc[v] << 32) | (uint64_t)(gi * 8u + v);
       }
-      cand[pos++] = key;
+      pos += on ? 1u : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      if ((pm >> v) & 1u) {
+        const uint32_t row = __ldg(a.slot_rows + gi * 8u + v);
+        cand[pos++] = ((uint64_t)acc[v] << 32) |
+                      (uint64_t)(row * (uint32_t)a.nshards + (uint32_t)a.shard_id);
+      }
     }
   }
+}
+
+// exclusive prefix and total over the warp of a per-lane count c < 16 (four
+// ballots instead of a shuffle chain)
+__device__ __forceinline__ uint32_t fs_prefix16(uint32_t c, unsigned below_me, uint32_t& tot) {
+  uint32_t pre = 0, t = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const unsigned m = __ballot_sync(0xffffffffu, (c >> b) & 1u);
+    pre += (uint32_t)__popc(m & below_me) << b;
+    t += (uint32_t)__popc(m) << b;
+  }
+  tot = t;
+  return pre;
 }
 
 // The deferred exact top-bigK: one warp per query over the buffer the scan
@@ -735,7 +758,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
     }
 
     // ---- A4 + A5 + A6 ----
-    FsSel st{0u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, kKeyInf};
+    FsSel st{0u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, kKeyInf};
     uint32_t my_dco = 0;
     const uint32_t nsrc = (uint32_t)np + nrefs;
     uint32_t s0 = 0;
@@ -872,18 +895,27 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
             c += __popc(pm[g]);
           }
           if (__any_sync(0xffffffffu, c != 0u)) {
-            const uint32_t inc = warp_incl_scan(c);
-            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-            uint32_t pos = st.n + inc - c;
+            uint32_t tot;
+            uint32_t pos = st.n;
+            if constexpr (GPL == 1) {
+              pos += fs_prefix16(c, below_me, tot);
+            } else {
+              const uint32_t inc = warp_incl_scan(c);
+              tot = __shfl_sync(0xffffffffu, inc, 31);
+              pos += inc - c;
+            }
 #pragma unroll
             for (int g = 0; g < GPL; ++g) fs_put(a, cand, hist, hsh, acc[g], pm[g], A[g].gi, st.exact, pos);
             st.n += tot;
             __syncwarp();
             if (!st.exact) {
               st.hcount += tot;
-              if (st.hcount >= bigK) {  // smallest bin whose cumulative count reaches bigK
+              // smallest bin whose cumulative count reaches bigK, refreshed once
+              // 32 more entries are counted (a stale bin is a valid, looser cut)
+              if (st.hcount >= bigK && st.hcount >= st.hlast + 32u) {
                 uint32_t bl;
                 st.bthr = fs_bsel256(hist, bigK, &bl);
+                st.hlast = st.hcount;
               }
             }
           }
