@@ -635,7 +635,7 @@ __device__ __forceinline__ uint32_t fs_prefix16(uint32_t c, unsigned below_me, u
 // massive-tie mode): histogram of its scores, then fs_finish (exact bigK-th
 // score, ids, ties by id).  Runs at high occupancy, apart from the lookups.
 constexpr int FF_WARPS = 8;
-__global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(FsArgs a) {
+__global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(const __grid_constant__ FsArgs a) {
   extern __shared__ __align__(16) uint8_t ff_smem[];
   const int lane = lane_id(), warp = warp_id();
   const uint32_t cap = (uint32_t)a.cap, bigK = (uint32_t)a.bigK;
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(FsArgs a) {
 // the coarse stage; it waits for that stage (griddepcontrol.wait) only before
 // it exits, so its completion implies the probes are ready for the scan.
 constexpr int FL_WARPS = 8;
-__global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(FsArgs a, uint4* luts) {
+__global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(const __grid_constant__ FsArgs a, uint4* luts) {
   extern __shared__ __align__(16) uint8_t fl_smem[];
   const int lane = lane_id(), warp = warp_id();
   float* cbs = reinterpret_cast<float*>(fl_smem);
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(FsArgs a, uint4* 
 // the group's end is chunk 0/1 of the lane's NEXT round's group, so a round's
 // DRAM latency overlaps the previous round's lookups.
 template <int MINB, int GPL, int NW>
-__global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
+__global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_constant__ FsArgs a) {
   constexpr int D = 4 / GPL;                 // ring slots per group
   constexpr uint32_t FS_ROUND = 256u * GPL;  // items appended per round at most
   const int dbg = kFsTiming ? a.dbg : 0;
@@ -928,8 +928,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(FsArgs a) {
 
     // ---- exact top-bigK of the buffer (here, or deferred to fs_finish_kernel) ----
     if (a.defer_buf) {
+      // only entries that can still be in the top-bigK (s <= the final bound;
+      // resolved keys in exact mode are all kept)
       uint64_t* dst = a.defer_buf + (size_t)q * cap;
-      for (uint32_t i = lane; i < st.n; i += 32) dst[i] = cand[i];
+      const uint32_t lim = st.exact ? 0xFFFFFFFFu
+                                    : min(st.tau, st.bthr >= (0xFFFFFFFFu >> hsh) ? 0xFFFFFFFFu
+                                                                                 : ((st.bthr + 1u) << hsh) - 1u);
+      uint32_t nout = 0;
+      for (uint32_t i0 = 0; i0 < st.n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint64_t v = i < st.n ? cand[i] : kKeyInf;
+        const bool k = i < st.n && (uint32_t)(v >> 32) <= lim;
+        const unsigned bal = __ballot_sync(0xffffffffu, k);
+        if (k) dst[nout + __popc(bal & below_me)] = v;
+        nout += __popc(bal);
+      }
+      st.n = nout;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
       if (lane == 0) {
