@@ -337,7 +337,7 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
         ex.defer_buf = dbuf;
         ex.defer_n = dn;
         st = launch_fastscan(idx, a, s, ex);
-        nk += defer ? 2 : 1;  // + the LUT kernel (+ the finish kernel)
+        nk += (defer ? 2 : 1) + (fastscan_order_on() && nq > 1 ? 1 : 0);  // + LUT (+ finish) (+ order)
       }
       cudaFreeAsync(luts, s);
       cudaFreeAsync(dbuf, s);

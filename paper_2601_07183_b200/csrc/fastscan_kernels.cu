@@ -143,6 +143,10 @@ struct FsArgs {
   // pass, instead of selecting in place
   uint64_t* defer_buf;
   uint32_t* defer_n;
+  const uint32_t* order;       // claim order of the queries (heavy first) or null
+  const uint32_t* list_items;  // N_l for the cost estimate (or own_cnt)
+  uint64_t cost_thr;           // a query is heavy when cost * nlist > cost_thr
+  int nlist;
   int dbg;                     // timing experiments only (RAIRS_FS_DBG bits): 1 no rounds, 2 no LUT, 4 no finish
 };
 
@@ -664,6 +668,24 @@ __global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(const __grid_c
   pdl_trigger();
 }
 
+// Claim order for the scan (longest-first, two classes): a query whose probed
+// lists hold more items than the batch's mean expectation (nprobe x mean N_l)
+// is put at the front, the others at the back, so the persistent warps take
+// the long queries first and the tail of the grid runs short ones.  Results do
+// not depend on the order (each query is independent).
+__global__ void fs_order_kernel(const __grid_constant__ FsArgs a, uint32_t* order) {
+  pdl_wait();  // probes
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < a.nq) {
+    const int32_t* pq = a.probes + q * a.pstride;
+    uint64_t cost = 0;
+    for (int i = 0; i < a.nprobe; ++i) cost += __ldg(a.list_items + __ldg(pq + i));
+    if (cost * (uint64_t)a.nlist > a.cost_thr) order[atomicAdd(&a.ctr[2], 1u)] = (uint32_t)q;
+    else order[a.nq - 1 - atomicAdd(&a.ctr[3], 1u)] = (uint32_t)q;
+  }
+  pdl_trigger();
+}
+
 // A3 for every query of the batch, one warp per query (O2: lane per
 // subquantizer, fp32 RN, ascending t; see fs_build_lut), into luts[q][M_pad].
 // Needs only the queries, so under programmatic dependent launch it overlaps
@@ -727,7 +749,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     // a query subset (a.qlist / *a.qcount: the list-major path's overflowed
     // queries) or every query
     if (a.qlist ? qq >= *a.qcount : qq >= (uint64_t)a.nq) break;
-    const int64_t q = a.qlist ? (int64_t)a.qlist[qq] : (int64_t)qq;
+    const int64_t q = a.qlist ? (int64_t)a.qlist[qq] : a.order ? (int64_t)a.order[qq] : (int64_t)qq;
     const int32_t* pq = a.probes + q * a.pstride;
 
     // ---- probe set: sorted copy (membership, R9) + per-probe reference prefix ----
@@ -978,6 +1000,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     if (done == a.total_warps - 1) {
       atomicExch(&a.ctr[0], 0u);
       atomicExch(&a.ctr[1], 0u);
+      atomicExch(&a.ctr[2], 0u);
+      atomicExch(&a.ctr[3], 0u);
     }
   }
 }
@@ -1036,9 +1060,9 @@ rairs_status fastscan_prepare(rairs_index_s* idx, cudaStream_t s) {
     fs_transpose_cb_kernel<<<(unsigned)ceil_div(idx->M * 16 * idx->dsub, 256), 256, 0, s>>>(
         idx->codebook, idx->M, idx->dsub, idx->cbT);
     RAIRS_CHECK_LAUNCH();
-    RAIRS_CUDA_TRY(cudaMalloc(&idx->fs_ctr, FS_SLOTS * 2 * sizeof(unsigned)));
-    RAIRS_CUDA_TRY(cudaMemsetAsync(idx->fs_ctr, 0, FS_SLOTS * 2 * sizeof(unsigned), s));
-    idx->device_bytes += (size_t)idx->M * 16 * idx->dsub * 4 + FS_SLOTS * 8;
+    RAIRS_CUDA_TRY(cudaMalloc(&idx->fs_ctr, FS_SLOTS * 4 * sizeof(unsigned)));
+    RAIRS_CUDA_TRY(cudaMemsetAsync(idx->fs_ctr, 0, FS_SLOTS * 4 * sizeof(unsigned), s));
+    idx->device_bytes += (size_t)idx->M * 16 * idx->dsub * 4 + FS_SLOTS * 16;
   }
   idx->fs_bytes = bytes;
   idx->device_bytes += bytes;
@@ -1176,7 +1200,7 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
   FsPlan pl;
   RAIRS_TRY(fs_plan(idx, sa, ex, pl));
   const unsigned slot = idx->fs_slot.fetch_add(1u) % FS_SLOTS;
-  pl.a.ctr = idx->fs_ctr + 2 * slot;
+  pl.a.ctr = idx->fs_ctr + 4 * slot;
   if (!ex.luts_ready) {  // A3 for the whole batch (overlaps the coarse stage's tail under PDL)
     const bool keepT = idx->M * 17 <= 16 * 1024 / 4;
     const size_t lsm = (size_t)pl.a.cb_smem + (size_t)FL_WARPS * (keepT ? 17 : 1) * idx->M * 4;
@@ -1189,6 +1213,23 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FL_WARPS), 148LL * per_sm));
     RAIRS_CUDA_TRY(launch_pdl(fs_lut_kernel, dim3(g), dim3(FL_WARPS * 32), lsm, s, pl.a,
                               const_cast<uint4*>(sa.luts)));
+  }
+  const bool use_order = fastscan_order_on();
+  uint32_t* order = nullptr;
+  struct OrderFree {
+    uint32_t*& p;
+    cudaStream_t s;
+    ~OrderFree() { if (p) cudaFreeAsync(p, s); }
+  } order_free{order, s};
+  if (use_order && !ex.qlist && sa.nq > 1) {
+    RAIRS_CUDA_TRY(ws_malloc(&order, (size_t)sa.nq * 4, s));
+    pl.a.order = order;
+    pl.a.list_items = idx->list_items ? idx->list_items : idx->own_cnt;
+    pl.a.nlist = (int)idx->nlist;
+    const uint64_t total = idx->list_items ? (uint64_t)idx->sum_list_items : (uint64_t)idx->n_live;
+    pl.a.cost_thr = (uint64_t)pl.a.nprobe * total;
+    const unsigned g = (unsigned)ceil_div(sa.nq, 256);
+    RAIRS_CUDA_TRY(launch_pdl(fs_order_kernel, dim3(g), dim3(256), 0, s, pl.a, order));
   }
   const bool kev = sa.kev[0] && sa.kev_used && !ex.tau_out && !ex.qlist;
   if (kev) RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[0], s));
@@ -1211,6 +1252,15 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     RAIRS_CUDA_TRY(launch_pdl(fs_finish_kernel, dim3(g), dim3(nw * 32), fsm, s, pl.a));
   }
   return RAIRS_OK;
+}
+
+// longest-first claim order for the scan (RAIRS_FS_ORDER=0: batch order)
+bool fastscan_order_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("RAIRS_FS_ORDER");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
 }
 
 int fastscan_cap(int bigK) { return std::max(512, next_pow2(bigK + fs_round_items() + 64)); }

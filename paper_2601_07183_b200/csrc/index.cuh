@@ -219,6 +219,7 @@ struct FsExtra {
   uint64_t* defer_buf = nullptr;      // deferred finish workspace [nq][fastscan_cap(bigK)]
   uint32_t* defer_n = nullptr;        // [nq]
 };
+bool fastscan_order_on();
 int fastscan_cap(int bigK);
 rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s,
                              const FsExtra& ex = FsExtra{});
