@@ -861,8 +861,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
         for (int g = 0; g < GPL; ++g)
 #pragma unroll
           for (int v = 0; v < 8; ++v) acc[g][v] = 0u;
-#pragma unroll 1
-        for (int c = 0; c < M4; c += D) {
+        // one iteration: chunks c .. c+D-1 consumed, each slot refilled from
+        // `nxt` (chunk c+D+s of this group, or chunk s of the next round's)
+        auto iter = [&](int c, const uint8_t* const (&nxt)[GPL]) {
           const uint4* L = lut + 4 * c;
           // the same chunks of the next round's groups into L2 (one round ahead
           // of their loads: the register ring alone covers L2 latency, not
@@ -876,16 +877,29 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
           for (int s = 0; s < D; ++s) {
 #pragma unroll
             for (int g = 0; g < GPL; ++g) {
-              // M4 % D == 0: chunk c + D + s of this group, or chunk s of the next
-              const uint8_t* f = c + D < M4 ? A[g].gp + (c + D + s) * 64 : nA[g].gp + s * 64;
               if (dbg & 32) R[g][s] = make_uint4(c, c * 3u, c * 5u, c * 7u);  // timing: no code loads
               lookup8(L[4 * s + 0], R[g][s].x, acc[g]);
               lookup8(L[4 * s + 1], R[g][s].y, acc[g]);
               lookup8(L[4 * s + 2], R[g][s].z, acc[g]);
               lookup8(L[4 * s + 3], R[g][s].w, acc[g]);
-              if (!(dbg & 32)) R[g][s] = ldg_nc_v4(f);
+              if (!(dbg & 32)) R[g][s] = ldg_nc_v4(nxt[g] + s * 64);
             }
           }
+        };
+        // M4 % D == 0; the last iteration is peeled (its refills come from the
+        // next round's groups), so the loop body has no address selects
+#pragma unroll 1
+        for (int c = 0; c < M4 - D; c += D) {
+          const uint8_t* nxt[GPL];
+#pragma unroll
+          for (int g = 0; g < GPL; ++g) nxt[g] = A[g].gp + (c + D) * 64;
+          iter(c, nxt);
+        }
+        {
+          const uint8_t* nxt[GPL];
+#pragma unroll
+          for (int g = 0; g < GPL; ++g) nxt[g] = nA[g].gp;
+          iter(M4 - D, nxt);
         }
         if (dbg & 8) {  // timing experiment: no selection (scores folded into the DCO sum)
           uint32_t x = 0;
