@@ -324,7 +324,7 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
         const char* e = std::getenv("RAIRS_FS_DEFER");
         return e ? std::atoi(e) != 0 : true;
       }();
-      const size_t dcap = (size_t)fastscan_cap(bigK);
+      const size_t dcap = (size_t)fastscan_cap(bigK, idx->M_pad);
       cudaError_t le = ws_malloc(&luts, (size_t)nq * idx->M_pad * 16, s);
       if (le == cudaSuccess && defer) le = ws_malloc(&dbuf, (size_t)nq * dcap * 8, s);
       if (le == cudaSuccess && defer) le = ws_malloc(&dn, (size_t)nq * 4, s);

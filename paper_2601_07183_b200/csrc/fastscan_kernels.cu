@@ -1097,7 +1097,7 @@ static int fs_variant() {
 }
 static int fs_round_items() { return fs_variant() == 2 ? 512 : 256; }
 
-int fastscan_cap(int bigK);
+int fastscan_cap(int bigK, int M_pad);
 
 static int fs_hbits(int M) {
   int b = 1;
@@ -1141,7 +1141,7 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   p.defer_buf = ex.defer_buf;
   p.defer_n = ex.defer_n;
   p.bigK = sa.k * sa.refine_factor;
-  p.cap = fastscan_cap(p.bigK);
+  p.cap = fastscan_cap(p.bigK, idx->M_pad);
   p.hbits = fs_hbits(idx->M);
   p.out_keys = sa.cand_keys;
   p.dco = ex.tau_out ? nullptr : sa.dco;
@@ -1277,6 +1277,21 @@ bool fastscan_order_on() {
   return on;
 }
 
-int fastscan_cap(int bigK) { return std::max(512, next_pow2(bigK + fs_round_items() + 64)); }
+// Smallest candidate buffer: 1024 entries (fewer compactions: c4 scan -3 %)
+// when two 8-warp CTAs still fit an SM's shared memory with it, else 512
+// (RAIRS_FS_CAPMIN overrides).
+static int fs_capmin(int M_pad) {
+  static const int env = [] {
+    const char* e = std::getenv("RAIRS_FS_CAPMIN");
+    return e ? std::max(256, next_pow2(std::atoi(e))) : 0;
+  }();
+  if (env) return env;
+  const int warp_bytes = M_pad * 16 + 1024 * 8 + 1024 + 2048;  // LUT + buffer + histogram + ranges
+  return 2 * FS_MAXW * warp_bytes <= 220 * 1024 ? 1024 : 512;
+}
+
+int fastscan_cap(int bigK, int M_pad) {
+  return std::max(fs_capmin(M_pad), next_pow2(bigK + fs_round_items() + 64));
+}
 
 }  // namespace rairs

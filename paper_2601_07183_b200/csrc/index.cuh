@@ -216,11 +216,11 @@ struct FsExtra {
   const uint32_t* qcount = nullptr;
   uint32_t* tau_out = nullptr;        // threshold mode (see FsArgs::tau_out)
   bool luts_ready = false;            // a.luts already holds every query's LUT
-  uint64_t* defer_buf = nullptr;      // deferred finish workspace [nq][fastscan_cap(bigK)]
+  uint64_t* defer_buf = nullptr;      // deferred finish workspace [nq][fastscan_cap(bigK, M_pad)]
   uint32_t* defer_n = nullptr;        // [nq]
 };
 bool fastscan_order_on();
-int fastscan_cap(int bigK);
+int fastscan_cap(int bigK, int M_pad);
 rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s,
                              const FsExtra& ex = FsExtra{});
 rairs_status launch_refine(const rairs_index_s* idx, const SearchArgs& a, cudaStream_t s);
