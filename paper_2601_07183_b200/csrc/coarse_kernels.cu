@@ -45,6 +45,13 @@ struct TopWArgs {
   const float* cnorm;  // [round_up(nl, 256)], +inf padding
   int dbg;             // timing experiments (RAIRS_COARSE_DBG): 1 = no epilogue work
   int a_res;           // the A tile (all K-chunks) stays resident in shared memory
+  // balanced schedule (lin = 1): the mtiles x ntiles (row tile, column tile)
+  // units in row-major order are cut into gridDim.x equal contiguous ranges,
+  // one per CTA; a range may cross row tiles (the row's lists are written at
+  // each crossing, as piece b - first CTA of the row).  lin = 0: grid
+  // (row tile, column split), tiles_per_split column tiles per CTA.
+  int lin;
+  int64_t total;       // mtiles * ntiles (lin)
   // output entries per (row, split): 32 on the register path (sorted), Wp1
   // on the shared-memory path (unsorted)
   float* out_v;        // [rows][nsplit][Wout]
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   // a_res: the row tile's A (all nk K-chunks) is loaded ONCE and stays resident
   // (every column tile of the CTA reuses it); the ring then carries B only
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (a.a_res ? nk : S) * FT_A_BYTES;
+  uint8_t* sB = smem + (a.a_res ? (a.lin ? 2 * nk : nk) : S) * FT_A_BYTES;
   float* lv = reinterpret_cast<float*>(sB + S * FT_B_BYTES);  // smem path only
   uint32_t* li = reinterpret_cast<uint32_t*>(lv + (KR > 0 ? 0 : Wp1 * FT_BM));
   // g staging: [32][128] on the shared-memory path (warps 0-3), [32][256] on the
@@ -92,14 +99,22 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint64_t* afull = tempty + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(afull + 1);
+  uint64_t* afull = tempty + 2;   // [2]: resident A of segment j in buffer j & 1
+  uint64_t* aempty = afull + 2;   // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * FT_BM;
-  const int split = blockIdx.y;
-  const int t_begin = split * a.tiles_per_split;
-  const int ntile = min(a.ntiles, t_begin + a.tiles_per_split) - t_begin;
+  // this CTA's units [u0, u1): unit u = row tile u / ntiles, column tile u % ntiles
+  int64_t u0, u1;
+  if (a.lin) {
+    u0 = (int64_t)blockIdx.x * a.total / gridDim.x;
+    u1 = (int64_t)(blockIdx.x + 1) * a.total / gridDim.x;
+  } else {
+    const int64_t tb = (int64_t)blockIdx.y * a.tiles_per_split;
+    u0 = (int64_t)blockIdx.x * a.ntiles + tb;
+    u1 = (int64_t)blockIdx.x * a.ntiles + min((int64_t)a.ntiles, tb + a.tiles_per_split);
+  }
+  const int ntile = (int)(u1 - u0);
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -110,7 +125,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       mbar_init(&tfull[k], 1);
       mbar_init(&tempty[k], FT_EPI_WARPS);
     }
-    mbar_init(afull, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&afull[k], 1);
+      mbar_init(&aempty[k], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (KR == 0 && warp < 4) {  // smem path: column half 0 only (see launcher)
@@ -126,12 +144,22 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
 
   if (warp == FT_PROD_WARP) {
     if (lane == 0 && ntile > 0) {  // TMA producer
-      int it = 0;
-      if (a.a_res) {
-        mbar_expect_tx(afull, (uint32_t)nk * FT_A_BYTES);
-        for (int kc = 0; kc < nk; ++kc) tma_load_2d(sA + kc * FT_A_BYTES, &tmA, kc * FT_BK, (int)m0, afull);
-      }
-      for (int t = 0; t < ntile; ++t) {
+      int it = 0, seg = -1;
+      int64_t cur_r = -1, r = u0 / a.ntiles;
+      int ct = (int)(u0 - r * a.ntiles);
+      for (int t = 0; t < ntile; ++t, ct = (ct + 1 == a.ntiles) ? (++r, 0) : ct + 1) {
+        const int m0 = (int)(r * FT_BM);
+        if (r != cur_r) {  // a new row tile: its resident A into buffer seg & 1
+          ++seg;
+          cur_r = r;
+          if (a.a_res) {
+            const int ab = seg & 1;
+            if (seg >= 2) mbar_wait(&aempty[ab], (uint32_t)((seg - 2) >> 1) & 1u);
+            mbar_expect_tx(&afull[ab], (uint32_t)nk * FT_A_BYTES);
+            for (int kc = 0; kc < nk; ++kc)
+              tma_load_2d(sA + (ab * nk + kc) * FT_A_BYTES, &tmA, kc * FT_BK, m0, &afull[ab]);
+          }
+        }
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % S;
           const uint32_t ph = (uint32_t)(it / S) & 1u;
@@ -140,18 +168,26 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
             mbar_expect_tx(&full[s], FT_B_BYTES);
           } else {
             mbar_expect_tx(&full[s], FT_A_BYTES + FT_B_BYTES);
-            tma_load_2d(sA + s * FT_A_BYTES, &tmA, kc * FT_BK, (int)m0, &full[s]);
+            tma_load_2d(sA + s * FT_A_BYTES, &tmA, kc * FT_BK, m0, &full[s]);
           }
-          tma_load_2d(sB + s * FT_B_BYTES, &tmB, kc * FT_BK, (t_begin + t) * FT_BN, &full[s]);
+          tma_load_2d(sB + s * FT_B_BYTES, &tmB, kc * FT_BK, ct * FT_BN, &full[s]);
         }
       }
     }
     __syncwarp();
   } else if (warp == FT_MMA_WARP) {
     if (lane == 0 && ntile > 0) {  // MMA issuer
-      int it = 0;
-      if (a.a_res) mbar_wait(afull, 0u);
-      for (int t = 0; t < ntile; ++t) {
+      int it = 0, seg = -1;
+      int64_t cur_r = -1, r = u0 / a.ntiles;
+      int ct = (int)(u0 - r * a.ntiles);
+      for (int t = 0; t < ntile; ++t, ct = (ct + 1 == a.ntiles) ? (++r, 0) : ct + 1) {
+        if (r != cur_r) {
+          // the previous row tile's MMAs release its A buffer when they complete
+          if (seg >= 0 && a.a_res) umma_commit(&aempty[seg & 1]);
+          ++seg;
+          cur_r = r;
+          if (a.a_res) mbar_wait(&afull[seg & 1], (uint32_t)(seg >> 1) & 1u);
+        }
         const int acc = t & 1;
         const uint32_t aph = (uint32_t)(t >> 1) & 1u;
         if (t >= 2) mbar_wait(&tempty[acc], aph ^ 1u);
@@ -162,7 +198,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
           const uint32_t ph = (uint32_t)(it / S) & 1u;
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(sA + (a.a_res ? kc : s) * FT_A_BYTES);
+          const uint64_t ad = umma_desc_sw128(sA + (a.a_res ? (seg & 1) * nk + kc : s) * FT_A_BYTES);
           const uint64_t bd = umma_desc_sw128(sB + s * FT_B_BYTES);
 #pragma unroll
           for (int k = 0; k < FT_BK / 8; ++k)  // K = 8 tf32 per MMA = 32 B = +2 desc units
@@ -187,12 +223,49 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       rv[i] = __int_as_float(0x7f800000);
       ri[i] = 0xFFFFFFFFu;
     }
-    for (int t = 0; t < ntile; ++t) {
+    // the lists of row tile r are written as piece `piece` of each row; the
+    // CTA holding the row tile's last column tile pads the later pieces
+    int64_t cur_r = -1;
+    int piece = 0;
+    auto flush = [&](int64_t r, bool row_end) {
+      const int64_t row = r * FT_BM + rrow;
+      if (row < a.rows) {
+        float* ov = a.out_v + ((row * a.nsplit + piece) * FT_HALVES + half) * KR;
+        uint32_t* oi = a.out_i + ((row * a.nsplit + piece) * FT_HALVES + half) * KR;
+#pragma unroll
+        for (int i = 0; i < KR; ++i) {
+          ov[i] = rv[i];
+          oi[i] = ri[i];
+        }
+        if (row_end)
+          for (int p2 = piece + 1; p2 < a.nsplit; ++p2)
+            for (int i = 0; i < KR; ++i) {
+              a.out_v[((row * a.nsplit + p2) * FT_HALVES + half) * KR + i] = __int_as_float(0x7f800000);
+              a.out_i[((row * a.nsplit + p2) * FT_HALVES + half) * KR + i] = 0xFFFFFFFFu;
+            }
+      }
+#pragma unroll
+      for (int i = 0; i < KR; ++i) {
+        rv[i] = __int_as_float(0x7f800000);
+        ri[i] = 0xFFFFFFFFu;
+      }
+    };
+    int64_t r = u0 / a.ntiles;
+    int ct = (int)(u0 - r * a.ntiles);
+    for (int t = 0; t < ntile; ++t, ct = (ct + 1 == a.ntiles) ? (++r, 0) : ct + 1) {
       const int acc = t & 1;
       const uint32_t aph = (uint32_t)(t >> 1) & 1u;
+      if (r != cur_r) {
+        if (cur_r >= 0) flush(cur_r, true);
+        cur_r = r;
+        // first CTA holding a unit of row tile r: the largest b with b*total/G <= r*ntiles
+        piece = a.lin ? (int)((int64_t)blockIdx.x -
+                              (((r * a.ntiles + 1) * gridDim.x + a.total - 1) / a.total - 1))
+                      : (int)blockIdx.y;
+      }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int col0 = (t_begin + t) * FT_BN;
+      const int col0 = ct * FT_BN;
       // TMEM reads are the epilogue's bound (LDTM ~64 B/clk/SM): the next chunk's
       // tcgen05.ld is in flight while this one is processed, and the
       // accumulator is released as soon as the last chunk is in registers
@@ -268,16 +341,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         }
       }
     }
-    const int64_t row = m0 + rrow;
-    if (row < a.rows) {
-      float* ov = a.out_v + ((row * a.nsplit + split) * FT_HALVES + half) * KR;
-      uint32_t* oi = a.out_i + ((row * a.nsplit + split) * FT_HALVES + half) * KR;
-#pragma unroll
-      for (int i = 0; i < KR; ++i) {
-        ov[i] = rv[i];
-        oi[i] = ri[i];
-      }
-    }
+    if (cur_r >= 0) flush(cur_r, a.lin && (u1 % a.ntiles) == 0);
   } else if (warp >= 4) {  // shared-memory path: warps 4-7 only release the accumulators
     for (int t = 0; t < ntile; ++t) {
       mbar_wait(&tfull[t & 1], (uint32_t)(t >> 1) & 1u);
@@ -295,7 +359,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       const uint32_t aph = (uint32_t)(t >> 1) & 1u;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int col0 = (t_begin + t) * FT_BN;
+      const int col0 = (int)((u0 + t) % a.ntiles) * FT_BN;
       for (int c = 0; c < FT_BN / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * FT_BN + c * 32), v);
@@ -325,10 +389,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    const int64_t row = m0 + tid;
+    const int64_t row = (int64_t)blockIdx.x * FT_BM + tid;  // lin = 0 on this path
     if (row < a.rows) {
-      float* ov = a.out_v + (row * a.nsplit + split) * Wp1;
-      uint32_t* oi = a.out_i + (row * a.nsplit + split) * Wp1;
+      float* ov = a.out_v + (row * a.nsplit + blockIdx.y) * Wp1;
+      uint32_t* oi = a.out_i + (row * a.nsplit + blockIdx.y) * Wp1;
       for (int i = 0; i < Wp1; ++i) {
         ov[i] = lv[i * FT_BM + tid];
         oi[i] = li[i * FT_BM + tid];
@@ -740,22 +804,37 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
   const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
   const int nkc = (int)ceil_div(d, FT_BK);
-  // A resident (loaded once per CTA) when it fits next to >= 3 B stages: the
-  // ring then moves 2/3 of the bytes per column tile (the TMA ingest bound)
-  const bool a_res = (size_t)nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2048 <= 227 * 1024;
-  int nstage;
-  if (a_res) {
-    nstage = (int)std::min<size_t>(6, (227 * 1024 - 2048 - lists_bytes - (size_t)nkc * FT_A_BYTES) / FT_B_BYTES);
-  } else {
-    nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
+  int nsm = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t ring_bytes = a_res ? (size_t)nkc * FT_A_BYTES + (size_t)nstage * FT_B_BYTES
-                                  : (size_t)nstage * (FT_A_BYTES + FT_B_BYTES);
-  if (1024 + ring_bytes + lists_bytes + 256 > 227 * 1024) {
+  static const bool lin_env = [] {
+    const char* e = std::getenv("RAIRS_COARSE_LIN");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  // smem plan for nab resident A buffers (0: A streamed with B per stage)
+  auto plan = [&](int nab, int& nstage, size_t& smem) {
+    if (nab > 0) {
+      nstage = (int)std::min<size_t>(6, (227 * 1024 - 2048 - lists_bytes - (size_t)nab * nkc * FT_A_BYTES) / FT_B_BYTES);
+    } else {
+      nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
+    }
+    const size_t ring_bytes = nab > 0 ? (size_t)nab * nkc * FT_A_BYTES + (size_t)nstage * FT_B_BYTES
+                                      : (size_t)nstage * (FT_A_BYTES + FT_B_BYTES);
+    smem = 1024 + ring_bytes + lists_bytes + (2 * nstage + 8) * 8 + 16;
+  };
+  // A resident (loaded once per row tile) when it fits next to >= 3 B stages:
+  // the ring then moves 2/3 of the bytes per column tile (the TMA ingest bound)
+  const bool a_res = (size_t)nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2048 <= 227 * 1024;
+  const bool a_res2 = (size_t)2 * nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2048 <= 227 * 1024;
+  int nstage = 0;
+  size_t smem = 0;
+  plan(a_res ? 1 : 0, nstage, smem);
+  if (smem > 227 * 1024) {
     set_error("coarse: shared memory budget exceeded");
     return RAIRS_E_UNSUPPORTED;
   }
-  const size_t smem = 1024 + ring_bytes + lists_bytes + (2 * nstage + 5) * 8 + 16;
   static bool attr_set = false;
   if (!attr_set) {
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<0>,
@@ -795,6 +874,26 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     nsplit = std::max(1, std::min(nsplit, 1024 / Wout));  // K2 merges nsplit * Wout <= 1024 keys
     const int tps = (int)ceil_div(ntiles, nsplit);
     nsplit = (int)ceil_div(ntiles, tps);
+    // balanced schedule: search-sized batches whose row tiles alone leave SMs
+    // idle (c4: 79 row tiles x 64 column tiles -> 148 ranges of ~34 units
+    // instead of 79 CTAs of 64: coarse 0.258 -> 0.245 ms), register lists, no
+    // capped lists, and long rows of column tiles (each piece restarts the
+    // top-W insertion: c2pl's 16 column tiles measured 0.095 -> 0.121 ms)
+    const int64_t total = mtiles * ntiles;
+    int lin = 0, nstage_k = nstage;
+    size_t smem_k = smem;
+    int64_t G = 0;
+    if (lin_env && reg && !capped && d < 512 && ntiles >= 32 && mtiles % nsm != 0 && mtiles < 4 * nsm &&
+        total >= 2 * nsm && !std::getenv("RAIRS_COARSE_NSPLIT")) {
+      G = nsm;
+      const int64_t minper = total / G;
+      const int pieces = (int)std::min<int64_t>(ntiles, ceil_div(ntiles, minper) + 1);
+      if (pieces * Wout <= 1024) {
+        lin = 1;
+        nsplit = pieces;
+        plan(a_res2 ? 2 : 0, nstage_k, smem_k);
+      }
+    }
     // register path: nsplit * FT_HALVES sorted lists of KR, each padded to a
     // power-of-2 run, merged in K2; shared-memory path: unsorted, fully sorted
     const int run = next_pow2(KR);
@@ -827,8 +926,10 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ta.nsplit = nsplit;
     ta.tiles_per_split = tps;
     ta.ntiles = ntiles;
-    ta.nstage = nstage;
-    ta.a_res = a_res ? 1 : 0;
+    ta.nstage = nstage_k;
+    ta.a_res = (lin ? a_res2 : a_res) ? 1 : 0;
+    ta.lin = lin;
+    ta.total = total;
     ta.cnorm = idx->cnorm;
     {
       const char* e = std::getenv("RAIRS_COARSE_DBG");
@@ -836,21 +937,21 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     }
     ta.out_v = vals;
     ta.out_i = ids;
-    const dim3 tgrid((unsigned)mtiles, (unsigned)nsplit);
+    const dim3 tgrid = lin ? dim3((unsigned)G, 1u) : dim3((unsigned)mtiles, (unsigned)nsplit);
     if (reg && KR == 10)
-      coarse_topw_kernel<10><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<10><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg && KR == 13)
-      coarse_topw_kernel<13><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<13><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg && KR == 16)
-      coarse_topw_kernel<16><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<16><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg && KR == 20)
-      coarse_topw_kernel<20><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<20><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg && KR == 24)
-      coarse_topw_kernel<24><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<24><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg)
-      coarse_topw_kernel<32><<<tgrid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<32><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else
-      coarse_topw_kernel<0><<<dim3((unsigned)mtiles, (unsigned)nsplit), FT_THREADS, smem, s>>>(tmA, tmB, ta);
+      coarse_topw_kernel<0><<<dim3((unsigned)mtiles, (unsigned)nsplit), FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     RAIRS_CHECK_LAUNCH();
     if (debug_sync_enabled()) {
       char what[160];
