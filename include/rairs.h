@@ -263,6 +263,30 @@ rairs_status rairs_get_stats(rairs_index_t idx, rairs_stats* out, int32_t reset)
  * Both modes produce identical candidates. */
 rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode);
 
+/* ---- SEIL list layout (NEXT-2) ----------------------------------------------
+ * 0 = cell-major (default, reading R10): list l owns its cells (l, j >= l)
+ * contiguously, remainders included, and list j holds (owner, slot, count)
+ * references to the cells (i < j, j); every vector is stored once.
+ * 1 = paper-literal SEIL (Alg. 4 SeilInsert): per
+ * cell floor(n/32) 32-item blocks stored once in list i and referenced from
+ * list j, the n % 32 remainder items duplicated into both lists'
+ * miscellaneous areas with the other list id embedded; searched per Alg. 5
+ * (SeilSearch) with the lists visited in ascending id (reading
+ * R9): references skipped when their owner was visited, misc items dropped
+ * after scoring when their other list was visited.  Same candidates and
+ * results as layout 0; the per-query DCO is the paper's DCO_paperSEIL (misc
+ * items scored in both lists).  Layout 1 is built from layout 0 when selected
+ * (host-side map + one device gather; synchronous, extra device memory about
+ * n * (M/2 + 8) bytes), rebuilt by rairs_add / rairs_remove_ids while
+ * selected, freed when 0 is selected; searches then take the query-major
+ * scan.  2 = both layouts kept: query-major scans read the paper-literal one
+ * (its remainders sit in contiguous misc areas instead of many short
+ * references, so fewer partially filled 8-item groups are scanned: c4 scan
+ * -6 %), list-major scans (rairs_set_scan_mode) the cell-major one.
+ * Errors: RAIRS_E_INVALID (NULL index, layout not 0/1/2), RAIRS_E_OOM,
+ * RAIRS_E_CUDA. */
+rairs_status rairs_set_seil_layout(rairs_index_t idx, int32_t layout);
+
 /* ---- stage timing (CUDA events on the search stream) ----------------------
  * When enabled, every search records events around its stages on its stream;
  * rairs_profile_read synchronises and returns the accumulated milliseconds

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = [
     "rairs_profile_read", "rairs_profile_read_kernel", "rairs_last_error", "rairs_version", "rairs_set_coarse_mode",
     "rairs_certify_fallbacks", "rairs_set_scan_mode", "rairs_profile_kernels",
     "rairs_search_plan", "rairs_add", "rairs_remove_ids", "rairs_get_stats",
-    "rairs_search_host_async",
+    "rairs_search_host_async", "rairs_set_seil_layout",
 ]
 
 
@@ -111,6 +111,7 @@ def lib() -> ctypes.CDLL:
         "rairs_set_coarse_mode": [_P, _I32],
         "rairs_certify_fallbacks": [_P, _P, _I32],
         "rairs_set_scan_mode": [_P, _I32],
+        "rairs_set_seil_layout": [_P, _I32],
         "rairs_profile_kernels": [_P, _P, _I32],
         "rairs_search_plan": [_P, _I64, _I32, _I32, _I32, _P, _P],
         "rairs_add": [_P, _P, _I64, _P, _P, _P],

@@ -174,6 +174,7 @@ static void free_index(rairs_index_s* x) {
   cudaFree(x->list_items); cudaFree(x->ref_item_off); cudaFree(x->list_base); cudaFree(x->list_ids);
   cudaFree(x->lm_order);
   cudaFree(x->codes_g); cudaFree(x->cbT); cudaFree(x->fs_ctr);
+  seil_paper_free(x);
   cudaFree(x->live_bits);
   cudaFree(x->labels); cudaFree(x->lab_sorted); cudaFree(x->lab_rows);
   for (auto& st : x->aux) if (st) cudaStreamDestroy(st);
@@ -622,6 +623,7 @@ static rairs_status relayout(rairs_index_s* idx, cudaStream_t s) {
   RAIRS_TRY(build_layout(idx, s));
   RAIRS_TRY(listmajor_prepare(idx, s));
   RAIRS_TRY(fastscan_prepare(idx, s));
+  if (idx->seil_layout != 0) RAIRS_TRY(seil_paper_prepare(idx, s));
   RAIRS_CUDA_TRY(cudaStreamSynchronize(s));
   return RAIRS_OK;
 }
@@ -954,6 +956,23 @@ rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode) {
   if (!idx) return invalid("index is NULL");
   if (mode < 0 || mode > 2) return invalid("scan mode must be 0 (auto), 1 (SIMT), 2 (list-major)");
   idx->scan_mode = mode;
+  return RAIRS_OK;
+}
+
+rairs_status rairs_set_seil_layout(rairs_index_t idx, int32_t layout) {
+  if (!idx) return invalid("index is NULL");
+  if (layout < 0 || layout > 2)
+    return invalid("SEIL layout must be 0 (cell-major), 1 (paper-literal) or 2 (paper-literal for query-major scans)");
+  if (layout != 0 && !idx->p_codes_g) {
+    cudaStream_t s = nullptr;
+    RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    RAIRS_CUDA_TRY(cudaDeviceSynchronize());
+    const rairs_status st = seil_paper_prepare(idx, s);
+    cudaStreamDestroy(s);
+    RAIRS_TRY(st);
+  }
+  if (layout == 0) seil_paper_free(idx);
+  idx->seil_layout = layout;
   return RAIRS_OK;
 }
 

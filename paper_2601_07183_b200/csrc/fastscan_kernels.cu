@@ -143,6 +143,16 @@ struct FsArgs {
   // pass, instead of selecting in place
   uint64_t* defer_buf;
   uint32_t* defer_n;
+  // paper-literal SEIL layout (seil_paper.cu): paper = 1 -> codes / slot_rows
+  // are that layout's and the work list follows Alg. 5
+  int paper;
+  const uint32_t* p_off;
+  const uint32_t* p_shared;
+  const uint32_t* p_misc;
+  const uint32_t* p_other;
+  const uint32_t* p_ref_start;
+  const uint32_t* p_ref_cnt;
+  int o_rl;                    // warp smem: misc list of each range (paper)
   const uint32_t* order;       // claim order of the queries (heavy first) or null
   const uint32_t* list_items;  // N_l for the cost estimate (or own_cnt)
   uint64_t cost_thr;           // a query is heavy when cost * nlist > cost_thr
@@ -296,12 +306,13 @@ struct FsTask {
   const uint8_t* gp;   // the group's 16-B column at m4 = 0 (a valid dummy when idle)
   uint32_t gi;         // group index (slot / 8)
   uint32_t vmask;      // items of the group inside the range (0 when idle)
+  uint32_t ml;         // paper layout: the list whose misc area holds the group, else ~0
 };
 
 __device__ __forceinline__ FsTask fs_task(uint32_t t, uint32_t ng_tot, uint32_t nr, const uint32_t* rs,
                                           const uint32_t* rc, const uint32_t* rg, const uint8_t* codes,
                                           uint64_t blk_bytes) {
-  FsTask k{codes, 0u, 0u};
+  FsTask k{codes, 0u, 0u, 0xFFFFFFFFu};
   if (t < ng_tot) {
     uint32_t lo = 0, hi = nr;  // largest r with rg[r] <= t
     while (hi - lo > 1) {
@@ -327,7 +338,7 @@ __device__ __forceinline__ FsTask fs_task(uint32_t t, uint32_t ng_tot, uint32_t 
 // On return r_lo holds the range of task t0 + 32 (the next round's).
 __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uint32_t ng_tot, uint32_t nr,
                                                 const uint32_t* rs, const uint32_t* rc, const uint32_t* rg,
-                                                const uint8_t* codes, uint64_t blk_bytes) {
+                                                const uint32_t* rl, const uint8_t* codes, uint64_t blk_bytes) {
   const int lane = lane_id();
   uint32_t r, adv;
   const uint32_t e = r_lo + 1 <= nr ? rg[r_lo + 1] : 0xFFFFFFFFu;  // end of range r_lo
@@ -346,10 +357,11 @@ __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uin
     r = r_lo + __popc(bits & (0xFFFFFFFFu >> (31 - lane)));
     adv = __popc(bits) + (__ballot_sync(0xffffffffu, at32 != 0) ? 1u : 0u);
   }
-  FsTask k{codes, 0u, 0u};
+  FsTask k{codes, 0u, 0u, 0xFFFFFFFFu};
   const uint32_t t = t0 + (uint32_t)lane;
   if (t < ng_tot) {
     const uint32_t st = rs[r], en = st + rc[r];
+    if (rl) k.ml = rl[r];
     const uint32_t gi = (st >> 3) + (t - rg[r]);
     const uint32_t g0 = gi * 8u;
     const uint32_t a0 = st > g0 ? st - g0 : 0u;
@@ -580,6 +592,21 @@ __device__ __forceinline__ uint32_t fs_pass(const uint32_t (&acc)[8], uint32_t v
   return pm & vmask;
 }
 
+// Paper layout, misc area of list ml (RemoveVectorIfVisited, Alg. 5 line 16):
+// an item whose embedded other list was visited before ml -- probed with a
+// smaller id (ascending visit order, reading R9) -- was scored there; drop it.
+__device__ __forceinline__ uint32_t fs_paper_drop(const FsArgs& a, uint32_t pm, uint32_t gi, uint32_t ml,
+                                                  const int32_t* Ps) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    if ((pm >> v) & 1u) {
+      const uint32_t o = __ldg(a.p_other + gi * 8u + v);
+      if (o < ml && fs_in_sorted(Ps, a.npp2, (int32_t)o)) pm &= ~(1u << v);
+    }
+  }
+  return pm;
+}
+
 // exact (massive-tie) mode: drop the items whose resolved key is >= tau_key
 __device__ __forceinline__ uint32_t fs_pass_exact(const FsArgs& a, const uint32_t (&accp)[8], uint32_t pm,
                                                   uint32_t gi, uint64_t tau_key) {
@@ -734,6 +761,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
   uint32_t* rs = reinterpret_cast<uint32_t*>(wb + a.o_rs);
   uint32_t* rc = reinterpret_cast<uint32_t*>(wb + a.o_rc);
   uint32_t* rg = reinterpret_cast<uint32_t*>(wb + a.o_rg);
+  uint32_t* rlp = a.paper ? reinterpret_cast<uint32_t*>(wb + a.o_rl) : nullptr;
   const int M4 = a.M_pad / 4;  // a multiple of 4 (M_pad % 16 == 0)
   const uint64_t blk_bytes = 16ull * (uint64_t)a.M_pad;
   const int np = a.nprobe;
@@ -782,20 +810,33 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     // ---- A4 + A5 + A6 ----
     FsSel st{0u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, kKeyInf};
     uint32_t my_dco = 0;
-    const uint32_t nsrc = (uint32_t)np + nrefs;
+    // sources: np owned ranges (paper layout: np shared-block ranges, then np
+    // misc areas), then the probed lists' references
+    const uint32_t npb = a.paper ? 2u * (uint32_t)np : (uint32_t)np;
+    const uint32_t nsrc = npb + nrefs;
     uint32_t s0 = 0;
     for (;;) {
       // (1) a batch of ranges: s < np -> owned range of probe s; else reference s - np
       uint32_t nr = 0;
       while (s0 < nsrc && nr <= FS_RCAP - 32) {
         const uint32_t s = s0 + lane;
-        uint32_t st0 = 0, cnt = 0;
-        if (s < (uint32_t)np) {
-          const int l = __ldg(pq + s);
-          st0 = __ldg(a.own_off + l);
-          cnt = __ldg(a.own_cnt + l);
+        uint32_t st0 = 0, cnt = 0, ml = 0xFFFFFFFFu;
+        if (s < npb) {
+          const bool misc = s >= (uint32_t)np;  // paper layout only
+          const int l = __ldg(pq + (misc ? s - (uint32_t)np : s));
+          if (!a.paper) {
+            st0 = __ldg(a.own_off + l);
+            cnt = __ldg(a.own_cnt + l);
+          } else if (!misc) {
+            st0 = __ldg(a.p_off + l);
+            cnt = __ldg(a.p_shared + l);
+          } else {
+            st0 = __ldg(a.p_off + l) + __ldg(a.p_shared + l);
+            cnt = __ldg(a.p_misc + l);
+            ml = (uint32_t)l;
+          }
         } else if (s < nsrc) {
-          const uint32_t e = s - (uint32_t)np;
+          const uint32_t e = s - npb;
           int lo = 0, hi = np;  // probe of reference e: largest i with pre[i] <= e
           while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -804,8 +845,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
           const uint32_t j = r0s[lo] + (e - pre[lo]);
           const int32_t o = __ldg(a.ref_owner + j);
           if (!fs_in_sorted(Ps, a.npp2, o)) {  // R9: owner not probed -> scan the cell here
-            st0 = __ldg(a.ref_start + j);
-            cnt = __ldg(a.ref_cnt + j);
+            st0 = __ldg((a.paper ? a.p_ref_start : a.ref_start) + j);
+            cnt = __ldg((a.paper ? a.p_ref_cnt : a.ref_cnt) + j);
           }
         }
         const bool has = cnt > 0;
@@ -814,6 +855,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
           const uint32_t p = nr + __popc(bal & below_me);
           rs[p] = st0;
           rc[p] = cnt;
+          if (rlp) rlp[p] = ml;
         }
         nr += __popc(bal);
         s0 += 32;
@@ -840,7 +882,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
       uint32_t r_lo = 0;  // range holding the first task of the next round to map
       FsTask A[GPL];
 #pragma unroll
-      for (int g = 0; g < GPL; ++g) A[g] = fs_round_task(32u * g, r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
+      for (int g = 0; g < GPL; ++g) A[g] = fs_round_task(32u * g, r_lo, ng_tot, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
       // per group a ring of D loop-carried chunk slots (chunk c in slot c % D),
       // each refilled right after it is consumed with the chunk D ahead (past
       // the group's end: chunk c % D of the lane's next-round group), so the
@@ -855,7 +897,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
         FsTask nA[GPL];
 #pragma unroll
         for (int g = 0; g < GPL; ++g)
-          nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, ng_tot, nr, rs, rc, rg, a.codes, blk_bytes);
+          nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, ng_tot, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
         uint32_t acc[GPL][8];
 #pragma unroll
         for (int g = 0; g < GPL; ++g)
@@ -927,6 +969,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
 #pragma unroll
           for (int g = 0; g < GPL; ++g) {
             pm[g] = mn <= lim ? fs_pass(acc[g], A[g].vmask, lim) : 0u;
+            if (pm[g] && A[g].ml != 0xFFFFFFFFu) pm[g] = fs_paper_drop(a, pm[g], A[g].gi, A[g].ml, Ps);
             if (st.exact && pm[g]) pm[g] = fs_pass_exact(a, acc[g], pm[g], A[g].gi, st.tau_key);
             c += __popc(pm[g]);
           }
@@ -1116,6 +1159,21 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   p = FsArgs{};
   p.codes = idx->codes_g;
   p.slot_rows = idx->slot_rows;
+  if (idx->seil_layout != 0) {
+    if (!idx->p_codes_g) {
+      set_error("fast scan: paper SEIL layout selected but not built");
+      return RAIRS_E_INTERNAL;
+    }
+    p.paper = 1;
+    p.codes = idx->p_codes_g;
+    p.slot_rows = idx->p_slot_rows;
+    p.p_off = idx->p_off;
+    p.p_shared = idx->p_shared;
+    p.p_misc = idx->p_misc;
+    p.p_other = idx->p_other;
+    p.p_ref_start = idx->p_ref_start;
+    p.p_ref_cnt = idx->p_ref_cnt;
+  }
   p.own_off = idx->own_off;
   p.own_cnt = idx->own_cnt;
   p.ref_ptr = idx->ref_ptr;
@@ -1170,6 +1228,7 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   p.o_rs = take(FS_RCAP * 4, 4);
   p.o_rc = take(FS_RCAP * 4, 4);
   p.o_rg = take((FS_RCAP + 1) * 4, 4);
+  p.o_rl = p.paper ? take(FS_RCAP * 4, 4) : 0;
   p.warp_bytes = (int)round_up(o, 16);
   if (p.cap * 8 < idx->M * 4 + 16) {
     set_error("fast scan: candidate buffer smaller than the LUT scratch");

@@ -83,6 +83,23 @@ struct rairs_index_s {
   unsigned* fs_ctr = nullptr;
   std::atomic<unsigned> fs_slot{0};
   int64_t fs_bytes = 0;
+  // paper-literal SEIL layout (Alg. 4; seil_paper.cu), built on
+  // demand: per list l, p_off[l] = region start (32-aligned), p_shared[l]
+  // items in shared 32-item blocks, then p_misc[l] misc items (p_other: the
+  // other list id embedded with each misc item, kNoOther in shared blocks);
+  // p_ref_start / p_ref_cnt: the shared blocks each reference (ref_ptr /
+  // ref_owner order) points at.  seil_layout 1 = searches use it (query-major
+  // only), 2 = query-major searches use it, list-major ones the cell-major layout.
+  int seil_layout = 0;
+  uint8_t* p_codes_g = nullptr;
+  uint32_t* p_slot_rows = nullptr;
+  uint32_t* p_other = nullptr;
+  uint32_t* p_off = nullptr;
+  uint32_t* p_shared = nullptr;
+  uint32_t* p_misc = nullptr;
+  uint32_t* p_ref_start = nullptr;
+  uint32_t* p_ref_cnt = nullptr;
+  int64_t p_slots = 0, p_bytes = 0;
   int64_t device_bytes = 0;
   int64_t layout_bytes = 0, lm_bytes = 0;  // parts of device_bytes rebuilt by add/remove
   // two auxiliary streams + fork/join events (list-major select/refine overlap)
@@ -220,6 +237,9 @@ struct FsExtra {
   uint32_t* defer_n = nullptr;        // [nq]
 };
 bool fastscan_order_on();
+// paper-literal SEIL layout (seil_paper.cu)
+rairs_status seil_paper_prepare(rairs_index_s* idx, cudaStream_t s);
+void seil_paper_free(rairs_index_s* idx);
 int fastscan_cap(int bigK, int M_pad);
 rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& a, cudaStream_t s,
                              const FsExtra& ex = FsExtra{});

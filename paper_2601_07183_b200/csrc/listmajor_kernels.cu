@@ -1306,6 +1306,7 @@ static bool lm_nu_ok(int NU) { return NU == 1 || NU == 2 || NU == 3 || NU == 4 |
 
 bool listmajor_ok(const rairs_index_s* idx, int64_t nq, int nprobe, int bigK) {
   if (idx->scan_mode == 1) return false;            // forced SIMT query-major scan
+  if (idx->seil_layout == 1) return false;          // paper-literal SEIL: query-major only
   // auto: the list-major contraction pays once a probed list is shared by
   // several queries of the batch (each list-task expands its codes once)
   if (idx->scan_mode == 0 && (double)nq * nprobe < LM_MIN_QUERIES_PER_LIST * idx->nlist)
