@@ -834,9 +834,10 @@ def main():
                     help="queries with exact ground truth for recall (0 = all)")
     ap.add_argument("--k1", type=int, default=1,
                     help="side line: the same index at k=1 (BJ configs[3]: k=1 and k=10)")
-    ap.add_argument("--seil-layout", default="auto", choices=["cell", "paper", "auto"],
-                    help="SEIL list layout searched (rairs_set_seil_layout): auto = the "
-                         "paper-literal layout for query-major scans, cell-major for list-major")
+    ap.add_argument("--seil-layout", default="cell", choices=["cell", "paper", "auto"],
+                    help="SEIL list layout searched (rairs_set_seil_layout): cell-major (R10), "
+                         "paper-literal (Alg. 4/5), or auto = paper-literal for query-major scans, "
+                         "cell-major for list-major. The other layout is measured in seil_layouts.")
     ap.add_argument("--seil-paper", type=int, default=1,
                     help="side line: the same index searched over the paper-literal SEIL layout "
                          "(Alg. 4/5; misc remainders duplicated) at the chosen nprobe")
