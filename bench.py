@@ -502,13 +502,15 @@ def scan_roofline(idx, spec, scan_mode, dco_local, Qd, k, nprobe, rf, scan_ms, p
     import torch
     M2 = spec.M // 2
     if scan_mode == "listmajor":
-        plist = idx.probed_list_items(Qd, k, nprobe, rf) if hasattr(idx, "probed_list_items") else None
-        code_b = (plist * M2) if plist is not None else None
-        score_b = (dco_local * 2 * 3) if plist is not None else None  # u16 rows: 1 write + 2 reads
-        alg = (code_b + score_b) if plist is not None else dco_local * M2
-        kern = ("lm_tensor_kernel (tcgen05 kind::i8 one-hot x LUT); time from events right around "
-                "its launch")
-        unit = "probed list-task codes once per batch + u16 score rows (1 write, 2 reads)"
+        # the kernel timed is lm_tensor_kernel: it reads each probed list-task's
+        # codes once per batch (N_l = owned items + referenced items) and writes
+        # the u16 score rows (2 B per scored (item, query) pair = DCO)
+        plist = probed_list_items(idx, Qd, k, nprobe, rf)
+        alg = plist * M2 + dco_local * 2
+        kern = ("lm_tensor_kernel (tcgen05 kind::i8 one-hot x LUT, bound by the one-hot expansion "
+                "into TMEM); time from events right around its launch")
+        unit = (f"M/2 = {M2} B per probed list-task item (codes once per batch: {int(plist)} items) "
+                "+ 2 B per scored (item, query) pair (u16 score rows written)")
     else:
         alg = dco_local * M2
         kern = ("fs_scan_kernel (query-major: SEIL work list + register-LUT prmt/dp4a fast scan "
@@ -536,6 +538,25 @@ def scan_roofline(idx, spec, scan_mode, dco_local, Qd, k, nprobe, rf, scan_ms, p
             "algorithmic_bytes_per_launch": int(alg), "algorithmic_bytes_per_unit": unit,
             "avg_launch_ms": round(scan_ms, 4),
             "stage": "fast-scan stage A3-A6 = LUT kernel + scan kernel + finish/selection"}
+
+
+def probed_list_items(idx, Qd, k, nprobe, rf):
+    """Items of the list-tasks the batch probes (each distinct probed list l
+    once: its owned items + the items of its references), from the exported
+    layout and one debug search's probe sets."""
+    import torch
+    L = idx.export_layout()
+    nl = L["own_cnt"].shape[0]
+    refs = torch.zeros(nl, dtype=torch.int64, device=L["own_cnt"].device)
+    if L["ref_cnt"].numel():
+        lst = torch.repeat_interleave(torch.arange(nl, device=refs.device), L["ref_ptr"][1:] - L["ref_ptr"][:-1])
+        refs.index_add_(0, lst, L["ref_cnt"])
+    n_l = L["own_cnt"] + refs
+    probes = idx.search_debug(Qd, k, nprobe, rf)["probes"].reshape(-1).long()
+    used = torch.zeros(nl, dtype=torch.bool, device=refs.device)
+    used[probes] = True
+    del L
+    return float(n_l[used].sum().item())
 
 
 def side_k1(idx, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream, steps):

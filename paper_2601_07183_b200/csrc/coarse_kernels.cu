@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     coarse_topw_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, TopWArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B aligned; offset from smem_raw so the compiler keeps the shared
+  // state space (plain LDS/STS, not generic loads, on the staging buffers)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = a.nstage, Wp1 = a.Wp1;
   const int nk = (a.d + FT_BK - 1) / FT_BK;
   // a_res: the row tile's A (all nk K-chunks) is loaded ONCE and stays resident

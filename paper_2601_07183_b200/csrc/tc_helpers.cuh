@@ -9,6 +9,10 @@
 
 namespace rairs {
 
+#ifndef MBAR_SUSPEND_NS
+#define MBAR_SUSPEND_NS 2000u
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -30,12 +34,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
 // Spin on an mbarrier phase.  A pipeline bug must fail fast instead of hanging
 // the GPU: after ~4 s (clock64 cycles at <= 2 GHz) the kernel traps, the
 // launch reports an error and the C ABI returns RAIRS_E_CUDA.
+// try_wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or ~the hint elapses) instead of re-issuing polls that take
+// issue slots from the warps doing the work
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase), "r"(MBAR_SUSPEND_NS) : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   if (mbar_try_wait(bar, phase)) return;
   const long long t0 = clock64();
-  for (uint32_t n = 1;; ++n) {  // the clock is checked every 256 polls (issue slots)
-    if (mbar_try_wait(bar, phase)) return;
-    if ((n & 255u) == 0 && clock64() - t0 > 8000000000LL) __trap();
+  for (uint32_t n = 1;; ++n) {  // the clock is checked every 16 polls
+    if (mbar_try_wait_sleep(bar, phase)) return;
+    if ((n & 15u) == 0 && clock64() - t0 > 8000000000LL) __trap();
   }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
