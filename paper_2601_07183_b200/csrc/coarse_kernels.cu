@@ -800,7 +800,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   const bool reg = Wp1 <= 32 || capped;
   // list length = W + 1 rounded up to an instantiated size: the insertion cost
   // and the pass threshold (the KR-th kept value) both shrink with KR
-  const int KR = Wp1 <= 10 ? 10 : Wp1 <= 13 ? 13 : Wp1 <= 16 ? 16 : Wp1 <= 20 ? 20
+  const int KR = Wp1 <= 10 ? 10 : Wp1 <= 11 ? 11 : Wp1 <= 12 ? 12 : Wp1 <= 13 ? 13 : Wp1 <= 16 ? 16 : Wp1 <= 20 ? 20
                : Wp1 <= 24 ? 24 : 32;
   const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
   const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
@@ -841,6 +841,10 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<0>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<10>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<11>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<12>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<13>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -941,6 +945,10 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     const dim3 tgrid = lin ? dim3((unsigned)G, 1u) : dim3((unsigned)mtiles, (unsigned)nsplit);
     if (reg && KR == 10)
       coarse_topw_kernel<10><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
+    else if (reg && KR == 11)
+      coarse_topw_kernel<11><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
+    else if (reg && KR == 12)
+      coarse_topw_kernel<12><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg && KR == 13)
       coarse_topw_kernel<13><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
     else if (reg && KR == 16)
