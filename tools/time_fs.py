@@ -39,4 +39,5 @@ for _ in range(reps):
     idx.search(Qd, spec.k, npb, spec.refine_factor)
 torch.cuda.synchronize()
 p = idx.profile_read(reset=True)
-print(cfg, npb, mode, {k: round(v / reps, 4) for k, v in p["ms"].items()})
+print(cfg, npb, mode, {k: round(v / reps, 4) for k, v in p["ms"].items()},
+      "uncertified/search", round(idx.certify_fallbacks(reset=True) / (reps + 3), 1))
