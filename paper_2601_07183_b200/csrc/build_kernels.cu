@@ -258,19 +258,7 @@ static rairs_status launch_probe_R(const ProbeArgs& a, cudaStream_t s) {
 // outputs as probe_exact_kernel (probes / RAIR pair / single).  Rows beyond
 // PX_CAP keep their flag for the tiled exact kernel.
 constexpr int PX_S = 64;
-constexpr int PX_CAP = 2048;
 constexpr int PX_T = 256;
-
-__global__ void flag_compact_kernel(const int32_t* __restrict__ flags, int64_t rows,
-                                    uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    if (flags[r]) {
-      const uint32_t i = atomicAdd(count, 1u);
-      if (i < (uint32_t)PX_CAP) list[i] = (uint32_t)r;
-    }
-  }
-}
 
 __device__ void cta_sort_pairs(uint64_t* k, uint32_t* id, int n) {
   for (int size = 2; size <= n; size <<= 1) {
@@ -419,35 +407,50 @@ __global__ void __launch_bounds__(PX_T) probe_merge_kernel(ProbeArgs a,
 }
 
 // Split-path exact fallback for flagged rows (large nlist); leaves flags set
-// only for rows it did not handle.  Returns RAIRS_OK without work when the
-// shape does not qualify.
-rairs_status launch_probe_split(const ProbeArgs& a, int32_t* flags, cudaStream_t s) {
-  if (a.rows <= 0 || !a.only_flagged || a.nl < 8192) return RAIRS_OK;
-  const int per = (int)ceil_div(a.nl, PX_S);
-  const int npow_s = next_pow2(std::max(per, a.L));
-  const int npow_m = next_pow2(PX_S * a.L);
-  const size_t sm_s = (size_t)npow_s * 12 + 8 + (size_t)a.d * 8 + (size_t)PX_T * 33 * 4;
-  const size_t sm_m = (size_t)npow_m * 12 + 8;
-  if (sm_s > 200 * 1024 || sm_m > 200 * 1024) return RAIRS_OK;
-  uint32_t *list = nullptr, *count = nullptr, *ti = nullptr;
-  uint64_t* tk = nullptr;
-  auto cleanup = [&]() { cudaFreeAsync(list, s); cudaFreeAsync(count, s); cudaFreeAsync(tk, s); cudaFreeAsync(ti, s); };
-#define PX_TRY(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { set_error(std::string(#x) + ": " + cudaGetErrorString(_e)); cleanup(); return RAIRS_E_CUDA; } } while (0)
-  PX_TRY(ws_malloc(&list, PX_CAP * 4, s));
-  PX_TRY(ws_malloc(&count, 4, s));
-  PX_TRY(ws_malloc(&tk, (size_t)PX_CAP * PX_S * a.L * 8, s));
-  PX_TRY(ws_malloc(&ti, (size_t)PX_CAP * PX_S * a.L * 4, s));
-  PX_TRY(cudaMemsetAsync(count, 0, 4, s));
-  flag_compact_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.rows, 256), 148 * 32)), 256, 0, s>>>(
-      a.only_flagged, a.rows, list, count);
-  PX_TRY(cudaFuncSetAttribute(probe_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
-  probe_split_kernel<<<148 * 4, PX_T, sm_s, s>>>(a, list, count, per, npow_s, tk, ti);
-  PX_TRY(cudaFuncSetAttribute(probe_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_m));
-  probe_merge_kernel<<<148 * 2, PX_T, sm_m, s>>>(a, list, count, npow_m, tk, ti, flags);
-  PX_TRY(cudaGetLastError());
-  cleanup();
+// only for rows it did not handle.  prepare: the workspace when the shape
+// qualifies (b.on), before the certify kernel that fills b.list / *count (no
+// separate compaction kernel or memset); launch: probe_split_kernel +
+// probe_merge_kernel (with no flagged row both exit at once).
+rairs_status probe_split_prepare(const ProbeArgs& a, ProbeSplitBufs& b, cudaStream_t s) {
+  b = ProbeSplitBufs{};
+  if (a.rows <= 0 || a.nl < 8192) return RAIRS_OK;
+  b.per = (int)ceil_div(a.nl, PX_S);
+  b.npow_s = next_pow2(std::max(b.per, a.L));
+  b.npow_m = next_pow2(PX_S * a.L);
+  b.sm_s = (size_t)b.npow_s * 12 + 8 + (size_t)a.d * 8 + (size_t)PX_T * 33 * 4;
+  b.sm_m = (size_t)b.npow_m * 12 + 8;
+  if (b.sm_s > 200 * 1024 || b.sm_m > 200 * 1024) return RAIRS_OK;
+  cudaError_t e = ws_malloc(&b.list, PX_CAP * 4, s);
+  if (e == cudaSuccess) e = ws_malloc(&b.tk, (size_t)PX_CAP * PX_S * a.L * 8, s);
+  if (e == cudaSuccess) e = ws_malloc(&b.ti, (size_t)PX_CAP * PX_S * a.L * 4, s);
+  if (e != cudaSuccess) {
+    probe_split_free(b, s);
+    set_error(std::string("probe split workspace: ") + cudaGetErrorString(e));
+    return RAIRS_E_OOM;
+  }
+  b.on = true;
   return RAIRS_OK;
-#undef PX_TRY
+}
+
+rairs_status probe_split_launch(const ProbeArgs& a, const ProbeSplitBufs& b, const uint32_t* count,
+                                int32_t* flags, cudaStream_t s) {
+  if (!b.on) return RAIRS_OK;
+  // plain launches: as programmatic dependent launches (split after certify,
+  // merge after split) the build's all-uncertified case faulted (an illegal
+  // address in the fallback chain; not understood, so not used)
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(probe_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.sm_s));
+  probe_split_kernel<<<148 * 4, PX_T, b.sm_s, s>>>(a, b.list, count, b.per, b.npow_s, b.tk, b.ti);
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(probe_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.sm_m));
+  probe_merge_kernel<<<148 * 2, PX_T, b.sm_m, s>>>(a, b.list, count, b.npow_m, b.tk, b.ti, flags);
+  RAIRS_CHECK_LAUNCH();
+  return RAIRS_OK;
+}
+
+void probe_split_free(ProbeSplitBufs& b, cudaStream_t s) {
+  cudaFreeAsync(b.list, s);
+  cudaFreeAsync(b.tk, s);
+  cudaFreeAsync(b.ti, s);
+  b = ProbeSplitBufs{};
 }
 
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s) {

@@ -502,6 +502,8 @@ struct CertArgs {
   int32_t* l2;
   int32_t* flags;
   unsigned* nflag;
+  uint32_t* split_list;   // split exact fallback (large nlist): flagged rows appended here
+  uint32_t* split_count;
   int stage_rows;      // stage the candidate centroid rows in shared memory
   size_t stage_off;    // byte offset of the staging area in dynamic smem
   size_t stage_warp;   // bytes per warp
@@ -697,6 +699,10 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
       if (!certified) {
         atomicAdd(a.nflag, 1u);
         atomicAdd(a.flags + a.rows, 1);  // per-call count: the fallback exits at once when 0
+        if (a.split_list) {
+          const uint32_t i = atomicAdd(a.split_count, 1u);
+          if (i < (uint32_t)PX_CAP) a.split_list[i] = (uint32_t)r;
+        }
       }
     }
     __syncwarp();
@@ -914,8 +920,9 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     int32_t* flags = nullptr;
     RAIRS_CUDA_TRY(ws_malloc(&vals, (size_t)nr * nsplit * Wout * 4, s));
     RAIRS_CUDA_TRY(ws_malloc(&ids, (size_t)nr * nsplit * Wout * 4, s));
-    RAIRS_CUDA_TRY(ws_malloc(&flags, (size_t)(nr + 1) * 4, s));
-    RAIRS_CUDA_TRY(cudaMemsetAsync(flags + nr, 0, 4, s));  // flagged-row count of this call
+    // flags[nr]: flagged-row count of this call; flags[nr + 1]: rows in the split list
+    RAIRS_CUDA_TRY(ws_malloc(&flags, (size_t)(nr + 2) * 4, s));
+    RAIRS_CUDA_TRY(cudaMemsetAsync(flags + nr, 0, 8, s));
     const float* Xc = X + (size_t)r0 * d;
     CUtensorMap tmA, tmB;
     if (!make_tmap_f32(&tmA, Xc, nr, d, FT_BM) || !make_tmap_f32(&tmB, idx->centroids, nl, d, FT_BN)) {
@@ -968,6 +975,30 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
                (long long)r0, (long long)(r0 + nr), (long long)rows, (const void*)X, (const void*)Xc);
       RAIRS_TRY(debug_sync_point(s, what));
     }
+    // exact fp64 recomputation of the (rare) uncertified rows (split path for
+    // large nlist: its workspace now, the certify kernel lists the rows)
+    ProbeArgs pa{};
+    pa.X = Xc;
+    pa.rows = nr;
+    pa.d = d;
+    pa.C = idx->centroids;
+    pa.nl = nl;
+    pa.L = L;
+    pa.mode = mode;
+    pa.lambda = lambda;
+    pa.strict = strict;
+    pa.out_idx = out_idx ? out_idx + r0 * L : nullptr;
+    pa.l1 = l1 ? l1 + r0 : nullptr;
+    pa.l2 = l2 ? l2 + r0 : nullptr;
+    pa.only_flagged = flags;
+    ProbeSplitBufs sb;
+    {
+      const rairs_status ps = probe_split_prepare(pa, sb, s);
+      if (ps != RAIRS_OK) {
+        cudaFreeAsync(vals, s); cudaFreeAsync(ids, s); cudaFreeAsync(flags, s);
+        return ps;
+      }
+    }
     CertArgs ca{};
     ca.vals = vals;
     ca.ids = ids;
@@ -994,6 +1025,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ca.l2 = l2 ? l2 + r0 : nullptr;
     ca.flags = flags;
     ca.nflag = nflag;
+    ca.split_list = sb.on ? sb.list : nullptr;
+    ca.split_count = reinterpret_cast<uint32_t*>(flags + nr + 1);
     // candidate-row staging (coalesced loads) when it fits next to the sort buffers
     const size_t stage_warp = round_up((size_t)std::min(W, nl) * (d + 4) * 4, 16) + (size_t)d * 8 + 16;
     ca.stage_off = round_up(csmem, 16);
@@ -1005,25 +1038,11 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     const int cgrid = (int)std::min<int64_t>(ceil_div(nr, CT_WARPS), 148 * 16);
     RAIRS_CUDA_TRY(launch_pdl(coarse_certify_kernel, dim3(cgrid), dim3(CT_THREADS), csmem_all, s, ca));
     RAIRS_DEBUG_POINT(s, "coarse_certify_kernel");
-    // exact fp64 recomputation of the (rare) uncertified rows
-    ProbeArgs pa{};
-    pa.X = Xc;
-    pa.rows = nr;
-    pa.d = d;
-    pa.C = idx->centroids;
-    pa.nl = nl;
-    pa.L = L;
-    pa.mode = mode;
-    pa.lambda = lambda;
-    pa.strict = strict;
-    pa.out_idx = ca.out_idx;
-    pa.l1 = ca.l1;
-    pa.l2 = ca.l2;
-    pa.only_flagged = flags;
-    rairs_status st = launch_probe_split(pa, flags, s);  // large nlist: split rows over CTAs
+    rairs_status st = probe_split_launch(pa, sb, reinterpret_cast<const uint32_t*>(flags + nr + 1), flags, s);
     pa.flag_count = true;  // flags[nr]: rows the certify flagged (the split path may clear some)
     if (st == RAIRS_OK) st = launch_probe_exact(pa, s);   // remaining flagged rows
     if (st == RAIRS_OK && debug_sync_enabled()) st = debug_sync_point(s, "probe_exact fallback");
+    probe_split_free(sb, s);
     cudaFreeAsync(vals, s);
     cudaFreeAsync(ids, s);
     cudaFreeAsync(flags, s);

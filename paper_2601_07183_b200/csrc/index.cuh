@@ -159,8 +159,22 @@ struct ProbeArgs {
   bool flag_count = false;      // only_flagged[rows] = number of flagged rows (0: exit at once)
 };
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s);
-// few flagged rows x many lists: split exact fallback (clears the flags it handles)
-rairs_status launch_probe_split(const ProbeArgs& a, int32_t* flags, cudaStream_t s);
+// few flagged rows x many lists: split exact fallback (clears the flags it handles).
+// prepare (before the certify kernel, which appends the flagged rows to
+// b.list / *count itself), launch (programmatic dependent launches), free.
+constexpr int PX_CAP = 2048;  // rows the split path takes per call (the rest: tiled kernel)
+struct ProbeSplitBufs {
+  uint32_t* list = nullptr;
+  uint64_t* tk = nullptr;
+  uint32_t* ti = nullptr;
+  int per = 0, npow_s = 0, npow_m = 0;
+  size_t sm_s = 0, sm_m = 0;
+  bool on = false;
+};
+rairs_status probe_split_prepare(const ProbeArgs& a, ProbeSplitBufs& b, cudaStream_t s);
+rairs_status probe_split_launch(const ProbeArgs& a, const ProbeSplitBufs& b, const uint32_t* count,
+                                int32_t* flags, cudaStream_t s);
+void probe_split_free(ProbeSplitBufs& b, cudaStream_t s);
 
 rairs_status train_kmeans(const float* X, int64_t n, int d, int k, int iters, uint64_t seed,
                           int64_t max_train, float* centroids_out, cudaStream_t s);
