@@ -780,6 +780,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     const int64_t q = a.qlist ? (int64_t)a.qlist[qq] : a.order ? (int64_t)a.order[qq] : (int64_t)qq;
     const int32_t* pq = a.probes + q * a.pstride;
 
+    // the query's LUT rows (fs_lut_kernel) into the warp's shared memory by
+    // cp.async: the copy runs while the probe set and range list are built
+    for (int m = lane; m < a.M_pad; m += 32)
+      cp_async16((uint32_t)__cvta_generic_to_shared(lut + m), a.luts + q * a.M_pad + m);
+    cp_async_commit();
+
     // ---- probe set: sorted copy (membership, R9) + per-probe reference prefix ----
     for (int i = lane; i < a.npp2; i += 32) Ps[i] = i < np ? __ldg(pq + i) : INT_MAX;
     for (int i = lane; i < 256; i += 32) hist[i] = 0u;
@@ -801,11 +807,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     if (lane == 0) pre[np] = nrefs;
 
     // ---- A3: LUT + uint8 quantisation (O2); T / mn scratch in the candidate buffer ----
-    {  // the query's LUT (fs_lut_kernel) into the warp's shared memory
-      const uint4* src_lut = a.luts + q * a.M_pad;
-      for (int m = lane; m < a.M_pad; m += 32) lut[m] = __ldg(src_lut + m);
-      __syncwarp();
-    }
+    cp_async_wait0();  // the LUT rows (issued at the query's start)
+    __syncwarp();
 
     // ---- A4 + A5 + A6 ----
     FsSel st{0u, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, kKeyInf};
