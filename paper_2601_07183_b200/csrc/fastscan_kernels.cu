@@ -34,6 +34,7 @@
 #include <cstdlib>
 
 #include "index.cuh"
+#include "lut_common.cuh"
 
 namespace rairs {
 
@@ -449,82 +450,6 @@ __device__ __noinline__ uint32_t fs_finish(const FsArgs& a, uint64_t* cand, uint
   return keep;
 }
 
-// O2 row T[m][0..15] (fp32 RN, ascending t, no FMA); cb = codebook [16][dsub][M]
-__device__ __forceinline__ void fs_lut_row(const float* __restrict__ qv, const float* cb, int m, int M,
-                                           int dsub, float (&T)[16]) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) T[j] = 0.0f;
-  for (int t = 0; t < dsub; ++t) {
-    const float qt = __ldg(qv + m * dsub + t);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float diff = __fsub_rn(qt, cb[((size_t)j * dsub + t) * M + m]);
-      T[j] = __fadd_rn(T[j], __fmul_rn(diff, diff));
-    }
-  }
-}
-
-// The O2 LUT of one query into the warp's shared memory (+ debug outputs).
-// Lane per subquantizer; pass 1 computes T (kept in `scratch` as [16][M] when
-// it fits, else recomputed in pass 2), mn_m and the span; pass 2 quantises.
-__device__ __noinline__ void fs_build_lut(const FsArgs& a, int64_t q, uint4* lut, float* scratch,
-                                          const float* cb, bool keepT) {
-  const int lane = lane_id();
-  const int M = a.M;
-  const float* qv = a.queries + q * a.d;
-  float* Ts = scratch;                          // [16][M] when keepT
-  float* mn = scratch + (keepT ? 16 * M : 0);   // [M]
-  float spanmax = 0.0f;
-  for (int m = lane; m < M; m += 32) {
-    float T[16];
-    fs_lut_row(qv, cb, m, M, a.dsub, T);
-    float lo = T[0], hi = T[0];
-#pragma unroll
-    for (int j = 1; j < 16; ++j) { lo = fminf(lo, T[j]); hi = fmaxf(hi, T[j]); }
-    if (keepT) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) Ts[j * M + m] = T[j];
-    }
-    mn[m] = lo;
-    spanmax = fmaxf(spanmax, __fsub_rn(hi, lo));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) spanmax = fmaxf(spanmax, __shfl_xor_sync(0xffffffffu, spanmax, o));
-  const bool pos = spanmax > 0.0f;
-  const float qa = pos ? __fdiv_rn(255.0f, spanmax) : 1.0f;
-  __syncwarp();
-  for (int m = lane; m < a.M_pad; m += 32) {
-    uint32_t wd[4] = {0u, 0u, 0u, 0u};
-    if (m < M && pos) {
-      float T[16];
-      if (keepT) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) T[j] = Ts[j * M + m];
-      } else {
-        fs_lut_row(qv, cb, m, M, a.dsub, T);
-      }
-      const float mnm = mn[m];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t v = (uint32_t)min(255, __float2int_rn(__fmul_rn(__fsub_rn(T[j], mnm), qa)));
-        wd[j >> 2] |= v << (8 * (j & 3));
-      }
-    }
-    const uint4 row = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-    lut[m] = row;
-    if (a.lut_q && m < M) reinterpret_cast<uint4*>(a.lut_q + (q * M + m) * 16)[0] = row;
-  }
-  if (lane == 0) {
-    if (a.lut_a) a.lut_a[q] = qa;
-    if (a.lut_b) {
-      float b = 0.0f;
-      for (int m = 0; m < M; ++m) b = __fadd_rn(b, mn[m]);
-      a.lut_b[q] = b;
-    }
-  }
-  __syncwarp();
-}
-
 // A full buffer: drop the entries above the bin threshold; if still too full,
 // cut at the exact bigK-th score (ties kept, histogram rebuilt); if even that
 // leaves too many (massive ties), switch to exact mode: resolved keys, sorted,
@@ -714,7 +639,7 @@ __global__ void fs_order_kernel(const __grid_constant__ FsArgs a, uint32_t* orde
 }
 
 // A3 for every query of the batch, one warp per query (O2: lane per
-// subquantizer, fp32 RN, ascending t; see fs_build_lut), into luts[q][M_pad].
+// subquantizer, fp32 RN, ascending t; see build_lut in lut_common.cuh), into luts[q][M_pad].
 // Needs only the queries, so under programmatic dependent launch it overlaps
 // the coarse stage; it waits for that stage (griddepcontrol.wait) only before
 // it exits, so its completion implies the probes are ready for the scan.
@@ -728,15 +653,17 @@ __global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(const __grid_cons
     __syncthreads();
   }
   const float* cb = a.cb_smem ? cbs : a.cbT;
+  const LutArgs la{a.queries, a.d, a.M, a.M_pad, a.dsub, a.cbT, luts, a.lut_q, a.lut_a, a.lut_b};
   const bool keepT = a.M * 17 <= 16 * 1024 / 4;  // [16][M] + [M] floats of scratch fit 16 KB
   float* scratch = reinterpret_cast<float*>(fl_smem + a.cb_smem) + (size_t)warp * (keepT ? 17 * a.M : a.M);
   for (int64_t q = (int64_t)blockIdx.x * FL_WARPS + warp; q < a.nq; q += (int64_t)gridDim.x * FL_WARPS) {
-    fs_build_lut(a, q, luts + q * a.M_pad, scratch, cb, keepT);
+    build_lut(la, q, luts + q * a.M_pad, scratch, cb, keepT);
     (void)lane;
   }
   pdl_wait();     // the coarse stage's probes are complete before this grid is
   pdl_trigger();
 }
+
 
 // One warp per query; see the file header.  A round scores 64 groups: lane
 // tasks t0 + lane and t0 + 32 + lane (two independent chains per lane, one
