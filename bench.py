@@ -413,6 +413,22 @@ def run_ours(args):
                          args.config)
     roof["stage_ms"] = round(scan_ms, 4)
     roof["stage_frac"] = round(roof["algorithmic_bytes_per_launch"] / (scan_ms / 1e3) / 1e9 / peak, 4)
+    roof_alu = None
+    if scan_mode == "simt":
+        # the query-major scan is bound by instruction issue, not HBM:
+        # its work in 4-bit LUT lookup-accumulates (DCO x M) against the issue
+        # ceiling of the prmt/dp4a formulation -- 8 lookups per 20 cycles per
+        # SMSP (per nibble word ~10 instructions on each of the alu and fma-heavy
+        # pipes, 0.5 warp-instructions/clk/SMSP each: tools/micro/pipe_rates.cu)
+        # x 32 lanes x 4 SMSPs x SMs x the SM clock sampled in the timed region
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk = (clocks or {}).get("sm_mhz") or 1965.0
+        peak_l = 8.0 / 20.0 * 32 * 4 * nsm * clk * 1e6
+        ach_l = dco_local * spec.M / (kern_ms / 1e3)
+        roof_alu = {"bound": "alu", "kernel": "fs_scan_kernel", "achieved": round(ach_l / 1e12, 3),
+                    "peak": round(peak_l / 1e12, 3), "unit": "T lookups/s", "frac": round(ach_l / peak_l, 4),
+                    "algorithmic_ops_per_launch": int(dco_local * spec.M),
+                    "peak_derivation": "8 lookups / 20 clk / SMSP x 32 lanes x 4 SMSPs x %d SMs x %.0f MHz" % (nsm, clk)}
 
     # ---------------- AIR + SEIL vs single assignment (the paper's comparison) ----
     vs_single = None
@@ -474,6 +490,7 @@ def run_ours(args):
                                      "pass of the same K steps with the library's stage/kernel events on "
                                      "(they break the kernels' PDL overlap, so `value` is timed without them)"},
             "roofline": roof,
+            "roofline_alu": roof_alu,
             "e2e": e2e, "gpu_launches": kernels,
             "coarse_uncertified_per_step": round(fallbacks / args.steps, 1),
             "latency_1q": lat,

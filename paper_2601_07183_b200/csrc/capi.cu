@@ -326,9 +326,10 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
         return e ? std::atoi(e) != 0 : true;
       }();
       const size_t dcap = (size_t)fastscan_cap(bigK, idx->M_pad);
+      const size_t dparts = (size_t)fastscan_parts(idx, nq, nprobe);  // split mode: one buffer per (query, part)
       cudaError_t le = ws_malloc(&luts, (size_t)nq * idx->M_pad * 16, s);
-      if (le == cudaSuccess && defer) le = ws_malloc(&dbuf, (size_t)nq * dcap * 8, s);
-      if (le == cudaSuccess && defer) le = ws_malloc(&dn, (size_t)nq * 4, s);
+      if (le == cudaSuccess && defer) le = ws_malloc(&dbuf, (size_t)nq * dparts * dcap * 8, s);
+      if (le == cudaSuccess && defer) le = ws_malloc(&dn, (size_t)nq * dparts * 4, s);
       if (le != cudaSuccess) {
         set_error(std::string("workspace: ") + cudaGetErrorString(le));
         st = RAIRS_E_OOM;
@@ -338,7 +339,8 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
         ex.defer_buf = dbuf;
         ex.defer_n = dn;
         st = launch_fastscan(idx, a, s, ex);
-        nk += (defer ? 2 : 1) + (fastscan_order_on() && nq > 1 ? 1 : 0);  // + LUT (+ finish) (+ order)
+        nk += (defer ? 2 : 1) + (dparts > 1 && defer ? 1 : 0) +
+              (fastscan_order_on() && nq > 1 && dparts == 1 ? 1 : 0);  // + LUT (+ finish) (+ merge) (+ order)
       }
       cudaFreeAsync(luts, s);
       cudaFreeAsync(dbuf, s);

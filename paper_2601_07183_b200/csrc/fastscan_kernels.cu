@@ -67,15 +67,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(addr));
-  return v;
-}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -155,6 +147,8 @@ struct FsArgs {
   const uint32_t* p_ref_cnt;
   int o_rl;                    // warp smem: misc list of each range (paper)
   const uint32_t* order;       // claim order of the queries (heavy first) or null
+  int parts;                   // work items per query (small batches: the query's group
+                               // tasks split into `parts` equal intervals, one warp each)
   const uint32_t* list_items;  // N_l for the cost estimate (or own_cnt)
   uint64_t cost_thr;           // a query is heavy when cost * nlist > cost_thr
   int nlist;
@@ -638,6 +632,38 @@ __global__ void fs_order_kernel(const __grid_constant__ FsArgs a, uint32_t* orde
   pdl_trigger();
 }
 
+// Split mode: query q's P parts each left their exact top-bigK keys, sorted
+// (resolved (s, id) keys: unique); one warp per query merges them -- bigK
+// rounds of a warp-wide minimum over the P list heads (P <= 64: lanes hold
+// the heads of parts lane and lane + 32).
+__global__ void __launch_bounds__(256) fs_merge_parts_kernel(const uint64_t* __restrict__ part_keys, int P,
+                                                              int bigK, int64_t nq, uint64_t* __restrict__ out_keys) {
+  const int lane = lane_id();
+  const int64_t q = (int64_t)blockIdx.x * 8 + warp_id();
+  pdl_wait();  // the parts' finish kernel
+  if (q >= nq) return;
+  const uint64_t* base = part_keys + (size_t)q * P * bigK;
+  int i0 = 0, i1 = 0;
+  uint64_t h0 = lane < P ? base[(size_t)lane * bigK] : kKeyInf;
+  uint64_t h1 = lane + 32 < P ? base[(size_t)(lane + 32) * bigK] : kKeyInf;
+  for (int i = 0; i < bigK; ++i) {
+    uint64_t m = h0 < h1 ? h0 : h1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(0xffffffffu, m, o);
+      m = x < m ? x : m;
+    }
+    if (lane == 0) out_keys[q * bigK + i] = m;
+    if (m == kKeyInf) continue;
+    if (h0 == m) {
+      h0 = ++i0 < bigK ? base[(size_t)lane * bigK + i0] : kKeyInf;
+    } else if (h1 == m) {
+      h1 = ++i1 < bigK ? base[(size_t)(lane + 32) * bigK + i1] : kKeyInf;
+    }
+  }
+  pdl_trigger();
+}
+
 // A3 for every query of the batch, one warp per query (O2: lane per
 // subquantizer, fp32 RN, ascending t; see build_lut in lut_common.cuh), into luts[q][M_pad].
 // Needs only the queries, so under programmatic dependent launch it overlaps
@@ -703,7 +729,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     qq = __shfl_sync(0xffffffffu, qq, 0);
     // a query subset (a.qlist / *a.qcount: the list-major path's overflowed
     // queries) or every query
-    if (a.qlist ? qq >= *a.qcount : qq >= (uint64_t)a.nq) break;
+    const uint32_t P = (uint32_t)a.parts;
+    if (a.qlist ? qq >= *a.qcount : qq >= (uint64_t)a.nq * P) break;
+    const uint32_t part = P > 1 ? qq % P : 0u;
+    if (P > 1) qq /= P;  // split mode: no query subset, no claim order
     const int64_t q = a.qlist ? (int64_t)a.qlist[qq] : a.order ? (int64_t)a.order[qq] : (int64_t)qq;
     const int32_t* pq = a.probes + q * a.pstride;
 
@@ -744,13 +773,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     // misc areas), then the probed lists' references
     const uint32_t npb = a.paper ? 2u * (uint32_t)np : (uint32_t)np;
     const uint32_t nsrc = npb + nrefs;
-    uint32_t s0 = 0;
-    for (;;) {
-      // (1) a batch of ranges: s < np -> owned range of probe s; else reference s - np
-      uint32_t nr = 0;
-      while (s0 < nsrc && nr <= FS_RCAP - 32) {
-        const uint32_t s = s0 + lane;
-        uint32_t st0 = 0, cnt = 0, ml = 0xFFFFFFFFu;
+    // the slot range of source s (empty when it does not exist or R9 skips it)
+    auto source = [&](uint32_t s, uint32_t& st0, uint32_t& cnt, uint32_t& ml) {
+        st0 = 0;
+        cnt = 0;
+        ml = 0xFFFFFFFFu;
         if (s < npb) {
           const bool misc = s >= (uint32_t)np;  // paper layout only
           const int l = __ldg(pq + (misc ? s - (uint32_t)np : s));
@@ -779,6 +806,32 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
             cnt = __ldg((a.paper ? a.p_ref_cnt : a.ref_cnt) + j);
           }
         }
+    };
+    // split mode: the query's total group tasks G (this part takes
+    // [part G / P, (part + 1) G / P)) and items (part 0 reports the DCO)
+    uint64_t g_lo = 0, g_hi = ~0ull;
+    if (P > 1) {
+      uint64_t G = 0, I = 0;
+      for (uint32_t sb = 0; sb < nsrc; sb += 32) {
+        uint32_t st0, cnt, ml;
+        source(sb + lane, st0, cnt, ml);
+        const uint32_t g = cnt ? ((st0 + cnt - 1) >> 3) - (st0 >> 3) + 1 : 0u;
+        G += __reduce_add_sync(0xffffffffu, g);
+        I += __reduce_add_sync(0xffffffffu, cnt);
+      }
+      g_lo = (uint64_t)part * G / P;
+      g_hi = (uint64_t)(part + 1) * G / P;
+      if (part == 0 && lane == 0) my_dco = (uint32_t)I;  // summed over lanes below
+    }
+    uint64_t g_base = 0;  // global task index of the batch's first task
+    uint32_t s0 = 0;
+    for (;;) {
+      // (1) a batch of ranges: s < np -> owned range of probe s; else reference s - np
+      uint32_t nr = 0;
+      while (s0 < nsrc && nr <= FS_RCAP - 32) {
+        const uint32_t s = s0 + lane;
+        uint32_t st0, cnt, ml;
+        source(s, st0, cnt, ml);
         const bool has = cnt > 0;
         const unsigned bal = __ballot_sync(0xffffffffu, has);
         if (has) {
@@ -800,7 +853,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
         if (r < nr) {
           const uint32_t sr = rs[r], c = rc[r];
           g = ((sr + c - 1) >> 3) - (sr >> 3) + 1;
-          my_dco += c;
+          if (P == 1) my_dco += c;
         }
         const uint32_t inc = warp_incl_scan(g);
         if (r < nr) rg[r] = ng_tot + inc - g;
@@ -808,11 +861,28 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
       }
       if (lane == 0) rg[nr] = ng_tot;
       __syncwarp();
-      // (3) rounds of 32 * GPL groups: lane tasks t0 + 32 g + lane, g < GPL
+      // (3) rounds of 32 * GPL groups: lane tasks t0 + 32 g + lane, g < GPL, over
+      // the batch's tasks [t_beg, t_end) (split mode: this part's interval)
+      uint32_t t_beg = 0, t_end = ng_tot;
+      if (P > 1) {
+        const uint64_t b0 = g_base, b1 = g_base + ng_tot;
+        t_beg = (uint32_t)(min(max(g_lo, b0), b1) - b0);
+        t_end = (uint32_t)(min(max(g_hi, b0), b1) - b0);
+      }
+      g_base += ng_tot;
+      if (t_beg >= t_end) {
+        __syncwarp();
+        continue;
+      }
       uint32_t r_lo = 0;  // range holding the first task of the next round to map
+      if (t_beg > 0) {    // the range holding t_beg: ranges with rg[r] <= t_beg, minus one
+        uint32_t c = 0;
+        for (uint32_t r = lane; r < nr; r += 32) c += rg[r] <= t_beg ? 1u : 0u;
+        r_lo = __reduce_add_sync(0xffffffffu, c) - 1u;
+      }
       FsTask A[GPL];
 #pragma unroll
-      for (int g = 0; g < GPL; ++g) A[g] = fs_round_task(32u * g, r_lo, ng_tot, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
+      for (int g = 0; g < GPL; ++g) A[g] = fs_round_task(t_beg + 32u * g, r_lo, t_end, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
       // per group a ring of D loop-carried chunk slots (chunk c in slot c % D),
       // each refilled right after it is consumed with the chunk D ahead (past
       // the group's end: chunk c % D of the lane's next-round group), so the
@@ -823,11 +893,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
       for (int g = 0; g < GPL; ++g)
 #pragma unroll
         for (int s = 0; s < D; ++s) R[g][s] = ldg_nc_v4(A[g].gp + s * 64);
-      for (uint32_t t0 = 0; t0 < ((dbg & 1) ? 0u : ng_tot); t0 += 32u * GPL) {
+      for (uint32_t t0 = t_beg; t0 < ((dbg & 1) ? 0u : t_end); t0 += 32u * GPL) {
         FsTask nA[GPL];
 #pragma unroll
         for (int g = 0; g < GPL; ++g)
-          nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, ng_tot, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
+          nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, t_end, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
         uint32_t acc[GPL][8];
 #pragma unroll
         for (int g = 0; g < GPL; ++g)
@@ -939,7 +1009,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
     if (a.defer_buf) {
       // only entries that can still be in the top-bigK (s <= the final bound;
       // resolved keys in exact mode are all kept)
-      uint64_t* dst = a.defer_buf + (size_t)q * cap;
+      const size_t item = P > 1 ? (size_t)q * P + part : (size_t)q;
+      uint64_t* dst = a.defer_buf + item * cap;
       const uint32_t lim = st.exact ? 0xFFFFFFFFu
                                     : min(st.tau, st.bthr >= (0xFFFFFFFFu >> hsh) ? 0xFFFFFFFFu
                                                                                  : ((st.bthr + 1u) << hsh) - 1u);
@@ -956,8 +1027,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) my_dco += __shfl_xor_sync(0xffffffffu, my_dco, o);
       if (lane == 0) {
-        a.defer_n[q] = st.n | (st.exact ? 0x80000000u : 0u);
-        if (a.dco) a.dco[q] = (int64_t)my_dco;
+        a.defer_n[item] = st.n | (st.exact ? 0x80000000u : 0u);
+        if (a.dco && (P == 1 || part == 0)) a.dco[q] = (int64_t)my_dco;
         if (a.dco_total) atomicAdd(a.dco_total, (unsigned long long)my_dco);
       }
       __syncwarp();
@@ -1087,6 +1158,7 @@ struct FsPlan {
 static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, const FsExtra& ex, FsPlan& pl) {
   FsArgs& p = pl.a;
   p = FsArgs{};
+  p.parts = 1;
   p.codes = idx->codes_g;
   p.slot_rows = idx->slot_rows;
   if (idx->seil_layout != 0) {
@@ -1186,7 +1258,7 @@ static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
   RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB, GPL, NW>,
                                                                pl.warps * 32, pl.smem));
   per_sm = std::max(per_sm, 1);
-  const int64_t need = ceil_div(pl.a.nq, pl.warps);
+  const int64_t need = ceil_div(pl.a.nq * std::max(pl.a.parts, 1), pl.warps);  // work items
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148LL * per_sm));
   pl.a.total_warps = grid * (unsigned)pl.warps;
   RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB, GPL, NW>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
@@ -1217,7 +1289,11 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     RAIRS_CUDA_TRY(launch_pdl(fs_lut_kernel, dim3(g), dim3(FL_WARPS * 32), lsm, s, pl.a,
                               const_cast<uint4*>(sa.luts)));
   }
-  const bool use_order = fastscan_order_on();
+  // small batches: each query's group tasks split over several warps
+  const int P = (!ex.qlist && !ex.tau_out && ex.defer_buf) ? fastscan_parts(idx, sa.nq, sa.nprobe) : 1;
+  pl.a.parts = P;
+  if (P > 1 && sa.dco) RAIRS_CUDA_TRY(cudaMemsetAsync(sa.dco, 0, (size_t)sa.nq * 8, s));
+  const bool use_order = fastscan_order_on() && P == 1;
   uint32_t* order = nullptr;
   struct OrderFree {
     uint32_t*& p;
@@ -1251,10 +1327,40 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     const size_t fsm = (size_t)nw * per;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)fsm));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, nw), 148 * 8));
-    RAIRS_CUDA_TRY(launch_pdl(fs_finish_kernel, dim3(g), dim3(nw * 32), fsm, s, pl.a));
+    FsArgs fa = pl.a;  // split mode: one finish per (query, part), sorted, then a merge
+    uint64_t* part_keys = nullptr;
+    if (P > 1) {
+      RAIRS_CUDA_TRY(ws_malloc(&part_keys, (size_t)sa.nq * P * pl.a.bigK * 8, s));
+      fa.nq = sa.nq * P;
+      fa.out_keys = part_keys;
+      fa.sorted_out = 1;
+    }
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(fa.nq, nw), 148 * 8));
+    RAIRS_CUDA_TRY(launch_pdl(fs_finish_kernel, dim3(g), dim3(nw * 32), fsm, s, fa));
+    if (P > 1) {
+      const cudaError_t le = launch_pdl(fs_merge_parts_kernel, dim3((unsigned)ceil_div(sa.nq, 8)), dim3(256), 0, s,
+                                        (const uint64_t*)part_keys, P, pl.a.bigK, sa.nq, pl.a.out_keys);
+      cudaFreeAsync(part_keys, s);
+      RAIRS_CUDA_TRY(le);
+    }
   }
   return RAIRS_OK;
+}
+
+// Work items per query of the query-major scan: a small batch whose queries
+// each score many items (c5 at nprobe 64: ~150k) splits each query's group
+// tasks over P warps, P ~ expected items / 4k (each part then finds its own
+// top-bigK: P x the selection work, so only when the scan work dominates),
+// capped at 64 and at the resident warps; RAIRS_FS_PARTS overrides.
+int fastscan_parts(const rairs_index_s* idx, int64_t nq, int nprobe) {
+  if (const char* e = std::getenv("RAIRS_FS_PARTS"))  // read per search (tests force split mode)
+    return std::max(1, std::min(64, std::atoi(e)));
+  constexpr int64_t kWarps = 148 * 16;  // resident scan warps (2 CTAs x 8 warps per SM)
+  if (nq <= 0 || nq * 2 > kWarps || idx->nlist <= 0) return 1;
+  const double items = (double)nprobe *
+                       ((double)(idx->list_items ? idx->sum_list_items : idx->n_live) / idx->nlist);
+  const int64_t p = std::min<int64_t>({64, kWarps / nq, (int64_t)(items / 4096.0)});
+  return (int)std::max<int64_t>(1, p);
 }
 
 // longest-first claim order for the scan (RAIRS_FS_ORDER=0: batch order)

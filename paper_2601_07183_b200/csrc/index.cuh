@@ -251,6 +251,7 @@ struct FsExtra {
   uint32_t* defer_n = nullptr;        // [nq]
 };
 bool fastscan_order_on();
+int fastscan_parts(const rairs_index_s* idx, int64_t nq, int nprobe);  // work items per query (defer buffers: nq x parts)
 // paper-literal SEIL layout (seil_paper.cu)
 rairs_status seil_paper_prepare(rairs_index_s* idx, cudaStream_t s);
 void seil_paper_free(rairs_index_s* idx);

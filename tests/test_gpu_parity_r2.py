@@ -22,7 +22,7 @@ import torch  # noqa: E402
 
 import paper_2601_07183_b200 as rb  # noqa: E402
 from synth import get_config, make_dataset  # noqa: E402
-from tests.test_gpu_parity import DEV, _t, assert_search_equal, gpu_search  # noqa: E402
+from tests.test_gpu_parity import DEV, _t, assert_search_equal, case, gpu_search  # noqa: E402
 
 
 def _oracle_index(oracle, X, nlist, M, seed=11):
@@ -209,3 +209,23 @@ def test_c5_full_size_sampled(oracle_mod):
     capped-list coarse path with its uncertified rows, the scan of one 10k batch
     (~98k items per query), refine; 16 queries and 5,000 rows checked."""
     _full_size_sampled(oracle_mod, "c5", 64, "auto", n_q=16, n_rows=5000, n_assign=2000)
+
+
+@pytest.mark.parametrize("parts", [2, 7, 64])
+@pytest.mark.parametrize("nq", [1, 5, 100])
+def test_split_query_parts_equal_oracle(oracle_mod, parts, nq):
+    """Small-batch split mode of the query-major scan (each query's group tasks
+    over `parts` warps, per-part exact top-bigK, then a P-way merge): the same
+    candidates, DCO and results as the oracle (RAIRS_FS_PARTS forces P)."""
+    import os
+    c = case(oracle_mod, "c1s")
+    idx = c.gpu_index()
+    Q = c.Q[:nq]
+    o = oracle_mod.search(c.X, c.l1, c.l2, c.codes, c.cent, c.cb, Q, 10, 16, 10)
+    os.environ["RAIRS_FS_PARTS"] = str(parts)
+    try:
+        g = gpu_search(idx, Q, 10, 16, 10, "simt")
+    finally:
+        del os.environ["RAIRS_FS_PARTS"]
+    assert_search_equal(g, o)
+    idx.free()
