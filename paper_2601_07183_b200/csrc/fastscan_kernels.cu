@@ -371,10 +371,10 @@ __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uin
 
 // the final top-bigK of one query's buffer (cold: one copy, not inlined)
 __device__ __noinline__ uint32_t fs_finish(const FsArgs& a, uint64_t* cand, uint32_t* hist, uint32_t n,
-                                           bool exact, int hsh) {
+                                           bool exact, int hsh, uint32_t cap) {
   const int lane = lane_id();
   const unsigned below_me = (1u << lane) - 1u;
-  const uint32_t bigK = (uint32_t)a.bigK, cap = (uint32_t)a.cap;
+  const uint32_t bigK = (uint32_t)a.bigK;
   uint32_t keep = n;
   if (exact) {
     for (uint32_t i = n + lane; i < cap; i += 32) cand[i] = kKeyInf;
@@ -585,12 +585,16 @@ __device__ __forceinline__ uint32_t fs_prefix16(uint32_t c, unsigned below_me, u
 // massive-tie mode): histogram of its scores, then fs_finish (exact bigK-th
 // score, ids, ties by id).  Runs at high occupancy, apart from the lookups.
 constexpr int FF_WARPS = 8;
+constexpr uint32_t FF_CAPS = 512;  // shared-memory entries per warp (a buffer of up to `cap`
+                                   // is cut to its bin threshold first; more: in global memory)
 __global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(const __grid_constant__ FsArgs a) {
   extern __shared__ __align__(16) uint8_t ff_smem[];
   const int lane = lane_id(), warp = warp_id();
+  const unsigned below_me = (1u << lane) - 1u;
   const uint32_t cap = (uint32_t)a.cap, bigK = (uint32_t)a.bigK;
-  uint64_t* cand = reinterpret_cast<uint64_t*>(ff_smem + (size_t)warp * (cap * 8 + 1024));
-  uint32_t* hist = reinterpret_cast<uint32_t*>(cand + cap);
+  const uint32_t caps = min(cap, FF_CAPS);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(ff_smem + (size_t)warp * (caps * 8 + 1024));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(cand + caps);
   const int hsh = a.hbits > 8 ? a.hbits - 8 : 0;
   pdl_wait();  // the scan kernel's buffers
   const int nw = blockDim.x >> 5;
@@ -598,17 +602,51 @@ __global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(const __grid_c
     const uint32_t nx = a.defer_n[q];
     const uint32_t n = nx & 0x7FFFFFFFu;
     const bool exact = (nx >> 31) != 0;
-    const uint64_t* src = a.defer_buf + (size_t)q * cap;
+    uint64_t* src = a.defer_buf + (size_t)q * cap;
     for (int i = lane; i < 256; i += 32) hist[i] = 0u;
     __syncwarp();
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint64_t v = src[i];
-      cand[i] = v;
-      if (!exact) atomicAdd(&hist[(uint32_t)(v >> 32) >> hsh], 1u);
+    uint64_t* buf = cand;  // where fs_finish works: shared memory, or the global buffer itself
+    uint32_t m = n, bcap = caps;
+    if (exact) {
+      if (n <= caps) {
+        for (uint32_t i = lane; i < n; i += 32) cand[i] = src[i];
+      } else {
+        buf = src;
+        bcap = cap;
+      }
+    } else {
+      for (uint32_t i = lane; i < n; i += 32) atomicAdd(&hist[(uint32_t)(src[i] >> 32) >> hsh], 1u);
+      __syncwarp();
+      if (n <= caps) {
+        for (uint32_t i = lane; i < n; i += 32) cand[i] = src[i];
+      } else {
+        // keep the entries whose bin is at most the bin of the bigK-th score
+        uint32_t bl;
+        const uint32_t bs = fs_bsel256(hist, bigK, &bl);
+        uint32_t cnt = 0;
+        for (uint32_t i = lane; i < n; i += 32) cnt += ((uint32_t)(src[i] >> 32) >> hsh) <= bs ? 1u : 0u;
+        m = __reduce_add_sync(0xffffffffu, cnt);
+        uint64_t* dst = cand;
+        if (m > caps) {  // rare (a wide bin): compact in place in the global buffer
+          dst = src;
+          bcap = cap;
+        }
+        uint32_t out = 0;
+        for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          const uint64_t v = i < n ? src[i] : kKeyInf;
+          const bool k = i < n && ((uint32_t)(v >> 32) >> hsh) <= bs;
+          const unsigned bal = __ballot_sync(0xffffffffu, k);
+          __syncwarp();
+          if (k) dst[out + __popc(bal & below_me)] = v;
+          out += __popc(bal);
+        }
+        buf = dst;
+      }
     }
     __syncwarp();
-    const uint32_t keep = fs_finish(a, cand, hist, n, exact, hsh);
-    for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? cand[i] : kKeyInf;
+    const uint32_t keep = fs_finish(a, buf, hist, m, exact, hsh, bcap);
+    for (uint32_t i = lane; i < bigK; i += 32) a.out_keys[q * bigK + i] = i < keep ? buf[i] : kKeyInf;
     __syncwarp();
   }
   pdl_trigger();
@@ -1034,7 +1072,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
       __syncwarp();
       continue;
     }
-    const uint32_t keep = (dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh);
+    const uint32_t keep = (dbg & 4) ? 0u : fs_finish(a, cand, hist, st.n, st.exact != 0, hsh, cap);
     if (a.tau_out) {  // threshold mode: the bigK-th smallest score (an upper bound, see FsArgs)
       uint32_t mx = 0;
       for (uint32_t i = lane; i < keep; i += 32) mx = max(mx, (uint32_t)(cand[i] >> 32));
@@ -1322,7 +1360,7 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     *sa.kev_used = true;
   }
   if (pl.a.defer_buf) {
-    const size_t per = (size_t)pl.a.cap * 8 + 1024;
+    const size_t per = (size_t)std::min<uint32_t>((uint32_t)pl.a.cap, FF_CAPS) * 8 + 1024;
     const int nw = (int)std::max<size_t>(1, std::min<size_t>(FF_WARPS, (200 * 1024) / per));
     const size_t fsm = (size_t)nw * per;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
