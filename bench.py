@@ -184,7 +184,7 @@ def build_workload(args, rank, world, dev):
                                 assignment=args.assignment, **kw)
         idx = sh.local
         del Xtrain
-    # SEIL list layout searched (auto: the paper-literal one for query-major scans)
+    # SEIL list layout searched (default hybrid: cell-major + copies of the tiny cross cells)
     idx.set_seil_layout(args.seil_layout)
     torch.cuda.synchronize()
     build_s = time.time() - t0
@@ -478,7 +478,9 @@ def run_ours(args):
                        "nprobe": chosen,
                        "assignment": args.assignment + "+SEIL(" + {"cell": "cell-major", "paper": "paper-literal",
                                                                  "auto": "paper-literal for query-major, "
-                                                                         "cell-major for list-major"}[args.seil_layout] + ")",
+                                                                         "cell-major for list-major",
+                                                                 "hybrid": "hybrid: cell-major + copies of "
+                                                                           "cross cells below 8 items"}[args.seil_layout] + ")",
                        "parallelism": f"index sharded id mod {world}" if world > 1 else "1 GPU",
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
             "recall%d@%d" % (k, k): round(recall, 4), "recall_sweep": sweep,
@@ -613,45 +615,50 @@ def side_k1(idx, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream, steps):
 
 def side_seil_layouts(idx, main_layout, Qd, k, nprobe, rf, gt_ids, gt_d64, nq_gt, flush, stream, steps,
                       dco_main, qps_main):
-    """The same index over the other SEIL list layout (NEXT-2): cell-major (R10:
-    every vector stored once, remainders in the owner's cell, short references)
-    vs the paper-literal one (Alg. 4/5: shared 32-item blocks stored once,
-    remainders duplicated into both lists' misc areas); same candidates,
-    recall, DCO per query and QPS under the main line's protocol (device
-    events, L2 flushed between steps)."""
+    """The same index over the other SEIL list layouts (NEXT-2): cell-major (R10:
+    every vector stored once, remainders in the owner's cell, short references),
+    the paper-literal one (Alg. 4/5: shared 32-item blocks stored once,
+    remainders duplicated into both lists' misc areas) and the hybrid one
+    (cell-major ranges + copies of the cross cells below 8 items); same
+    candidates and recall; DCO per query and QPS under the main line's
+    protocol (device events, L2 flushed between steps)."""
     import torch
-    main_name = "paper" if (main_layout != "cell" and idx.scan_path(Qd.shape[0], k, nprobe, rf) == "simt") \
-        else "cell"
-    other = "cell" if main_name == "paper" else "paper"
-    bytes0 = idx.info()["device_bytes"]
-    idx.set_seil_layout(other)
-    extra = idx.info()["device_bytes"] - bytes0
-    try:
-        ids, dists, dco = idx.search(Qd, k, nprobe, rf, return_dco=True)
-        rec = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], k)
-        for _ in range(3):
-            idx.search(Qd, k, nprobe, rf)
-        t = 0.0
-        for _ in range(steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            idx.search(Qd, k, nprobe, rf)
-            e1.record(stream)
-            e1.synchronize()
-            t += e0.elapsed_time(e1)
-    finally:
-        idx.set_seil_layout(main_layout)
+    simt = idx.scan_path(Qd.shape[0], k, nprobe, rf) == "simt"
+    main_name = {"cell": "cell", "paper": "paper", "auto": "paper", "hybrid": "hybrid"}[main_layout] \
+        if simt else "cell"
     nq = Qd.shape[0]
-    res = {main_name: {"qps": round(qps_main, 1), "dco_per_query": round(dco_main, 1), "main_line": True},
-           other: {"qps": round(nq * steps / (t / 1e3), 1), "dco_per_query": round(float(dco.sum().item()) / nq, 1),
-                   "recall": round(rec, 4), "main_line": False}}
+    res = {main_name: {"qps": round(qps_main, 1), "dco_per_query": round(dco_main, 1), "main_line": True}}
+    for other in ("cell", "paper", "hybrid"):
+        if other == main_name:
+            continue
+        bytes0 = idx.info()["device_bytes"]
+        idx.set_seil_layout(other)
+        extra = idx.info()["device_bytes"] - bytes0
+        try:
+            ids, dists, dco = idx.search(Qd, k, nprobe, rf, return_dco=True)
+            rec = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], k)
+            for _ in range(3):
+                idx.search(Qd, k, nprobe, rf)
+            t = 0.0
+            for _ in range(steps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                idx.search(Qd, k, nprobe, rf)
+                e1.record(stream)
+                e1.synchronize()
+                t += e0.elapsed_time(e1)
+        finally:
+            idx.set_seil_layout(main_layout)
+        res[other] = {"qps": round(nq * steps / (t / 1e3), 1),
+                      "dco_per_query": round(float(dco.sum().item()) / nq, 1),
+                      "recall": round(rec, 4), "main_line": False, "device_bytes_delta_of_switch": int(extra)}
     res["nprobe"] = nprobe
     res["scan_path"] = idx.scan_path(Qd.shape[0], k, nprobe, rf)
-    res["dco_ratio_paper_over_cell"] = round(res["paper"]["dco_per_query"] / max(1.0, res["cell"]["dco_per_query"]), 4)
-    res["qps_ratio_paper_over_cell"] = round(res["paper"]["qps"] / max(1.0, res["cell"]["qps"]), 4)
-    res["device_bytes_delta_of_switch"] = int(extra)
+    for o in ("paper", "hybrid"):
+        res[f"dco_ratio_{o}_over_cell"] = round(res[o]["dco_per_query"] / max(1.0, res["cell"]["dco_per_query"]), 4)
+        res[f"qps_ratio_{o}_over_cell"] = round(res[o]["qps"] / max(1.0, res["cell"]["qps"]), 4)
     return res
 
 
@@ -874,13 +881,14 @@ def main():
                     help="queries with exact ground truth for recall (0 = all)")
     ap.add_argument("--k1", type=int, default=1,
                     help="side line: the same index at k=1 (BJ configs[3]: k=1 and k=10)")
-    ap.add_argument("--seil-layout", default="cell", choices=["cell", "paper", "auto"],
+    ap.add_argument("--seil-layout", default="hybrid", choices=["cell", "paper", "auto", "hybrid"],
                     help="SEIL list layout searched (rairs_set_seil_layout): cell-major (R10), "
                          "paper-literal (Alg. 4/5), or auto = paper-literal for query-major scans, "
-                         "cell-major for list-major. The other layout is measured in seil_layouts.")
+                         "cell-major for list-major, or hybrid (cell-major + copies of cross cells "
+                         "below 8 items). The other layouts are measured in seil_layouts.")
     ap.add_argument("--seil-paper", type=int, default=1,
-                    help="side line: the same index searched over the paper-literal SEIL layout "
-                         "(Alg. 4/5; misc remainders duplicated) at the chosen nprobe")
+                    help="side line: the same index searched over the other SEIL layouts "
+                         "(cell-major, paper-literal Alg. 4/5, hybrid) at the chosen nprobe")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

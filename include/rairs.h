@@ -283,7 +283,14 @@ rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode);
  * (its remainders sit in contiguous misc areas instead of many short
  * references, so fewer partially filled 8-item groups are scanned: c4 scan
  * -6 %), list-major scans (rairs_set_scan_mode) the cell-major one.
- * Errors: RAIRS_E_INVALID (NULL index, layout not 0/1/2), RAIRS_E_OOM,
+ * 3 = hybrid (not in the paper; same results, U(q) of R9): query-major scans
+ * read, per list, its cell-major owned range followed by copies of the cross
+ * cells (i < l, l) with fewer than 8 items (one nibble group), each dropped
+ * after scoring when its owner i was probed (RemoveVectorIfVisited, Alg. 5
+ * line 16); larger cells stay references.  DCO = the cell-major DCO + the
+ * copied items whose owner was also probed.  List-major scans read the
+ * cell-major layout.
+ * Errors: RAIRS_E_INVALID (NULL index, layout not 0..3), RAIRS_E_OOM,
  * RAIRS_E_CUDA. */
 rairs_status rairs_set_seil_layout(rairs_index_t idx, int32_t layout);
 

@@ -963,18 +963,24 @@ rairs_status rairs_set_scan_mode(rairs_index_t idx, int32_t mode) {
 
 rairs_status rairs_set_seil_layout(rairs_index_t idx, int32_t layout) {
   if (!idx) return invalid("index is NULL");
-  if (layout < 0 || layout > 2)
-    return invalid("SEIL layout must be 0 (cell-major), 1 (paper-literal) or 2 (paper-literal for query-major scans)");
-  if (layout != 0 && !idx->p_codes_g) {
+  if (layout < 0 || layout > 3)
+    return invalid("SEIL layout must be 0 (cell-major), 1 (paper-literal), 2 (paper-literal for query-major "
+                   "scans) or 3 (hybrid for query-major scans)");
+  const int kind = layout == 3 ? 3 : 1;
+  const int prev = idx->seil_layout;
+  idx->seil_layout = layout;
+  if (layout != 0 && (!idx->p_codes_g || idx->p_kind != kind)) {
     cudaStream_t s = nullptr;
     RAIRS_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     RAIRS_CUDA_TRY(cudaDeviceSynchronize());
     const rairs_status st = seil_paper_prepare(idx, s);
     cudaStreamDestroy(s);
-    RAIRS_TRY(st);
+    if (st != RAIRS_OK) {
+      idx->seil_layout = idx->p_codes_g ? prev : 0;
+      return st;
+    }
   }
   if (layout == 0) seil_paper_free(idx);
-  idx->seil_layout = layout;
   return RAIRS_OK;
 }
 

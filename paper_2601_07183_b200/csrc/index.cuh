@@ -90,7 +90,12 @@ struct rairs_index_s {
   // p_ref_start / p_ref_cnt: the shared blocks each reference (ref_ptr /
   // ref_owner order) points at.  seil_layout 1 = searches use it (query-major
   // only), 2 = query-major searches use it, list-major ones the cell-major layout.
+  // 3 = the hybrid layout in the same arrays (seil_paper.cu): each list's
+  // cell-major owned range unchanged, then misc copies of the cross cells
+  // (i < l, l) smaller than one 8-item group; larger cells stay references.
+  // p_kind = the layout the p_* arrays hold (1 paper-literal, 3 hybrid).
   int seil_layout = 0;
+  int p_kind = 0;
   uint8_t* p_codes_g = nullptr;
   uint32_t* p_slot_rows = nullptr;
   uint32_t* p_other = nullptr;

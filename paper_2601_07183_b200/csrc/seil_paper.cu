@@ -23,6 +23,7 @@
 // smaller than its list.  The scanned item count is the paper's
 // DCO_paperSEIL (oracle O12); the candidates equal the cell-major ones.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -30,6 +31,12 @@
 namespace rairs {
 
 constexpr uint32_t kNoOther = 0xFFFFFFFFu;
+// hybrid layout: cells below one 8-item group are copied (RAIRS_SEIL_TINY
+// overrides it, for measurement)
+static uint32_t seil_tiny() {
+  const char* e = getenv("RAIRS_SEIL_TINY");
+  return e ? (uint32_t)std::max(0, atoi(e)) : 8u;
+}
 
 static inline unsigned sp_grid(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 32));
@@ -74,6 +81,7 @@ void seil_paper_free(rairs_index_s* idx) {
   idx->device_bytes -= idx->p_bytes;
   idx->p_bytes = 0;
   idx->p_slots = 0;
+  idx->p_kind = 0;
 }
 
 rairs_status seil_paper_prepare(rairs_index_s* idx, cudaStream_t s) {
@@ -115,58 +123,115 @@ rairs_status seil_paper_prepare(rairs_index_s* idx, cudaStream_t s) {
       p = q;
     }
   }
-  // regions (line 16): 32-aligned, [shared][misc own][misc copies]
+  const bool hybrid = idx->seil_layout == 3;
+  const uint32_t kTiny = seil_tiny();
   std::vector<uint32_t> p_off(nlist), p_shared(nlist), p_misc(nlist);
-  int64_t off = 0;
-  for (int l = 0; l < nlist; ++l) {
-    p_off[l] = (uint32_t)off;
-    p_shared[l] = (uint32_t)shared[l];
-    p_misc[l] = (uint32_t)(misc_own[l] + misc_copy[l]);
-    off += round_up(shared[l] + misc_own[l] + misc_copy[l], 32);
-  }
-  if (off >= (int64_t)0xFFFFFFFFll) {
-    set_error("paper SEIL layout: slot count exceeds 2^32");
-    return RAIRS_E_UNSUPPORTED;
-  }
-  const int64_t p_slots = std::max<int64_t>(off, 32);
-  std::vector<uint32_t> map((size_t)p_slots, kNoOther), other((size_t)p_slots, kNoOther);
-  std::vector<uint32_t> sh(nlist), mo(nlist), mc(nlist);
-  for (int l = 0; l < nlist; ++l) {
-    sh[l] = p_off[l];
-    mo[l] = p_off[l] + p_shared[l];
-    mc[l] = (uint32_t)(p_off[l] + p_shared[l] + misc_own[l]);
-  }
-  // shared-block start of every cell (the references' bptr), by cell-major start
-  std::vector<uint32_t> cell_start((size_t)cells.size()), cell_bptr((size_t)cells.size()),
-      cell_full((size_t)cells.size());
-  for (size_t c = 0; c < cells.size(); ++c) {  // lines 17-32
-    const Cell& x = cells[c];
-    const uint32_t full = 32 * (x.n / 32);
-    cell_start[c] = x.start;
-    cell_bptr[c] = sh[x.l];
-    cell_full[c] = full;
-    for (uint32_t p = 0; p < full; ++p) map[sh[x.l]++] = x.start + p;  // shared blocks
-    for (uint32_t p = full; p < x.n; ++p) {                            // misc, both lists
-      map[mo[x.l]] = x.start + p;
-      other[mo[x.l]++] = x.j;
-      if (x.j != x.l) {
-        map[mc[x.j]] = x.start + p;
-        other[mc[x.j]++] = x.l;
+  std::vector<uint32_t> map, other;
+  std::vector<uint32_t> p_ref_start((size_t)std::max<int64_t>(nr, 1), 0), p_ref_cnt((size_t)std::max<int64_t>(nr, 1), 0);
+  int64_t p_slots = 0;
+  if (hybrid) {
+    // hybrid: per list l, [its cell-major owned range, unchanged][misc: copies
+    // of the cross cells (i < l, l) with n < kTiny items, ascending i].  A
+    // copy is dropped when its owner i was probed (fs_paper_drop: i < l
+    // always), so U(q) is the cell-major one; the larger cells stay references.
+    std::vector<int64_t> copies(nlist, 0);
+    for (const Cell& x : cells)
+      if (x.j != x.l && x.n < kTiny) copies[x.j] += x.n;
+    int64_t off = 0;
+    for (int l = 0; l < nlist; ++l) {
+      p_off[l] = (uint32_t)off;
+      p_shared[l] = own_cnt[l];
+      p_misc[l] = (uint32_t)copies[l];
+      off += round_up((int64_t)own_cnt[l] + copies[l], 32);
+    }
+    if (off >= (int64_t)0xFFFFFFFFll) {
+      set_error("hybrid SEIL layout: slot count exceeds 2^32");
+      return RAIRS_E_UNSUPPORTED;
+    }
+    p_slots = std::max<int64_t>(off, 32);
+    map.assign((size_t)p_slots, kNoOther);
+    other.assign((size_t)p_slots, kNoOther);
+    std::vector<uint32_t> mc(nlist);
+    for (int l = 0; l < nlist; ++l) {
+      mc[l] = p_off[l] + own_cnt[l];
+      for (uint32_t t = 0; t < own_cnt[l]; ++t) map[p_off[l] + t] = own_off[l] + t;
+    }
+    std::vector<uint32_t> cell_start((size_t)cells.size()), cell_pos((size_t)cells.size()),
+        cell_n((size_t)cells.size());
+    for (size_t c = 0; c < cells.size(); ++c) {
+      const Cell& x = cells[c];
+      cell_start[c] = x.start;
+      cell_pos[c] = p_off[x.l] + (x.start - own_off[x.l]);
+      cell_n[c] = x.n;
+      if (x.j != x.l && x.n < kTiny)
+        for (uint32_t p = 0; p < x.n; ++p) {
+          map[mc[x.j]] = x.start + p;
+          other[mc[x.j]++] = x.l;
+        }
+    }
+    for (int64_t e = 0; e < nr; ++e) {
+      const auto it = std::lower_bound(cell_start.begin(), cell_start.end(), ref_start[e]);
+      if (it == cell_start.end() || *it != ref_start[e]) {
+        set_error("hybrid SEIL layout: reference without its cell");
+        return RAIRS_E_INTERNAL;
+      }
+      const size_t c = (size_t)(it - cell_start.begin());
+      p_ref_start[e] = cell_pos[c];
+      p_ref_cnt[e] = cell_n[c] < kTiny ? 0u : cell_n[c];
+    }
+  } else {
+    // regions (line 16): 32-aligned, [shared][misc own][misc copies]
+    int64_t off = 0;
+    for (int l = 0; l < nlist; ++l) {
+      p_off[l] = (uint32_t)off;
+      p_shared[l] = (uint32_t)shared[l];
+      p_misc[l] = (uint32_t)(misc_own[l] + misc_copy[l]);
+      off += round_up(shared[l] + misc_own[l] + misc_copy[l], 32);
+    }
+    if (off >= (int64_t)0xFFFFFFFFll) {
+      set_error("paper SEIL layout: slot count exceeds 2^32");
+      return RAIRS_E_UNSUPPORTED;
+    }
+    p_slots = std::max<int64_t>(off, 32);
+    map.assign((size_t)p_slots, kNoOther);
+    other.assign((size_t)p_slots, kNoOther);
+    std::vector<uint32_t> sh(nlist), mo(nlist), mc(nlist);
+    for (int l = 0; l < nlist; ++l) {
+      sh[l] = p_off[l];
+      mo[l] = p_off[l] + p_shared[l];
+      mc[l] = (uint32_t)(p_off[l] + p_shared[l] + misc_own[l]);
+    }
+    // shared-block start of every cell (the references' bptr), by cell-major start
+    std::vector<uint32_t> cell_start((size_t)cells.size()), cell_bptr((size_t)cells.size()),
+        cell_full((size_t)cells.size());
+    for (size_t c = 0; c < cells.size(); ++c) {  // lines 17-32
+      const Cell& x = cells[c];
+      const uint32_t full = 32 * (x.n / 32);
+      cell_start[c] = x.start;
+      cell_bptr[c] = sh[x.l];
+      cell_full[c] = full;
+      for (uint32_t p = 0; p < full; ++p) map[sh[x.l]++] = x.start + p;  // shared blocks
+      for (uint32_t p = full; p < x.n; ++p) {                            // misc, both lists
+        map[mo[x.l]] = x.start + p;
+        other[mo[x.l]++] = x.j;
+        if (x.j != x.l) {
+          map[mc[x.j]] = x.start + p;
+          other[mc[x.j]++] = x.l;
+        }
       }
     }
-  }
-  // the references of list j (cell-major order = ascending owner): the shared
-  // blocks of cell (owner, j) in the owner's region
-  std::vector<uint32_t> p_ref_start((size_t)std::max<int64_t>(nr, 1), 0), p_ref_cnt((size_t)std::max<int64_t>(nr, 1), 0);
-  for (int64_t e = 0; e < nr; ++e) {
-    const auto it = std::lower_bound(cell_start.begin(), cell_start.end(), ref_start[e]);
-    if (it == cell_start.end() || *it != ref_start[e]) {
-      set_error("paper SEIL layout: reference without its cell");
-      return RAIRS_E_INTERNAL;
+    // the references of list j (cell-major order = ascending owner): the shared
+    // blocks of cell (owner, j) in the owner's region
+    for (int64_t e = 0; e < nr; ++e) {
+      const auto it = std::lower_bound(cell_start.begin(), cell_start.end(), ref_start[e]);
+      if (it == cell_start.end() || *it != ref_start[e]) {
+        set_error("paper SEIL layout: reference without its cell");
+        return RAIRS_E_INTERNAL;
+      }
+      const size_t c = (size_t)(it - cell_start.begin());
+      p_ref_start[e] = cell_bptr[c];
+      p_ref_cnt[e] = cell_full[c];
     }
-    const size_t c = (size_t)(it - cell_start.begin());
-    p_ref_start[e] = cell_bptr[c];
-    p_ref_cnt[e] = cell_full[c];
   }
 
   const int M4 = idx->M_pad / 4;
@@ -208,6 +273,7 @@ rairs_status seil_paper_prepare(rairs_index_s* idx, cudaStream_t s) {
   SP_TRY(cudaGetLastError());
   SP_TRY(cudaStreamSynchronize(s));
   cudaFree(d_map);
+  idx->p_kind = hybrid ? 3 : 1;
 #undef SP_TRY
   return RAIRS_OK;
 }

@@ -269,13 +269,16 @@ class Index:
         """auto | simt (query-major LUT-lookup scan) | listmajor (tcgen05 one-hot x LUT)."""
         check(lib().rairs_set_scan_mode(self._h, self.SCAN_MODES[mode]), "rairs_set_scan_mode")
 
-    SEIL_LAYOUTS = {"cell": 0, "paper": 1, "auto": 2}
+    SEIL_LAYOUTS = {"cell": 0, "paper": 1, "auto": 2, "hybrid": 3}
 
     def set_seil_layout(self, layout: str = "cell"):
         """cell (cell-major SEIL, every vector stored once) | paper (the paper's
         layout: shared 32-item blocks + duplicated misc areas, Alg. 4/5; query-major
         scan only) | auto (both kept: query-major scans read the paper layout,
-        list-major scans the cell-major one)."""
+        list-major scans the cell-major one) | hybrid (query-major scans read each
+        list's cell-major range plus copies of the cross cells below 8 items,
+        dropped when their owner was probed; list-major scans the cell-major
+        layout)."""
         check(lib().rairs_set_seil_layout(self._h, self.SEIL_LAYOUTS[layout]), "rairs_set_seil_layout")
 
     def certify_fallbacks(self, reset: bool = True) -> int:
