@@ -64,6 +64,12 @@ struct TopWArgs {
 // replacement costs W+1 steps without divergence -- an insertion sort costs up
 // to W+1 divergent shifts per value).  Ties at the boundary may keep either
 // entry: the certificate only needs every excluded list to have g >= g_(W+1).
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ void topw_rescan(const float* lv, int Wp1, int r, float& mx, int& mp) {
   mx = -__int_as_float(0x7f800000);
   mp = 0;
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % S;
           const uint32_t ph = (uint32_t)(it / S) & 1u;
-          if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
+          if (it >= S) (a.dbg & 2) ? mbar_wait(&empty[s], ph ^ 1u) : mbar_wait_lazy(&empty[s], ph ^ 1u);
           if (a.a_res) {
             mbar_expect_tx(&full[s], FT_B_BYTES);
           } else {
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         }
         const int acc = t & 1;
         const uint32_t aph = (uint32_t)(t >> 1) & 1u;
-        if (t >= 2) mbar_wait(&tempty[acc], aph ^ 1u);
+        if (t >= 2) (a.dbg & 2) ? mbar_wait(&tempty[acc], aph ^ 1u) : mbar_wait_lazy(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t dt = tmem + (uint32_t)(acc * FT_BN);
         for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -287,8 +293,14 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
           g[4 * q4 + 2] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 2]), cn.z);
           g[4 * q4 + 3] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 3]), cn.w);
         }
+        // three-input minimum tree (FMNMX3): 16 instructions, depth 4
+        float m1[11];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) gmin = fminf(gmin, g[j]);
+        for (int j = 0; j < 10; ++j) m1[j] = fmin3f(g[3 * j], g[3 * j + 1], g[3 * j + 2]);
+        m1[10] = fminf(g[30], g[31]);
+        const float m2a = fmin3f(m1[0], m1[1], m1[2]), m2b = fmin3f(m1[3], m1[4], m1[5]);
+        const float m2c = fmin3f(m1[6], m1[7], m1[8]), m2d = fminf(m1[9], m1[10]);
+        gmin = fminf(fmin3f(m2a, m2b, m2c), m2d);
         const float thr = rv[KR - 1];
         if (!__any_sync(0xffffffffu, gmin < thr)) return;
         uint32_t pass = 0;
@@ -577,7 +589,7 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
           float4 r[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            if (i0 + u < Wc) {
+            if (i0 + u < Wc && keys[i0 + u] != kKeyInf) {  // (a short union: no row)
               const uint32_t l = (uint32_t)(keys[i0 + u] & 0xFFFFFFFFu);
               r[u] = __ldg(reinterpret_cast<const float4*>(a.C + (size_t)l * a.d) + t4);
             }
@@ -592,7 +604,7 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
       for (int t = lane; t < a.d; t += 32) xd[t] = (double)xr[t];
       __syncwarp();
       for (int i = lane; i < a.npow_w; i += 32) {
-        if (i < Wc) {
+        if (i < Wc && keys[i] != kKeyInf) {
           const float4* c4 = reinterpret_cast<const float4*>(cs) + i * rs4;
           const double2* x2 = reinterpret_cast<const double2*>(xd);
           double acc = 0.0;
@@ -616,7 +628,7 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
       __syncwarp();
     } else
     for (int i = lane; i < a.npow_w; i += 32) {
-      if (i < Wc) {
+      if (i < Wc && keys[i] != kKeyInf) {
         const uint32_t l = (uint32_t)(keys[i] & 0xFFFFFFFFu);
         const float* c = a.C + (size_t)l * a.d;
         double acc = 0.0;
@@ -663,7 +675,7 @@ __global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs 
       // Alg. 3 lines 3-11 over the first L = N_CANDS exact lists (fp64, O4)
       const int start = a.strict ? 1 : 0;
       double loss = 0.0;
-      const bool ok = (lane >= start) && (lane < a.L);
+      const bool ok = (lane >= start) && (lane < a.L) && ci[0] != 0xFFFFFFFFu && ci[lane] != 0xFFFFFFFFu;
       if (ok) {
         const float* c0 = a.C + (size_t)ci[0] * a.d;
         const float* cj = a.C + (size_t)ci[lane] * a.d;
@@ -771,6 +783,36 @@ rairs_status coarse_prepare(rairs_index_s* idx, cudaStream_t s) {
   return RAIRS_OK;
 }
 
+template <int KR>
+static cudaError_t launch_topw_kr(dim3 grid, size_t smem, cudaStream_t s, const CUtensorMap& tmA,
+                                  const CUtensorMap& tmB, const TopWArgs& ta) {
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      coarse_topw_kernel<KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (attr != cudaSuccess) return attr;
+  coarse_topw_kernel<KR><<<grid, FT_THREADS, smem, s>>>(tmA, tmB, ta);
+  return cudaGetLastError();
+}
+
+// KR = 0: the shared-memory path (grid of row tiles x column splits)
+static cudaError_t launch_topw(int KR, dim3 grid, dim3 grid_smem, size_t smem, cudaStream_t s,
+                               const CUtensorMap& tmA, const CUtensorMap& tmB, const TopWArgs& ta) {
+  switch (KR) {
+    case 0: return launch_topw_kr<0>(grid_smem, smem, s, tmA, tmB, ta);
+    case 6: return launch_topw_kr<6>(grid, smem, s, tmA, tmB, ta);
+    case 7: return launch_topw_kr<7>(grid, smem, s, tmA, tmB, ta);
+    case 8: return launch_topw_kr<8>(grid, smem, s, tmA, tmB, ta);
+    case 9: return launch_topw_kr<9>(grid, smem, s, tmA, tmB, ta);
+    case 10: return launch_topw_kr<10>(grid, smem, s, tmA, tmB, ta);
+    case 11: return launch_topw_kr<11>(grid, smem, s, tmA, tmB, ta);
+    case 12: return launch_topw_kr<12>(grid, smem, s, tmA, tmB, ta);
+    case 13: return launch_topw_kr<13>(grid, smem, s, tmA, tmB, ta);
+    case 16: return launch_topw_kr<16>(grid, smem, s, tmA, tmB, ta);
+    case 20: return launch_topw_kr<20>(grid, smem, s, tmA, tmB, ta);
+    case 24: return launch_topw_kr<24>(grid, smem, s, tmA, tmB, ta);
+    default: return launch_topw_kr<32>(grid, smem, s, tmA, tmB, ta);
+  }
+}
+
 static int coarse_width(int nl, int L) { return std::min(nl, L + 8 + L / 8); }
 
 bool coarse_fused_ok(const rairs_index_s* idx, int L) {
@@ -806,8 +848,20 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   const bool reg = Wp1 <= 32 || capped;
   // list length = W + 1 rounded up to an instantiated size: the insertion cost
   // and the pass threshold (the KR-th kept value) both shrink with KR
-  const int KR = Wp1 <= 10 ? 10 : Wp1 <= 11 ? 11 : Wp1 <= 12 ? 12 : Wp1 <= 13 ? 13 : Wp1 <= 16 ? 16 : Wp1 <= 20 ? 20
-               : Wp1 <= 24 ? 24 : 32;
+  // Half lists (>= 8 column tiles): each (row, split, half) list keeps only
+  // ceil((W + 1) / 2) + 1 entries and K2 bounds the excluded lists by the
+  // union's (W+1)-th value AND every full list's last value (as for capped
+  // lists): about the same certificate (the union of two half lists of k holds
+  // every value below min(last0, last1), ~the 2k-th overall), at a fraction
+  // of the insertion work (fewer insertions, shorter networks).
+  static const bool half_env = [] {
+    const char* e = std::getenv("RAIRS_COARSE_HALFLISTS");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  const bool short_lists = half_env && !capped && Wp1 <= 32 && nl_tiles >= 8;
+  const int kw = short_lists ? (Wp1 + 1) / 2 + 1 : std::max(Wp1, 10);
+  const int KR = kw <= 6 ? 6 : kw <= 7 ? 7 : kw <= 8 ? 8 : kw <= 9 ? 9 : kw <= 10 ? 10 : kw <= 11 ? 11
+               : kw <= 12 ? 12 : kw <= 13 ? 13 : kw <= 16 ? 16 : kw <= 20 ? 20 : kw <= 24 ? 24 : 32;
   const int Wout = reg ? KR * FT_HALVES : Wp1;  // entries per (row, split)
   const int lists_bytes = reg ? 32 * FT_BM * FT_HALVES * 4 : Wp1 * FT_BM * 8 + 32 * FT_BM * 4;
   const int nkc = (int)ceil_div(d, FT_BK);
@@ -841,28 +895,6 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   if (smem > 227 * 1024) {
     set_error("coarse: shared memory budget exceeded");
     return RAIRS_E_UNSUPPORTED;
-  }
-  static bool attr_set = false;
-  if (!attr_set) {
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<0>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<10>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<11>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<12>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<13>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<16>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<20>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<24>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    RAIRS_CUDA_TRY(cudaFuncSetAttribute(coarse_topw_kernel<32>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
   }
   const int64_t CH = 1 << 21;  // rows per chunk (bounds the candidate buffers)
   const int npow_w = next_pow2(std::max(W, 2));
@@ -950,24 +982,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ta.out_v = vals;
     ta.out_i = ids;
     const dim3 tgrid = lin ? dim3((unsigned)G, 1u) : dim3((unsigned)mtiles, (unsigned)nsplit);
-    if (reg && KR == 10)
-      coarse_topw_kernel<10><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg && KR == 11)
-      coarse_topw_kernel<11><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg && KR == 12)
-      coarse_topw_kernel<12><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg && KR == 13)
-      coarse_topw_kernel<13><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg && KR == 16)
-      coarse_topw_kernel<16><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg && KR == 20)
-      coarse_topw_kernel<20><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg && KR == 24)
-      coarse_topw_kernel<24><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else if (reg)
-      coarse_topw_kernel<32><<<tgrid, FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
-    else
-      coarse_topw_kernel<0><<<dim3((unsigned)mtiles, (unsigned)nsplit), FT_THREADS, smem_k, s>>>(tmA, tmB, ta);
+    RAIRS_CUDA_TRY(launch_topw(reg ? KR : 0, tgrid, dim3((unsigned)mtiles, (unsigned)nsplit), smem_k, s,
+                               tmA, tmB, ta));
     RAIRS_CHECK_LAUNCH();
     if (debug_sync_enabled()) {
       char what[160];
@@ -1016,7 +1032,7 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     ca.strict = strict;
     ca.cmax = idx->cmax;
     ca.npow_c = npow_c;
-    ca.capped_kr = capped ? KR : 0;
+    ca.capped_kr = (capped || short_lists) ? KR : 0;
     ca.sorted_kr = reg ? KR : 0;
     ca.run = run;
     ca.npow_w = npow_w;

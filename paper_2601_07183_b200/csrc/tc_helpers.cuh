@@ -53,6 +53,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     if ((n & 15u) == 0 && clock64() - t0 > 8000000000LL) __trap();
   }
 }
+// For single-thread roles that are not on the critical path (a TMA producer
+// waiting for a free ring slot, the MMA issuer waiting for the epilogue to
+// release an accumulator): poll with a short sleep between polls, so the
+// waiting thread's warp takes no issue slots from the epilogue warps.
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t phase) {
+  if (mbar_try_wait(bar, phase)) return;
+  const long long t0 = clock64();
+  for (uint32_t n = 1;; ++n) {
+    __nanosleep(96);
+    if (mbar_try_wait(bar, phase)) return;
+    if ((n & 15u) == 0 && clock64() - t0 > 8000000000LL) __trap();
+  }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
                                             uint64_t* bar) {
   asm volatile(
