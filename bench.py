@@ -583,34 +583,60 @@ def probed_list_items(idx, Qd, k, nprobe, rf):
 def side_k1(idx, Qd, spec, gt_ids, gt_d64, nq_gt, flush, stream, steps):
     """BJ configs[3] asks for k=1 as well as k=10: the same index and protocol,
     k = 1 with K_FACTOR 10, smallest swept nprobe with
-    recall1@1 >= 0.95, device-timed steps (L2 flushed between them)."""
+    recall1@1 >= 0.95, device-timed steps (L2 flushed between them).  When
+    K_FACTOR 10 plateaus below 0.95 (bigK = 10 PQ candidates hold the true
+    nearest neighbour too rarely: a raw-PQ cap, not an nprobe one), the
+    refine factor is raised (25, 50, 100) until the target is reached; the
+    K_FACTOR 10 plateau is kept in the line as `k_factor_10`."""
     import torch
-    rf = spec.refine_factor
-    chosen, rec, sweep = None, None, []
-    for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
-        ids, dists = idx.search(Qd, 1, npb, rf)
-        r = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], 1)
-        sweep.append({"nprobe": npb, "recall": round(r, 4)})
-        chosen, rec = npb, r
-        if r >= 0.95 or plateaued(sweep):
-            break
-    for _ in range(3):
-        idx.search(Qd, 1, chosen, rf)
-    t = 0.0
-    for _ in range(steps):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        idx.search(Qd, 1, chosen, rf)
-        e1.record(stream)
-        e1.synchronize()
-        t += e0.elapsed_time(e1)
     nq = Qd.shape[0]
-    return {"metric": "QPS at recall1@1>=0.95", "k": 1, "refine_factor": rf, "nprobe": chosen,
+
+    def sweep_rf(rf):
+        chosen, rec, sweep = None, None, []
+        for npb in [p for p in NPROBE_SWEEP if p <= spec.nlist]:
+            ids, dists = idx.search(Qd, 1, npb, rf)
+            r = recall_at_k(ids[:nq_gt], gt_ids, gt_d64, dists[:nq_gt], 1)
+            sweep.append({"nprobe": npb, "recall": round(r, 4)})
+            chosen, rec = npb, r
+            if r >= 0.95 or plateaued(sweep):
+                break
+        return chosen, rec, sweep
+
+    def timed(rf, npb):
+        for _ in range(3):
+            idx.search(Qd, 1, npb, rf)
+        t = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            idx.search(Qd, 1, npb, rf)
+            e1.record(stream)
+            e1.synchronize()
+            t += e0.elapsed_time(e1)
+        return t / steps
+
+    rf0 = spec.refine_factor
+    chosen, rec, sweep = sweep_rf(rf0)
+    ms = timed(rf0, chosen)
+    line = {"metric": "QPS at recall1@1>=0.95", "k": 1, "refine_factor": rf0, "nprobe": chosen,
             "recall1@1": round(rec, 4), "recall_sweep": sweep,
-            "value": round(nq * steps / (t / 1e3), 1), "unit": "queries/s",
-            "ms_per_step": round(t / steps, 4)}
+            "value": round(nq / (ms / 1e3), 1), "unit": "queries/s", "ms_per_step": round(ms, 4)}
+    if rec >= 0.95:
+        return line
+    base = dict(line)
+    for rf in (25, 50, 100):
+        chosen, rec, sweep = sweep_rf(rf)
+        ms = timed(rf, chosen)
+        line = {"metric": "QPS at recall1@1>=0.95", "k": 1, "refine_factor": rf, "nprobe": chosen,
+                "recall1@1": round(rec, 4), "recall_sweep": sweep,
+                "value": round(nq / (ms / 1e3), 1), "unit": "queries/s", "ms_per_step": round(ms, 4)}
+        if rec >= 0.95:
+            break
+    line["k_factor_10"] = {k: base[k] for k in ("refine_factor", "nprobe", "recall1@1", "value", "ms_per_step")}
+    line["k_factor_10"]["note"] = "K_FACTOR 10 (P:2016-2017) plateaus below 0.95 on this data"
+    return line
 
 
 def side_seil_layouts(idx, main_layout, Qd, k, nprobe, rf, gt_ids, gt_d64, nq_gt, flush, stream, steps,

@@ -95,6 +95,35 @@ __device__ __forceinline__ void lookup8(const uint4& T, uint32_t w, uint32_t (&a
   acc[7] = __dp4a(r1, 0x01000000u, acc[7]);
 }
 
+// the same 8 lookups with the sums packed in pairs: dp2a adds byte 2p with
+// weight 1 and byte 2p+1 with weight 2^15 into one u32, so items (2p, 2p+1)
+// share an accumulator (item 2p in bits 0-14, exact while M_pad * 255 < 2^15,
+// i.e. M_pad <= 128; item 2p+1 in bits 15-31): 4 instead of 8 fma-pipe
+// instructions per word.  fs_unpack splits them after the group's last word.
+__device__ __forceinline__ void lookup8p(const uint4& T, uint32_t w, uint32_t (&acc)[4]) {
+  const uint32_t x = w & 0x77777777u;
+  const uint32_t xh = __umulhi(x, 0x10000u);
+  const uint32_t w4 = w << 4;
+  const uint32_t m0 = prmt(w4, w, 0xD9C8u);
+  const uint32_t m1 = prmt(w4, w, 0xFBEAu);
+  const uint32_t lo0 = prmt(T.x, T.y, x), hi0 = prmt(T.z, T.w, x);
+  const uint32_t lo1 = prmt(T.x, T.y, xh), hi1 = prmt(T.z, T.w, xh);
+  const uint32_t r0 = (lo0 & ~m0) | (hi0 & m0);
+  const uint32_t r1 = (lo1 & ~m1) | (hi1 & m1);
+  acc[0] = __dp2a_lo(0x80000001u, r0, acc[0]);
+  acc[1] = __dp2a_hi(0x80000001u, r0, acc[1]);
+  acc[2] = __dp2a_lo(0x80000001u, r1, acc[2]);
+  acc[3] = __dp2a_hi(0x80000001u, r1, acc[3]);
+}
+
+__device__ __forceinline__ void fs_unpack(const uint32_t (&p)[4], uint32_t (&acc)[8]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[2 * i] = p[i] & 0x7FFFu;
+    acc[2 * i + 1] = p[i] >> 15;
+  }
+}
+
 struct FsArgs {
   const uint8_t* codes;        // group layout
   const uint32_t* slot_rows;
@@ -735,7 +764,7 @@ __global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(const __grid_cons
 // 16-B code loads in flight: consuming chunk c issues chunk c + 2, which past
 // the group's end is chunk 0/1 of the lane's NEXT round's group, so a round's
 // DRAM latency overlaps the previous round's lookups.
-template <int MINB, int GPL, int NW>
+template <int MINB, int GPL, int NW, bool PK>
 __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_constant__ FsArgs a) {
   constexpr int D = 4 / GPL;                 // ring slots per group
   constexpr uint32_t FS_ROUND = 256u * GPL;  // items appended per round at most
@@ -937,10 +966,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
         for (int g = 0; g < GPL; ++g)
           nA[g] = fs_round_task(t0 + 32u * (GPL + g), r_lo, t_end, nr, rs, rc, rg, rlp, a.codes, blk_bytes);
         uint32_t acc[GPL][8];
+        uint32_t accp[GPL][4];
 #pragma unroll
-        for (int g = 0; g < GPL; ++g)
+        for (int g = 0; g < GPL; ++g) {
 #pragma unroll
           for (int v = 0; v < 8; ++v) acc[g][v] = 0u;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) accp[g][v] = 0u;
+        }
         // one iteration: chunks c .. c+D-1 consumed, each slot refilled from
         // `nxt` (chunk c+D+s of this group, or chunk s of the next round's)
         auto iter = [&](int c, const uint8_t* const (&nxt)[GPL]) {
@@ -958,10 +991,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
 #pragma unroll
             for (int g = 0; g < GPL; ++g) {
               if (dbg & 32) R[g][s] = make_uint4(c, c * 3u, c * 5u, c * 7u);  // timing: no code loads
-              lookup8(L[4 * s + 0], R[g][s].x, acc[g]);
-              lookup8(L[4 * s + 1], R[g][s].y, acc[g]);
-              lookup8(L[4 * s + 2], R[g][s].z, acc[g]);
-              lookup8(L[4 * s + 3], R[g][s].w, acc[g]);
+              if constexpr (PK) {
+                lookup8p(L[4 * s + 0], R[g][s].x, accp[g]);
+                lookup8p(L[4 * s + 1], R[g][s].y, accp[g]);
+                lookup8p(L[4 * s + 2], R[g][s].z, accp[g]);
+                lookup8p(L[4 * s + 3], R[g][s].w, accp[g]);
+              } else {
+                lookup8(L[4 * s + 0], R[g][s].x, acc[g]);
+                lookup8(L[4 * s + 1], R[g][s].y, acc[g]);
+                lookup8(L[4 * s + 2], R[g][s].z, acc[g]);
+                lookup8(L[4 * s + 3], R[g][s].w, acc[g]);
+              }
               if (!(dbg & 32)) R[g][s] = ldg_nc_v4(nxt[g] + s * 64);
             }
           }
@@ -980,6 +1020,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_con
 #pragma unroll
           for (int g = 0; g < GPL; ++g) nxt[g] = nA[g].gp;
           iter(M4 - D, nxt);
+        }
+        if constexpr (PK) {
+#pragma unroll
+          for (int g = 0; g < GPL; ++g) fs_unpack(accp[g], acc[g]);
         }
         if (dbg & 8) {  // timing experiment: no selection (scores folded into the DCO sum)
           uint32_t x = 0;
@@ -1179,6 +1223,15 @@ static int fs_variant() {
 }
 static int fs_round_items() { return fs_variant() == 2 ? 512 : 256; }
 
+// packed pair sums (lookup8p, M_pad <= 128); RAIRS_FS_PACK=0: one u32 per item
+static bool fastscan_pack_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("RAIRS_FS_PACK");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 int fastscan_cap(int bigK, int M_pad);
 
 static int fs_hbits(int M) {
@@ -1286,20 +1339,20 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   return RAIRS_OK;
 }
 
-template <int MINB, int GPL, int NW>
+template <int MINB, int GPL, int NW, bool PK>
 static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
   pl.warps = std::min(pl.warps, NW);
   pl.smem = (size_t)pl.warps * pl.a.warp_bytes;
-  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB, GPL, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB, GPL, NW, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pl.smem));
   int per_sm = 0;
-  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB, GPL, NW>,
+  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB, GPL, NW, PK>,
                                                                pl.warps * 32, pl.smem));
   per_sm = std::max(per_sm, 1);
   const int64_t need = ceil_div(pl.a.nq * std::max(pl.a.parts, 1), pl.warps);  // work items
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148LL * per_sm));
   pl.a.total_warps = grid * (unsigned)pl.warps;
-  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB, GPL, NW>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
+  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB, GPL, NW, PK>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
   return RAIRS_OK;
 }
 
@@ -1351,9 +1404,12 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
   const bool kev = sa.kev[0] && sa.kev_used && !ex.tau_out && !ex.qlist;
   if (kev) RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[0], s));
   switch (fs_variant()) {
-    case 1: RAIRS_TRY((fs_launch<3, 1, 8>(pl, s))); break;
-    case 2: RAIRS_TRY((fs_launch<2, 2, 8>(pl, s))); break;
-    default: RAIRS_TRY((fs_launch<2, 1, 8>(pl, s))); break;
+    case 1: RAIRS_TRY((fs_launch<3, 1, 8, false>(pl, s))); break;
+    case 2: RAIRS_TRY((fs_launch<2, 2, 8, false>(pl, s))); break;
+    default:
+      if (idx->M_pad <= 128 && fastscan_pack_on()) RAIRS_TRY((fs_launch<2, 1, 8, true>(pl, s)));
+      else RAIRS_TRY((fs_launch<2, 1, 8, false>(pl, s)));
+      break;
   }
   if (kev) {
     RAIRS_CUDA_TRY(cudaEventRecord(sa.kev[1], s));
