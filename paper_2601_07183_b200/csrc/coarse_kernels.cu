@@ -109,6 +109,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
   uint64_t* afull = tempty + 2;   // [2]: resident A of segment j in buffer j & 1
   uint64_t* aempty = afull + 2;   // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(aempty + 2);
+  // ||c||^2 of the current 32-column chunk, per epilogue warp (32 floats): each
+  // lane loads one value a chunk ahead, the warp reads them back broadcast
+  float* cbuf_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tslot) +
+                                             ((16u - (smem_u32(tslot) & 15u)) & 15u) + 16u);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // this CTA's units [u0, u1): unit u = row tile u / ntiles, column tile u % ntiles
@@ -259,6 +263,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
     };
     int64_t r = u0 / a.ntiles;
     int ct = (int)(u0 - r * a.ntiles);
+    constexpr int CPW = FT_BN / 32 / FT_HALVES;  // chunks per warp per tile (4)
+    static_assert(CPW % 2 == 0, "chunks come in pairs");
+    const int cb = half * CPW;
+    float* cbuf = cbuf_all + warp * 32;
+    float cnl = ntile > 0 ? __ldg(a.cnorm + ct * FT_BN + cb * 32 + lane) : 0.0f;  // first chunk's
     for (int t = 0; t < ntile; ++t, ct = (ct + 1 == a.ntiles) ? (++r, 0) : ct + 1) {
       const int acc = t & 1;
       const uint32_t aph = (uint32_t)(t >> 1) & 1u;
@@ -278,16 +287,25 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
       // accumulator is released as soon as the last chunk is in registers
       auto process = [&](uint32_t (&v)[32], int c) {
         if ((a.dbg & 1) && t > 0) return;  // timing experiment: MMA + TMA only after tile 0
-        // g = ||c||^2 - 2 q.c; ||c||^2 of the chunk's 32 columns by 8 broadcast
-        // 16-B loads; the chunk minimum decides (warp-wide) whether any value
-        // can enter a list -- the common case after the first tiles costs one
-        // FFMA + one FMNMX per value
-        const float4* cn4 = reinterpret_cast<const float4*>(a.cnorm + col0 + c * 32);
+        // g = ||c||^2 - 2 q.c; ||c||^2 of the chunk's 32 columns: lane j's value
+        // (loaded one chunk ahead) through the warp's shared slot, read back by 8
+        // broadcast 16-B loads; the chunk minimum decides (warp-wide) whether
+        // any value can enter a list -- the common case after the first tiles
+        // costs one FFMA + one FMNMX per value
+        __syncwarp();
+        cbuf[lane] = cnl;
+        __syncwarp();
+        {  // the warp's next chunk: c + 1 of this tile, else chunk cb of the next tile
+          const int nc = c + 1 < cb + CPW ? c + 1 : cb;
+          const int ncol0 = c + 1 < cb + CPW ? col0 : (ct + 1 == a.ntiles ? 0 : ct + 1) * FT_BN;
+          cnl = __ldg(a.cnorm + ncol0 + nc * 32 + lane);
+        }
+        const float4* cn4 = reinterpret_cast<const float4*>(cbuf);
         float g[32];
         float gmin = __int_as_float(0x7f800000);
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4) {
-          const float4 cn = __ldg(cn4 + q4);
+          const float4 cn = cn4[q4];
           g[4 * q4 + 0] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 0]), cn.x);
           g[4 * q4 + 1] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 1]), cn.y);
           g[4 * q4 + 2] = fmaf(-2.0f, __uint_as_float(v[4 * q4 + 2]), cn.z);
@@ -330,9 +348,6 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
           }
         }
             };
-      constexpr int CPW = FT_BN / 32 / FT_HALVES;  // chunks per warp per tile (4)
-      static_assert(CPW % 2 == 0, "chunks come in pairs");
-      const int cb = half * CPW;
       const uint32_t tbase = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * FT_BN);
       uint32_t va[32], vb[32];
       tmem_ld32_nowait(tbase + (uint32_t)(cb * 32), va);
@@ -877,18 +892,18 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
   // smem plan for nab resident A buffers (0: A streamed with B per stage)
   auto plan = [&](int nab, int& nstage, size_t& smem) {
     if (nab > 0) {
-      nstage = (int)std::min<size_t>(6, (227 * 1024 - 2048 - lists_bytes - (size_t)nab * nkc * FT_A_BYTES) / FT_B_BYTES);
+      nstage = (int)std::min<size_t>(6, (227 * 1024 - 2304 - lists_bytes - (size_t)nab * nkc * FT_A_BYTES) / FT_B_BYTES);
     } else {
       nstage = (lists_bytes <= 80 * 1024) ? 3 : 2;
     }
     const size_t ring_bytes = nab > 0 ? (size_t)nab * nkc * FT_A_BYTES + (size_t)nstage * FT_B_BYTES
                                       : (size_t)nstage * (FT_A_BYTES + FT_B_BYTES);
-    smem = 1024 + ring_bytes + lists_bytes + (2 * nstage + 8) * 8 + 16;
+    smem = 1024 + ring_bytes + lists_bytes + (2 * nstage + 8) * 8 + 16 + 32 + FT_EPI_WARPS * 32 * 4;
   };
   // A resident (loaded once per row tile) when it fits next to >= 3 B stages:
   // the ring then moves 2/3 of the bytes per column tile (the TMA ingest bound)
-  const bool a_res = (size_t)nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2048 <= 227 * 1024;
-  const bool a_res2 = (size_t)2 * nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2048 <= 227 * 1024;
+  const bool a_res = (size_t)nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2304 <= 227 * 1024;
+  const bool a_res2 = (size_t)2 * nkc * FT_A_BYTES + 3 * FT_B_BYTES + lists_bytes + 2304 <= 227 * 1024;
   int nstage = 0;
   size_t smem = 0;
   plan(a_res ? 1 : 0, nstage, smem);

@@ -764,9 +764,9 @@ __global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(const __grid_cons
 // 16-B code loads in flight: consuming chunk c issues chunk c + 2, which past
 // the group's end is chunk 0/1 of the lane's NEXT round's group, so a round's
 // DRAM latency overlaps the previous round's lookups.
-template <int MINB, int GPL, int NW, bool PK>
+template <int MINB, int GPL, int NW, bool PK, int DR = 4>
 __global__ void __launch_bounds__(NW * 32, MINB) fs_scan_kernel(const __grid_constant__ FsArgs a) {
-  constexpr int D = 4 / GPL;                 // ring slots per group
+  constexpr int D = DR / GPL;                // ring slots per group
   constexpr uint32_t FS_ROUND = 256u * GPL;  // items appended per round at most
   const int dbg = kFsTiming ? a.dbg : 0;
   extern __shared__ __align__(16) uint8_t fs_smem[];
@@ -1223,6 +1223,17 @@ static int fs_variant() {
 }
 static int fs_round_items() { return fs_variant() == 2 ? 512 : 256; }
 
+// ring slots per lane: 6 when M_pad / 4 is a multiple of 6 and the sums are
+// packed (c4: 6 chunks = 24 nibble words of lead per load, scan 232 -> 226 us),
+// else 4 (RAIRS_FS_RING=4 forces 4)
+static int fastscan_ring() {
+  static const int v = [] {
+    const char* e = std::getenv("RAIRS_FS_RING");
+    return e ? std::atoi(e) : 6;
+  }();
+  return v;
+}
+
 // packed pair sums (lookup8p, M_pad <= 128); RAIRS_FS_PACK=0: one u32 per item
 static bool fastscan_pack_on() {
   static const bool on = [] {
@@ -1339,20 +1350,20 @@ static rairs_status fs_plan(const rairs_index_s* idx, const SearchArgs& sa, cons
   return RAIRS_OK;
 }
 
-template <int MINB, int GPL, int NW, bool PK>
+template <int MINB, int GPL, int NW, bool PK, int DR = 4>
 static rairs_status fs_launch(FsPlan& pl, cudaStream_t s) {
   pl.warps = std::min(pl.warps, NW);
   pl.smem = (size_t)pl.warps * pl.a.warp_bytes;
-  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB, GPL, NW, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_scan_kernel<MINB, GPL, NW, PK, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)pl.smem));
   int per_sm = 0;
-  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB, GPL, NW, PK>,
+  RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fs_scan_kernel<MINB, GPL, NW, PK, DR>,
                                                                pl.warps * 32, pl.smem));
   per_sm = std::max(per_sm, 1);
   const int64_t need = ceil_div(pl.a.nq * std::max(pl.a.parts, 1), pl.warps);  // work items
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148LL * per_sm));
   pl.a.total_warps = grid * (unsigned)pl.warps;
-  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB, GPL, NW, PK>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
+  RAIRS_CUDA_TRY(launch_pdl(fs_scan_kernel<MINB, GPL, NW, PK, DR>, dim3(grid), dim3(pl.warps * 32), pl.smem, s, pl.a));
   return RAIRS_OK;
 }
 
@@ -1407,7 +1418,9 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     case 1: RAIRS_TRY((fs_launch<3, 1, 8, false>(pl, s))); break;
     case 2: RAIRS_TRY((fs_launch<2, 2, 8, false>(pl, s))); break;
     default:
-      if (idx->M_pad <= 128 && fastscan_pack_on()) RAIRS_TRY((fs_launch<2, 1, 8, true>(pl, s)));
+      if (idx->M_pad <= 128 && fastscan_pack_on() && fastscan_ring() == 6 && (idx->M_pad / 4) % 6 == 0)
+        RAIRS_TRY((fs_launch<2, 1, 8, true, 6>(pl, s)));
+      else if (idx->M_pad <= 128 && fastscan_pack_on()) RAIRS_TRY((fs_launch<2, 1, 8, true>(pl, s)));
       else RAIRS_TRY((fs_launch<2, 1, 8, false>(pl, s)));
       break;
   }
