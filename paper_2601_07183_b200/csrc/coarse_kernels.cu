@@ -44,6 +44,7 @@ struct TopWArgs {
   int nl, d, Wp1, nsplit, tiles_per_split, ntiles, nstage;
   const float* cnorm;  // [round_up(nl, 256)], +inf padding
   int dbg;             // timing experiments (RAIRS_COARSE_DBG): 1 = no epilogue work
+  uint32_t lazy_ns;     // sleep between polls of the producer / MMA single-thread waits
   int a_res;           // the A tile (all K-chunks) stays resident in shared memory
   // balanced schedule (lin = 1): the mtiles x ntiles (row tile, column tile)
   // units in row-major order are cut into gridDim.x equal contiguous ranges,
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % S;
           const uint32_t ph = (uint32_t)(it / S) & 1u;
-          if (it >= S) (a.dbg & 2) ? mbar_wait(&empty[s], ph ^ 1u) : mbar_wait_lazy(&empty[s], ph ^ 1u);
+          if (it >= S) (a.dbg & 2) ? mbar_wait(&empty[s], ph ^ 1u) : mbar_wait_lazy(&empty[s], ph ^ 1u, a.lazy_ns);
           if (a.a_res) {
             mbar_expect_tx(&full[s], FT_B_BYTES);
           } else {
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
         }
         const int acc = t & 1;
         const uint32_t aph = (uint32_t)(t >> 1) & 1u;
-        if (t >= 2) (a.dbg & 2) ? mbar_wait(&tempty[acc], aph ^ 1u) : mbar_wait_lazy(&tempty[acc], aph ^ 1u);
+        if (t >= 2) (a.dbg & 2) ? mbar_wait(&tempty[acc], aph ^ 1u) : mbar_wait_lazy(&tempty[acc], aph ^ 1u, a.lazy_ns);
         tc_fence_after();
         const uint32_t dt = tmem + (uint32_t)(acc * FT_BN);
         for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -993,6 +994,8 @@ rairs_status launch_coarse_fused(const rairs_index_s* idx, const float* X, int64
     {
       const char* e = std::getenv("RAIRS_COARSE_DBG");
       ta.dbg = e ? std::atoi(e) : 0;
+      const char* z = std::getenv("RAIRS_COARSE_LAZY_NS");
+      ta.lazy_ns = z ? (uint32_t)std::atoi(z) : 96u;
     }
     ta.out_v = vals;
     ta.out_i = ids;

@@ -136,10 +136,51 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
   __shared__ double qs[D];
   __shared__ uint64_t rk[RS_MAXK];
   __shared__ uint32_t gids[RS_ROWS];
-  __shared__ uint32_t nvalid;
+  __shared__ uint32_t nvalid_s[2];
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int myrow = warp + 8 * lane;  // lane j (< 16) fetches the key of row warp + 8j
   const int nch = (bigK + RS_ROWS - 1) / RS_ROWS;
+  // one chunk per query (bigK <= 128): the top-k of query u - 1 (warp 0, from
+  // the other half of the double-buffered keys) overlaps the fp64 sums of
+  // query u (warps 4-7), so the selection's latency leaves the critical path
+  const bool pipe = nch == 1;
+  const int ci = pipe ? (warp >= 4 ? tid - 128 : RS_ROWS) : tid;  // candidate this thread sums
+  auto select_topk = [&](const uint64_t* kb, int64_t qq, uint32_t nv) {
+    // warp 0: lane j holds keys j, j+32, j+64, j+96; k rounds of a warp-wide
+    // minimum (high word, then the low word among the lanes holding the high
+    // minimum); keys are unique, so exactly one lane drops the winner
+    uint64_t kr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) kr[u] = (lane + 32 * u < bigK) ? kb[lane + 32 * u] : kKeyInf;
+    uint64_t lm = kr[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) lm = kr[u] < lm ? kr[u] : lm;
+    int r = 0;
+    for (; r < k; ++r) {
+      const uint32_t mh = __reduce_min_sync(0xffffffffu, (uint32_t)(lm >> 32));
+      const uint32_t ml = __reduce_min_sync(0xffffffffu, (uint32_t)(lm >> 32) == mh ? (uint32_t)lm : 0xFFFFFFFFu);
+      const uint64_t m = ((uint64_t)mh << 32) | ml;
+      if (m == kKeyInf) break;
+      if (lane == 0) {
+        out_ids[qq * k + r] = (int64_t)ml;
+        out_dists[qq * k + r] = __uint_as_float(mh);
+      }
+      if (lm == m) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kr[u] = kr[u] == m ? kKeyInf : kr[u];
+        lm = kr[0];
+#pragma unroll
+        for (int u = 1; u < 4; ++u) lm = kr[u] < lm ? kr[u] : lm;
+      }
+    }
+    for (int i = r + lane; i < k; i += 32) {
+      out_ids[qq * k + i] = -1;
+      out_dists[qq * k + i] = __int_as_float(0x7f800000);
+    }
+    if (lane == 0 && refined) atomicAdd(refined, (unsigned long long)nv);
+  };
+  int par = 0;          // pipe: key buffer of the current query
+  int64_t qprev = -1;   // pipe: query whose keys wait in buffer par ^ 1
   // candidate rows are read once: evict them first from L2, so the gather does
   // not push out the score rows the concurrent selection streams
   uint64_t l2pol;
@@ -191,7 +232,7 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     if (lane < 16 && myrow < crow) gids[myrow] = gid;
     if (c == 0) {
       if (tid < D) qs[tid] = (double)qv;
-      if (tid == 0) nvalid = 0;
+      if (tid == 0) nvalid_s[par] = 0;
     }
     __syncthreads();
     int64_t q2 = qn;
@@ -202,11 +243,12 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
       key_next = load_key(q2, c2);
       if (cn == 0 && tid < D) qv = __ldg(queries + qn * D + tid);
     }
-    if (tid < crow) {
-      const uint32_t g = gids[tid];
+    if (pipe && warp == 0 && qprev >= 0) select_topk(rk + (par ^ 1) * RS_ROWS, qprev, nvalid_s[par ^ 1]);
+    if (ci < crow) {
+      const uint32_t g = gids[ci];
       uint64_t out = kKeyInf;
       if (g != 0xFFFFFFFFu) {
-        const float4* xr = reinterpret_cast<const float4*>(tile + tid * RSF);
+        const float4* xr = reinterpret_cast<const float4*>(tile + ci * RSF);
         double acc = 0.0;
 #pragma unroll 8
         for (int i = 0; i < D4; ++i) {
@@ -219,12 +261,16 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
         }
         out = ((uint64_t)__float_as_uint(__double2float_rn(acc)) << 32) |
               (labels ? labels[g / (uint32_t)G] : g);  // results carry the caller's ids
-        atomicAdd(&nvalid, 1u);
+        atomicAdd(&nvalid_s[par], 1u);
       }
-      rk[c * RS_ROWS + tid] = out;
+      rk[(pipe ? par : c) * RS_ROWS + ci] = out;
     }
     __syncthreads();  // tile / gids free for the next unit; rk complete after the last chunk
-    if (c == nch - 1) {
+    if (pipe) {
+      qprev = q;
+      par ^= 1;
+    } else if (c == nch - 1) {
+      const uint32_t nvalid = nvalid_s[0];
       for (int i = tid; i < bigK; i += RS_THREADS) {
         const uint64_t kc = rk[i];
         if (kc != kKeyInf) {
@@ -249,6 +295,7 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
     qn = q2;
     cn = c2;
   }
+  if (pipe && warp == 0 && qprev >= 0) select_topk(rk + (par ^ 1) * RS_ROWS, qprev, nvalid_s[par ^ 1]);
 }
 
 template <int D4>

@@ -57,11 +57,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // waiting for a free ring slot, the MMA issuer waiting for the epilogue to
 // release an accumulator): poll with a short sleep between polls, so the
 // waiting thread's warp takes no issue slots from the epilogue warps.
-__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t phase) {
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t phase, uint32_t ns = 96u) {
   if (mbar_try_wait(bar, phase)) return;
   const long long t0 = clock64();
   for (uint32_t n = 1;; ++n) {
-    __nanosleep(96);
+    __nanosleep(ns);
     if (mbar_try_wait(bar, phase)) return;
     if ((n & 15u) == 0 && clock64() - t0 > 8000000000LL) __trap();
   }
