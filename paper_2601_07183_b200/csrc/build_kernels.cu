@@ -446,6 +446,28 @@ rairs_status probe_split_launch(const ProbeArgs& a, const ProbeSplitBufs& b, con
   return RAIRS_OK;
 }
 
+__global__ void probe_iota_kernel(uint32_t* list, uint32_t* count, uint32_t rows) {
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) list[i] = i;
+  if (threadIdx.x == 0) *count = rows;
+}
+
+// Small batches (rows <= PX_CAP - 1, large nlist): every row through the split
+// exact path (O1 for all rows: no TF32 GEMM, no certificate).  *done = false
+// when the shape does not qualify (the caller takes the fused path).
+rairs_status launch_probe_split_all(const ProbeArgs& a, cudaStream_t s, bool* done) {
+  *done = false;
+  if (a.rows <= 0 || a.rows >= PX_CAP || a.mode != 0) return RAIRS_OK;
+  ProbeSplitBufs b;
+  RAIRS_TRY(probe_split_prepare(a, b, s));
+  if (!b.on) return RAIRS_OK;
+  uint32_t* count = b.list + (PX_CAP - 1);  // past the rows: the row count
+  probe_iota_kernel<<<1, 256, 0, s>>>(b.list, count, (uint32_t)a.rows);
+  rairs_status st = probe_split_launch(a, b, count, nullptr, s);
+  probe_split_free(b, s);
+  if (st == RAIRS_OK) *done = true;
+  return st;
+}
+
 void probe_split_free(ProbeSplitBufs& b, cudaStream_t s) {
   cudaFreeAsync(b.list, s);
   cudaFreeAsync(b.tk, s);

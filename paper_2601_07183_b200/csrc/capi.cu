@@ -287,7 +287,22 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
     RAIRS_CUDA_TRY(cudaEventRecord(idx->h2d_ev[1], idx->h2d));
     RAIRS_CUDA_TRY(cudaStreamWaitEvent(s, idx->h2d_ev[1], 0));
   }
-  if (coarse_fused_ok(idx, nprobe)) {
+  bool small_done = false;
+  if (idx->coarse_mode == 0 && nq <= coarse_small_rows()) {  // small batch (auto mode): exact fp64 coarse, split over CTAs
+    ProbeArgs pa{};
+    pa.X = queries;
+    pa.rows = nq;
+    pa.d = idx->d;
+    pa.C = idx->centroids;
+    pa.nl = idx->nlist;
+    pa.L = nprobe;
+    pa.mode = 0;
+    pa.out_idx = probes;
+    st = launch_probe_split_all(pa, s, &small_done);
+    if (small_done) nk += 3;  // iota + split + merge
+  }
+  if (small_done || st != RAIRS_OK) {
+  } else if (coarse_fused_ok(idx, nprobe)) {
     st = launch_coarse_fused(idx, queries, nq, nprobe, 0, 0.0, 0, probes, nullptr, nullptr,
                              idx->certify_fallbacks, s);
     nk += 3;  // topw + certify + exact fallback

@@ -831,6 +831,16 @@ static cudaError_t launch_topw(int KR, dim3 grid, dim3 grid_smem, size_t smem, c
 
 static int coarse_width(int nl, int L) { return std::min(nl, L + 8 + L / 8); }
 
+// small search batches: every row through the split exact path (c4 one query:
+// coarse 0.105 ms on the tensor-core path, whose cost is mostly fixed)
+int coarse_small_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("RAIRS_COARSE_SMALL");
+    return e ? std::atoi(e) : 16;
+  }();
+  return v;
+}
+
 bool coarse_fused_ok(const rairs_index_s* idx, int L) {
   if (idx->coarse_mode == 1) return false;  // forced exact
   if ((idx->d & 3) != 0 || !tma_available()) return false;

@@ -357,8 +357,8 @@ __device__ __forceinline__ FsTask fs_task(uint32_t t, uint32_t ng_tot, uint32_t 
 
 // The lane tasks of one round (tasks t0 .. t0+31) without a per-lane search:
 // r_lo = the range holding task t0; lane j looks at the start of range
-// r_lo + j, the boundaries that fall inside the round are OR-reduced into a
-// 32-bit mask, and lane L's range is r_lo + (boundaries at positions <= L).
+// r_lo + 1 + j, the boundaries that fall inside the round are OR-reduced into
+// a 32-bit mask, and lane L's range is r_lo + (boundaries at positions <= L).
 // On return r_lo holds the range of task t0 + 32 (the next round's).
 __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uint32_t ng_tot, uint32_t nr,
                                                 const uint32_t* rs, const uint32_t* rc, const uint32_t* rg,
@@ -370,9 +370,13 @@ __device__ __forceinline__ FsTask fs_round_task(uint32_t t0, uint32_t& r_lo, uin
     r = r_lo;
     adv = e == t0 + 32u ? 1u : 0u;
   } else {
-    const uint32_t j = r_lo + (uint32_t)lane;
+    // lane j inspects range r_lo + 1 + j: the ranges that can start at
+    // positions 1 .. 32 of the round (every range holds >= 1 task), so a range
+    // starting right after 31 one-task ranges (position 32) is seen too and
+    // r_lo keeps holding the next round's first task
+    const uint32_t j = r_lo + 1u + (uint32_t)lane;
     uint32_t bit = 0, at32 = 0;
-    if (lane > 0 && j < nr) {
+    if (j < nr) {
       const uint32_t d = rg[j] - t0;  // >= 1: range r_lo holds t0
       if (d < 32) bit = 1u << d;
       at32 = d == 32 ? 1u : 0u;

@@ -164,6 +164,12 @@ struct ProbeArgs {
   bool flag_count = false;      // only_flagged[rows] = number of flagged rows (0: exit at once)
 };
 rairs_status launch_probe_exact(const ProbeArgs& a, cudaStream_t s);
+// every row through the split exact path when rows < PX_CAP and nlist is large
+// (small search batches: no TF32 GEMM / certificate); *done = false otherwise
+rairs_status launch_probe_split_all(const ProbeArgs& a, cudaStream_t s, bool* done);
+// search batches of at most this many queries take launch_probe_split_all
+// (RAIRS_COARSE_SMALL; 0 disables)
+int coarse_small_rows();
 // few flagged rows x many lists: split exact fallback (clears the flags it handles).
 // prepare (before the certify kernel, which appends the flagged rows to
 // b.list / *count itself), launch (programmatic dependent launches), free.

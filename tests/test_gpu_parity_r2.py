@@ -23,6 +23,7 @@ import torch  # noqa: E402
 import paper_2601_07183_b200 as rb  # noqa: E402
 from synth import get_config, make_dataset  # noqa: E402
 from tests.test_gpu_parity import DEV, _t, assert_search_equal, case, gpu_search  # noqa: E402
+from tests.test_gpu_seil_paper import _hybrid_extra  # noqa: E402
 
 
 def _oracle_index(oracle, X, nlist, M, seed=11):
@@ -228,4 +229,58 @@ def test_split_query_parts_equal_oracle(oracle_mod, parts, nq):
     finally:
         del os.environ["RAIRS_FS_PARTS"]
     assert_search_equal(g, o)
+    idx.free()
+
+
+@pytest.mark.parametrize("nq", [1, 5, 16, 17])
+def test_small_batch_coarse_split_path(oracle_mod, nq):
+    """Search batches of <= 16 queries over >= 8,192 lists take the split exact
+    coarse path for every row (no TF32 GEMM / certificate); 17 queries take
+    the tensor-core path.  Both must give O1's probes and the oracle's
+    results (Alg. 3 / O1, O10)."""
+    spec = get_config("c0s", n=30000, nq=nq, d=32, M=16, nlist=8192)
+    X, Q = make_dataset(spec)
+    rows = X[np.random.default_rng(5).permutation(X.shape[0])[:20000]]
+    cent = rows[np.random.default_rng(6).permutation(rows.shape[0])[:8192]].copy()
+    cb = oracle_mod.pq_train(rows, 16, iters=2, seed=1)
+    l1, l2 = oracle_mod.assign(X, cent, "air")
+    codes = oracle_mod.encode(X, cb)
+    idx = rb.Index.build(_t(X), 8192, 16, centroids=_t(cent), codebook=_t(cb))
+    Qd = _t(Q)
+    for k, nprobe, rf in ((10, 3, 10), (5, 40, 4)):
+        pt = idx.search_debug(Qd, k, nprobe, rf)["probes"].cpu().numpy()
+        assert np.array_equal(pt, oracle_mod.probe(Q, cent, nprobe))
+        o = oracle_mod.search(X, l1, l2, codes, cent, cb, Q, k, nprobe, rf)
+        assert_search_equal(gpu_search(idx, Q, k, nprobe, rf), o)
+    idx.free()
+
+
+@pytest.mark.parametrize("layout", ["cell", "paper", "hybrid"])
+def test_runs_of_one_group_ranges(oracle_mod, layout):
+    """8,192 lists of ~4 vectors and AIR references: a query's SEIL work list
+    (Alg. 5) holds long runs of one-group ranges (short owned ranges and
+    references).  A round whose 32 tasks each start a new range must hand
+    the next round the range starting at position 32 (a range there was
+    once skipped: DCO still equal, one item never scored).  40 queries: the
+    unsplit query-major scan; nprobe 3 and 40."""
+    spec = get_config("c0s", n=30000, nq=40, d=32, M=16, nlist=8192)
+    X, Q = make_dataset(spec)
+    rows = X[np.random.default_rng(5).permutation(X.shape[0])[:20000]]
+    cent = rows[np.random.default_rng(6).permutation(rows.shape[0])[:8192]].copy()
+    cb = oracle_mod.pq_train(rows, 16, iters=2, seed=1)
+    l1, l2 = oracle_mod.assign(X, cent, "air")
+    codes = oracle_mod.encode(X, cb)
+    idx = rb.Index.build(_t(X), 8192, 16, centroids=_t(cent), codebook=_t(cb))
+    idx.set_seil_layout(layout)
+    for k, nprobe, rf in ((10, 3, 10), (5, 40, 4)):
+        o = oracle_mod.search(X, l1, l2, codes, cent, cb, Q, k, nprobe, rf)
+        g = gpu_search(idx, Q, k, nprobe, rf, "simt")
+        if layout == "paper":  # the paper-literal layout's DCO is O12's DCO_paperSEIL
+            want = oracle_mod.dco_variants(l1, l2, 8192, o["probes"])[1]
+            assert np.array_equal(g["dco"], np.asarray(want).reshape(g["dco"].shape))
+            g = dict(g, dco=o["dco"][:, 0])
+        elif layout == "hybrid":  # + the tiny cross cells probed from both sides
+            assert np.array_equal(g["dco"], o["dco"][:, 0] + _hybrid_extra(l1, l2, o["probes"]))
+            g = dict(g, dco=o["dco"][:, 0])
+        assert_search_equal(g, o)
     idx.free()
