@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(PX_T) probe_merge_kernel(ProbeArgs a,
 // probe_merge_kernel (with no flagged row both exit at once).
 rairs_status probe_split_prepare(const ProbeArgs& a, ProbeSplitBufs& b, cudaStream_t s) {
   b = ProbeSplitBufs{};
-  if (a.rows <= 0 || a.nl < 8192) return RAIRS_OK;
+  static const bool off = [] {  // RAIRS_COARSE_SPLIT=0: the tiled exact kernel takes every flagged row
+    const char* e = std::getenv("RAIRS_COARSE_SPLIT");
+    return e && std::atoi(e) == 0;
+  }();
+  if (a.rows <= 0 || a.nl < 8192 || off) return RAIRS_OK;
   b.per = (int)ceil_div(a.nl, PX_S);
   b.npow_s = next_pow2(std::max(b.per, a.L));
   b.npow_m = next_pow2(PX_S * a.L);

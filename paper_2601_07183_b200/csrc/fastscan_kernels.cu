@@ -647,12 +647,29 @@ __global__ void __launch_bounds__(FF_WARPS * 32) fs_finish_kernel(const __grid_c
         buf = src;
         bcap = cap;
       }
+    } else if (n <= caps) {
+      // one pass (four 8-B loads in flight per lane): copy into shared memory
+      // and histogram
+      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = i0 + 32u * u + lane;
+          v[u] = i < n ? src[i] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = i0 + 32u * u + lane;
+          if (i < n) {
+            cand[i] = v[u];
+            atomicAdd(&hist[(uint32_t)(v[u] >> 32) >> hsh], 1u);
+          }
+        }
+      }
     } else {
       for (uint32_t i = lane; i < n; i += 32) atomicAdd(&hist[(uint32_t)(src[i] >> 32) >> hsh], 1u);
       __syncwarp();
-      if (n <= caps) {
-        for (uint32_t i = lane; i < n; i += 32) cand[i] = src[i];
-      } else {
+      {
         // keep the entries whose bin is at most the bin of the bigK-th score
         uint32_t bl;
         const uint32_t bs = fs_bsel256(hist, bigK, &bl);
