@@ -425,18 +425,24 @@ def run_ours(args):
     if scan_mode == "simt":
         # the query-major scan is bound by instruction issue, not HBM:
         # its work in 4-bit LUT lookup-accumulates (DCO x M) against the issue
-        # ceiling of the prmt/dp4a formulation -- 8 lookups per 20 cycles per
-        # SMSP (per nibble word ~10 instructions on each of the alu and fma-heavy
-        # pipes, 0.5 warp-instructions/clk/SMSP each: tools/micro/pipe_rates.cu)
-        # x 32 lanes x 4 SMSPs x SMs x the SM clock sampled in the timed region
+        # ceiling of the kernel's word formulation -- per nibble word (8
+        # lookups) 9 alu-pipe instructions (and, 6 prmt, 2 lop3) at 0.5
+        # warp-instructions/clk/SMSP (tools/micro/pipe_rates.cu): 18 cycles
+        # with the pair-packed dp2a sums (M_pad <= 128: ~6 fma-pipe
+        # instructions), 20 cycles with one dp4a per item (~10 on the fma-heavy
+        # pipe) -- x 32 lanes x 4 SMSPs x SMs x the SM clock sampled in the
+        # timed region
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         clk = (clocks or {}).get("sm_mhz") or 1965.0
-        peak_l = 8.0 / 20.0 * 32 * 4 * nsm * clk * 1e6
+        m_pad = -(-spec.M // 16) * 16
+        cyc = 18.0 if (m_pad <= 128 and os.environ.get("RAIRS_FS_PACK", "1") != "0") else 20.0
+        peak_l = 8.0 / cyc * 32 * 4 * nsm * clk * 1e6
         ach_l = dco_local * spec.M / (kern_ms / 1e3)
         roof_alu = {"bound": "alu", "kernel": "fs_scan_kernel", "achieved": round(ach_l / 1e12, 3),
                     "peak": round(peak_l / 1e12, 3), "unit": "T lookups/s", "frac": round(ach_l / peak_l, 4),
                     "algorithmic_ops_per_launch": int(dco_local * spec.M),
-                    "peak_derivation": "8 lookups / 20 clk / SMSP x 32 lanes x 4 SMSPs x %d SMs x %.0f MHz" % (nsm, clk)}
+                    "peak_derivation": "8 lookups / %d clk / SMSP x 32 lanes x 4 SMSPs x %d SMs x %.0f MHz"
+                                       % (cyc, nsm, clk)}
 
     # ---------------- AIR + SEIL vs single assignment (the paper's comparison) ----
     vs_single = None
