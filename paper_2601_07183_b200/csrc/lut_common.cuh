@@ -24,11 +24,13 @@ __device__ __forceinline__ void lut_row(const float* __restrict__ qv, const floa
                                         int dsub, float (&T)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) T[j] = 0.0f;
+  const int S = dsub * M;  // entry stride (the codebook is < 2^31 floats)
   for (int t = 0; t < dsub; ++t) {
     const float qt = __ldg(qv + m * dsub + t);
+    const float* c = cb + t * M + m;  // entry j of (t, m) at c[j * S]
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float diff = __fsub_rn(qt, cb[((size_t)j * dsub + t) * M + m]);
+      const float diff = __fsub_rn(qt, c[j * S]);
       T[j] = __fadd_rn(T[j], __fmul_rn(diff, diff));
     }
   }
