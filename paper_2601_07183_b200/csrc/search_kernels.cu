@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(RS_THREADS) refine_stage_kernel(
   // not push out the score rows the concurrent selection streams
   uint64_t l2pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l2pol));
+  pdl_wait();  // the candidate keys of the preceding selection kernel
   // software pipeline: keys of unit u + 2 and rows of unit u + 1 are in
   // flight while unit u is computed (the row loads never wait on a key load)
   auto load_key = [&](int64_t q, int c) -> uint64_t {
@@ -308,11 +309,14 @@ static rairs_status launch_refine_stage(const rairs_index_s* idx, const SearchAr
   RAIRS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, refine_stage_kernel<D4>,
                                                                RS_THREADS, smem));
   const int grid = (int)std::min<int64_t>(a.nq, (int64_t)148 * std::max(occ, 1));
-  refine_stage_kernel<D4><<<grid, RS_THREADS, smem, s>>>(a.cand_keys, a.nq, bigK, a.k, a.queries,
-                                                          idx->X, idx->nshards, idx->labels,
-                                                          a.counters ? a.counters + 1 : nullptr,
-                                                          a.out_ids, a.out_dists);
-  RAIRS_CHECK_LAUNCH();
+  // programmatic dependent launch: the CTAs are resident while the selection
+  // kernel drains; pdl_wait() orders the key reads
+  RAIRS_CUDA_TRY(launch_pdl(refine_stage_kernel<D4>, dim3(grid), dim3(RS_THREADS), smem, s,
+                            (const uint64_t*)a.cand_keys, (int64_t)a.nq, bigK, (int)a.k,
+                            (const float*)a.queries, (const float*)idx->X, (int)idx->nshards,
+                            (const uint32_t*)idx->labels,
+                            a.counters ? a.counters + 1 : (unsigned long long*)nullptr,
+                            (int64_t*)a.out_ids, (float*)a.out_dists));
   return RAIRS_OK;
 }
 
