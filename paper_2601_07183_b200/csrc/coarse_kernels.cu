@@ -441,6 +441,9 @@ __global__ void __launch_bounds__(FT_THREADS, 1)
 // K2: merge splits, exact fp64 re-rank, certify, emit probes / assignment.
 constexpr int CT_THREADS = 256;
 constexpr int CT_WARPS = CT_THREADS / 32;
+#ifndef CT_MINB
+#define CT_MINB 3  // certify CTAs per SM the register budget is sized for (4: 64 registers, rematerialised thread ids and spills; 3: coarse stage -4.5 us on c4)
+#endif
 
 __device__ __forceinline__ uint32_t ord_f32(float f) {
   const uint32_t u = __float_as_uint(f);
@@ -540,7 +543,7 @@ struct CertArgs {
   }
 };
 
-__global__ void __launch_bounds__(CT_THREADS, 4) coarse_certify_kernel(CertArgs a) {
+__global__ void __launch_bounds__(CT_THREADS, CT_MINB) coarse_certify_kernel(CertArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = warp_id(), lane = lane_id();
   pdl_wait();  // the top-W lists of coarse_topw_kernel
