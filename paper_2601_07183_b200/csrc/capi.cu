@@ -354,8 +354,8 @@ static rairs_status search_impl(rairs_index_s* idx, const float* queries, int64_
         ex.defer_buf = dbuf;
         ex.defer_n = dn;
         st = launch_fastscan(idx, a, s, ex);
-        nk += (defer ? 2 : 1) + (dparts > 1 && defer ? 1 : 0) +
-              (fastscan_order_on() && nq > 1 && dparts == 1 ? 1 : 0);  // + LUT (+ finish) (+ merge) (+ order)
+        nk += (defer ? 2 : 1) + (dparts > 1 && defer ? 1 : 0);  // + LUT (+ finish) (+ merge); the
+                                                                // claim order comes from the LUT kernel
       }
       cudaFreeAsync(luts, s);
       cudaFreeAsync(dbuf, s);

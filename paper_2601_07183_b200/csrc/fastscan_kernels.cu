@@ -775,6 +775,17 @@ __global__ void __launch_bounds__(FL_WARPS * 32) fs_lut_kernel(const __grid_cons
     (void)lane;
   }
   pdl_wait();     // the coarse stage's probes are complete before this grid is
+  if (a.order) {  // the scan's claim order (fs_order_kernel's work, one launch fewer)
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.nq;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const int32_t* pq = a.probes + q * a.pstride;
+      uint64_t cost = 0;
+      for (int i = 0; i < a.nprobe; ++i) cost += __ldg(a.list_items + __ldg(pq + i));
+      uint32_t* ord = const_cast<uint32_t*>(a.order);
+      if (cost * (uint64_t)a.nlist > a.cost_thr) ord[atomicAdd(&a.ctr[2], 1u)] = (uint32_t)q;
+      else ord[a.nq - 1 - atomicAdd(&a.ctr[3], 1u)] = (uint32_t)q;
+    }
+  }
   pdl_trigger();
 }
 
@@ -1399,7 +1410,27 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
   RAIRS_TRY(fs_plan(idx, sa, ex, pl));
   const unsigned slot = idx->fs_slot.fetch_add(1u) % FS_SLOTS;
   pl.a.ctr = idx->fs_ctr + 4 * slot;
-  if (!ex.luts_ready) {  // A3 for the whole batch (overlaps the coarse stage's tail under PDL)
+  // small batches: each query's group tasks split over several warps
+  const int P = (!ex.qlist && !ex.tau_out && ex.defer_buf) ? fastscan_parts(idx, sa.nq, sa.nprobe) : 1;
+  pl.a.parts = P;
+  if (P > 1 && sa.dco) RAIRS_CUDA_TRY(cudaMemsetAsync(sa.dco, 0, (size_t)sa.nq * 8, s));
+  const bool use_order = fastscan_order_on() && P == 1 && !ex.qlist && sa.nq > 1;
+  uint32_t* order = nullptr;
+  struct OrderFree {
+    uint32_t*& p;
+    cudaStream_t s;
+    ~OrderFree() { if (p) cudaFreeAsync(p, s); }
+  } order_free{order, s};
+  if (use_order) {
+    RAIRS_CUDA_TRY(ws_malloc(&order, (size_t)sa.nq * 4, s));
+    pl.a.order = order;
+    pl.a.list_items = idx->list_items ? idx->list_items : idx->own_cnt;
+    pl.a.nlist = (int)idx->nlist;
+    const uint64_t total = idx->list_items ? (uint64_t)idx->sum_list_items : (uint64_t)idx->n_live;
+    pl.a.cost_thr = (uint64_t)pl.a.nprobe * total;
+  }
+  if (!ex.luts_ready) {  // A3 for the whole batch (overlaps the coarse stage's tail under PDL);
+                         // with the claim order computed after its wait on the coarse stage
     const bool keepT = idx->M * 17 <= 16 * 1024 / 4;
     const size_t lsm = (size_t)pl.a.cb_smem + (size_t)FL_WARPS * (keepT ? 17 : 1) * idx->M * 4;
     RAIRS_CUDA_TRY(cudaFuncSetAttribute(fs_lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1411,25 +1442,7 @@ rairs_status launch_fastscan(rairs_index_s* idx, const SearchArgs& sa, cudaStrea
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sa.nq, FL_WARPS), 148LL * per_sm));
     RAIRS_CUDA_TRY(launch_pdl(fs_lut_kernel, dim3(g), dim3(FL_WARPS * 32), lsm, s, pl.a,
                               const_cast<uint4*>(sa.luts)));
-  }
-  // small batches: each query's group tasks split over several warps
-  const int P = (!ex.qlist && !ex.tau_out && ex.defer_buf) ? fastscan_parts(idx, sa.nq, sa.nprobe) : 1;
-  pl.a.parts = P;
-  if (P > 1 && sa.dco) RAIRS_CUDA_TRY(cudaMemsetAsync(sa.dco, 0, (size_t)sa.nq * 8, s));
-  const bool use_order = fastscan_order_on() && P == 1;
-  uint32_t* order = nullptr;
-  struct OrderFree {
-    uint32_t*& p;
-    cudaStream_t s;
-    ~OrderFree() { if (p) cudaFreeAsync(p, s); }
-  } order_free{order, s};
-  if (use_order && !ex.qlist && sa.nq > 1) {
-    RAIRS_CUDA_TRY(ws_malloc(&order, (size_t)sa.nq * 4, s));
-    pl.a.order = order;
-    pl.a.list_items = idx->list_items ? idx->list_items : idx->own_cnt;
-    pl.a.nlist = (int)idx->nlist;
-    const uint64_t total = idx->list_items ? (uint64_t)idx->sum_list_items : (uint64_t)idx->n_live;
-    pl.a.cost_thr = (uint64_t)pl.a.nprobe * total;
+  } else if (use_order) {
     const unsigned g = (unsigned)ceil_div(sa.nq, 256);
     RAIRS_CUDA_TRY(launch_pdl(fs_order_kernel, dim3(g), dim3(256), 0, s, pl.a, order));
   }
