@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(PX_T) probe_split_kernel(ProbeArgs a,
   uint32_t* ids = reinterpret_cast<uint32_t*>(keys + npow);
   double* xs = reinterpret_cast<double*>(ids + npow + (npow & 1));
   float* tile = reinterpret_cast<float*>(xs + a.d);  // [PX_T][33]
+  pdl_wait();  // launched with launch_pdl: the flagged-row list and count of the previous kernel
   const int64_t n = min(*count, (uint32_t)PX_CAP);
   for (int64_t w = blockIdx.x; w < n * PX_S; w += gridDim.x) {
     const int64_t i = w / PX_S;
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(PX_T) probe_merge_kernel(ProbeArgs a,
   extern __shared__ __align__(16) unsigned char sm[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(sm);
   uint32_t* ids = reinterpret_cast<uint32_t*>(keys + npow);
+  pdl_wait();  // launched with launch_pdl: the flagged-row list and count of the previous kernel
   const int64_t n = min(*count, (uint32_t)PX_CAP);
   const int L = a.L, lane = lane_id(), warp = warp_id();
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
@@ -439,14 +441,16 @@ rairs_status probe_split_prepare(const ProbeArgs& a, ProbeSplitBufs& b, cudaStre
 rairs_status probe_split_launch(const ProbeArgs& a, const ProbeSplitBufs& b, const uint32_t* count,
                                 int32_t* flags, cudaStream_t s) {
   if (!b.on) return RAIRS_OK;
-  // plain launches: as programmatic dependent launches (split after certify,
-  // merge after split) the build's all-uncertified case faulted (an illegal
-  // address in the fallback chain; not understood, so not used)
+  // programmatic dependent launches: both kernels wait (griddepcontrol.wait)
+  // before reading the list / count / partial lists of their predecessor (an
+  // earlier PDL version without the waits read them too early and faulted)
   RAIRS_CUDA_TRY(cudaFuncSetAttribute(probe_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.sm_s));
-  probe_split_kernel<<<148 * 4, PX_T, b.sm_s, s>>>(a, b.list, count, b.per, b.npow_s, b.tk, b.ti);
+  RAIRS_CUDA_TRY(launch_pdl(probe_split_kernel, dim3(148 * 4), dim3(PX_T), b.sm_s, s, a,
+                            (const uint32_t*)b.list, count, b.per, b.npow_s, b.tk, b.ti));
   RAIRS_CUDA_TRY(cudaFuncSetAttribute(probe_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.sm_m));
-  probe_merge_kernel<<<148 * 2, PX_T, b.sm_m, s>>>(a, b.list, count, b.npow_m, b.tk, b.ti, flags);
-  RAIRS_CHECK_LAUNCH();
+  RAIRS_CUDA_TRY(launch_pdl(probe_merge_kernel, dim3(148 * 2), dim3(PX_T), b.sm_m, s, a,
+                            (const uint32_t*)b.list, count, b.npow_m, (const uint64_t*)b.tk,
+                            (const uint32_t*)b.ti, flags));
   return RAIRS_OK;
 }
 
